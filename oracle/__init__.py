@@ -1,0 +1,186 @@
+"""CPU oracle for the APS gradient synchronisation (arXiv 1911.08907).
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import this
+package.  The product path (``paper_1911_08907_b200``) never imports it and
+shares no code with it.
+
+The arithmetic lives in ``aps_oracle.c`` (plain C, binary64 unless the paper
+fixes binary32); this module only builds it with gcc and marshals numpy
+arrays through ctypes.  Every function cites the paper passage it follows in
+the C source.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+SRC = HERE / "aps_oracle.c"
+LIB = HERE / "liboracle.so"
+
+EMPTY = -(2**31)       # FindMaxExp of an all-zero tensor ("-INF", Alg. 1)
+NONFINITE = 2**31 - 1
+OK, ERR_ARG, ERR_FORMAT, ERR_NONFINITE = 0, 1, 2, 6
+TILE = 128
+
+
+def build(force: bool = False) -> Path:
+    """Compile aps_oracle.c with gcc (IEEE binary32/64, no contraction)."""
+    if force or not LIB.exists() or LIB.stat().st_mtime < SRC.stat().st_mtime:
+        tmp = LIB.with_suffix(f".so.tmp{os.getpid()}")
+        subprocess.check_call(
+            ["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-fno-fast-math",
+             "-ffp-contract=off", "-fexcess-precision=standard", "-Wall", "-Wextra",
+             "-o", str(tmp), str(SRC), "-lm"])
+        os.replace(tmp, LIB)
+    return LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        L = ctypes.CDLL(str(build()))
+        i32, i64, u32, f32 = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, ctypes.c_float
+        vp = ctypes.c_void_p
+        L.oracle_format_valid.argtypes = [ctypes.c_int, ctypes.c_int]
+        L.oracle_bias.argtypes = [ctypes.c_int]
+        L.oracle_cast1.argtypes = [f32, ctypes.c_int, ctypes.c_int]
+        L.oracle_cast1.restype = u32
+        L.oracle_decode1.argtypes = [u32, ctypes.c_int, ctypes.c_int]
+        L.oracle_decode1.restype = f32
+        L.oracle_cast.argtypes = [vp, vp, i64, ctypes.c_int, ctypes.c_int]
+        L.oracle_decode.argtypes = [vp, vp, i64, ctypes.c_int, ctypes.c_int]
+        L.oracle_find_max_exp.argtypes = [vp, i64, ctypes.c_int]
+        L.oracle_find_max_exp.restype = i32
+        L.oracle_scale_exp.argtypes = [ctypes.c_int, i32]
+        L.oracle_scale_exp.restype = i32
+        L.oracle_scale.argtypes = [f32, i32]
+        L.oracle_scale.restype = f32
+        L.oracle_ring_add.argtypes = [u32, u32, ctypes.c_int, ctypes.c_int]
+        L.oracle_ring_add.restype = u32
+        L.oracle_unscale1.argtypes = [u32, i32, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int]
+        L.oracle_unscale1.restype = f32
+        L.oracle_total_tiles.argtypes = [ctypes.c_int, ctypes.c_int, vp]
+        L.oracle_total_tiles.restype = i64
+        L.oracle_packed_bytes.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp]
+        L.oracle_packed_bytes.restype = i64
+        L.oracle_pack.argtypes = [vp, i64, ctypes.c_int, vp]
+        L.oracle_unpack.argtypes = [vp, i64, ctypes.c_int, vp]
+        L.oracle_aps_sync.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp,
+                                      vp, ctypes.c_int, vp, vp, vp, vp]
+        _lib = L
+    return _lib
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def bias(e: int) -> int:
+    return lib().oracle_bias(e)
+
+
+def format_valid(e: int, m: int) -> bool:
+    return lib().oracle_format_valid(e, m) == OK
+
+
+def cast(x, e: int, m: int) -> np.ndarray:
+    """O6: fp32 -> (e,m) codes (uint32), RNE, gradual underflow, IEEE overflow."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    out = np.empty(x.shape, dtype=np.uint32)
+    rc = lib().oracle_cast(_ptr(x), _ptr(out), x.size, e, m)
+    if rc:
+        raise ValueError(f"oracle_cast rc={rc}")
+    return out
+
+
+def decode(codes, e: int, m: int) -> np.ndarray:
+    c = np.ascontiguousarray(codes, dtype=np.uint32)
+    out = np.empty(c.shape, dtype=np.float32)
+    rc = lib().oracle_decode(_ptr(c), _ptr(out), c.size, e, m)
+    if rc:
+        raise ValueError(f"oracle_decode rc={rc}")
+    return out
+
+
+def find_max_exp(g, N: int) -> int:
+    g = np.ascontiguousarray(g, dtype=np.float32)
+    return lib().oracle_find_max_exp(_ptr(g), g.size, N)
+
+
+def scale_exp(e: int, E: int) -> int:
+    return lib().oracle_scale_exp(e, E)
+
+
+def scale(g: float, ft: int) -> float:
+    return lib().oracle_scale(g, ft)
+
+
+def ring_add(a: int, b: int, e: int, m: int) -> int:
+    return lib().oracle_ring_add(a, b, e, m)
+
+
+def unscale1(s: int, ft: int, N: int, average: int, e: int, m: int) -> float:
+    return lib().oracle_unscale1(s, ft, N, average, e, m)
+
+
+def total_tiles(p: int, numels) -> int:
+    n = np.ascontiguousarray(numels, dtype=np.int64)
+    return lib().oracle_total_tiles(p, n.size, _ptr(n))
+
+
+def packed_bytes(p: int, e: int, m: int, numels) -> int:
+    n = np.ascontiguousarray(numels, dtype=np.int64)
+    return lib().oracle_packed_bytes(p, e, m, n.size, _ptr(n))
+
+
+def pack(codes, b: int) -> np.ndarray:
+    c = np.ascontiguousarray(codes, dtype=np.uint32)
+    out = np.zeros((c.size * b + 7) // 8, dtype=np.uint8)
+    lib().oracle_pack(_ptr(c), c.size, b, _ptr(out))
+    return out
+
+
+def unpack(buf, n: int, b: int) -> np.ndarray:
+    buf = np.ascontiguousarray(buf, dtype=np.uint8)
+    out = np.empty(n, dtype=np.uint32)
+    lib().oracle_unpack(_ptr(buf), n, b, _ptr(out))
+    return out
+
+
+class SyncResult:
+    def __init__(self, rc, ftilde, packed, reduced, out):
+        self.rc, self.ftilde, self.packed, self.reduced, self.out = rc, ftilde, packed, reduced, out
+
+
+def aps_sync(grads, e: int, m: int, average: int = 1, want_packed: bool = True,
+             want_out: bool = True) -> SyncResult:
+    """Full APS sync (Alg. 1) over p simulated ranks.
+
+    ``grads[r][l]`` is rank r's fp32 gradient of layer l (numpy).  Returns the
+    scale exponents f~, each rank's packed codes, the reduced packed codes
+    every rank ends with, and the unscaled/averaged fp32 outputs.
+    """
+    p = len(grads)
+    nl = len(grads[0])
+    numels = np.array([np.asarray(g).size for g in grads[0]], dtype=np.int64)
+    flat = [np.ascontiguousarray(grads[r][l], dtype=np.float32) for r in range(p) for l in range(nl)]
+    gptrs = (ctypes.c_void_p * len(flat))(*[a.ctypes.data for a in flat])
+    nbytes = packed_bytes(p, e, m, numels)
+    ft = np.zeros(nl, dtype=np.int32)
+    packed = np.zeros((p, nbytes), dtype=np.uint8) if want_packed else None
+    reduced = np.zeros(nbytes, dtype=np.uint8)
+    outs = [np.empty(int(n), dtype=np.float32) for n in numels] if want_out else None
+    optrs = (ctypes.c_void_p * nl)(*[a.ctypes.data for a in outs]) if want_out else None
+    rc = lib().oracle_aps_sync(p, e, m, nl, _ptr(numels), gptrs, average, _ptr(ft),
+                               _ptr(packed) if want_packed else None, _ptr(reduced),
+                               optrs)
+    return SyncResult(rc, ft, packed, reduced, outs)

@@ -1,0 +1,384 @@
+/*
+ * aps_oracle.c -- plain, slow, obviously-correct CPU oracle for the APS
+ * (Auto-Precision Scaling, arXiv 1911.08907) gradient synchronisation.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.
+ * The product path (paper_1911_08907_b200/, libaps.so) never links, calls
+ * or executes anything under oracle/.  This file shares no code, header,
+ * table or constant generator with the CUDA path.
+ *
+ * Citations: "P:n" is a line of the paper's LaTeX source, with
+ * the algorithm / equation / table it falls in.  "A<k>" is a reading of the
+ * paper listed in DESIGN.md (section "Readings").  "O<k>" is an oracle step
+ * of SURVEY.md section 8(c).
+ *
+ * Arithmetic: every value is carried in IEEE binary64 where the paper gives
+ * no precision; the operations the paper performs in fp32 (Alg. 1's scale
+ * g*2^f, the low-precision accumulator's fp32 add that CPD re-quantises, the
+ * cast back and the unscale) are done in binary32 exactly as written.
+ * Requires FLT_EVAL_METHOD == 0 (x86-64 SSE) and no -ffast-math /
+ * -ffp-contract.
+ *
+ * Pins (tests/test_oracle_*.py): Table 2 ranges, torch dtype equivalence
+ * (float8_e5m2, float16, bfloat16, float8_e4m3fn below 248), brute-force
+ * argmin enumeration, the paper's worked shifts (Fig. aps_comparing), the
+ * no-overflow invariant, (8,23) transparency, exact-rounding of the ring add
+ * and numpy.packbits for the layout.  Parity of the ring-chunk layout (O7)
+ * is a design rule with no paper pin: "parity unpinned (layout)" -- see
+ * DESIGN.md.
+ */
+#include <float.h>
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#if !defined(FLT_EVAL_METHOD) || FLT_EVAL_METHOD != 0
+#error "oracle needs FLT_EVAL_METHOD == 0 so float arithmetic is IEEE binary32"
+#endif
+
+/* status codes, same numeric values as the product's, written here independently */
+enum { OR_OK = 0, OR_ERR_ARG = 1, OR_ERR_FORMAT = 2, OR_ERR_NONFINITE = 6 };
+
+#define OR_TILE 128 /* O7: elements per tile (design rule, not in the paper) */
+#define OR_EMPTY INT32_MIN  /* FindMaxExp of an all-zero tensor: "-INF" (Alg. 1) */
+#define OR_NONFINITE INT32_MAX
+
+/* ------------------------------------------------------------------ */
+/* O1  Format.  Table `precision_range` P:184-198; Alg. 1 P:237-242.   */
+/* ------------------------------------------------------------------ */
+
+/* Validity (A-readings in DESIGN.md): 2 <= e <= 8 (e = 1 has bias 0 and no
+ * normal numbers), 0 <= m <= 23, 1 + e + m <= 32.  CPD: "exp bits <= 8 and
+ * man bits <= 23". */
+int oracle_format_valid(int e, int m)
+{
+    if (e < 2 || e > 8 || m < 0 || m > 23 || 1 + e + m > 32) return OR_ERR_FORMAT;
+    return OR_OK;
+}
+
+/* upper_bound_exp <- 2^(exp_bits-1) - 1   (Alg. 1 line 1) */
+int oracle_bias(int e) { return (1 << (e - 1)) - 1; }
+
+/* ------------------------------------------------------------------ */
+/* O1  decode: code -> value.  IEEE-style layout s | E | M, sign MSB.  */
+/* normal (1 + M/2^m) * 2^(E-bias); subnormal M * 2^(1-bias-m);        */
+/* all-ones exponent reserved (M = 0: Inf, else NaN).                  */
+/* ------------------------------------------------------------------ */
+float oracle_decode1(uint32_t code, int e, int m)
+{
+    const int bias = oracle_bias(e);
+    const uint32_t sign = (code >> (e + m)) & 1u;
+    const uint32_t E = (code >> m) & ((1u << e) - 1u);
+    const uint32_t M = code & ((m == 0) ? 0u : ((1u << m) - 1u));
+    double v;
+    if (E == (1u << e) - 1u) {
+        v = (M == 0) ? INFINITY : NAN;
+    } else if (E == 0) {
+        v = ldexp((double)M, 1 - bias - m);
+    } else {
+        v = ldexp(1.0 + ldexp((double)M, -m), (int)E - bias);
+    }
+    if (sign) v = -v;
+    return (float)v; /* every finite value of a format with e<=8, m<=23 is exact in binary32 */
+}
+
+/* encode a non-negative value v that is EXACTLY representable in (e,m),
+ * or equal to 2^(bias+1) (the stand-in for +Inf in O6). */
+static uint32_t encode_magnitude(double v, int e, int m)
+{
+    const int bias = oracle_bias(e);
+    if (v == 0.0) return 0u;
+    if (v >= ldexp(1.0, bias + 1)) return ((1u << e) - 1u) << m; /* Inf */
+    if (v < ldexp(1.0, 1 - bias)) {                              /* subnormal: E = 0 */
+        double M = v / ldexp(1.0, 1 - bias - m);
+        return (uint32_t)M;
+    }
+    int k;
+    double f = frexp(v, &k); /* v = f * 2^k, f in [0.5, 1) */
+    (void)f;
+    k -= 1;                  /* v in [2^k, 2^(k+1)) */
+    double M = (v / ldexp(1.0, k) - 1.0) * ldexp(1.0, m);
+    return ((uint32_t)(k + bias) << m) | (uint32_t)M;
+}
+
+/* ------------------------------------------------------------------ */
+/* O6  Cast(x, exp_bit, man_bit): round-to-nearest-even into   */
+/* (e,m) with gradual underflow ("smaller than 2^-16 ... cast to 0",   */
+/* P:278, A10) and IEEE overflow ("greater than 2^15 will overflow and */
+/* cast to INF", A11).  Ties go to the candidate whose          */
+/* magnitude code is even (A9; equals IEEE ties-to-even for m >= 1).   */
+/* Method: the two representable neighbours lo <= |x| < hi are found   */
+/* from the quantum of |x|'s binade; 2|x| is compared with lo + hi.    */
+/* All of it is exact in binary64.                                     */
+/* ------------------------------------------------------------------ */
+uint32_t oracle_cast1(float x, int e, int m)
+{
+    const int bias = oracle_bias(e);
+    const uint32_t sbit = (signbit(x) ? 1u : 0u) << (e + m);
+    const uint32_t inf_code = sbit | (((1u << e) - 1u) << m);
+    if (isnan(x)) /* canonical NaN: mantissa MSB set; m = 0 has no NaN code (A12) */
+        return (m > 0) ? (inf_code | (1u << (m - 1))) : inf_code;
+    if (isinf(x)) return inf_code;
+
+    const double a = fabs((double)x);
+    if (a == 0.0) return sbit;                       /* signed zero (A15) */
+    if (a >= ldexp(1.0, bias + 1)) return inf_code;  /* past every candidate */
+
+    int k;
+    (void)frexp(a, &k);
+    k -= 1;                                          /* a in [2^k, 2^(k+1)) */
+    const int qexp = ((k > 1 - bias) ? k : (1 - bias)) - m;
+    const double quantum = ldexp(1.0, qexp);         /* spacing of (e,m) values around a */
+    const double lo = floor(a / quantum) * quantum;  /* largest value <= a */
+    const double hi = lo + quantum;                  /* smallest value >  a (2^(bias+1) = Inf) */
+    const uint32_t clo = encode_magnitude(lo, e, m);
+    const uint32_t chi = encode_magnitude(hi, e, m);
+    uint32_t mag;
+    if (2.0 * a < lo + hi) mag = clo;
+    else if (2.0 * a > lo + hi) mag = chi;
+    else mag = (clo % 2u == 0u) ? clo : chi;        /* tie: even code */
+    return sbit | mag;
+}
+
+int oracle_cast(const float *x, uint32_t *codes, int64_t n, int e, int m)
+{
+    if (oracle_format_valid(e, m)) return OR_ERR_FORMAT;
+    if (n < 0 || (n > 0 && (!x || !codes))) return OR_ERR_ARG;
+    for (int64_t i = 0; i < n; ++i) codes[i] = oracle_cast1(x[i], e, m);
+    return OR_OK;
+}
+
+int oracle_decode(const uint32_t *codes, float *x, int64_t n, int e, int m)
+{
+    if (oracle_format_valid(e, m)) return OR_ERR_FORMAT;
+    if (n < 0 || (n > 0 && (!x || !codes))) return OR_ERR_ARG;
+    for (int64_t i = 0; i < n; ++i) x[i] = oracle_decode1(codes[i], e, m);
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------ */
+/* O2/O3  FindMaxExp(g * N)   (Alg. 1 line 3; function P:260-271)*/
+/*   max over i != 0 of ceil(log2(abs(i)))  ->  -INF for an all-zero   */
+/*   tensor.  Reading A2: the product N*|g_i| is taken exactly (Eq. 4, */
+/*   P:375, writes ceil(log2|N*g^|)).  Reading A5: exact ceil(log2)    */
+/*   also for fp32 subnormals.  ceil(log2(.)) is monotone, so the max  */
+/*   over elements equals ceil(log2(N * max|g_i|)).                    */
+/*   Returns OR_EMPTY (A3), or OR_NONFINITE when any element is Inf/NaN*/
+/*   (A4).                                                             */
+/* ------------------------------------------------------------------ */
+static int32_t ceil_log2_exact(double v) /* v > 0, exact */
+{
+    int k;
+    double f = frexp(v, &k); /* v = f * 2^k with f in [0.5, 1) */
+    return (f == 0.5) ? (k - 1) : k;
+}
+
+int32_t oracle_find_max_exp(const float *g, int64_t n, int N)
+{
+    int32_t max_exp = OR_EMPTY; /* "max_exp <- -INF" */
+    for (int64_t i = 0; i < n; ++i) {
+        if (!isfinite(g[i])) return OR_NONFINITE;
+        if (g[i] != 0.0f) {                                     /* "if i != 0" */
+            int32_t t = ceil_log2_exact((double)N * fabs((double)g[i])); /* ceil(log2(abs(N*i))) */
+            if (t > max_exp) max_exp = t;
+        }
+    }
+    return max_exp;
+}
+
+/* O4  f~ <- upper_bound_exp - AllReduce(max_grad_exp, MAX)   (Alg. 1 line 4,
+ * P:246; Eq. (4) P:375 with p^ = 2^upper_bound_exp, reading A1).
+ * All-zero layer: f~ = 0 (A3). */
+int32_t oracle_scale_exp(int e, int32_t E)
+{
+    if (E == OR_EMPTY) return 0;
+    return oracle_bias(e) - E;
+}
+
+/* O5  g <- g * 2^f~  (Alg. 1 line 5): one binary32 result, RNE,
+ * gradual underflow (A8: ldexpf semantics).  (double)g * 2^f is exact in
+ * binary64 for every f~ that can arise, so the only rounding is the cast to
+ * float. */
+float oracle_scale(float g, int32_t ft) { return (float)ldexp((double)g, ft); }
+
+/* O8 helper: one low-precision accumulation step as CPD simulates it
+ * (reading A13): the addends are cast back to fp32, added in
+ * fp32, and the sum is re-quantised. */
+uint32_t oracle_ring_add(uint32_t acc, uint32_t addend, int e, int m)
+{
+    float s = oracle_decode1(acc, e, m) + oracle_decode1(addend, e, m); /* fl32 add */
+    return oracle_cast1(s, e, m);
+}
+
+/* O10  g <- Cast(low_g, 8, 23); g <- g / 2^f~   (Alg. 1 lines 7-8,
+ * P:254-256), then the average over N ranks (north_star; reading A16):
+ * out = fl32( fl32(dec(s) * 2^-f~) / N ). */
+float oracle_unscale1(uint32_t s, int32_t ft, int N, int average, int e, int m)
+{
+    float g = oracle_decode1(s, e, m);               /* Cast(low_g, 8, 23): exact */
+    float t = (float)ldexp((double)g, -ft);          /* g / 2^f~, one binary32 rounding */
+    if (average) t = t / (float)N;                   /* IEEE binary32 division */
+    return t;
+}
+
+/* ------------------------------------------------------------------ */
+/* O7  Layout (design rule; parity unpinned by the paper).            */
+/*   Layer l occupies T_l = ceil(n_l / 128) tiles from tile offset    */
+/*   o_l = sum_{k<l} T_k (caller's layer order); T = sum T_l;         */
+/*   T' = p * ceil(T / p); chunk c = tiles [c T'/p, (c+1) T'/p).      */
+/* O11 Pack: code i of the whole buffer occupies bits [i b, (i+1) b), */
+/*   LSB-first, in a little-endian byte stream (tile t = bytes        */
+/*   [16 b t, 16 b (t+1)) ).  Padding codes are +0.                    */
+/* ------------------------------------------------------------------ */
+int64_t oracle_total_tiles(int p, int n_layers, const int64_t *numels)
+{
+    int64_t T = 0;
+    for (int l = 0; l < n_layers; ++l) T += (numels[l] + OR_TILE - 1) / OR_TILE;
+    return ((T + p - 1) / p) * p; /* T' */
+}
+
+int64_t oracle_packed_bytes(int p, int e, int m, int n_layers, const int64_t *numels)
+{
+    if (oracle_format_valid(e, m) || p < 1 || n_layers < 1 || !numels) return -1;
+    const int b = 1 + e + m;
+    return 16 * (int64_t)b * oracle_total_tiles(p, n_layers, numels);
+}
+
+void oracle_put_code(uint8_t *buf, int64_t i, int b, uint32_t code)
+{
+    for (int j = 0; j < b; ++j) {
+        int64_t bit = i * b + j;
+        uint8_t mask = (uint8_t)(1u << (bit % 8));
+        if ((code >> j) & 1u) buf[bit / 8] |= mask;
+        else buf[bit / 8] &= (uint8_t)~mask;
+    }
+}
+
+uint32_t oracle_get_code(const uint8_t *buf, int64_t i, int b)
+{
+    uint32_t code = 0;
+    for (int j = 0; j < b; ++j) {
+        int64_t bit = i * b + j;
+        if ((buf[bit / 8] >> (bit % 8)) & 1u) code |= (1u << j);
+    }
+    return code;
+}
+
+int oracle_pack(const uint32_t *codes, int64_t n, int b, uint8_t *out)
+{
+    if (b < 1 || b > 32 || n < 0) return OR_ERR_ARG;
+    for (int64_t i = 0; i < n; ++i) oracle_put_code(out, i, b, codes[i]);
+    return OR_OK;
+}
+
+int oracle_unpack(const uint8_t *buf, int64_t n, int b, uint32_t *codes)
+{
+    if (b < 1 || b > 32 || n < 0) return OR_ERR_ARG;
+    for (int64_t i = 0; i < n; ++i) codes[i] = oracle_get_code(buf, i, b);
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------ */
+/* Whole APS synchronisation for p simulated ranks, Alg. 1 */
+/* in the paper's order: FindMaxExp -> AllReduce(MAX) -> f~ -> scale   */
+/* -> Cast -> AllReduce(SUM) as a ring with a re-       */
+/* quantise after every add -> Cast back -> unscale (and   */
+/* average, A16).                                                      */
+/*                                                                     */
+/* grads: p * n_layers host pointers, rank-major (grads[r*n_layers+l]).*/
+/* ftilde_out[n_layers]; packed_out: p * packed_bytes or NULL (each    */
+/* rank's codes after Cast, O11); reduced_out: packed_bytes or NULL    */
+/* (the codes every rank holds after the all-reduce, O8/O9); out:      */
+/* n_layers host pointers (fp32), or NULL.                             */
+/* Returns OR_OK, OR_ERR_ARG, OR_ERR_FORMAT or OR_ERR_NONFINITE.       */
+/* ------------------------------------------------------------------ */
+int oracle_aps_sync(int p, int e, int m, int n_layers, const int64_t *numels,
+                    const float *const *grads, int average, int32_t *ftilde_out,
+                    uint8_t *packed_out, uint8_t *reduced_out, float *const *out)
+{
+    if (oracle_format_valid(e, m)) return OR_ERR_FORMAT;
+    if (p < 1 || n_layers < 1 || !numels || !grads) return OR_ERR_ARG;
+    for (int l = 0; l < n_layers; ++l)
+        if (numels[l] < 1) return OR_ERR_ARG;
+
+    const int b = 1 + e + m;
+    const int64_t Tp = oracle_total_tiles(p, n_layers, numels); /* T' */
+    const int64_t ncodes = Tp * OR_TILE;
+    const int64_t chunk_codes = (Tp / p) * OR_TILE;
+    const int64_t nbytes = 16 * (int64_t)b * Tp;
+
+    /* Alg. 1 line 3: max_grad_exp <- FindMaxExp(g * N), on every rank;
+     * line 4: AllReduce(max_grad_exp, MAX). */
+    int32_t *E = (int32_t *)malloc(sizeof(int32_t) * (size_t)n_layers);
+    int32_t *ft = (int32_t *)malloc(sizeof(int32_t) * (size_t)n_layers);
+    int nonfinite = 0;
+    for (int l = 0; l < n_layers; ++l) {
+        int32_t Emax = OR_EMPTY;
+        for (int r = 0; r < p; ++r) {
+            int32_t Er = oracle_find_max_exp(grads[(size_t)r * n_layers + l], numels[l], p);
+            if (Er == OR_NONFINITE) nonfinite = 1;
+            if (Er > Emax) Emax = Er;
+        }
+        E[l] = Emax;
+        ft[l] = oracle_scale_exp(e, Emax); /* f~ <- upper_bound_exp - E */
+        if (ftilde_out) ftilde_out[l] = ft[l];
+    }
+    if (nonfinite) { /* A4: outputs unspecified, the error is reported */
+        free(E); free(ft);
+        return OR_ERR_NONFINITE;
+    }
+
+    /* Alg. 1 lines 5-6: g <- g * 2^f~ ; low_g <- Cast(g, exp_bit, man_bit),
+     * placed in the O7 layout (padding codes are +0). */
+    uint32_t *q = (uint32_t *)calloc((size_t)p * (size_t)ncodes, sizeof(uint32_t));
+    for (int r = 0; r < p; ++r) {
+        int64_t tile_off = 0;
+        for (int l = 0; l < n_layers; ++l) {
+            const float *g = grads[(size_t)r * n_layers + l];
+            uint32_t *dst = q + (size_t)r * ncodes + tile_off * OR_TILE;
+            for (int64_t i = 0; i < numels[l]; ++i)
+                dst[i] = oracle_cast1(oracle_scale(g[i], ft[l]), e, m);
+            tile_off += (numels[l] + OR_TILE - 1) / OR_TILE;
+        }
+        if (packed_out) {
+            uint8_t *pk = packed_out + (size_t)r * (size_t)nbytes;
+            memset(pk, 0, (size_t)nbytes);
+            oracle_pack(q + (size_t)r * ncodes, ncodes, b, pk);
+        }
+    }
+
+    /* Alg. 1 line 7: low_g <- AllReduce(low_g, SUM), as a ring with
+     * the low-precision accumulator re-quantising after each add.
+     * O8: chunk c is accumulated in rank order c+1, c+2, ..., c (the owner
+     * adds last, "add a local gradient with the summation of all other
+     * nodes' local gradients in the last step").  O9: every rank then holds
+     * the same codes. */
+    uint32_t *s = (uint32_t *)calloc((size_t)ncodes, sizeof(uint32_t));
+    for (int c = 0; c < p; ++c) {
+        for (int64_t i = c * chunk_codes; i < (c + 1) * chunk_codes; ++i) {
+            uint32_t acc = q[(size_t)((c + 1) % p) * ncodes + i];
+            for (int j = 2; j <= p; ++j)
+                acc = oracle_ring_add(acc, q[(size_t)((c + j) % p) * ncodes + i], e, m);
+            s[i] = acc;
+        }
+    }
+    if (reduced_out) {
+        memset(reduced_out, 0, (size_t)nbytes);
+        oracle_pack(s, ncodes, b, reduced_out);
+    }
+
+    /* Alg. 1 lines 8-9: g <- Cast(low_g, 8, 23); g <- g / 2^f~; average. */
+    if (out) {
+        int64_t tile_off = 0;
+        for (int l = 0; l < n_layers; ++l) {
+            const uint32_t *src = s + tile_off * OR_TILE;
+            for (int64_t i = 0; i < numels[l]; ++i)
+                out[l][i] = oracle_unscale1(src[i], ft[l], p, average, e, m);
+            tile_off += (numels[l] + OR_TILE - 1) / OR_TILE;
+        }
+    }
+    free(q); free(s); free(E); free(ft);
+    return OR_OK;
+}
