@@ -1,0 +1,206 @@
+/*
+ * aps.h -- C ABI of libaps, a B200-native (sm_100a) implementation of the
+ * data-parallel hot path of Auto-Precision Scaling (APS, arXiv 1911.08907):
+ * layer-wise low-precision gradient synchronisation.
+ *
+ * Paper citations ("P:n") are lines of the paper's LaTeX source with the
+ * algorithm / equation / table they fall in.  Readings of ambiguous passages
+ * ("A<k>") are listed in DESIGN.md.
+ *
+ * The method (Alg. 1 `alg:APS_grad`), per layer g of the gradient
+ * list, with customised float (exp_bit, man_bit) and N ranks:
+ *   upper_bound_exp <- 2^(exp_bit-1) - 1
+ *   max_grad_exp    <- FindMaxExp(g * N)
+ *   f~              <- upper_bound_exp - AllReduce(max_grad_exp, MAX)   (Eq. 4)
+ *   g               <- g * 2^f~
+ *   low_g           <- Cast(g, exp_bit, man_bit)  round-to-nearest-even
+ *   low_g           <- AllReduce(low_g, SUM)  ring, re-quantised after
+ *                      every add as CPD's low-precision accumulator
+ *   g               <- Cast(low_g, 8, 23) / 2^f~, then / N
+ *
+ * Calls map to the method as:
+ *   aps_layer_scales   -> FindMaxExp on every layer + AllReduce(E, MAX)
+ *   aps_quantize_pack  -> f~, scale, Cast, pack into sub-32-bit codes
+ *   aps_allreduce      -> the ring reduce-scatter (re-quantise after each add)
+ *                         and all-gather of the packed codes
+ *   aps_unscale        -> Cast back, unscale, average
+ *   aps_sync           -> the four in order
+ *
+ * CONVENTIONS
+ *  - Memory: every tensor pointer is a DEVICE pointer unless the name says
+ *    host.  The library never allocates device memory: gradients, outputs and
+ *    the workspace belong to the caller (e.g. torch).  NCCL communicators and
+ *    CUDA streams are borrowed and must outlive the context.
+ *  - Ordering: every call is enqueued on the context's stream and returns
+ *    before the GPU work finishes, unless marked [sync].
+ *  - Errors: every call returns an aps_status and never throws or aborts
+ *    across the ABI; aps_last_error() gives a message.  CUDA and NCCL errors
+ *    are captured as APS_ERR_CUDA / APS_ERR_NCCL.  Non-finite gradients are a
+ *    deferred error: the device raises a flag, outputs are unspecified, and
+ *    aps_status_sync() returns APS_ERR_NONFINITE (reading A4).
+ *  - Formats: 2 <= exp_bits <= 8, 0 <= man_bits <= 23, 1+exp_bits+man_bits
+ *    <= 32 (CPD: "number of exponent bits <= 8 and number of mantissa bits
+ *    <= 23").  exp_bits = 1 (bias 0, no normal numbers) is rejected.
+ *  - Layers: numels[l] >= 1 (int64; up to 2^31 tiles), layer buffers 16-byte
+ *    aligned (APS_ERR_ALIGN otherwise).  Any numel is legal; tails are masked.
+ *
+ * PACKED LAYOUT (design rule, not in the paper):
+ *  - b = 1 + exp_bits + man_bits bits per code; code = s | E | M, sign MSB,
+ *    IEEE-style, all-ones exponent reserved for Inf/NaN (Table
+ *    `precision_range`).
+ *  - tile = 128 codes = 16*b bytes.  Layer l occupies ceil(n_l/128) tiles
+ *    from tile offset sum_{k<l} ceil(n_k/128); padding codes are +0.  The
+ *    tile count is padded to T' = p * ceil(T/p); chunk c (c = 0..p-1) is
+ *    tiles [c T'/p, (c+1) T'/p).
+ *  - code i of the buffer occupies bits [i*b, (i+1)*b), LSB-first, in a
+ *    little-endian byte stream (b = 8: a plain uint8 array).
+ *  - Ring order (reading A14): chunk c is accumulated in rank order
+ *    c+1, c+2, ..., c (the owner adds last), every add re-quantised; after
+ *    the all-gather every rank holds identical codes.
+ */
+#ifndef APS_H_
+#define APS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct aps_ctx aps_ctx;
+
+typedef enum {
+    APS_OK = 0,
+    APS_ERR_ARG = 1,        /* bad argument (NULL, size, rank, n_layers...) */
+    APS_ERR_FORMAT = 2,     /* (exp_bits, man_bits) outside the valid set */
+    APS_ERR_ALIGN = 3,      /* a layer / workspace pointer is misaligned */
+    APS_ERR_CUDA = 4,       /* a CUDA runtime error (launch, copy) */
+    APS_ERR_NCCL = 5,       /* an NCCL error */
+    APS_ERR_NONFINITE = 6,  /* a gradient held Inf/NaN (deferred; see aps_status_sync) */
+    APS_ERR_STATE = 7       /* call out of order, or no workspace set */
+} aps_status;
+
+/* Create a context.
+ *   exp_bits, man_bits : the customised float (Alg. 1 inputs exp_bit, man_bit)
+ *   world_size, rank   : N (Alg. 1 input) and this process's rank
+ *   n_layers, numels   : host array [n_layers] of gradient element counts, in
+ *                        the caller's layer order (the packed layout order)
+ *   nccl_comm          : ncclComm_t (borrowed) of world_size ranks, or NULL.
+ *                        NULL with world_size == 1: single GPU.  NULL with
+ *                        world_size > 1: a SIMULATED rank (test mode): the
+ *                        collectives must then go through aps_sim_*.
+ *   cuda_stream        : cudaStream_t (borrowed); NULL = legacy default stream
+ * Does not touch the device. */
+aps_status aps_init(aps_ctx **out, int exp_bits, int man_bits, int world_size, int rank,
+                    int n_layers, const int64_t *numels, void *nccl_comm, void *cuda_stream);
+
+/* Bytes of device workspace the context needs (packed buffer, one ring
+ * receive chunk, layer and work tables, exponent vectors). */
+size_t aps_workspace_bytes(const aps_ctx *ctx);
+
+/* Attach caller-owned device workspace (>= aps_workspace_bytes, 256-byte
+ * aligned).  Zero-fills it and uploads the layer tables (enqueued). */
+aps_status aps_set_workspace(aps_ctx *ctx, void *dev, size_t bytes);
+
+/* FindMaxExp(g * N) for every layer (Alg. 1 line 3): the local
+ * exponent E_l = ceil(log2(N * max_i |g_l[i]|)) (exact, readings A2/A5;
+ * INT32_MIN for an all-zero layer, A3; INT32_MAX if any element is non-finite,
+ * A4), one fused multi-tensor kernel; then AllReduce(E, MAX) over the
+ * communicator (int32 per layer, reading A6).
+ *   grads : host array [n_layers] of device fp32 pointers (16-byte aligned). */
+aps_status aps_layer_scales(aps_ctx *ctx, const float *const *grads);
+
+/* f~_l = upper_bound_exp - E_l (0 for an all-zero layer), y = g * 2^f~ (one
+ * binary32 rounding, reading A8), Cast(y, exp_bits, man_bits) with
+ * round-to-nearest-even, gradual underflow (A10) and IEEE overflow
+ * (A11), packed into the workspace's packed buffer (layout above).
+ * Requires aps_layer_scales first. */
+aps_status aps_quantize_pack(aps_ctx *ctx, const float *const *grads);
+
+/* AllReduce(low_g, SUM) (Alg. 1 line 7) as a ring: p-1 reduce-scatter
+ * steps over ncclSend/ncclRecv of packed bytes, each followed by the
+ * unpack-add-requantise-repack kernel s <- Cast(fl32(dec(recv) + dec(own)))
+ * (reading A13), then an all-gather of the packed chunks.  No-op
+ * for world_size == 1.  Requires aps_quantize_pack first. */
+aps_status aps_allreduce(aps_ctx *ctx);
+
+/* out_l = fl32( fl32(dec(s) * 2^-f~_l) / N )  (Alg. 1 lines 8-9, P:254-256;
+ * average = 0 skips the division, reading A16).
+ *   out : host array [n_layers] of device fp32 pointers; may alias grads. */
+aps_status aps_unscale(aps_ctx *ctx, float *const *out, int average);
+
+/* aps_layer_scales, aps_quantize_pack, aps_allreduce, aps_unscale in order,
+ * in place on grads. */
+aps_status aps_sync(aps_ctx *ctx, float *const *grads, int average);
+
+/* End-to-end entry with HOST buffers: copies host_in[l] (pinned host fp32)
+ * into dev_grads[l], runs aps_sync in place, copies the result to host_out[l]
+ * (pinned host fp32, may equal host_in).  All enqueued on the stream. */
+aps_status aps_sync_host(aps_ctx *ctx, const float *const *host_in, float *const *dev_grads,
+                         float *const *host_out, int average);
+
+/* Select the hardware cvt.rn.satfinite.{e5m2,e4m3}x2 converters for (5,2) /
+ * (4,3) (default on where available; bit-identical to the generic path on
+ * the APS path, reading A12 -- the -m gpu tests check it) or the generic
+ * bit-arithmetic codec (enable = 0).  Environment APS_HW_CVT=0 sets the
+ * default off. */
+aps_status aps_set_hw_convert(aps_ctx *ctx, int enable);
+
+/* [sync] Wait for the stream; return APS_ERR_NONFINITE (and clear the flag)
+ * if a non-finite gradient was seen since the last call, else APS_OK. */
+aps_status aps_status_sync(aps_ctx *ctx);
+
+/* [sync] Copy the scale exponents f~[n_layers] of the last quantize to host. */
+aps_status aps_get_scales(aps_ctx *ctx, int32_t *host_out);
+
+/* Device pointer and size of the packed buffer (valid after set_workspace). */
+aps_status aps_get_packed(aps_ctx *ctx, const void **dev, size_t *bytes);
+
+/* Layout queries (host only, no device): tiles T' and packed bytes 16*b*T'. */
+aps_status aps_layout(int world_size, int exp_bits, int man_bits, int n_layers,
+                      const int64_t *numels, int64_t *total_tiles, int64_t *packed_bytes);
+
+/* Ring schedule (host only): at reduce-scatter step `step` (0..p-2) rank
+ * `rank` sends chunk (rank-1-step) mod p to rank+1 and receives chunk
+ * (rank-2-step) mod p from rank-1, which it reduces into its own copy. */
+aps_status aps_ring_step(int world_size, int rank, int step, int *send_chunk, int *recv_chunk);
+
+const char *aps_last_error(const aps_ctx *ctx);
+aps_status aps_destroy(aps_ctx *ctx);
+const char *aps_version(void);
+
+/* ---- NCCL plumbing (so callers need no NCCL binding) ---------------- */
+/* Write a fresh ncclUniqueId (128 bytes) to host_uid. */
+aps_status aps_nccl_unique_id(void *host_uid, size_t bytes);
+/* ncclCommInitRank; *comm_out receives an ncclComm_t owned by the caller. */
+aps_status aps_nccl_comm_init(void **comm_out, const void *host_uid, int world_size, int rank);
+aps_status aps_nccl_comm_destroy(void *comm);
+
+/* ---- test mode: p simulated ranks on one device --------------------- */
+/* ctxs[p] created with nccl_comm == NULL and world_size == p, ranks 0..p-1,
+ * sharing one stream.  grads: host array [p * n_layers], rank-major.
+ * aps_sim_layer_scales = every rank's aps_layer_scales + the MAX exchange;
+ * aps_sim_allreduce = the same ring schedule and reduce kernel as
+ * aps_allreduce with device-to-device copies in place of send/recv. */
+aps_status aps_sim_layer_scales(aps_ctx *const *ctxs, int p, const float *const *grads);
+aps_status aps_sim_allreduce(aps_ctx *const *ctxs, int p);
+
+/* ---- test only: the device cast on arbitrary inputs ------------------ */
+/* codes[i] = Cast(in[i]) (uint32 per code, unpacked); exercises Inf/NaN and
+ * overflow, which APS never reaches.  hw = 1 selects the hardware
+ * cvt.rn.satfinite.{e5m2,e4m3}x2 path used for (5,2)/(4,3) on the APS path
+ * (exact only for |x| < (2 - 2^-(m+1)) * 2^bias, reading A12). */
+aps_status aps_debug_cast(const float *in, uint32_t *codes, int64_t n, int exp_bits,
+                          int man_bits, int hw, void *cuda_stream);
+aps_status aps_debug_decode(const uint32_t *codes, float *out, int64_t n, int exp_bits,
+                            int man_bits, int hw, void *cuda_stream);
+/* Reduce step on its own: own[i] <- Cast(fl32(dec(recv[i]) + dec(own[i]))),
+ * over n_tiles tiles of packed codes. */
+aps_status aps_debug_ring_reduce(uint8_t *own, const uint8_t *recv, int64_t n_tiles,
+                                 int exp_bits, int man_bits, int hw, void *cuda_stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* APS_H_ */

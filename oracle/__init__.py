@@ -76,6 +76,9 @@ def lib():
         L.oracle_unpack.argtypes = [vp, i64, ctypes.c_int, vp]
         L.oracle_aps_sync.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp,
                                       vp, ctypes.c_int, vp, vp, vp, vp]
+        L.oracle_ring_add_n.argtypes = [vp, vp, vp, i64, ctypes.c_int, ctypes.c_int]
+        L.oracle_unscale_n.argtypes = [vp, vp, i64, i32, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int]
+        L.oracle_scale_cast_n.argtypes = [vp, vp, i64, i32, ctypes.c_int, ctypes.c_int]
         _lib = L
     return _lib
 
@@ -126,6 +129,28 @@ def scale(g: float, ft: int) -> float:
 
 def ring_add(a: int, b: int, e: int, m: int) -> int:
     return lib().oracle_ring_add(a, b, e, m)
+
+
+def ring_add_n(acc, addend, e: int, m: int) -> np.ndarray:
+    a = np.ascontiguousarray(acc, dtype=np.uint32)
+    b = np.ascontiguousarray(addend, dtype=np.uint32)
+    out = np.empty(a.shape, dtype=np.uint32)
+    lib().oracle_ring_add_n(_ptr(a), _ptr(b), _ptr(out), a.size, e, m)
+    return out
+
+
+def unscale_n(s, ft: int, N: int, average: int, e: int, m: int) -> np.ndarray:
+    c = np.ascontiguousarray(s, dtype=np.uint32)
+    out = np.empty(c.shape, dtype=np.float32)
+    lib().oracle_unscale_n(_ptr(c), _ptr(out), c.size, ft, N, average, e, m)
+    return out
+
+
+def scale_cast_n(g, ft: int, e: int, m: int) -> np.ndarray:
+    x = np.ascontiguousarray(g, dtype=np.float32)
+    out = np.empty(x.shape, dtype=np.uint32)
+    lib().oracle_scale_cast_n(_ptr(x), _ptr(out), x.size, ft, e, m)
+    return out
 
 
 def unscale1(s: int, ft: int, N: int, average: int, e: int, m: int) -> float:

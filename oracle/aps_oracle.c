@@ -382,3 +382,27 @@ int oracle_aps_sync(int p, int e, int m, int n_layers, const int64_t *numels,
     free(q); free(s); free(E); free(ft);
     return OR_OK;
 }
+
+/* Element-wise O8 step over arrays (loop over oracle_ring_add; test helper). */
+int oracle_ring_add_n(const uint32_t *acc, const uint32_t *addend, uint32_t *out, int64_t n, int e, int m)
+{
+    if (oracle_format_valid(e, m)) return OR_ERR_FORMAT;
+    for (int64_t i = 0; i < n; ++i) out[i] = oracle_ring_add(acc[i], addend[i], e, m);
+    return OR_OK;
+}
+
+/* Element-wise O10 over arrays (loop over oracle_unscale1; test helper). */
+int oracle_unscale_n(const uint32_t *s, float *out, int64_t n, int32_t ft, int N, int average, int e, int m)
+{
+    if (oracle_format_valid(e, m)) return OR_ERR_FORMAT;
+    for (int64_t i = 0; i < n; ++i) out[i] = oracle_unscale1(s[i], ft, N, average, e, m);
+    return OR_OK;
+}
+
+/* Element-wise O5+O6 over arrays: codes[i] = Cast(g[i] * 2^f~) (test helper). */
+int oracle_scale_cast_n(const float *g, uint32_t *codes, int64_t n, int32_t ft, int e, int m)
+{
+    if (oracle_format_valid(e, m)) return OR_ERR_FORMAT;
+    for (int64_t i = 0; i < n; ++i) codes[i] = oracle_cast1(oracle_scale(g[i], ft), e, m);
+    return OR_OK;
+}

@@ -1,0 +1,47 @@
+"""Build libaps.so in-tree with nvcc for sm_100a (no JIT, no torch extension
+machinery): the .so travels with the repo to the GPU box."""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+LIB = PKG / "libaps.so"
+SOURCES = [CSRC / "aps_kernels.cu", CSRC / "aps_api.cpp"]
+HEADERS = [CSRC / "aps_numerics.cuh", CSRC / "aps_internal.h", ROOT / "include" / "aps.h"]
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+
+def nccl_dirs() -> tuple[Path, Path]:
+    import nvidia.nccl  # torch's bundled NCCL (one NCCL per process)
+    base = Path(list(nvidia.nccl.__path__)[0])
+    return base / "include", base / "lib"
+
+
+def build(force: bool = False, verbose: bool = False) -> Path:
+    newest = max(p.stat().st_mtime for p in SOURCES + HEADERS)
+    if not force and LIB.exists() and LIB.stat().st_mtime >= newest:
+        return LIB
+    inc, lib = nccl_dirs()
+    tmp = LIB.with_suffix(f".so.tmp{os.getpid()}")
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+           "-Xcompiler", "-fPIC,-O2", "-shared", "-Xptxas", "-v" if verbose else "-O3",
+           f"-I{ROOT / 'include'}", f"-I{inc}", *map(str, SOURCES), "-o", str(tmp),
+           f"-L{lib}", "-l:libnccl.so.2", f"-Xlinker", f"-rpath={lib}"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("nvcc failed building libaps.so")
+    if verbose:
+        sys.stderr.write(r.stderr)
+    os.replace(tmp, LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    print(LIB)

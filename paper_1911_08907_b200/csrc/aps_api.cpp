@@ -1,0 +1,520 @@
+// aps_api.cpp -- the C ABI of libaps (include/aps.h): context, workspace,
+// phase checks, and the ring orchestration over NCCL send/recv (Alg. 1's
+// AllReduce(low_g, SUM), as the ring all-reduce of P:410 / P:528).
+#include "aps.h"
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "aps_internal.h"
+
+namespace {
+
+enum Phase { kNone = 0, kLocalScales = 1, kScales = 2, kPacked = 3, kReduced = 4 };
+
+constexpr size_t kAlign = 256;
+inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+}  // namespace
+
+struct aps_ctx {
+    int e = 0, m = 0, b = 0, world = 1, rank = 0, n_layers = 0;
+    bool sim = false;
+    bool hw = true;
+    ncclComm_t comm = nullptr;
+    cudaStream_t stream = nullptr;
+    std::vector<int64_t> numels;
+    std::vector<aps::Item> items;
+    std::vector<aps::LayerDev> layers;
+    int64_t tiles = 0;        // T' (padded to a multiple of world)
+    int64_t packed_bytes = 0; // 16 * b * T'
+    int64_t chunk_bytes = 0;  // packed_bytes / world
+    // workspace carve-up
+    uint8_t *ws = nullptr;
+    size_t ws_bytes = 0, need = 0;
+    size_t off_packed = 0, off_recv = 0, off_items = 0, off_layers = 0, off_src = 0, off_dst = 0,
+           off_amax = 0, off_count = 0, off_eloc = 0, off_eglob = 0, off_ft = 0, off_flag = 0;
+    aps::DevTables t{};
+    std::vector<const float *> src_cache;
+    std::vector<float *> dst_cache;
+    int phase = kNone;
+    std::string err;
+};
+
+namespace {
+
+aps_status fail(aps_ctx *c, aps_status s, const std::string &msg)
+{
+    if (c) c->err = msg;
+    return s;
+}
+
+#define APS_CUDA(ctx, expr)                                                                   \
+    do {                                                                                      \
+        cudaError_t e_ = (expr);                                                              \
+        if (e_ != cudaSuccess)                                                                \
+            return fail((ctx), APS_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+#define APS_NCCL(ctx, expr)                                                                   \
+    do {                                                                                      \
+        ncclResult_t r_ = (expr);                                                             \
+        if (r_ != ncclSuccess)                                                                \
+            return fail((ctx), APS_ERR_NCCL, std::string(#expr) + ": " + ncclGetErrorString(r_)); \
+    } while (0)
+
+bool format_ok(int e, int m) { return e >= 2 && e <= 8 && m >= 0 && m <= 23 && 1 + e + m <= 32; }
+
+int64_t layer_tiles(int64_t n) { return (n + aps::kTile - 1) / aps::kTile; }
+
+// Upload the per-call pointer table if it changed (rarely: DDP buckets and
+// optimizer-owned .grad buffers are stable).
+template <class P>
+aps_status upload_ptrs(aps_ctx *c, std::vector<P> &cache, P const *ptrs, size_t off)
+{
+    bool same = cache.size() == (size_t)c->n_layers;
+    for (int l = 0; l < c->n_layers; ++l) {
+        if (!ptrs[l]) return fail(c, APS_ERR_ARG, "NULL layer pointer");
+        if (reinterpret_cast<uintptr_t>(ptrs[l]) % 16u)
+            return fail(c, APS_ERR_ALIGN, "layer buffer not 16-byte aligned (layer " + std::to_string(l) + ")");
+        if (same && cache[l] != ptrs[l]) same = false;
+    }
+    if (same) return APS_OK;
+    cache.assign(ptrs, ptrs + c->n_layers);
+    APS_CUDA(c, cudaMemcpyAsync(c->ws + off, cache.data(), sizeof(P) * (size_t)c->n_layers,
+                                cudaMemcpyHostToDevice, c->stream));
+    return APS_OK;
+}
+
+aps_status need_ws(aps_ctx *c)
+{
+    if (!c) return APS_ERR_ARG;
+    if (!c->ws) return fail(c, APS_ERR_STATE, "no workspace set (aps_set_workspace)");
+    return APS_OK;
+}
+
+// Ring schedule (reading A14): chunk c accumulates in rank order c+1, ..., c.
+inline int mod(int a, int p) { return ((a % p) + p) % p; }
+inline int send_chunk(int p, int r, int s) { return mod(r - 1 - s, p); }
+inline int recv_chunk(int p, int r, int s) { return mod(r - 2 - s, p); }
+
+}  // namespace
+
+extern "C" {
+
+const char *aps_version(void) { return "libaps 0.1 (sm_100a)"; }
+
+aps_status aps_layout(int world_size, int exp_bits, int man_bits, int n_layers, const int64_t *numels,
+                      int64_t *total_tiles, int64_t *packed_bytes)
+{
+    if (!format_ok(exp_bits, man_bits)) return APS_ERR_FORMAT;
+    if (world_size < 1 || n_layers < 1 || !numels) return APS_ERR_ARG;
+    int64_t T = 0;
+    for (int l = 0; l < n_layers; ++l) {
+        if (numels[l] < 1) return APS_ERR_ARG;
+        T += layer_tiles(numels[l]);
+    }
+    const int64_t Tp = (T + world_size - 1) / world_size * world_size;
+    if (total_tiles) *total_tiles = Tp;
+    if (packed_bytes) *packed_bytes = 16 * (int64_t)(1 + exp_bits + man_bits) * Tp;
+    return APS_OK;
+}
+
+aps_status aps_ring_step(int world_size, int rank, int step, int *send_c, int *recv_c)
+{
+    if (world_size < 1 || rank < 0 || rank >= world_size || step < 0 || step > world_size - 2)
+        return APS_ERR_ARG;
+    if (send_c) *send_c = send_chunk(world_size, rank, step);
+    if (recv_c) *recv_c = recv_chunk(world_size, rank, step);
+    return APS_OK;
+}
+
+aps_status aps_init(aps_ctx **out, int exp_bits, int man_bits, int world_size, int rank, int n_layers,
+                    const int64_t *numels, void *nccl_comm, void *cuda_stream)
+{
+    if (!out) return APS_ERR_ARG;
+    *out = nullptr;
+    if (!format_ok(exp_bits, man_bits)) return APS_ERR_FORMAT;
+    if (world_size < 1 || rank < 0 || rank >= world_size || n_layers < 1 || !numels) return APS_ERR_ARG;
+    if (n_layers > (1 << 24)) return APS_ERR_ARG;
+    aps_ctx *c = new (std::nothrow) aps_ctx();
+    if (!c) return APS_ERR_ARG;
+    c->e = exp_bits;
+    c->m = man_bits;
+    c->b = 1 + exp_bits + man_bits;
+    c->world = world_size;
+    c->rank = rank;
+    c->n_layers = n_layers;
+    c->comm = static_cast<ncclComm_t>(nccl_comm);
+    c->sim = (world_size > 1 && !nccl_comm);
+    c->stream = static_cast<cudaStream_t>(cuda_stream);
+    c->hw = aps::hw_available(exp_bits, man_bits);
+    if (const char *env = std::getenv("APS_HW_CVT")) c->hw = c->hw && std::atoi(env) != 0;
+    if (c->comm) {
+        int nr = 0;
+        if (ncclCommCount(c->comm, &nr) != ncclSuccess || nr != world_size) {
+            delete c;
+            return APS_ERR_ARG;
+        }
+    }
+    c->numels.assign(numels, numels + n_layers);
+    int64_t toff = 0;
+    for (int l = 0; l < n_layers; ++l) {
+        if (numels[l] < 1) {
+            delete c;
+            return APS_ERR_ARG;
+        }
+        const int64_t T = layer_tiles(numels[l]);
+        if (T > INT32_MAX) {
+            delete c;
+            return APS_ERR_ARG;
+        }
+        aps::LayerDev L{};
+        L.numel = numels[l];
+        L.tile_off = toff;
+        L.n_items = 0;
+        for (int64_t t0 = 0; t0 < T; t0 += aps::kItemTiles) {
+            aps::Item it{};
+            it.layer = l;
+            it.tile_begin = (int32_t)t0;
+            it.n_tiles = (int32_t)std::min<int64_t>(aps::kItemTiles, T - t0);
+            c->items.push_back(it);
+            ++L.n_items;
+        }
+        c->layers.push_back(L);
+        toff += T;
+    }
+    if (c->items.size() > (size_t)INT32_MAX) {
+        delete c;
+        return APS_ERR_ARG;
+    }
+    c->tiles = (toff + world_size - 1) / world_size * world_size;
+    c->packed_bytes = 16 * (int64_t)c->b * c->tiles;
+    c->chunk_bytes = c->packed_bytes / world_size;
+    // workspace layout
+    size_t o = 0;
+    c->off_packed = o; o = align_up(o + (size_t)c->packed_bytes);
+    c->off_recv = o;   o = align_up(o + (world_size > 1 ? (size_t)c->chunk_bytes : 0));
+    c->off_items = o;  o = align_up(o + sizeof(aps::Item) * c->items.size());
+    c->off_layers = o; o = align_up(o + sizeof(aps::LayerDev) * c->layers.size());
+    c->off_src = o;    o = align_up(o + sizeof(void *) * (size_t)n_layers);
+    c->off_dst = o;    o = align_up(o + sizeof(void *) * (size_t)n_layers);
+    c->off_amax = o;   o = align_up(o + 4 * (size_t)n_layers);
+    c->off_count = o;  o = align_up(o + 4 * (size_t)n_layers);
+    c->off_eloc = o;   o = align_up(o + 4 * (size_t)n_layers);
+    c->off_eglob = o;  o = align_up(o + 4 * (size_t)n_layers);
+    c->off_ft = o;     o = align_up(o + 4 * (size_t)n_layers);
+    c->off_flag = o;   o = align_up(o + 4);
+    c->need = o;
+    *out = c;
+    return APS_OK;
+}
+
+size_t aps_workspace_bytes(const aps_ctx *c) { return c ? c->need : 0; }
+
+aps_status aps_set_workspace(aps_ctx *c, void *dev, size_t bytes)
+{
+    if (!c || !dev) return APS_ERR_ARG;
+    if (reinterpret_cast<uintptr_t>(dev) % kAlign) return fail(c, APS_ERR_ALIGN, "workspace not 256-byte aligned");
+    if (bytes < c->need) return fail(c, APS_ERR_ARG, "workspace too small");
+    c->ws = static_cast<uint8_t *>(dev);
+    c->ws_bytes = bytes;
+    APS_CUDA(c, cudaMemsetAsync(c->ws, 0, c->need, c->stream));
+    APS_CUDA(c, cudaMemcpyAsync(c->ws + c->off_items, c->items.data(), sizeof(aps::Item) * c->items.size(),
+                                cudaMemcpyHostToDevice, c->stream));
+    APS_CUDA(c, cudaMemcpyAsync(c->ws + c->off_layers, c->layers.data(),
+                                sizeof(aps::LayerDev) * c->layers.size(), cudaMemcpyHostToDevice, c->stream));
+    aps::DevTables &t = c->t;
+    t.items = reinterpret_cast<const aps::Item *>(c->ws + c->off_items);
+    t.layers = reinterpret_cast<const aps::LayerDev *>(c->ws + c->off_layers);
+    t.src = reinterpret_cast<const float *const *>(c->ws + c->off_src);
+    t.dst = reinterpret_cast<float *const *>(c->ws + c->off_dst);
+    t.amax = reinterpret_cast<uint32_t *>(c->ws + c->off_amax);
+    t.count = reinterpret_cast<uint32_t *>(c->ws + c->off_count);
+    t.E_local = reinterpret_cast<int32_t *>(c->ws + c->off_eloc);
+    // one rank: the global exponent vector IS the local one (no collective, no copy)
+    t.E_glob = reinterpret_cast<int32_t *>(c->ws + (c->world == 1 ? c->off_eloc : c->off_eglob));
+    t.ftilde = reinterpret_cast<int32_t *>(c->ws + c->off_ft);
+    t.flag = reinterpret_cast<uint32_t *>(c->ws + c->off_flag);
+    t.packed = c->ws + c->off_packed;
+    t.n_items = (int)c->items.size();
+    t.n_layers = c->n_layers;
+    c->src_cache.clear();
+    c->dst_cache.clear();
+    c->phase = kNone;
+    return APS_OK;
+}
+
+aps_status aps_set_hw_convert(aps_ctx *c, int enable)
+{
+    if (!c) return APS_ERR_ARG;
+    c->hw = enable && aps::hw_available(c->e, c->m);
+    return APS_OK;
+}
+
+aps_status aps_layer_scales(aps_ctx *c, const float *const *grads)
+{
+    if (aps_status s = need_ws(c)) return s;
+    if (!grads) return fail(c, APS_ERR_ARG, "grads is NULL");
+    if (aps_status s = upload_ptrs<const float *>(c, c->src_cache, grads, c->off_src)) return s;
+    APS_CUDA(c, aps::launch_absmax_exp(c->t, c->world, c->stream));
+    if (c->world == 1) {
+        c->phase = kScales;
+    } else if (c->sim) {
+        c->phase = kLocalScales;  // aps_sim_layer_scales completes the exchange
+    } else {
+        // AllReduce(max_grad_exp, MAX) (Alg. 1 line 4): int32 per layer
+        APS_NCCL(c, ncclAllReduce(c->t.E_local, c->t.E_glob, (size_t)c->n_layers, ncclInt32, ncclMax,
+                                  c->comm, c->stream));
+        c->phase = kScales;
+    }
+    return APS_OK;
+}
+
+aps_status aps_quantize_pack(aps_ctx *c, const float *const *grads)
+{
+    if (aps_status s = need_ws(c)) return s;
+    if (c->phase < kScales) return fail(c, APS_ERR_STATE, "aps_quantize_pack before aps_layer_scales");
+    if (!grads) return fail(c, APS_ERR_ARG, "grads is NULL");
+    if (aps_status s = upload_ptrs<const float *>(c, c->src_cache, grads, c->off_src)) return s;
+    APS_CUDA(c, aps::launch_quant_pack(c->t, c->e, c->m, c->hw, c->stream));
+    c->phase = kPacked;
+    return APS_OK;
+}
+
+aps_status aps_allreduce(aps_ctx *c)
+{
+    if (aps_status s = need_ws(c)) return s;
+    if (c->phase != kPacked) return fail(c, APS_ERR_STATE, "aps_allreduce before aps_quantize_pack");
+    if (c->world == 1) {
+        c->phase = kReduced;
+        return APS_OK;
+    }
+    if (c->sim) return fail(c, APS_ERR_STATE, "simulated rank: use aps_sim_allreduce");
+    const int p = c->world, r = c->rank;
+    uint8_t *packed = c->t.packed;
+    uint8_t *recv = c->ws + c->off_recv;
+    const size_t cb = (size_t)c->chunk_bytes;
+    const int64_t chunk_tiles = c->tiles / p;
+    // reduce-scatter: p-1 steps, each a send/recv of packed bytes then the
+    // unpack-add-requantise-repack kernel (same stream: ordered)
+    for (int s = 0; s < p - 1; ++s) {
+        const int sc = send_chunk(p, r, s), rc = recv_chunk(p, r, s);
+        APS_NCCL(c, ncclGroupStart());
+        APS_NCCL(c, ncclSend(packed + (size_t)sc * cb, cb, ncclUint8, mod(r + 1, p), c->comm, c->stream));
+        APS_NCCL(c, ncclRecv(recv, cb, ncclUint8, mod(r - 1, p), c->comm, c->stream));
+        APS_NCCL(c, ncclGroupEnd());
+        APS_CUDA(c, aps::launch_ring_reduce(packed + (size_t)rc * cb, recv, chunk_tiles, c->e, c->m, c->hw,
+                                            c->stream));
+    }
+    // all-gather of the reduced chunks (pure data movement; rank r owns chunk r)
+    APS_NCCL(c, ncclAllGather(packed + (size_t)r * cb, packed, cb, ncclUint8, c->comm, c->stream));
+    c->phase = kReduced;
+    return APS_OK;
+}
+
+aps_status aps_unscale(aps_ctx *c, float *const *out, int average)
+{
+    if (aps_status s = need_ws(c)) return s;
+    if (c->phase < kPacked || (c->world > 1 && c->phase < kReduced))
+        return fail(c, APS_ERR_STATE, "aps_unscale before aps_allreduce");
+    if (!out) return fail(c, APS_ERR_ARG, "out is NULL");
+    if (aps_status s = upload_ptrs<float *>(c, c->dst_cache, out, c->off_dst)) return s;
+    APS_CUDA(c, aps::launch_unpack_unscale(c->t, c->e, c->m, c->hw, c->world, average, c->stream));
+    return APS_OK;
+}
+
+aps_status aps_sync(aps_ctx *c, float *const *grads, int average)
+{
+    const float *const *g = const_cast<const float *const *>(grads);
+    if (aps_status s = aps_layer_scales(c, g)) return s;
+    if (aps_status s = aps_quantize_pack(c, g)) return s;
+    if (aps_status s = aps_allreduce(c)) return s;
+    return aps_unscale(c, grads, average);
+}
+
+aps_status aps_sync_host(aps_ctx *c, const float *const *host_in, float *const *dev_grads,
+                         float *const *host_out, int average)
+{
+    if (aps_status s = need_ws(c)) return s;
+    if (!host_in || !dev_grads || !host_out) return fail(c, APS_ERR_ARG, "NULL pointer array");
+    for (int l = 0; l < c->n_layers; ++l)
+        APS_CUDA(c, cudaMemcpyAsync(dev_grads[l], host_in[l], 4 * (size_t)c->numels[l], cudaMemcpyHostToDevice,
+                                    c->stream));
+    if (aps_status s = aps_sync(c, dev_grads, average)) return s;
+    for (int l = 0; l < c->n_layers; ++l)
+        APS_CUDA(c, cudaMemcpyAsync(host_out[l], dev_grads[l], 4 * (size_t)c->numels[l], cudaMemcpyDeviceToHost,
+                                    c->stream));
+    return APS_OK;
+}
+
+aps_status aps_status_sync(aps_ctx *c)
+{
+    if (aps_status s = need_ws(c)) return s;
+    uint32_t flag = 0;
+    APS_CUDA(c, cudaMemcpyAsync(&flag, c->t.flag, 4, cudaMemcpyDeviceToHost, c->stream));
+    APS_CUDA(c, cudaStreamSynchronize(c->stream));
+    if (flag) {
+        APS_CUDA(c, cudaMemsetAsync(c->t.flag, 0, 4, c->stream));
+        return fail(c, APS_ERR_NONFINITE, "non-finite gradient seen (outputs unspecified)");
+    }
+    return APS_OK;
+}
+
+aps_status aps_get_scales(aps_ctx *c, int32_t *host_out)
+{
+    if (aps_status s = need_ws(c)) return s;
+    if (!host_out) return APS_ERR_ARG;
+    APS_CUDA(c, cudaMemcpyAsync(host_out, c->t.ftilde, 4 * (size_t)c->n_layers, cudaMemcpyDeviceToHost, c->stream));
+    APS_CUDA(c, cudaStreamSynchronize(c->stream));
+    return APS_OK;
+}
+
+aps_status aps_get_packed(aps_ctx *c, const void **dev, size_t *bytes)
+{
+    if (aps_status s = need_ws(c)) return s;
+    if (dev) *dev = c->t.packed;
+    if (bytes) *bytes = (size_t)c->packed_bytes;
+    return APS_OK;
+}
+
+const char *aps_last_error(const aps_ctx *c) { return c ? c->err.c_str() : "NULL context"; }
+
+aps_status aps_destroy(aps_ctx *c)
+{
+    delete c;
+    return APS_OK;
+}
+
+// ---------------------------------------------------------------- NCCL plumbing
+aps_status aps_nccl_unique_id(void *host_uid, size_t bytes)
+{
+    if (!host_uid || bytes < sizeof(ncclUniqueId)) return APS_ERR_ARG;
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return APS_ERR_NCCL;
+    std::memcpy(host_uid, &id, sizeof(id));
+    return APS_OK;
+}
+
+aps_status aps_nccl_comm_init(void **comm_out, const void *host_uid, int world_size, int rank)
+{
+    if (!comm_out || !host_uid || world_size < 1 || rank < 0 || rank >= world_size) return APS_ERR_ARG;
+    ncclUniqueId id;
+    std::memcpy(&id, host_uid, sizeof(id));
+    ncclComm_t comm = nullptr;
+    if (ncclCommInitRank(&comm, world_size, id, rank) != ncclSuccess) return APS_ERR_NCCL;
+    *comm_out = comm;
+    return APS_OK;
+}
+
+aps_status aps_nccl_comm_destroy(void *comm)
+{
+    if (!comm) return APS_ERR_ARG;
+    return ncclCommDestroy(static_cast<ncclComm_t>(comm)) == ncclSuccess ? APS_OK : APS_ERR_NCCL;
+}
+
+// ---------------------------------------------------------------- simulated ranks (test mode)
+static aps_status sim_check(aps_ctx *const *ctxs, int p)
+{
+    if (!ctxs || p < 2 || p > 64) return APS_ERR_ARG;
+    for (int r = 0; r < p; ++r) {
+        aps_ctx *c = ctxs[r];
+        if (!c || !c->sim || c->world != p || c->rank != r) return APS_ERR_ARG;
+        if (!c->ws) return fail(c, APS_ERR_STATE, "no workspace");
+        if (c->stream != ctxs[0]->stream || c->e != ctxs[0]->e || c->m != ctxs[0]->m ||
+            c->packed_bytes != ctxs[0]->packed_bytes || c->hw != ctxs[0]->hw)
+            return fail(c, APS_ERR_ARG, "simulated ranks differ in stream/format/layout");
+    }
+    return APS_OK;
+}
+
+aps_status aps_sim_layer_scales(aps_ctx *const *ctxs, int p, const float *const *grads)
+{
+    if (aps_status s = sim_check(ctxs, p)) return s;
+    if (!grads) return APS_ERR_ARG;
+    for (int r = 0; r < p; ++r)
+        if (aps_status s = aps_layer_scales(ctxs[r], grads + (size_t)r * ctxs[r]->n_layers)) return s;
+    std::vector<int32_t *> dst(p);
+    std::vector<const int32_t *> src(p);
+    for (int r = 0; r < p; ++r) {
+        dst[r] = ctxs[r]->t.E_glob;
+        src[r] = ctxs[r]->t.E_local;
+    }
+    APS_CUDA(ctxs[0], aps::launch_sim_max(dst.data(), src.data(), p, ctxs[0]->n_layers, ctxs[0]->stream));
+    for (int r = 0; r < p; ++r) ctxs[r]->phase = kScales;
+    return APS_OK;
+}
+
+aps_status aps_sim_allreduce(aps_ctx *const *ctxs, int p)
+{
+    if (aps_status s = sim_check(ctxs, p)) return s;
+    for (int r = 0; r < p; ++r)
+        if (ctxs[r]->phase != kPacked) return fail(ctxs[r], APS_ERR_STATE, "sim allreduce before quantize");
+    aps_ctx *c0 = ctxs[0];
+    const size_t cb = (size_t)c0->chunk_bytes;
+    const int64_t chunk_tiles = c0->tiles / p;
+    cudaStream_t st = c0->stream;
+    for (int s = 0; s < p - 1; ++s) {
+        // the "send/recv": rank r receives chunk recv_chunk(p, r, s) from rank r-1,
+        // which sends exactly that chunk (send_chunk(p, r-1, s) == recv_chunk(p, r, s))
+        for (int r = 0; r < p; ++r) {
+            aps_ctx *me = ctxs[r], *prev = ctxs[mod(r - 1, p)];
+            const int rc = recv_chunk(p, r, s);
+            APS_CUDA(me, cudaMemcpyAsync(me->ws + me->off_recv, prev->t.packed + (size_t)rc * cb, cb,
+                                         cudaMemcpyDeviceToDevice, st));
+        }
+        for (int r = 0; r < p; ++r) {
+            aps_ctx *me = ctxs[r];
+            const int rc = recv_chunk(p, r, s);
+            APS_CUDA(me, aps::launch_ring_reduce(me->t.packed + (size_t)rc * cb, me->ws + me->off_recv,
+                                                 chunk_tiles, me->e, me->m, me->hw, st));
+        }
+    }
+    for (int r = 0; r < p; ++r)
+        for (int q = 0; q < p; ++q)
+            if (q != r)
+                APS_CUDA(ctxs[r], cudaMemcpyAsync(ctxs[r]->t.packed + (size_t)q * cb, ctxs[q]->t.packed + (size_t)q * cb,
+                                                  cb, cudaMemcpyDeviceToDevice, st));
+    for (int r = 0; r < p; ++r) ctxs[r]->phase = kReduced;
+    return APS_OK;
+}
+
+// ---------------------------------------------------------------- debug
+aps_status aps_debug_cast(const float *in, uint32_t *codes, int64_t n, int e, int m, int hw, void *stream)
+{
+    if (!format_ok(e, m)) return APS_ERR_FORMAT;
+    if (n < 0 || (n > 0 && (!in || !codes))) return APS_ERR_ARG;
+    if (hw && !aps::hw_available(e, m)) return APS_ERR_FORMAT;
+    return aps::launch_debug_cast(in, codes, n, e, m, hw != 0, static_cast<cudaStream_t>(stream)) == cudaSuccess
+               ? APS_OK : APS_ERR_CUDA;
+}
+
+aps_status aps_debug_decode(const uint32_t *codes, float *out, int64_t n, int e, int m, int hw, void *stream)
+{
+    if (!format_ok(e, m)) return APS_ERR_FORMAT;
+    if (n < 0 || (n > 0 && (!out || !codes))) return APS_ERR_ARG;
+    if (hw && !aps::hw_available(e, m)) return APS_ERR_FORMAT;
+    return aps::launch_debug_decode(codes, out, n, e, m, hw != 0, static_cast<cudaStream_t>(stream)) == cudaSuccess
+               ? APS_OK : APS_ERR_CUDA;
+}
+
+aps_status aps_debug_ring_reduce(uint8_t *own, const uint8_t *recv, int64_t n_tiles, int e, int m, int hw,
+                                 void *stream)
+{
+    if (!format_ok(e, m)) return APS_ERR_FORMAT;
+    if (n_tiles < 0 || (n_tiles > 0 && (!own || !recv))) return APS_ERR_ARG;
+    if (hw && !aps::hw_available(e, m)) return APS_ERR_FORMAT;
+    return aps::launch_ring_reduce(own, recv, n_tiles, e, m, hw != 0, static_cast<cudaStream_t>(stream)) == cudaSuccess
+               ? APS_OK : APS_ERR_CUDA;
+}
+
+}  // extern "C"

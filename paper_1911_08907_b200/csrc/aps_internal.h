@@ -1,0 +1,61 @@
+// aps_internal.h -- declarations shared by aps_kernels.cu and aps_api.cpp
+// (host-side launchers; no device code).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace aps {
+
+constexpr int kTile = 128;        // codes per tile (layout rule, aps.h)
+constexpr int kItemTiles = 64;    // tiles per work item (one CTA): 8192 elements
+constexpr int kThreads = 256;
+
+// One work item = a tile-aligned slice of one layer, processed by one CTA.
+struct Item {
+    int32_t layer;
+    int32_t tile_begin;  // within the layer
+    int32_t n_tiles;
+    int32_t pad;
+};
+
+struct LayerDev {
+    int64_t numel;
+    int64_t tile_off;    // first tile of the layer in the packed buffer
+    int32_t n_items;
+    int32_t pad0;
+    int64_t pad1;
+};
+
+struct DevTables {
+    const Item *items;
+    const LayerDev *layers;
+    const float *const *src;  // [n_layers] gradient pointers
+    float *const *dst;        // [n_layers] output pointers
+    uint32_t *amax;           // [n_layers] running abs-max bits (self-resetting)
+    uint32_t *count;          // [n_layers] finished-CTA counters (self-resetting)
+    int32_t *E_local;         // [n_layers]
+    int32_t *E_glob;          // [n_layers]
+    int32_t *ftilde;          // [n_layers]
+    uint32_t *flag;           // non-finite flag
+    uint8_t *packed;          // packed codes
+    int n_items;
+    int n_layers;
+};
+
+cudaError_t launch_absmax_exp(const DevTables &t, int world, cudaStream_t s);
+cudaError_t launch_quant_pack(const DevTables &t, int e, int m, bool hw, cudaStream_t s);
+cudaError_t launch_unpack_unscale(const DevTables &t, int e, int m, bool hw, int world, int average,
+                                  cudaStream_t s);
+cudaError_t launch_ring_reduce(uint8_t *own, const uint8_t *recv, int64_t n_tiles, int e, int m,
+                               bool hw, cudaStream_t s);
+cudaError_t launch_sim_max(int32_t *const *E_glob, const int32_t *const *E_local, int p,
+                           int n_layers, cudaStream_t s);
+cudaError_t launch_debug_cast(const float *in, uint32_t *codes, int64_t n, int e, int m, bool hw,
+                              cudaStream_t s);
+cudaError_t launch_debug_decode(const uint32_t *codes, float *out, int64_t n, int e, int m,
+                                bool hw, cudaStream_t s);
+
+// true when (e,m) has a hardware converter that is exact on the APS path
+inline bool hw_available(int e, int m) { return (e == 5 && m == 2) || (e == 4 && m == 3); }
+
+}  // namespace aps

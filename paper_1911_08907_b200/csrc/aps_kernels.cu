@@ -1,0 +1,671 @@
+// aps_kernels.cu -- the sm_100a kernels of the APS hot path:
+//   a1  absmax_exp      FindMaxExp(g * N) for every layer, one launch      (Alg. 1)
+//   a3/a4 quant_pack    f~ = upper_bound_exp - E; Cast(g * 2^f~) ; pack    (Alg. 1)
+//   a5  ring_reduce     s <- Cast(fl32(dec(recv) + dec(own)))             (Alg. 1)
+//   a7  unpack_unscale  Cast(s, 8, 23) / 2^f~ / N                         (Alg. 1)
+// All are HBM-bound streaming kernels (no dense contraction: tensor cores do
+// not apply).  Design: one CTA per tile-aligned work item of <= 8192
+// elements of one layer (a multi-tensor launch covers every layer), 128-bit
+// coalesced loads (ld.global.nc.L1::no_allocate) and coalesced stores;
+// b = 8/16/32 pack directly from registers, other widths go through a
+// per-warp shared-memory tile.
+#include <cstdint>
+#include <climits>
+#include <algorithm>
+
+#include "aps_internal.h"
+#include "aps_numerics.cuh"
+
+namespace aps {
+
+// ------------------------------------------------------------------ codecs
+// Uniform interface: enc(float)->code, dec(code)->float (finite codes),
+// dec_any (all codes), b(), and optionally enc4/dec4 for byte codes.
+template <int E, int M>
+struct CGen {
+    static constexpr int kB = 1 + E + M;
+    static constexpr bool kVec4 = false;
+    __device__ __forceinline__ int b() const { return kB; }
+    __device__ __forceinline__ uint32_t enc(float y) const
+    {
+        constexpr Fmt F = make_fmt(E, M);
+        return encode(F, y);
+    }
+    __device__ __forceinline__ float dec(uint32_t c) const
+    {
+        constexpr Fmt F = make_fmt(E, M);
+        return decode_finite(F, c);
+    }
+    __device__ __forceinline__ float dec_any(uint32_t c) const
+    {
+        constexpr Fmt F = make_fmt(E, M);
+        return decode(F, c);
+    }
+};
+
+template <bool E4M3>
+struct CHw {
+    static constexpr int kB = 8;
+    static constexpr bool kVec4 = true;
+    __device__ __forceinline__ int b() const { return 8; }
+    __device__ __forceinline__ uint32_t enc(float y) const
+    {
+        return (E4M3 ? cvt_e4m3x2(0.f, y) : cvt_e5m2x2(0.f, y)) & 0xffu;
+    }
+    __device__ __forceinline__ float dec(uint32_t c) const
+    {
+        return E4M3 ? e4m3x2_to_f32x2(c & 0xffu).x : e5m2x2_to_f32x2(c & 0xffu).x;
+    }
+    __device__ __forceinline__ float dec_any(uint32_t c) const { return dec(c); }
+    __device__ __forceinline__ uint32_t enc4(float4 v) const
+    {
+        const uint32_t lo = E4M3 ? cvt_e4m3x2(v.y, v.x) : cvt_e5m2x2(v.y, v.x);
+        const uint32_t hi = E4M3 ? cvt_e4m3x2(v.w, v.z) : cvt_e5m2x2(v.w, v.z);
+        return lo | (hi << 16);
+    }
+    __device__ __forceinline__ float4 dec4(uint32_t w) const
+    {
+        const float2 a = E4M3 ? e4m3x2_to_f32x2(w & 0xffffu) : e5m2x2_to_f32x2(w & 0xffffu);
+        const float2 c = E4M3 ? e4m3x2_to_f32x2(w >> 16) : e5m2x2_to_f32x2(w >> 16);
+        return make_float4(a.x, a.y, c.x, c.y);
+    }
+};
+
+struct CRt {
+    static constexpr int kB = 0;  // runtime width
+    static constexpr bool kVec4 = false;
+    Fmt F;
+    __device__ __forceinline__ int b() const { return F.b; }
+    __device__ __forceinline__ uint32_t enc(float y) const { return encode(F, y); }
+    __device__ __forceinline__ float dec(uint32_t c) const { return decode_finite(F, c); }
+    __device__ __forceinline__ float dec_any(uint32_t c) const { return decode(F, c); }
+};
+
+// ------------------------------------------------------------------ memory helpers
+__device__ __forceinline__ float4 ld_stream4(const float4 *p)
+{
+    float4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+// 4 consecutive fp32 of a layer starting at element e0, zero-filled past n.
+__device__ __forceinline__ float4 load_group(const float *g, int64_t e0, int64_t n)
+{
+    if (e0 + 4 <= n) return ld_stream4(reinterpret_cast<const float4 *>(g + e0));
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (e0 + 0 < n) v.x = g[e0 + 0];
+    if (e0 + 1 < n) v.y = g[e0 + 1];
+    if (e0 + 2 < n) v.z = g[e0 + 2];
+    return v;
+}
+
+__device__ __forceinline__ void store_group(float *o, int64_t e0, int64_t n, float4 v)
+{
+    if (e0 + 4 <= n) {
+        *reinterpret_cast<float4 *>(o + e0) = v;
+        return;
+    }
+    if (e0 + 0 < n) o[e0 + 0] = v.x;
+    if (e0 + 1 < n) o[e0 + 1] = v.y;
+    if (e0 + 2 < n) o[e0 + 2] = v.z;
+}
+
+// ------------------------------------------------------------------ power-of-two scaling
+// y = fl32(x * 2^k) with one rounding (ldexpf semantics, reading A8).  For
+// k in [-149, 127] 2^k is an exact fp32 (subnormal below -126) and a single
+// FMUL rounds once; outside, the product is formed exactly in fp64 and
+// rounded once to fp32.
+struct Pow2 {
+    float f;
+    double d;
+    bool wide;
+    __device__ __forceinline__ explicit Pow2(int k)
+    {
+        wide = (k < -149 || k > 127);
+        f = (k >= -126) ? __uint_as_float((uint32_t)(k + 127) << 23)
+                        : __uint_as_float(1u << ((k + 149) & 31));
+        d = __longlong_as_double((long long)(uint64_t)(min(max(k, -1022), 1023) + 1023) << 52);
+    }
+    __device__ __forceinline__ float apply(float x) const
+    {
+        return wide ? __double2float_rn((double)x * d) : __fmul_rn(x, f);
+    }
+    __device__ __forceinline__ float4 apply4(float4 v) const
+    {
+        return make_float4(apply(v.x), apply(v.y), apply(v.z), apply(v.w));
+    }
+};
+
+// ------------------------------------------------------------------ per-element 4-wide helpers
+template <class C>
+__device__ __forceinline__ uint32_t enc4_bytes(const C &c, float4 v)
+{
+    if constexpr (C::kVec4) {
+        return c.enc4(v);
+    } else {
+        return c.enc(v.x) | (c.enc(v.y) << 8) | (c.enc(v.z) << 16) | (c.enc(v.w) << 24);
+    }
+}
+
+template <class C>
+__device__ __forceinline__ float4 dec4_bytes(const C &c, uint32_t w)
+{
+    if constexpr (C::kVec4) {
+        return c.dec4(w);
+    } else {
+        return make_float4(c.dec(w & 0xffu), c.dec((w >> 8) & 0xffu), c.dec((w >> 16) & 0xffu),
+                           c.dec(w >> 24));
+    }
+}
+
+// packed group of 4 codes for the direct widths
+template <int B> struct Word4;
+template <> struct Word4<8> { using T = uint32_t; };
+template <> struct Word4<16> { using T = uint2; };
+template <> struct Word4<32> { using T = uint4; };
+
+template <int B, class C>
+__device__ __forceinline__ typename Word4<B>::T pack4(const C &c, float4 v)
+{
+    if constexpr (B == 8) {
+        return enc4_bytes(c, v);
+    } else if constexpr (B == 16) {
+        return make_uint2(c.enc(v.x) | (c.enc(v.y) << 16), c.enc(v.z) | (c.enc(v.w) << 16));
+    } else {
+        return make_uint4(c.enc(v.x), c.enc(v.y), c.enc(v.z), c.enc(v.w));
+    }
+}
+
+template <int B, class C>
+__device__ __forceinline__ float4 unpack4(const C &c, typename Word4<B>::T w)
+{
+    if constexpr (B == 8) {
+        return dec4_bytes(c, w);
+    } else if constexpr (B == 16) {
+        return make_float4(c.dec(w.x & 0xffffu), c.dec(w.x >> 16), c.dec(w.y & 0xffffu),
+                           c.dec(w.y >> 16));
+    } else {
+        return make_float4(c.dec(w.x), c.dec(w.y), c.dec(w.z), c.dec(w.w));
+    }
+}
+
+// ------------------------------------------------------------------ generic-width tile packing
+// Tile = 128 codes = 4*b words.  Word w holds bits [32w, 32w+32) of the
+// LSB-first code stream.
+__device__ __forceinline__ uint32_t assemble_word(const uint32_t *codes, int w, int b)
+{
+    const int bit0 = w * 32;
+    int k = bit0 / b;
+    const int off = bit0 - k * b;
+    uint64_t acc = (uint64_t)codes[k] >> off;
+    int have = b - off;
+    ++k;
+    while (have < 32 && k < kTile) {
+        acc |= (uint64_t)codes[k] << have;
+        have += b;
+        ++k;
+    }
+    return (uint32_t)acc;
+}
+
+// code k of a tile whose words are in shared memory (words[4b] is a zero pad)
+__device__ __forceinline__ uint32_t extract_code(const uint32_t *words, int k, int b)
+{
+    const int bit = k * b;
+    const int w = bit >> 5;
+    const int sh = bit & 31;
+    const uint32_t v = __funnelshift_r(words[w], words[w + 1], sh);
+    return b == 32 ? v : (v & ((1u << b) - 1u));
+}
+
+// ------------------------------------------------------------------ a1: absmax + local exponent
+__device__ __forceinline__ uint32_t absbits4(float4 v)
+{
+    const uint32_t a = max(__float_as_uint(v.x) & 0x7fffffffu, __float_as_uint(v.y) & 0x7fffffffu);
+    const uint32_t b = max(__float_as_uint(v.z) & 0x7fffffffu, __float_as_uint(v.w) & 0x7fffffffu);
+    return max(a, b);
+}
+
+// E = ceil(log2(N * A)) exactly (N*A is exact in binary64); sentinels for
+// an all-zero layer (A3) and non-finite input (A4).  The abs bits of fp32
+// are monotone in |x|, so the max is order-independent and bit-exact.
+__device__ __forceinline__ int32_t exponent_of(uint32_t abits, int N)
+{
+    if (abits == 0u) return INT32_MIN;
+    if (abits >= 0x7f800000u) return INT32_MAX;
+    const double d = (double)__uint_as_float(abits) * (double)N;
+    const uint64_t bits = (uint64_t)__double_as_longlong(d);
+    const int k = (int)(bits >> 52) - 1023;       // d in [2^k, 2^(k+1))
+    return (bits & ((1ull << 52) - 1ull)) ? k + 1 : k;
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) absmax_exp_kernel(DevTables t, int N)
+{
+    const Item it = t.items[blockIdx.x];
+    const LayerDev L = t.layers[it.layer];
+    const float *g = t.src[it.layer];
+    const int64_t begin = (int64_t)it.tile_begin * kTile;
+    const int64_t n = min((int64_t)it.n_tiles * kTile, L.numel - begin);
+    const float4 *g4 = reinterpret_cast<const float4 *>(g + begin);
+    constexpr int kFull4 = kItemTiles * kTile / 4;  // float4 groups in a full item
+    constexpr int kPer = kFull4 / NT;
+    uint32_t mx = 0;
+    if (n == kItemTiles * kTile) {
+        float4 v[kPer];
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) v[j] = ld_stream4(g4 + threadIdx.x + j * NT);
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) mx = max(mx, absbits4(v[j]));
+    } else {
+        const int64_t n4 = n >> 2;
+        for (int64_t i = threadIdx.x; i < n4; i += NT) mx = max(mx, absbits4(ld_stream4(g4 + i)));
+        for (int64_t i = (n4 << 2) + threadIdx.x; i < n; i += NT)
+            mx = max(mx, __float_as_uint(g[begin + i]) & 0x7fffffffu);
+    }
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    __shared__ uint32_t s_max[NT / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) s_max[warp] = mx;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t v = lane < NT / 32 ? s_max[lane] : 0u;
+        v = __reduce_max_sync(0xffffffffu, v);
+        if (lane == 0) {
+            atomicMax(&t.amax[it.layer], v);
+            __threadfence();
+            const uint32_t done = atomicAdd(&t.count[it.layer], 1u);
+            if (done == (uint32_t)L.n_items - 1u) {  // last CTA of this layer
+                __threadfence();
+                const uint32_t A = atomicExch(&t.amax[it.layer], 0u);
+                t.count[it.layer] = 0u;
+                t.E_local[it.layer] = exponent_of(A, N);
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ a3+a4: scale, cast, pack
+__device__ __forceinline__ int scale_exponent(const DevTables &t, int layer, int bias, bool lead)
+{
+    const int32_t E = t.E_glob[layer];
+    int ft = (E == INT32_MIN) ? 0 : bias - E;   // f~ = upper_bound_exp - E (Alg. 1)
+    if (E == INT32_MAX) {                        // non-finite somewhere: flag (A4)
+        ft = 0;
+        if (lead) atomicOr(t.flag, 1u);
+    }
+    if (lead) t.ftilde[layer] = ft;
+    return ft;
+}
+
+// direct widths 8/16/32: group of 4 fp32 -> one 4-code word group
+template <int B, class C, int NT>
+__global__ void __launch_bounds__(NT) quant_pack_direct_kernel(DevTables t, C c, int bias)
+{
+    const Item it = t.items[blockIdx.x];
+    const LayerDev L = t.layers[it.layer];
+    const float *g = t.src[it.layer];
+    const int ft = scale_exponent(t, it.layer, bias, it.tile_begin == 0 && threadIdx.x == 0);
+    const Pow2 s(ft);
+    const int64_t begin = (int64_t)it.tile_begin * kTile;
+    const int64_t n = min((int64_t)it.n_tiles * kTile, L.numel - begin);
+    using W = typename Word4<B>::T;
+    W *out = reinterpret_cast<W *>(t.packed + (L.tile_off + it.tile_begin) * (16 * B));
+    const float *gb = g + begin;
+    constexpr int kFull4 = kItemTiles * kTile / 4;
+    constexpr int kPer = kFull4 / NT;
+    if (n == kItemTiles * kTile && !s.wide) {
+        float4 v[kPer];
+        const float4 *g4 = reinterpret_cast<const float4 *>(gb);
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) v[j] = ld_stream4(g4 + threadIdx.x + j * NT);
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) {
+            const float4 y = make_float4(__fmul_rn(v[j].x, s.f), __fmul_rn(v[j].y, s.f),
+                                         __fmul_rn(v[j].z, s.f), __fmul_rn(v[j].w, s.f));
+            out[threadIdx.x + j * NT] = pack4<B>(c, y);
+        }
+    } else {
+        const int ng = it.n_tiles * (kTile / 4);
+        for (int gi = threadIdx.x; gi < ng; gi += NT) {
+            const float4 v = load_group(gb, (int64_t)gi * 4, n);
+            out[gi] = pack4<B>(c, s.apply4(v));
+        }
+    }
+}
+
+// any width: per-warp tile through shared memory
+template <class C, int NT>
+__global__ void __launch_bounds__(NT) quant_pack_tile_kernel(DevTables t, C c, int bias)
+{
+    __shared__ __align__(16) uint32_t s_codes[NT / 32][kTile];
+    const Item it = t.items[blockIdx.x];
+    const LayerDev L = t.layers[it.layer];
+    const float *g = t.src[it.layer];
+    const int ft = scale_exponent(t, it.layer, bias, it.tile_begin == 0 && threadIdx.x == 0);
+    const Pow2 s(ft);
+    const int b = c.b();
+    const int64_t begin = (int64_t)it.tile_begin * kTile;
+    const int64_t n = min((int64_t)it.n_tiles * kTile, L.numel - begin);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t *codes = s_codes[warp];
+    uint32_t *out = reinterpret_cast<uint32_t *>(t.packed) + (L.tile_off + it.tile_begin) * (4 * b);
+    for (int tt = warp; tt < it.n_tiles; tt += NT / 32) {
+        const int64_t e0 = (int64_t)tt * kTile + lane * 4;
+        const float4 y = s.apply4(load_group(g + begin, e0, n));
+        *reinterpret_cast<uint4 *>(codes + lane * 4) =
+            make_uint4(c.enc(y.x), c.enc(y.y), c.enc(y.z), c.enc(y.w));
+        __syncwarp();
+        uint32_t *ow = out + (int64_t)tt * (4 * b);
+        for (int w = lane; w < 4 * b; w += 32) ow[w] = assemble_word(codes, w, b);
+        __syncwarp();
+    }
+}
+
+// ------------------------------------------------------------------ a7: unpack, unscale, average
+struct Unscale {
+    Pow2 s;
+    bool div;       // non-power-of-two N: IEEE division
+    float inv_n;    // 2^-log2(N) for power-of-two N
+    float n_f;
+    bool average;
+    __device__ __forceinline__ Unscale(int ft, int N, int avg) : s(-ft)
+    {
+        average = avg != 0;
+        div = (N & (N - 1)) != 0;
+        n_f = (float)N;
+        inv_n = div ? 1.f : __uint_as_float((uint32_t)(127 - (31 - __clz(N))) << 23);
+    }
+    __device__ __forceinline__ float apply(float v) const
+    {
+        float x = s.apply(v);
+        if (average) x = div ? __fdiv_rn(x, n_f) : __fmul_rn(x, inv_n);
+        return x;
+    }
+    __device__ __forceinline__ float4 apply4(float4 v) const
+    {
+        return make_float4(apply(v.x), apply(v.y), apply(v.z), apply(v.w));
+    }
+};
+
+template <int B, class C, int NT>
+__global__ void __launch_bounds__(NT) unpack_unscale_direct_kernel(DevTables t, C c, int N, int avg)
+{
+    const Item it = t.items[blockIdx.x];
+    const LayerDev L = t.layers[it.layer];
+    float *o = t.dst[it.layer];
+    const Unscale us(t.ftilde[it.layer], N, avg);
+    const int64_t begin = (int64_t)it.tile_begin * kTile;
+    const int64_t n = min((int64_t)it.n_tiles * kTile, L.numel - begin);
+    using W = typename Word4<B>::T;
+    const W *in = reinterpret_cast<const W *>(t.packed + (L.tile_off + it.tile_begin) * (16 * B));
+    float *ob = o + begin;
+    constexpr int kFull4 = kItemTiles * kTile / 4;
+    constexpr int kPer = kFull4 / NT;
+    if (n == kItemTiles * kTile) {
+        W w[kPer];
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) w[j] = in[threadIdx.x + j * NT];
+        float4 *o4 = reinterpret_cast<float4 *>(ob);
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) o4[threadIdx.x + j * NT] = us.apply4(unpack4<B>(c, w[j]));
+    } else {
+        const int64_t ng = (n + 3) / 4;
+        for (int64_t gi = threadIdx.x; gi < ng; gi += NT)
+            store_group(ob, gi * 4, n, us.apply4(unpack4<B>(c, in[gi])));
+    }
+}
+
+template <class C, int NT>
+__global__ void __launch_bounds__(NT) unpack_unscale_tile_kernel(DevTables t, C c, int N, int avg)
+{
+    __shared__ __align__(16) uint32_t s_words[NT / 32][kTile + 1];
+    const Item it = t.items[blockIdx.x];
+    const LayerDev L = t.layers[it.layer];
+    float *o = t.dst[it.layer];
+    const Unscale us(t.ftilde[it.layer], N, avg);
+    const int b = c.b();
+    const int64_t begin = (int64_t)it.tile_begin * kTile;
+    const int64_t n = min((int64_t)it.n_tiles * kTile, L.numel - begin);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t *words = s_words[warp];
+    const uint32_t *in = reinterpret_cast<const uint32_t *>(t.packed) + (L.tile_off + it.tile_begin) * (4 * b);
+    for (int tt = warp; tt < it.n_tiles; tt += NT / 32) {
+        const uint32_t *iw = in + (int64_t)tt * (4 * b);
+        for (int w = lane; w < 4 * b; w += 32) words[w] = iw[w];
+        if (lane == 0) words[4 * b] = 0u;
+        __syncwarp();
+        const int k0 = lane * 4;
+        const float4 v = make_float4(c.dec(extract_code(words, k0, b)), c.dec(extract_code(words, k0 + 1, b)),
+                                     c.dec(extract_code(words, k0 + 2, b)), c.dec(extract_code(words, k0 + 3, b)));
+        store_group(o + begin, (int64_t)tt * kTile + k0, n, us.apply4(v));
+        __syncwarp();
+    }
+}
+
+// ------------------------------------------------------------------ a5: ring reduce step
+// own[i] <- Cast(fl32(dec(recv[i]) + dec(own[i])))   (re-quantise after the add, A13)
+template <int B, class C, int NT>
+__global__ void __launch_bounds__(NT) ring_reduce_direct_kernel(uint8_t *own, const uint8_t *recv,
+                                                                 int64_t n_groups, C c)
+{
+    using W = typename Word4<B>::T;
+    W *o = reinterpret_cast<W *>(own);
+    const W *r = reinterpret_cast<const W *>(recv);
+    for (int64_t gi = blockIdx.x * (int64_t)NT + threadIdx.x; gi < n_groups; gi += (int64_t)gridDim.x * NT) {
+        const float4 a = unpack4<B>(c, r[gi]);
+        const float4 b = unpack4<B>(c, o[gi]);
+        const float4 s = make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z),
+                                     __fadd_rn(a.w, b.w));
+        o[gi] = pack4<B>(c, s);
+    }
+}
+
+template <class C, int NT>
+__global__ void __launch_bounds__(NT) ring_reduce_tile_kernel(uint8_t *own, const uint8_t *recv,
+                                                               int64_t n_tiles, C c)
+{
+    __shared__ __align__(16) uint32_t s_a[NT / 32][kTile + 1];
+    __shared__ __align__(16) uint32_t s_b[NT / 32][kTile + 1];
+    const int b = c.b();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t *wa = s_a[warp], *wb = s_b[warp];
+    uint32_t *o = reinterpret_cast<uint32_t *>(own);
+    const uint32_t *r = reinterpret_cast<const uint32_t *>(recv);
+    const int64_t warps = (int64_t)gridDim.x * (NT / 32);
+    for (int64_t tt = blockIdx.x * (int64_t)(NT / 32) + warp; tt < n_tiles; tt += warps) {
+        uint32_t *ow = o + tt * (4 * b);
+        const uint32_t *rw = r + tt * (4 * b);
+        for (int w = lane; w < 4 * b; w += 32) {
+            wa[w] = rw[w];
+            wb[w] = ow[w];
+        }
+        if (lane == 0) wa[4 * b] = wb[4 * b] = 0u;
+        __syncwarp();
+        uint32_t res[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int k = lane * 4 + j;
+            res[j] = c.enc(__fadd_rn(c.dec(extract_code(wa, k, b)), c.dec(extract_code(wb, k, b))));
+        }
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 4; ++j) wa[lane * 4 + j] = res[j];  // reuse as code array
+        __syncwarp();
+        for (int w = lane; w < 4 * b; w += 32) ow[w] = assemble_word(wa, w, b);
+        __syncwarp();
+    }
+}
+
+// ------------------------------------------------------------------ sim: MAX exchange of E
+struct PtrArr {
+    const int32_t *src[64];
+    int32_t *dst[64];
+};
+
+__global__ void sim_max_kernel(PtrArr a, int p, int n_layers)
+{
+    for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < n_layers; l += gridDim.x * blockDim.x) {
+        int32_t m = INT32_MIN;
+        for (int r = 0; r < p; ++r) m = max(m, a.src[r][l]);
+        for (int r = 0; r < p; ++r) a.dst[r][l] = m;
+    }
+}
+
+// ------------------------------------------------------------------ debug
+template <class C>
+__global__ void debug_cast_kernel(const float *in, uint32_t *codes, int64_t n, C c)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        codes[i] = c.enc(in[i]);
+}
+
+template <class C>
+__global__ void debug_decode_kernel(const uint32_t *codes, float *out, int64_t n, C c)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = c.dec_any(codes[i]);
+}
+
+// ------------------------------------------------------------------ dispatch
+// Calls f(codec) with the compiled specialisation for the config formats,
+// the hardware fp8 codec when requested, else the runtime codec.
+template <class F>
+cudaError_t with_codec(int e, int m, bool hw, F &&f)
+{
+    if (hw && e == 5 && m == 2) return f(CHw<false>{});
+    if (hw && e == 4 && m == 3) return f(CHw<true>{});
+    if (e == 5 && m == 2) return f(CGen<5, 2>{});
+    if (e == 4 && m == 3) return f(CGen<4, 3>{});
+    if (e == 3 && m == 0) return f(CGen<3, 0>{});
+    if (e == 5 && m == 6) return f(CGen<5, 6>{});
+    if (e == 5 && m == 10) return f(CGen<5, 10>{});
+    if (e == 8 && m == 7) return f(CGen<8, 7>{});
+    if (e == 8 && m == 23) return f(CGen<8, 23>{});
+    CRt c;
+    c.F = make_fmt(e, m);
+    return f(c);
+}
+
+static int sm_count()
+{
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+cudaError_t launch_absmax_exp(const DevTables &t, int world, cudaStream_t s)
+{
+    if (t.n_items == 0) return cudaSuccess;
+    absmax_exp_kernel<kThreads><<<t.n_items, kThreads, 0, s>>>(t, world);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_quant_pack(const DevTables &t, int e, int m, bool hw, cudaStream_t s)
+{
+    const int bias = (1 << (e - 1)) - 1;
+    return with_codec(e, m, hw, [&](auto c) -> cudaError_t {
+        using C = decltype(c);
+        const int b = 1 + e + m;
+        if constexpr (C::kB == 8 || C::kB == 16 || C::kB == 32) {
+            quant_pack_direct_kernel<C::kB, C, kThreads><<<t.n_items, kThreads, 0, s>>>(t, c, bias);
+        } else if constexpr (C::kB == 0) {
+            if (b == 8) quant_pack_direct_kernel<8, C, kThreads><<<t.n_items, kThreads, 0, s>>>(t, c, bias);
+            else if (b == 16) quant_pack_direct_kernel<16, C, kThreads><<<t.n_items, kThreads, 0, s>>>(t, c, bias);
+            else if (b == 32) quant_pack_direct_kernel<32, C, kThreads><<<t.n_items, kThreads, 0, s>>>(t, c, bias);
+            else quant_pack_tile_kernel<C, kThreads><<<t.n_items, kThreads, 0, s>>>(t, c, bias);
+        } else {
+            quant_pack_tile_kernel<C, kThreads><<<t.n_items, kThreads, 0, s>>>(t, c, bias);
+        }
+        return cudaGetLastError();
+    });
+}
+
+cudaError_t launch_unpack_unscale(const DevTables &t, int e, int m, bool hw, int world, int average,
+                                  cudaStream_t s)
+{
+    return with_codec(e, m, hw, [&](auto c) -> cudaError_t {
+        using C = decltype(c);
+        const int b = 1 + e + m;
+        if constexpr (C::kB == 8 || C::kB == 16 || C::kB == 32) {
+            unpack_unscale_direct_kernel<C::kB, C, kThreads><<<t.n_items, kThreads, 0, s>>>(t, c, world, average);
+        } else if constexpr (C::kB == 0) {
+            if (b == 8) unpack_unscale_direct_kernel<8, C, kThreads><<<t.n_items, kThreads, 0, s>>>(t, c, world, average);
+            else if (b == 16) unpack_unscale_direct_kernel<16, C, kThreads><<<t.n_items, kThreads, 0, s>>>(t, c, world, average);
+            else if (b == 32) unpack_unscale_direct_kernel<32, C, kThreads><<<t.n_items, kThreads, 0, s>>>(t, c, world, average);
+            else unpack_unscale_tile_kernel<C, kThreads><<<t.n_items, kThreads, 0, s>>>(t, c, world, average);
+        } else {
+            unpack_unscale_tile_kernel<C, kThreads><<<t.n_items, kThreads, 0, s>>>(t, c, world, average);
+        }
+        return cudaGetLastError();
+    });
+}
+
+cudaError_t launch_ring_reduce(uint8_t *own, const uint8_t *recv, int64_t n_tiles, int e, int m,
+                               bool hw, cudaStream_t s)
+{
+    if (n_tiles <= 0) return cudaSuccess;
+    return with_codec(e, m, hw, [&](auto c) -> cudaError_t {
+        using C = decltype(c);
+        const int b = 1 + e + m;
+        const int64_t n_groups = n_tiles * (kTile / 4);
+        const int grid_direct = (int)std::min<int64_t>((n_groups + kThreads - 1) / kThreads, (int64_t)sm_count() * 8);
+        const int grid_tile = (int)std::min<int64_t>((n_tiles + kThreads / 32 - 1) / (kThreads / 32), (int64_t)sm_count() * 8);
+        if constexpr (C::kB == 8 || C::kB == 16 || C::kB == 32) {
+            ring_reduce_direct_kernel<C::kB, C, kThreads><<<grid_direct, kThreads, 0, s>>>(own, recv, n_groups, c);
+        } else if constexpr (C::kB == 0) {
+            if (b == 8) ring_reduce_direct_kernel<8, C, kThreads><<<grid_direct, kThreads, 0, s>>>(own, recv, n_groups, c);
+            else if (b == 16) ring_reduce_direct_kernel<16, C, kThreads><<<grid_direct, kThreads, 0, s>>>(own, recv, n_groups, c);
+            else if (b == 32) ring_reduce_direct_kernel<32, C, kThreads><<<grid_direct, kThreads, 0, s>>>(own, recv, n_groups, c);
+            else ring_reduce_tile_kernel<C, kThreads><<<grid_tile, kThreads, 0, s>>>(own, recv, n_tiles, c);
+        } else {
+            ring_reduce_tile_kernel<C, kThreads><<<grid_tile, kThreads, 0, s>>>(own, recv, n_tiles, c);
+        }
+        return cudaGetLastError();
+    });
+}
+
+cudaError_t launch_sim_max(int32_t *const *E_glob, const int32_t *const *E_local, int p, int n_layers,
+                           cudaStream_t s)
+{
+    if (p > 64) return cudaErrorInvalidValue;
+    PtrArr a{};
+    for (int r = 0; r < p; ++r) {
+        a.src[r] = E_local[r];
+        a.dst[r] = E_glob[r];
+    }
+    sim_max_kernel<<<(n_layers + 255) / 256, 256, 0, s>>>(a, p, n_layers);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_debug_cast(const float *in, uint32_t *codes, int64_t n, int e, int m, bool hw,
+                              cudaStream_t s)
+{
+    if (n <= 0) return cudaSuccess;
+    return with_codec(e, m, hw, [&](auto c) -> cudaError_t {
+        const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 16);
+        debug_cast_kernel<<<grid, 256, 0, s>>>(in, codes, n, c);
+        return cudaGetLastError();
+    });
+}
+
+cudaError_t launch_debug_decode(const uint32_t *codes, float *out, int64_t n, int e, int m, bool hw,
+                                cudaStream_t s)
+{
+    if (n <= 0) return cudaSuccess;
+    return with_codec(e, m, hw, [&](auto c) -> cudaError_t {
+        const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 16);
+        debug_decode_kernel<<<grid, 256, 0, s>>>(codes, out, n, c);
+        return cudaGetLastError();
+    });
+}
+
+}  // namespace aps
