@@ -249,6 +249,7 @@ def main():
     ctx = aps.ApsContext(e, m, numels, world_size=world, rank=rank, nccl_comm=comm, stream=stream,
                          device=dev, hw_convert=not args.no_hw)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush_rd = torch.zeros(256 << 20, dtype=torch.uint8, device=dev)
 
     def step(evs=None):
         if evs: evs[0].record(stream)
@@ -276,7 +277,8 @@ def main():
     with ClockSampler(local) as clk:
         for k in range(K):
             if not args.no_flush:
-                flush.zero_()                 # > L2 (126 MB): every step starts cold
+                flush.zero_()                 # write > L2 (126 MB): evicts the step's data ...
+                flush_rd.sum(dtype=torch.int32)   # ... and leaves L2 clean (no dirty write-backs)
             step(events[k])
         torch.cuda.synchronize()
     if world > 1:
@@ -352,7 +354,7 @@ def main():
         "scaling": "weak", "vs_baseline": None, "dtype": "f32->u8 codes" if b == 8 else f"f32->{b}-bit codes",
         "data": "synthetic (seeded normal per layer, binade spread 2^-24..2^-4, 0.5% zeros)",
         "config": {"workload": name, "format": f"1/{e}/{m}", "n_layers": len(numels), "elements": L,
-                   "ranks": world, "hw_convert": ctx_hw(ctx, args), "l2": "flushed (256 MiB write) between timed steps"
+                   "ranks": world, "hw_convert": ctx_hw(ctx, args), "l2": "flushed (256 MiB write + 256 MiB read) between timed steps"
                    if not args.no_flush else "not flushed", "parallelism": f"dp{world}",
                    "packed_bytes": packed_bytes},
         "roofline": roof, "phases": phases, "gpu_launches": launches_per_step * K,

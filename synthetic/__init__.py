@@ -104,7 +104,8 @@ def edge_case_layers(p: int, seed: int = SEED) -> list[list[np.ndarray]]:
         layers.append(np.zeros(300, np.float32))                                   # all zero
         layers.append(np.array([rng.standard_normal()], np.float32))               # 1 element
         layers.append(np.array([0.0], np.float32) if r % 2 else np.array([-0.0], np.float32))
-        sub = (rng.integers(1, 2**23, 517) * rng.choice([-1, 1], 517)).astype(np.int32)
+        sub = rng.integers(1, 2**23, 517).astype(np.uint32)
+        sub |= rng.integers(0, 2, 517).astype(np.uint32) << np.uint32(31)
         layers.append(sub.view(np.float32))                                       # fp32 subnormals
         pw = rng.standard_normal(1000).astype(np.float32) * np.float32(0.25)
         pw[np.abs(pw) > 0.5] = 0.5
