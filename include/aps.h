@@ -131,8 +131,13 @@ aps_status aps_allreduce(aps_ctx *ctx);
 aps_status aps_unscale(aps_ctx *ctx, float *const *out, int average);
 
 /* aps_layer_scales, aps_quantize_pack, aps_allreduce, aps_unscale in order,
- * in place on grads. */
+ * in place on grads.  With world_size == 1 the four run as ONE fused
+ * persistent launch (no collective separates FindMaxExp from Cast). */
 aps_status aps_sync(aps_ctx *ctx, float *const *grads, int average);
+
+/* As aps_sync, reading grads and writing the result to out (out may alias
+ * grads; out[l] 16-byte aligned, numels[l] fp32). */
+aps_status aps_sync_out(aps_ctx *ctx, const float *const *grads, float *const *out, int average);
 
 /* End-to-end entry with HOST buffers: copies host_in[l] (pinned host fp32)
  * into dev_grads[l], runs aps_sync in place, copies the result to host_out[l]

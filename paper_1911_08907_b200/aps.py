@@ -23,7 +23,7 @@ STATUS_NAMES = {0: "APS_OK", 1: "APS_ERR_ARG", 2: "APS_ERR_FORMAT", 3: "APS_ERR_
 # every symbol include/aps.h declares
 EXPORTS = [
     "aps_init", "aps_workspace_bytes", "aps_set_workspace", "aps_set_hw_convert",
-    "aps_layer_scales", "aps_quantize_pack", "aps_allreduce", "aps_unscale", "aps_sync",
+    "aps_layer_scales", "aps_quantize_pack", "aps_allreduce", "aps_unscale", "aps_sync", "aps_sync_out",
     "aps_sync_host", "aps_status_sync", "aps_get_scales", "aps_get_packed", "aps_layout",
     "aps_ring_step", "aps_last_error", "aps_destroy", "aps_version", "aps_nccl_unique_id",
     "aps_nccl_comm_init", "aps_nccl_comm_destroy", "aps_sim_layer_scales", "aps_sim_allreduce",
@@ -61,6 +61,7 @@ def load(path: Path | str | None = None):
         "aps_allreduce": ([vp], i32),
         "aps_unscale": ([vp, vp, i32], i32),
         "aps_sync": ([vp, vp, i32], i32),
+        "aps_sync_out": ([vp, vp, vp, i32], i32),
         "aps_sync_host": ([vp, vp, vp, vp, i32], i32),
         "aps_status_sync": ([vp], i32),
         "aps_get_scales": ([vp, vp], i32),
@@ -202,6 +203,9 @@ class ApsContext:
 
     def sync(self, grads, average: bool = True):
         self._check(self.L.aps_sync(self.h, self._ptrs(grads), int(average)), "aps_sync")
+
+    def sync_out(self, grads, out, average: bool = True):
+        self._check(self.L.aps_sync_out(self.h, self._ptrs(grads), self._ptrs(out), int(average)), "aps_sync_out")
 
     def sync_host(self, host_in, dev_grads, host_out, average: bool = True):
         self._check(self.L.aps_sync_host(self.h, self._ptrs(host_in), self._ptrs(dev_grads),

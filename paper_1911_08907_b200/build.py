@@ -11,8 +11,8 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libaps.so"
-SOURCES = [CSRC / "aps_kernels.cu", CSRC / "aps_api.cpp"]
-HEADERS = [CSRC / "aps_numerics.cuh", CSRC / "aps_internal.h", ROOT / "include" / "aps.h"]
+SOURCES = [CSRC / "aps_kernels.cu", CSRC / "aps_stream.cu", CSRC / "aps_api.cpp"]
+HEADERS = [CSRC / "aps_numerics.cuh", CSRC / "aps_device.cuh", CSRC / "aps_internal.h", ROOT / "include" / "aps.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 

@@ -42,11 +42,13 @@ struct aps_ctx {
     uint8_t *ws = nullptr;
     size_t ws_bytes = 0, need = 0;
     size_t off_packed = 0, off_recv = 0, off_items = 0, off_layers = 0, off_src = 0, off_dst = 0,
-           off_amax = 0, off_count = 0, off_eloc = 0, off_eglob = 0, off_ft = 0, off_flag = 0;
+           off_amax = 0, off_count = 0, off_eloc = 0, off_eglob = 0, off_ft = 0, off_flag = 0, off_ready = 0;
     aps::DevTables t{};
     std::vector<const float *> src_cache;
     std::vector<float *> dst_cache;
     int phase = kNone;
+    bool stream_engine = true;  // persistent TMA-bulk kernels (aps_stream.cu) vs simple grid kernels
+    uint32_t gen = 0;           // generation stamp of the fused p = 1 launch
     std::string err;
 };
 
@@ -159,6 +161,7 @@ aps_status aps_init(aps_ctx **out, int exp_bits, int man_bits, int world_size, i
     c->stream = static_cast<cudaStream_t>(cuda_stream);
     c->hw = aps::hw_available(exp_bits, man_bits);
     if (const char *env = std::getenv("APS_HW_CVT")) c->hw = c->hw && std::atoi(env) != 0;
+    if (const char *env = std::getenv("APS_ENGINE")) c->stream_engine = std::strcmp(env, "simple") != 0;
     if (c->comm) {
         int nr = 0;
         if (ncclCommCount(c->comm, &nr) != ncclSuccess || nr != world_size) {
@@ -214,6 +217,7 @@ aps_status aps_init(aps_ctx **out, int exp_bits, int man_bits, int world_size, i
     c->off_eglob = o;  o = align_up(o + 4 * (size_t)n_layers);
     c->off_ft = o;     o = align_up(o + 4 * (size_t)n_layers);
     c->off_flag = o;   o = align_up(o + 4);
+    c->off_ready = o;  o = align_up(o + 4 * (size_t)n_layers);
     c->need = o;
     *out = c;
     return APS_OK;
@@ -245,6 +249,8 @@ aps_status aps_set_workspace(aps_ctx *c, void *dev, size_t bytes)
     t.E_glob = reinterpret_cast<int32_t *>(c->ws + (c->world == 1 ? c->off_eloc : c->off_eglob));
     t.ftilde = reinterpret_cast<int32_t *>(c->ws + c->off_ft);
     t.flag = reinterpret_cast<uint32_t *>(c->ws + c->off_flag);
+    t.ready = reinterpret_cast<uint32_t *>(c->ws + c->off_ready);
+    c->gen = 0;
     t.packed = c->ws + c->off_packed;
     t.n_items = (int)c->items.size();
     t.n_layers = c->n_layers;
@@ -266,7 +272,8 @@ aps_status aps_layer_scales(aps_ctx *c, const float *const *grads)
     if (aps_status s = need_ws(c)) return s;
     if (!grads) return fail(c, APS_ERR_ARG, "grads is NULL");
     if (aps_status s = upload_ptrs<const float *>(c, c->src_cache, grads, c->off_src)) return s;
-    APS_CUDA(c, aps::launch_absmax_exp(c->t, c->world, c->stream));
+    APS_CUDA(c, c->stream_engine ? aps::launch_stream_absmax(c->t, c->world, c->stream)
+                                 : aps::launch_absmax_exp(c->t, c->world, c->stream));
     if (c->world == 1) {
         c->phase = kScales;
     } else if (c->sim) {
@@ -286,7 +293,10 @@ aps_status aps_quantize_pack(aps_ctx *c, const float *const *grads)
     if (c->phase < kScales) return fail(c, APS_ERR_STATE, "aps_quantize_pack before aps_layer_scales");
     if (!grads) return fail(c, APS_ERR_ARG, "grads is NULL");
     if (aps_status s = upload_ptrs<const float *>(c, c->src_cache, grads, c->off_src)) return s;
-    APS_CUDA(c, aps::launch_quant_pack(c->t, c->e, c->m, c->hw, c->stream));
+    cudaError_t e = c->stream_engine ? aps::launch_stream_quant(c->t, c->e, c->m, c->hw, c->stream)
+                                     : cudaErrorNotSupported;
+    if (e == cudaErrorNotSupported) e = aps::launch_quant_pack(c->t, c->e, c->m, c->hw, c->stream);
+    APS_CUDA(c, e);
     c->phase = kPacked;
     return APS_OK;
 }
@@ -329,17 +339,40 @@ aps_status aps_unscale(aps_ctx *c, float *const *out, int average)
         return fail(c, APS_ERR_STATE, "aps_unscale before aps_allreduce");
     if (!out) return fail(c, APS_ERR_ARG, "out is NULL");
     if (aps_status s = upload_ptrs<float *>(c, c->dst_cache, out, c->off_dst)) return s;
-    APS_CUDA(c, aps::launch_unpack_unscale(c->t, c->e, c->m, c->hw, c->world, average, c->stream));
+    cudaError_t e = c->stream_engine
+                        ? aps::launch_stream_unpack(c->t, c->e, c->m, c->hw, c->world, average, c->stream)
+                        : cudaErrorNotSupported;
+    if (e == cudaErrorNotSupported)
+        e = aps::launch_unpack_unscale(c->t, c->e, c->m, c->hw, c->world, average, c->stream);
+    APS_CUDA(c, e);
     return APS_OK;
+}
+
+aps_status aps_sync_out(aps_ctx *c, const float *const *grads, float *const *out, int average)
+{
+    if (aps_status s = need_ws(c)) return s;
+    if (!grads || !out) return fail(c, APS_ERR_ARG, "NULL pointer array");
+    if (c->world == 1 && c->stream_engine) {
+        // one rank: FindMaxExp -> f~ -> Cast -> pack -> Cast back -> unscale in one launch
+        if (aps_status s = upload_ptrs<const float *>(c, c->src_cache, grads, c->off_src)) return s;
+        if (aps_status s = upload_ptrs<float *>(c, c->dst_cache, out, c->off_dst)) return s;
+        if (++c->gen == 0) c->gen = 1;
+        cudaError_t e = aps::launch_stream_fused_p1(c->t, c->e, c->m, c->hw, average, c->gen, c->stream);
+        if (e != cudaErrorNotSupported) {
+            APS_CUDA(c, e);
+            c->phase = kReduced;
+            return APS_OK;
+        }
+    }
+    if (aps_status s = aps_layer_scales(c, grads)) return s;
+    if (aps_status s = aps_quantize_pack(c, grads)) return s;
+    if (aps_status s = aps_allreduce(c)) return s;
+    return aps_unscale(c, out, average);
 }
 
 aps_status aps_sync(aps_ctx *c, float *const *grads, int average)
 {
-    const float *const *g = const_cast<const float *const *>(grads);
-    if (aps_status s = aps_layer_scales(c, g)) return s;
-    if (aps_status s = aps_quantize_pack(c, g)) return s;
-    if (aps_status s = aps_allreduce(c)) return s;
-    return aps_unscale(c, grads, average);
+    return aps_sync_out(c, const_cast<const float *const *>(grads), grads, average);
 }
 
 aps_status aps_sync_host(aps_ctx *c, const float *const *host_in, float *const *dev_grads,

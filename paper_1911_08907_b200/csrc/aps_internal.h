@@ -37,6 +37,7 @@ struct DevTables {
     int32_t *E_glob;          // [n_layers]
     int32_t *ftilde;          // [n_layers]
     uint32_t *flag;           // non-finite flag
+    uint32_t *ready;          // [n_layers] generation stamp: E of the layer is final (fused p=1 path)
     uint8_t *packed;          // packed codes
     int n_items;
     int n_layers;
@@ -54,6 +55,21 @@ cudaError_t launch_debug_cast(const float *in, uint32_t *codes, int64_t n, int e
                               cudaStream_t s);
 cudaError_t launch_debug_decode(const uint32_t *codes, float *out, int64_t n, int e, int m,
                                 bool hw, cudaStream_t s);
+
+int sm_count();
+
+// Persistent TMA-bulk streaming engine (aps_stream.cu): one CTA per SM, a
+// producer warp feeding a multi-stage shared-memory ring with
+// cp.async.bulk, eight consumer warps.
+cudaError_t launch_stream_absmax(const DevTables &t, int world, cudaStream_t s);
+cudaError_t launch_stream_quant(const DevTables &t, int e, int m, bool hw, cudaStream_t s);
+cudaError_t launch_stream_unpack(const DevTables &t, int e, int m, bool hw, int world, int average,
+                                 cudaStream_t s);
+// p = 1: FindMaxExp -> f~ -> Cast -> pack -> Cast back -> unscale in ONE
+// launch (phase A: abs-max of every work item, forward; phase B: quantise +
+// unscale, reverse order so the second read of the gradients hits L2).
+cudaError_t launch_stream_fused_p1(const DevTables &t, int e, int m, bool hw, int average, uint32_t gen,
+                                   cudaStream_t s);
 
 // true when (e,m) has a hardware converter that is exact on the APS path
 inline bool hw_available(int e, int m) { return (e == 5 && m == 2) || (e == 4 && m == 3); }

@@ -13,234 +13,9 @@
 #include <climits>
 #include <algorithm>
 
-#include "aps_internal.h"
-#include "aps_numerics.cuh"
+#include "aps_device.cuh"
 
 namespace aps {
-
-// ------------------------------------------------------------------ codecs
-// Uniform interface: enc(float)->code, dec(code)->float (finite codes),
-// dec_any (all codes), b(), and optionally enc4/dec4 for byte codes.
-template <int E, int M>
-struct CGen {
-    static constexpr int kB = 1 + E + M;
-    static constexpr bool kVec4 = false;
-    __device__ __forceinline__ int b() const { return kB; }
-    __device__ __forceinline__ uint32_t enc(float y) const
-    {
-        constexpr Fmt F = make_fmt(E, M);
-        return encode(F, y);
-    }
-    __device__ __forceinline__ float dec(uint32_t c) const
-    {
-        constexpr Fmt F = make_fmt(E, M);
-        return decode_finite(F, c);
-    }
-    __device__ __forceinline__ float dec_any(uint32_t c) const
-    {
-        constexpr Fmt F = make_fmt(E, M);
-        return decode(F, c);
-    }
-};
-
-template <bool E4M3>
-struct CHw {
-    static constexpr int kB = 8;
-    static constexpr bool kVec4 = true;
-    __device__ __forceinline__ int b() const { return 8; }
-    __device__ __forceinline__ uint32_t enc(float y) const
-    {
-        return (E4M3 ? cvt_e4m3x2(0.f, y) : cvt_e5m2x2(0.f, y)) & 0xffu;
-    }
-    __device__ __forceinline__ float dec(uint32_t c) const
-    {
-        return E4M3 ? e4m3x2_to_f32x2(c & 0xffu).x : e5m2x2_to_f32x2(c & 0xffu).x;
-    }
-    __device__ __forceinline__ float dec_any(uint32_t c) const { return dec(c); }
-    __device__ __forceinline__ uint32_t enc4(float4 v) const
-    {
-        const uint32_t lo = E4M3 ? cvt_e4m3x2(v.y, v.x) : cvt_e5m2x2(v.y, v.x);
-        const uint32_t hi = E4M3 ? cvt_e4m3x2(v.w, v.z) : cvt_e5m2x2(v.w, v.z);
-        return lo | (hi << 16);
-    }
-    __device__ __forceinline__ float4 dec4(uint32_t w) const
-    {
-        const float2 a = E4M3 ? e4m3x2_to_f32x2(w & 0xffffu) : e5m2x2_to_f32x2(w & 0xffffu);
-        const float2 c = E4M3 ? e4m3x2_to_f32x2(w >> 16) : e5m2x2_to_f32x2(w >> 16);
-        return make_float4(a.x, a.y, c.x, c.y);
-    }
-};
-
-struct CRt {
-    static constexpr int kB = 0;  // runtime width
-    static constexpr bool kVec4 = false;
-    Fmt F;
-    __device__ __forceinline__ int b() const { return F.b; }
-    __device__ __forceinline__ uint32_t enc(float y) const { return encode(F, y); }
-    __device__ __forceinline__ float dec(uint32_t c) const { return decode_finite(F, c); }
-    __device__ __forceinline__ float dec_any(uint32_t c) const { return decode(F, c); }
-};
-
-// ------------------------------------------------------------------ memory helpers
-__device__ __forceinline__ float4 ld_stream4(const float4 *p)
-{
-    float4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
-                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
-                 : "l"(p));
-    return r;
-}
-
-// 4 consecutive fp32 of a layer starting at element e0, zero-filled past n.
-__device__ __forceinline__ float4 load_group(const float *g, int64_t e0, int64_t n)
-{
-    if (e0 + 4 <= n) return ld_stream4(reinterpret_cast<const float4 *>(g + e0));
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (e0 + 0 < n) v.x = g[e0 + 0];
-    if (e0 + 1 < n) v.y = g[e0 + 1];
-    if (e0 + 2 < n) v.z = g[e0 + 2];
-    return v;
-}
-
-__device__ __forceinline__ void store_group(float *o, int64_t e0, int64_t n, float4 v)
-{
-    if (e0 + 4 <= n) {
-        *reinterpret_cast<float4 *>(o + e0) = v;
-        return;
-    }
-    if (e0 + 0 < n) o[e0 + 0] = v.x;
-    if (e0 + 1 < n) o[e0 + 1] = v.y;
-    if (e0 + 2 < n) o[e0 + 2] = v.z;
-}
-
-// ------------------------------------------------------------------ power-of-two scaling
-// y = fl32(x * 2^k) with one rounding (ldexpf semantics, reading A8).  For
-// k in [-149, 127] 2^k is an exact fp32 (subnormal below -126) and a single
-// FMUL rounds once; outside, the product is formed exactly in fp64 and
-// rounded once to fp32.
-struct Pow2 {
-    float f;
-    double d;
-    bool wide;
-    __device__ __forceinline__ explicit Pow2(int k)
-    {
-        wide = (k < -149 || k > 127);
-        f = (k >= -126) ? __uint_as_float((uint32_t)(k + 127) << 23)
-                        : __uint_as_float(1u << ((k + 149) & 31));
-        d = __longlong_as_double((long long)(uint64_t)(min(max(k, -1022), 1023) + 1023) << 52);
-    }
-    __device__ __forceinline__ float apply(float x) const
-    {
-        return wide ? __double2float_rn((double)x * d) : __fmul_rn(x, f);
-    }
-    __device__ __forceinline__ float4 apply4(float4 v) const
-    {
-        return make_float4(apply(v.x), apply(v.y), apply(v.z), apply(v.w));
-    }
-};
-
-// ------------------------------------------------------------------ per-element 4-wide helpers
-template <class C>
-__device__ __forceinline__ uint32_t enc4_bytes(const C &c, float4 v)
-{
-    if constexpr (C::kVec4) {
-        return c.enc4(v);
-    } else {
-        return c.enc(v.x) | (c.enc(v.y) << 8) | (c.enc(v.z) << 16) | (c.enc(v.w) << 24);
-    }
-}
-
-template <class C>
-__device__ __forceinline__ float4 dec4_bytes(const C &c, uint32_t w)
-{
-    if constexpr (C::kVec4) {
-        return c.dec4(w);
-    } else {
-        return make_float4(c.dec(w & 0xffu), c.dec((w >> 8) & 0xffu), c.dec((w >> 16) & 0xffu),
-                           c.dec(w >> 24));
-    }
-}
-
-// packed group of 4 codes for the direct widths
-template <int B> struct Word4;
-template <> struct Word4<8> { using T = uint32_t; };
-template <> struct Word4<16> { using T = uint2; };
-template <> struct Word4<32> { using T = uint4; };
-
-template <int B, class C>
-__device__ __forceinline__ typename Word4<B>::T pack4(const C &c, float4 v)
-{
-    if constexpr (B == 8) {
-        return enc4_bytes(c, v);
-    } else if constexpr (B == 16) {
-        return make_uint2(c.enc(v.x) | (c.enc(v.y) << 16), c.enc(v.z) | (c.enc(v.w) << 16));
-    } else {
-        return make_uint4(c.enc(v.x), c.enc(v.y), c.enc(v.z), c.enc(v.w));
-    }
-}
-
-template <int B, class C>
-__device__ __forceinline__ float4 unpack4(const C &c, typename Word4<B>::T w)
-{
-    if constexpr (B == 8) {
-        return dec4_bytes(c, w);
-    } else if constexpr (B == 16) {
-        return make_float4(c.dec(w.x & 0xffffu), c.dec(w.x >> 16), c.dec(w.y & 0xffffu),
-                           c.dec(w.y >> 16));
-    } else {
-        return make_float4(c.dec(w.x), c.dec(w.y), c.dec(w.z), c.dec(w.w));
-    }
-}
-
-// ------------------------------------------------------------------ generic-width tile packing
-// Tile = 128 codes = 4*b words.  Word w holds bits [32w, 32w+32) of the
-// LSB-first code stream.
-__device__ __forceinline__ uint32_t assemble_word(const uint32_t *codes, int w, int b)
-{
-    const int bit0 = w * 32;
-    int k = bit0 / b;
-    const int off = bit0 - k * b;
-    uint64_t acc = (uint64_t)codes[k] >> off;
-    int have = b - off;
-    ++k;
-    while (have < 32 && k < kTile) {
-        acc |= (uint64_t)codes[k] << have;
-        have += b;
-        ++k;
-    }
-    return (uint32_t)acc;
-}
-
-// code k of a tile whose words are in shared memory (words[4b] is a zero pad)
-__device__ __forceinline__ uint32_t extract_code(const uint32_t *words, int k, int b)
-{
-    const int bit = k * b;
-    const int w = bit >> 5;
-    const int sh = bit & 31;
-    const uint32_t v = __funnelshift_r(words[w], words[w + 1], sh);
-    return b == 32 ? v : (v & ((1u << b) - 1u));
-}
-
-// ------------------------------------------------------------------ a1: absmax + local exponent
-__device__ __forceinline__ uint32_t absbits4(float4 v)
-{
-    const uint32_t a = max(__float_as_uint(v.x) & 0x7fffffffu, __float_as_uint(v.y) & 0x7fffffffu);
-    const uint32_t b = max(__float_as_uint(v.z) & 0x7fffffffu, __float_as_uint(v.w) & 0x7fffffffu);
-    return max(a, b);
-}
-
-// E = ceil(log2(N * A)) exactly (N*A is exact in binary64); sentinels for
-// an all-zero layer (A3) and non-finite input (A4).  The abs bits of fp32
-// are monotone in |x|, so the max is order-independent and bit-exact.
-__device__ __forceinline__ int32_t exponent_of(uint32_t abits, int N)
-{
-    if (abits == 0u) return INT32_MIN;
-    if (abits >= 0x7f800000u) return INT32_MAX;
-    const double d = (double)__uint_as_float(abits) * (double)N;
-    const uint64_t bits = (uint64_t)__double_as_longlong(d);
-    const int k = (int)(bits >> 52) - 1023;       // d in [2^k, 2^(k+1))
-    return (bits & ((1ull << 52) - 1ull)) ? k + 1 : k;
-}
 
 template <int NT>
 __global__ void __launch_bounds__(NT) absmax_exp_kernel(DevTables t, int N)
@@ -286,19 +61,6 @@ __global__ void __launch_bounds__(NT) absmax_exp_kernel(DevTables t, int N)
             }
         }
     }
-}
-
-// ------------------------------------------------------------------ a3+a4: scale, cast, pack
-__device__ __forceinline__ int scale_exponent(const DevTables &t, int layer, int bias, bool lead)
-{
-    const int32_t E = t.E_glob[layer];
-    int ft = (E == INT32_MIN) ? 0 : bias - E;   // f~ = upper_bound_exp - E (Alg. 1)
-    if (E == INT32_MAX) {                        // non-finite somewhere: flag (A4)
-        ft = 0;
-        if (lead) atomicOr(t.flag, 1u);
-    }
-    if (lead) t.ftilde[layer] = ft;
-    return ft;
 }
 
 // direct widths 8/16/32: group of 4 fp32 -> one 4-code word group
@@ -364,32 +126,6 @@ __global__ void __launch_bounds__(NT) quant_pack_tile_kernel(DevTables t, C c, i
         __syncwarp();
     }
 }
-
-// ------------------------------------------------------------------ a7: unpack, unscale, average
-struct Unscale {
-    Pow2 s;
-    bool div;       // non-power-of-two N: IEEE division
-    float inv_n;    // 2^-log2(N) for power-of-two N
-    float n_f;
-    bool average;
-    __device__ __forceinline__ Unscale(int ft, int N, int avg) : s(-ft)
-    {
-        average = avg != 0;
-        div = (N & (N - 1)) != 0;
-        n_f = (float)N;
-        inv_n = div ? 1.f : __uint_as_float((uint32_t)(127 - (31 - __clz(N))) << 23);
-    }
-    __device__ __forceinline__ float apply(float v) const
-    {
-        float x = s.apply(v);
-        if (average) x = div ? __fdiv_rn(x, n_f) : __fmul_rn(x, inv_n);
-        return x;
-    }
-    __device__ __forceinline__ float4 apply4(float4 v) const
-    {
-        return make_float4(apply(v.x), apply(v.y), apply(v.z), apply(v.w));
-    }
-};
 
 template <int B, class C, int NT>
 __global__ void __launch_bounds__(NT) unpack_unscale_direct_kernel(DevTables t, C c, int N, int avg)
@@ -530,27 +266,7 @@ __global__ void debug_decode_kernel(const uint32_t *codes, float *out, int64_t n
         out[i] = c.dec_any(codes[i]);
 }
 
-// ------------------------------------------------------------------ dispatch
-// Calls f(codec) with the compiled specialisation for the config formats,
-// the hardware fp8 codec when requested, else the runtime codec.
-template <class F>
-cudaError_t with_codec(int e, int m, bool hw, F &&f)
-{
-    if (hw && e == 5 && m == 2) return f(CHw<false>{});
-    if (hw && e == 4 && m == 3) return f(CHw<true>{});
-    if (e == 5 && m == 2) return f(CGen<5, 2>{});
-    if (e == 4 && m == 3) return f(CGen<4, 3>{});
-    if (e == 3 && m == 0) return f(CGen<3, 0>{});
-    if (e == 5 && m == 6) return f(CGen<5, 6>{});
-    if (e == 5 && m == 10) return f(CGen<5, 10>{});
-    if (e == 8 && m == 7) return f(CGen<8, 7>{});
-    if (e == 8 && m == 23) return f(CGen<8, 23>{});
-    CRt c;
-    c.F = make_fmt(e, m);
-    return f(c);
-}
-
-static int sm_count()
+int sm_count()
 {
     static int n = 0;
     if (!n) {

@@ -30,11 +30,19 @@ def _to_dev(grads):
     return [[torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in r] for r in grads]
 
 
-def run_gpu(aps, grads, e, m, hw, average=1):
-    """Returns (ftilde, packed per rank (after quantize), reduced, outputs) from the GPU."""
+def run_gpu(aps, grads, e, m, hw, average=1, fused=False):
+    """Returns (ftilde, packed per rank (after quantize), reduced, outputs) from the GPU.
+    fused: p = 1 through aps_sync_out (one fused launch) instead of the four calls."""
     p = len(grads)
     numels = [a.size for a in grads[0]]
     dev = _to_dev(grads)
+    if p == 1 and fused:
+        ctx = aps.ApsContext(e, m, numels, hw_convert=hw)
+        outs = [torch.empty_like(t) for t in dev[0]]
+        ctx.sync_out(dev[0], outs, average=bool(average))
+        assert ctx.status_sync() == 0
+        packed = ctx.packed().cpu().numpy()
+        return ctx.scales(), [packed], packed, [o.cpu().numpy() for o in outs], [ctx]
     if p == 1:
         ctx = aps.ApsContext(e, m, numels, hw_convert=hw)
         ctx.layer_scales(dev[0])
@@ -66,10 +74,10 @@ def run_gpu(aps, grads, e, m, hw, average=1):
     return ctxs[0].scales(), packed, reduced[0], outs[0], ctxs
 
 
-def check(aps, orc, grads, e, m, hw, average=1):
-    ref = orc.aps_sync(grads, e, m, average=average)
+def check(aps, orc, grads, e, m, hw, average=1, fused=False, ref=None):
+    ref = ref or orc.aps_sync(grads, e, m, average=average)
     assert ref.rc == 0
-    ft, packed, reduced, outs, _ = run_gpu(aps, grads, e, m, hw, average)
+    ft, packed, reduced, outs, _ = run_gpu(aps, grads, e, m, hw, average, fused)
     assert np.array_equal(ft, ref.ftilde), "f~ differs"
     for r in range(len(grads)):
         if not np.array_equal(packed[r], ref.packed[r]):
@@ -86,28 +94,61 @@ def check(aps, orc, grads, e, m, hw, average=1):
 
 # ----------------------------------------------------------------- p = 1
 
+@pytest.fixture(params=["stream", "simple"])
+def engine(request, monkeypatch):
+    """libaps kernel engine: persistent TMA-bulk kernels, or the simple grid kernels."""
+    monkeypatch.setenv("APS_ENGINE", request.param)
+    return request.param
+
+
+@pytest.mark.parametrize("fused", [True, False], ids=["fused", "calls"])
 @pytest.mark.parametrize("fmt,hw", FORMATS, ids=FMT_IDS)
-def test_p1_c1_and_edges(aps, orc, fmt, hw):
+def test_p1_c1_and_edges(aps, orc, fmt, hw, fused, engine):
     e, m = fmt
-    grads = synthetic.make_grads(synthetic.C1_NUMELS + [1000, 1, 9408, 130], 1)
-    check(aps, orc, grads, e, m, hw)
-    check(aps, orc, synthetic.edge_case_layers(1), e, m, hw, average=0)
+    grads = synthetic.make_grads(synthetic.C1_NUMELS + [1000, 1, 9408, 130, 8195, 16387], 1)
+    check(aps, orc, grads, e, m, hw, fused=fused)
+    check(aps, orc, synthetic.edge_case_layers(1), e, m, hw, average=0, fused=fused)
 
 
 @pytest.mark.parametrize("fmt,hw", [((5, 2), True), ((5, 2), False), ((3, 0), False), ((5, 6), False),
                                     ((5, 10), False), ((4, 3), True)], ids=lambda x: str(x))
 def test_p1_resnet50_full(aps, orc, fmt, hw):
-    """Config 2 at N = 1 (the bench workload): 161 tensors, 25,557,032 elements."""
+    """Config 2 at N = 1 (the bench workload, bench's launch configuration:
+    the fused single launch), 161 tensors, 25,557,032 elements; also the
+    four separate calls."""
     e, m = fmt
     grads = synthetic.make_grads(synthetic.RESNET50_NUMELS, 1)
-    check(aps, orc, grads, e, m, hw)
+    ref = orc.aps_sync(grads, e, m, average=1)
+    check(aps, orc, grads, e, m, hw, fused=True, ref=ref)
+    check(aps, orc, grads, e, m, hw, fused=False, ref=ref)
+
+
+def test_p1_fused_repeated_and_inplace(aps, orc):
+    """The generation-stamped fused launch: many syncs in a row (fresh data
+    each time, alternating in-place and out-of-place) stay bit-exact."""
+    numels = synthetic.C1_NUMELS + [77, 9408]
+    ctx = aps.ApsContext(5, 2, numels)
+    for it in range(6):
+        grads = synthetic.make_grads(numels, 1, seed=synthetic.SEED + 100 + it)
+        ref = orc.aps_sync(grads, 5, 2)
+        g = [torch.from_numpy(a).cuda() for a in grads[0]]
+        if it % 2:
+            ctx.sync(g)
+            out = g
+        else:
+            out = [torch.empty_like(t) for t in g]
+            ctx.sync_out(g, out)
+        assert ctx.status_sync() == 0
+        assert np.array_equal(ctx.scales(), ref.ftilde)
+        for a, b in zip(out, ref.out):
+            assert np.array_equal(a.cpu().numpy().view(np.uint32), b.view(np.uint32))
 
 
 # ----------------------------------------------------------------- simulated ranks
 
 @pytest.mark.parametrize("p", [2, 3, 4, 8])
 @pytest.mark.parametrize("fmt,hw", FORMATS, ids=FMT_IDS)
-def test_sim_c1(aps, orc, fmt, hw, p):
+def test_sim_c1(aps, orc, fmt, hw, p, engine):
     """Config 1 (4K/64K/256K layers) plus ragged layers, p simulated ranks."""
     e, m = fmt
     grads = synthetic.make_grads(synthetic.C1_NUMELS + [1000, 1, 130], p)
