@@ -2,33 +2,40 @@
 // APS kernels for sm_100a.
 //
 // Every hot kernel of the path streams each gradient element through the SM
-// once per pass (4 B read, b/8 B written, or the reverse), so it is bound by
-// HBM bandwidth, and short (~20 us at ResNet-50 size): CTA launch ramp and
-// tail matter as much as steady-state bandwidth.  The engine therefore runs
-// ONE persistent CTA per SM:
-//   warp 8 (producer, one elected lane): for each work item assigned to the
-//     CTA (static round-robin), waits for a free stage, arms the stage's
-//     mbarrier with the byte count and issues one cp.async.bulk
-//     global->shared copy (the TMA bulk-copy engine; up to 32 KB per item),
-//     with an L2 eviction-priority hint;
-//   warps 0..7 (consumers): wait on the stage's mbarrier, compute from shared
-//     memory, write results with coalesced 128-bit stores, and release the
-//     stage.
-// Six 32 KB stages give 192 KB in flight per SM (~28 MB chip-wide), far
-// above the bandwidth-latency product, with no registers tied up in loads.
+// once per pass, so it is bound by HBM bandwidth, and short (~20 us at
+// ResNet-50 size): CTA launch ramp and tail matter as much as steady-state
+// bandwidth.  The engine runs ONE persistent CTA per SM with three roles:
+//
+//   producer (warp 8, one lane): per work item (static round-robin over the
+//     CTAs) waits for a free stage, resolves the item's side information
+//     (f~ of its layer -- the global/acquire loads happen here, kStages
+//     items ahead of the consumers), arms the stage's `full` mbarrier with
+//     the byte count and issues one cp.async.bulk global->shared copy (TMA
+//     bulk engine, <= 32 KB, L2 eviction-priority hint);
+//   consumers (warps 0..7): wait `full`, each warp transforms a contiguous
+//     1024-element chunk in shared memory (results written in place or into
+//     the stage's code area), then its lane 0 writes the chunk back with
+//     cp.async.bulk shared->global stores, waits until the stage has been
+//     read, and arrives on `done`;
+//   finisher (warp 9, one lane): waits `done`, does the per-item global
+//     bookkeeping that needs fences/atomics (abs-max combine, last-item
+//     detection, publishing E_l) and frees the stage (`empty`).
+// No register is tied up in loads or stores, the per-item latency of fences
+// and atomics is off the consumers' path, and loads/stores are issued by the
+// bulk-copy engine.
 //
 // Fused p = 1 path (launch_stream_fused_p1): with one rank there is no
 // collective between FindMaxExp and Cast, so a single launch does
-//   phase A  abs-max of every work item (forward order; L2 evict_last hint),
-//            the last item of a layer publishes E_l with a release store of
-//            the call's generation stamp;
-//   phase B  per item, in REVERSE order: wait (acquire) for E_l, then
-//            f~, scale, Cast, pack (codes to the packed buffer) and
-//            Cast back, unscale, average -> fp32 output.
+//   phase A  abs-max of every work item (forward order; L2 evict_last hint);
+//            the finisher of a layer's last item publishes E_l with a
+//            release store of the call's generation stamp;
+//   phase B  per item, in REVERSE order: the producer waits (acquire) for
+//            E_l, then the consumers scale, Cast, pack (codes -> packed
+//            buffer) and Cast back, unscale, average (fp32 -> output).
 // Reverse order makes the second read of the gradients hit the data phase A
-// left in the 126 MB L2 most recently.  Every CTA finishes all of its phase A
-// items before its first phase B item and the grid is co-resident
-// (cooperative launch), so the waits cannot deadlock.
+// left in the 126 MB L2 most recently.  Every producer issues all of its
+// phase A items before its first phase B wait, and phase A items never wait,
+// so with a co-resident grid (cooperative launch) the waits cannot deadlock.
 #include <cstdint>
 #include <algorithm>
 #include <climits>
@@ -37,18 +44,29 @@
 
 namespace aps {
 
-constexpr int kStageBytes = kItemTiles * kTile * 4;  // 32 KB: one work item of fp32
-constexpr int kStages = 6;
+constexpr int kF32Bytes = kItemTiles * kTile * 4;  // 32 KB: one work item of fp32
 constexpr int kConsWarps = 8;
-constexpr int kConsThreads = kConsWarps * 32;
-constexpr int kStreamThreads = kConsThreads + 32;
+constexpr int kChunk = kItemTiles * kTile / kConsWarps;  // 1024 elements per consumer warp
+constexpr int kStreamThreads = (kConsWarps + 2) * 32;
+constexpr int kSmemBudget = 200 * 1024;
 
+template <int CodeBytes>
+struct StageCfg {
+    static constexpr int kStageBytes = kF32Bytes + CodeBytes;
+    static constexpr int kStages = std::min(8, kSmemBudget / kStageBytes);
+};
+
+struct StageInfo {
+    int ft;  // f~ of the item's layer (quantise / fused phase B)
+};
+
+template <int Stages, int StageBytes>
 struct StreamSmem {
-    alignas(128) uint8_t stage[kStages][kStageBytes];
-    alignas(8) uint64_t full[kStages];
-    uint64_t empty[kStages];
-    uint32_t red[2][kConsWarps];
-    int32_t bcast[2];
+    alignas(1024) uint8_t stage[Stages][StageBytes];
+    uint32_t scratch[kConsWarps][kTile];  // per-warp code tile (generic widths)
+    uint64_t full[Stages], done[Stages], empty[Stages];
+    uint32_t part[Stages][kConsWarps];
+    StageInfo info[Stages];
 };
 
 // ------------------------------------------------------------------ PTX wrappers
@@ -108,13 +126,19 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
         ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
         : "memory");
 }
+// TMA bulk copy shared -> global (bulk async-group completion).
+__device__ __forceinline__ void bulk_s2g(void *dst, const void *src, uint32_t bytes)
+{
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_smem()
 {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void bar_consumers()
-{
-    asm volatile("bar.sync 1, %0;" ::"n"(kConsThreads) : "memory");
 }
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t *p)
 {
@@ -129,53 +153,10 @@ __device__ __forceinline__ void st_release(uint32_t *p, uint32_t v)
 
 struct Load {
     const void *src;
-    uint32_t bytes;  // multiple of 16
-    bool keep;       // L2 evict_last (data will be read again) vs evict_first
+    uint32_t bytes;     // multiple of 16
+    uint32_t dst_off;   // byte offset within the stage
+    bool keep;          // L2 evict_last (data will be read again) vs evict_first
 };
-
-// ------------------------------------------------------------------ the engine
-template <class Op>
-__global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const Op op)
-{
-    extern __shared__ __align__(128) uint8_t smem_raw[];
-    StreamSmem &S = *reinterpret_cast<StreamSmem *>(smem_raw);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(&S.full[s], 1);
-            mbar_init(&S.empty[s], kConsWarps);
-        }
-        fence_mbarrier_init();
-    }
-    __syncthreads();
-    const int nw = op.n_work();
-    if (warp == kConsWarps) {  // ---------------- producer
-        if (lane == 0) {
-            const uint64_t keep = policy_evict_last(), stream = policy_evict_first();
-            int i = 0;
-            for (int w = blockIdx.x; w < nw; w += gridDim.x, ++i) {
-                const int s = i % kStages;
-                const uint32_t ph = (uint32_t)(i / kStages) & 1u;
-                mbar_wait(&S.empty[s], ph ^ 1u);
-                const Load ld = op.load(w);
-                mbar_arrive_expect_tx(&S.full[s], ld.bytes);
-                if (ld.bytes) bulk_g2s(S.stage[s], ld.src, ld.bytes, &S.full[s], ld.keep ? keep : stream);
-            }
-        }
-        return;
-    }
-    // ---------------- consumers
-    int i = 0;
-    for (int w = blockIdx.x; w < nw; w += gridDim.x, ++i) {
-        const int s = i % kStages;
-        const uint32_t ph = (uint32_t)(i / kStages) & 1u;
-        mbar_wait(&S.full[s], ph);
-        op.process(w, S.stage[s], S, i);
-        if (Op::kWritesStage) fence_proxy_async_smem();  // generic writes before the next TMA write
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&S.empty[s]);
-    }
-}
 
 // ------------------------------------------------------------------ item helpers
 struct ItemView {
@@ -198,14 +179,14 @@ __device__ __forceinline__ ItemView view(const DevTables &t, int k)
 __device__ __forceinline__ Load grad_load(const DevTables &t, int k, bool keep)
 {
     const ItemView v = view(t, k);
-    return Load{t.src[v.it.layer] + v.begin, (uint32_t)(v.cnt >> 2) * 16u, keep};
+    return Load{t.src[v.it.layer] + v.begin, (uint32_t)(v.cnt >> 2) * 16u, 0u, keep};
 }
 
 // fp32 group j (elements 4j..4j+3) of an item: from the stage when it was
 // bulk-copied, else (the < 4-element tail of a layer) from global memory.
-__device__ __forceinline__ float4 stage_group(const uint8_t *stage, const float *g, int j, int cnt)
+__device__ __forceinline__ float4 stage_group(const float4 *s4, const float *g, int j, int cnt)
 {
-    if (4 * j + 4 <= cnt) return reinterpret_cast<const float4 *>(stage)[j];
+    if (4 * j + 4 <= cnt) return s4[j];
     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
     const int e0 = 4 * j;
     if (e0 + 0 < cnt) v.x = g[e0 + 0];
@@ -214,226 +195,326 @@ __device__ __forceinline__ float4 stage_group(const uint8_t *stage, const float 
     return v;
 }
 
-// a1: abs-max of the item, combined per layer; the last item of a layer
-// writes E_l (and, when gen != 0, publishes it with a release store).
-__device__ __forceinline__ void absmax_consume(const DevTables &t, int N, const ItemView &v, const uint8_t *stage,
-                                               StreamSmem &S, int i, uint32_t gen)
+// Store the warp's chunk of fp32 results (in the stage) to out[], the < 4
+// element tail with plain stores.  elems0: first element of the chunk.
+__device__ __forceinline__ void store_chunk_f32(float *out, const float4 *s4, int elems0, int cnt, int lane)
 {
-    const int n4 = v.cnt >> 2;
-    const float4 *s4 = reinterpret_cast<const float4 *>(stage);
-    uint32_t mx = 0;
-#pragma unroll 8
-    for (int j = threadIdx.x; j < n4; j += kConsThreads) mx = max(mx, absbits4(s4[j]));
-    if ((int)threadIdx.x < (v.cnt & 3))
-        mx = max(mx, __float_as_uint(t.src[v.it.layer][v.begin + 4 * n4 + threadIdx.x]) & 0x7fffffffu);
-    mx = __reduce_max_sync(0xffffffffu, mx);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (lane == 0) S.red[i & 1][warp] = mx;
-    bar_consumers();
-    if (threadIdx.x == 0) {
-        uint32_t m = 0;
+    const int n = min(kChunk, cnt - elems0);
+    if (n <= 0) return;
+    const int n16 = n & ~3;
+    if (lane == 0 && n16) bulk_s2g(out + elems0, s4 + elems0 / 4, (uint32_t)n16 * 4u);
+    if (lane < (n & 3)) {
+        const float *sf = reinterpret_cast<const float *>(s4);
+        out[elems0 + n16 + lane] = sf[elems0 + n16 + lane];
+    }
+}
+
+// f~ of the item's layer, resolved by the producer (ftilde[] / flag written
+// by the producer that handles the layer's first item).
+__device__ __forceinline__ int producer_ftilde(const DevTables &t, const ItemView &v, int bias, uint32_t gen)
+{
+    if (gen)
+        while (ld_acquire(&t.ready[v.it.layer]) != gen) __nanosleep(32);
+    return scale_exponent(t, v.it.layer, bias, v.it.tile_begin == 0);
+}
+
+// finisher side of a1: combine the item's abs-max into the layer; the last
+// item of the layer writes E_l (and publishes it when gen != 0).
+__device__ __forceinline__ void absmax_finish(const DevTables &t, int N, int k, const uint32_t *part, uint32_t gen)
+{
+    const Item it = t.items[k];
+    uint32_t m = 0;
 #pragma unroll
-        for (int k = 0; k < kConsWarps; ++k) m = max(m, S.red[i & 1][k]);
-        const int l = v.it.layer;
-        atomicMax(&t.amax[l], m);
+    for (int w = 0; w < kConsWarps; ++w) m = max(m, part[w]);
+    const int l = it.layer;
+    atomicMax(&t.amax[l], m);
+    __threadfence();
+    const uint32_t done = atomicAdd(&t.count[l], 1u);
+    if (done == (uint32_t)t.layers[l].n_items - 1u) {
         __threadfence();
-        const uint32_t done = atomicAdd(&t.count[l], 1u);
-        if (done == (uint32_t)v.L.n_items - 1u) {
+        const uint32_t A = atomicExch(&t.amax[l], 0u);
+        t.count[l] = 0u;
+        t.E_local[l] = exponent_of(A, N);
+        if (gen) {
             __threadfence();
-            const uint32_t A = atomicExch(&t.amax[l], 0u);
-            t.count[l] = 0u;
-            t.E_local[l] = exponent_of(A, N);
-            if (gen) {
-                __threadfence();
-                st_release(&t.ready[l], gen);
+            st_release(&t.ready[l], gen);
+        }
+    }
+}
+
+// consumer side of a1: the warp's abs-max over its chunk
+__device__ __forceinline__ uint32_t absmax_chunk(const DevTables &t, const ItemView &v, const float4 *s4, int warp,
+                                                 int lane)
+{
+    uint32_t mx = 0;
+    const int g0 = warp * (kChunk / 4);
+    const int n4 = v.cnt >> 2;
+#pragma unroll
+    for (int k = 0; k < kChunk / 4 / 32; ++k) {
+        const int j = g0 + lane + 32 * k;
+        if (j < n4) mx = max(mx, absbits4(s4[j]));
+    }
+    if (warp == kConsWarps - 1 && lane < (v.cnt & 3))
+        mx = max(mx, __float_as_uint(t.src[v.it.layer][v.begin + 4 * n4 + lane]) & 0x7fffffffu);
+    return __reduce_max_sync(0xffffffffu, mx);
+}
+
+// consumer side of a3/a4 (+ a7 when Fuse) for the warp's chunk.
+// Codes go to `codes` (the stage's code area, bulk-stored to the packed
+// buffer); with Fuse the unscaled fp32 result overwrites the stage in place
+// and is bulk-stored to the output.
+template <class C, bool Fuse>
+__device__ __forceinline__ void quant_chunk(const DevTables &t, const C &c, const ItemView &v, uint8_t *stage,
+                                            uint8_t *codes, uint32_t *scratch, int ft, int avg, int warp, int lane)
+{
+    constexpr int B = C::kB;
+    float4 *s4 = reinterpret_cast<float4 *>(stage);
+    const float *g = t.src[v.it.layer] + v.begin;
+    const Pow2 s(ft);
+    const Unscale us(ft, 1, avg);
+    const int g0 = warp * (kChunk / 4);
+    const int tiles_w = min(kChunk / kTile, v.it.n_tiles - warp * (kChunk / kTile));  // tiles in this chunk
+    if (tiles_w <= 0) return;
+    if constexpr (B == 8 || B == 16 || B == 32) {
+        using W = typename Word4<B>::T;
+        W *cw = reinterpret_cast<W *>(codes);
+#pragma unroll
+        for (int k = 0; k < kChunk / 4 / 32; ++k) {
+            const int j = g0 + lane + 32 * k;
+            if (j < v.it.n_tiles * (kTile / 4)) {
+                const float4 x = stage_group(s4, g, j, v.cnt);
+                const W code = pack4<B>(c, s.apply4(x));
+                cw[j] = code;
+                if (Fuse) s4[j] = us.apply4(unpack4<B>(c, code));
             }
         }
+    } else {
+        const int b = B;
+        uint32_t *cw = reinterpret_cast<uint32_t *>(codes);
+        for (int tt = 0; tt < tiles_w; ++tt) {
+            const int j = g0 + tt * (kTile / 4) + lane;
+            const float4 y = s.apply4(stage_group(s4, g, j, v.cnt));
+            const uint4 cd = make_uint4(c.enc(y.x), c.enc(y.y), c.enc(y.z), c.enc(y.w));
+            __syncwarp();
+            *reinterpret_cast<uint4 *>(scratch + 4 * lane) = cd;
+            if (Fuse) s4[j] = us.apply4(make_float4(c.dec(cd.x), c.dec(cd.y), c.dec(cd.z), c.dec(cd.w)));
+            __syncwarp();
+            uint32_t *ow = cw + (int64_t)(warp * (kChunk / kTile) + tt) * (4 * b);
+            for (int w = lane; w < 4 * b; w += 32) ow[w] = assemble_word(scratch, w, b);
+        }
     }
+    fence_proxy_async_smem();
+    __syncwarp();
+    const int64_t tile0 = v.L.tile_off + v.it.tile_begin + warp * (kChunk / kTile);
+    if (lane == 0)
+        bulk_s2g(t.packed + tile0 * (16 * B), codes + (size_t)warp * (kChunk / kTile) * (16 * B),
+                 (uint32_t)(tiles_w * 16 * B));
+    if (Fuse) store_chunk_f32(t.dst[v.it.layer] + v.begin, s4, warp * kChunk, v.cnt, lane);
 }
 
-// a3+a4 (+ a7 when Fuse): scale, Cast, pack; optionally Cast back, unscale
-template <int B, class C, bool Fuse>
-__device__ __forceinline__ void quant_consume_direct(const DevTables &t, const C &c, const ItemView &v,
-                                                     const uint8_t *stage, int ft, int N, int avg)
+// consumer side of a7 for the warp's chunk: codes (loaded into the stage's
+// code area) -> fp32 in the stage -> bulk store.
+template <class C>
+__device__ __forceinline__ void unpack_chunk(const DevTables &t, const C &c, const ItemView &v, uint8_t *stage,
+                                             const uint8_t *codes, int N, int avg, int warp, int lane)
 {
-    using W = typename Word4<B>::T;
-    W *out = reinterpret_cast<W *>(t.packed + (v.L.tile_off + v.it.tile_begin) * (16 * B));
-    const float *g = t.src[v.it.layer] + v.begin;
-    float *o = Fuse ? t.dst[v.it.layer] + v.begin : nullptr;
-    const Pow2 s(ft);
-    const Unscale us(ft, N, avg);
-    const int ng = v.it.n_tiles * (kTile / 4);
-    if (!s.wide) {
-#pragma unroll 4
-        for (int j = threadIdx.x; j < ng; j += kConsThreads) {
-            const float4 x = stage_group(stage, g, j, v.cnt);
-            const float4 y = make_float4(__fmul_rn(x.x, s.f), __fmul_rn(x.y, s.f), __fmul_rn(x.z, s.f),
-                                         __fmul_rn(x.w, s.f));
-            const W code = pack4<B>(c, y);
-            out[j] = code;
-            if (Fuse) store_group(o, 4 * j, v.cnt, us.apply4(unpack4<B>(c, code)));
+    constexpr int B = C::kB;
+    float4 *s4 = reinterpret_cast<float4 *>(stage);
+    const Unscale us(t.ftilde[v.it.layer], N, avg);
+    const int g0 = warp * (kChunk / 4);
+    const int tiles_w = min(kChunk / kTile, v.it.n_tiles - warp * (kChunk / kTile));
+    if (tiles_w <= 0) return;
+    if constexpr (B == 8 || B == 16 || B == 32) {
+        using W = typename Word4<B>::T;
+        const W *cw = reinterpret_cast<const W *>(codes);
+#pragma unroll
+        for (int k = 0; k < kChunk / 4 / 32; ++k) {
+            const int j = g0 + lane + 32 * k;
+            if (j < v.it.n_tiles * (kTile / 4)) s4[j] = us.apply4(unpack4<B>(c, cw[j]));
         }
     } else {
-        for (int j = threadIdx.x; j < ng; j += kConsThreads) {
-            const W code = pack4<B>(c, s.apply4(stage_group(stage, g, j, v.cnt)));
-            out[j] = code;
-            if (Fuse) store_group(o, 4 * j, v.cnt, us.apply4(unpack4<B>(c, code)));
+        const int b = B;
+        const uint32_t *cw = reinterpret_cast<const uint32_t *>(codes);
+        for (int tt = 0; tt < tiles_w; ++tt) {
+            const uint32_t *words = cw + (int64_t)(warp * (kChunk / kTile) + tt) * (4 * b);  // words[4b]: masked
+            const int k0 = lane * 4;
+            const float4 d = make_float4(c.dec(extract_code(words, k0, b)), c.dec(extract_code(words, k0 + 1, b)),
+                                         c.dec(extract_code(words, k0 + 2, b)), c.dec(extract_code(words, k0 + 3, b)));
+            s4[g0 + tt * (kTile / 4) + lane] = us.apply4(d);
         }
     }
-}
-
-template <class C, bool Fuse>
-__device__ __forceinline__ void quant_consume_tile(const DevTables &t, const C &c, const ItemView &v,
-                                                   uint8_t *stage, int ft, int N, int avg)
-{
-    const int b = c.b();
-    uint32_t *out = reinterpret_cast<uint32_t *>(t.packed) + (v.L.tile_off + v.it.tile_begin) * (4 * b);
-    const float *g = t.src[v.it.layer] + v.begin;
-    float *o = Fuse ? t.dst[v.it.layer] + v.begin : nullptr;
-    const Pow2 s(ft);
-    const Unscale us(ft, N, avg);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint32_t *codes_all = reinterpret_cast<uint32_t *>(stage);
-    for (int tt = warp; tt < v.it.n_tiles; tt += kConsWarps) {
-        const int j = tt * (kTile / 4) + lane;
-        const float4 y = s.apply4(stage_group(stage, g, j, v.cnt));
-        const uint4 cd = make_uint4(c.enc(y.x), c.enc(y.y), c.enc(y.z), c.enc(y.w));
-        uint32_t *codes = codes_all + tt * kTile;  // in place over the tile's fp32
-        __syncwarp();
-        *reinterpret_cast<uint4 *>(codes + 4 * lane) = cd;
-        __syncwarp();
-        uint32_t *ow = out + (int64_t)tt * (4 * b);
-        for (int w = lane; w < 4 * b; w += 32) ow[w] = assemble_word(codes, w, b);
-        if (Fuse) {
-            const float4 d = make_float4(c.dec(cd.x), c.dec(cd.y), c.dec(cd.z), c.dec(cd.w));
-            store_group(o, 4 * j, v.cnt, us.apply4(d));
-        }
-    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    store_chunk_f32(t.dst[v.it.layer] + v.begin, s4, warp * kChunk, v.cnt, lane);
 }
 
 // ------------------------------------------------------------------ ops
+// An Op provides: kCodeBytes (stage code area), n_work(), produce(w, info)
+// -> Load, consume(w, stage, info, scratch, warp, lane) -> partial, and
+// finish(w, partials).
 struct AbsmaxOp {
-    static constexpr bool kWritesStage = false;
+    static constexpr int kCodeBytes = 0;
     DevTables t;
     int N;
     __device__ int n_work() const { return t.n_items; }
-    __device__ Load load(int w) const { return grad_load(t, w, true); }
-    __device__ void process(int w, uint8_t *stage, StreamSmem &S, int i) const
+    __device__ Load produce(int w, StageInfo &) const { return grad_load(t, w, true); }
+    __device__ uint32_t consume(int w, uint8_t *stage, const StageInfo &, uint32_t *, int warp, int lane) const
     {
-        absmax_consume(t, N, view(t, w), stage, S, i, 0u);
+        return absmax_chunk(t, view(t, w), reinterpret_cast<const float4 *>(stage), warp, lane);
     }
+    __device__ void finish(int w, const uint32_t *part) const { absmax_finish(t, N, w, part, 0u); }
 };
-
-// f~ of a layer (Alg. 1 line 4) from the final E, broadcast to the consumers
-__device__ __forceinline__ int layer_ftilde(const DevTables &t, const ItemView &v, int bias, StreamSmem &S, int i,
-                                            uint32_t gen)
-{
-    if (threadIdx.x == 0) {
-        if (gen)
-            while (ld_acquire(&t.ready[v.it.layer]) != gen) __nanosleep(32);
-        S.bcast[i & 1] = scale_exponent(t, v.it.layer, bias, v.it.tile_begin == 0);
-    }
-    bar_consumers();
-    return S.bcast[i & 1];
-}
 
 template <class C>
 struct QuantOp {
-    static constexpr bool kWritesStage = !(C::kB == 8 || C::kB == 16 || C::kB == 32);
+    static constexpr int kCodeBytes = kItemTiles * 16 * C::kB;
     DevTables t;
     C c;
     int bias;
-    // reverse order: the items phase a1 read last are still in L2
+    // reverse order: the items a1 read last are still in L2
     __device__ int n_work() const { return t.n_items; }
     __device__ int item(int w) const { return t.n_items - 1 - w; }
-    __device__ Load load(int w) const { return grad_load(t, item(w), false); }
-    __device__ void process(int w, uint8_t *stage, StreamSmem &S, int i) const
+    __device__ Load produce(int w, StageInfo &info) const
     {
-        const ItemView v = view(t, item(w));
-        const int ft = layer_ftilde(t, v, bias, S, i, 0u);
-        if constexpr (C::kB == 8 || C::kB == 16 || C::kB == 32)
-            quant_consume_direct<C::kB, C, false>(t, c, v, stage, ft, 1, 0);
-        else
-            quant_consume_tile<C, false>(t, c, v, stage, ft, 1, 0);
+        info.ft = producer_ftilde(t, view(t, item(w)), bias, 0u);
+        return grad_load(t, item(w), false);
     }
+    __device__ uint32_t consume(int w, uint8_t *stage, const StageInfo &info, uint32_t *scratch, int warp,
+                                int lane) const
+    {
+        quant_chunk<C, false>(t, c, view(t, item(w)), stage, stage + kF32Bytes, scratch, info.ft, 0, warp, lane);
+        return 0u;
+    }
+    __device__ void finish(int, const uint32_t *) const {}
 };
 
 template <class C>
 struct UnpackOp {
-    static constexpr bool kWritesStage = false;
+    static constexpr int kCodeBytes = kItemTiles * 16 * C::kB;
     DevTables t;
     C c;
     int N, avg;
     __device__ int n_work() const { return t.n_items; }
-    __device__ Load load(int w) const
+    __device__ Load produce(int w, StageInfo &) const
     {
         const Item it = t.items[w];
         const LayerDev L = t.layers[it.layer];
-        const int b = c.b();
-        return Load{t.packed + (L.tile_off + it.tile_begin) * (16 * b), (uint32_t)(16 * b * it.n_tiles), false};
+        return Load{t.packed + (L.tile_off + it.tile_begin) * (16 * C::kB), (uint32_t)(16 * C::kB * it.n_tiles),
+                    (uint32_t)kF32Bytes, false};
     }
-    __device__ void process(int w, uint8_t *stage, StreamSmem &S, int i) const
+    __device__ uint32_t consume(int w, uint8_t *stage, const StageInfo &, uint32_t *, int warp, int lane) const
     {
-        const ItemView v = view(t, w);
-        const Unscale us(t.ftilde[v.it.layer], N, avg);
-        float *o = t.dst[v.it.layer] + v.begin;
-        if constexpr (C::kB == 8 || C::kB == 16 || C::kB == 32) {
-            using W = typename Word4<C::kB>::T;
-            const W *in = reinterpret_cast<const W *>(stage);
-            const int ng = (v.cnt + 3) >> 2;
-#pragma unroll 4
-            for (int j = threadIdx.x; j < ng; j += kConsThreads)
-                store_group(o, 4 * j, v.cnt, us.apply4(unpack4<C::kB>(c, in[j])));
-        } else {
-            const int b = c.b();
-            const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-            const uint32_t *words_all = reinterpret_cast<const uint32_t *>(stage);
-            for (int tt = warp; tt < v.it.n_tiles; tt += kConsWarps) {
-                const uint32_t *words = words_all + tt * (4 * b);  // words[4b] reads the next tile / pad: masked
-                const int k0 = lane * 4;
-                const float4 d = make_float4(c.dec(extract_code(words, k0, b)), c.dec(extract_code(words, k0 + 1, b)),
-                                             c.dec(extract_code(words, k0 + 2, b)),
-                                             c.dec(extract_code(words, k0 + 3, b)));
-                store_group(o, tt * kTile + k0, v.cnt, us.apply4(d));
-            }
-        }
+        unpack_chunk<C>(t, c, view(t, w), stage, stage + kF32Bytes, N, avg, warp, lane);
+        return 0u;
     }
+    __device__ void finish(int, const uint32_t *) const {}
 };
 
 template <class C>
 struct FusedP1Op {
-    static constexpr bool kWritesStage = !(C::kB == 8 || C::kB == 16 || C::kB == 32);
+    static constexpr int kCodeBytes = kItemTiles * 16 * C::kB;
     DevTables t;
     C c;
     int bias, avg;
     uint32_t gen;
     __device__ int n_work() const { return 2 * t.n_items; }
-    __device__ Load load(int w) const
+    __device__ int item_b(int w) const { return 2 * t.n_items - 1 - w; }
+    __device__ Load produce(int w, StageInfo &info) const
     {
-        return w < t.n_items ? grad_load(t, w, true) : grad_load(t, 2 * t.n_items - 1 - w, false);
+        if (w < t.n_items) return grad_load(t, w, true);
+        info.ft = producer_ftilde(t, view(t, item_b(w)), bias, gen);
+        return grad_load(t, item_b(w), false);
     }
-    __device__ void process(int w, uint8_t *stage, StreamSmem &S, int i) const
+    __device__ uint32_t consume(int w, uint8_t *stage, const StageInfo &info, uint32_t *scratch, int warp,
+                                int lane) const
     {
-        if (w < t.n_items) {
-            absmax_consume(t, 1, view(t, w), stage, S, i, gen);
-            return;
-        }
-        const ItemView v = view(t, 2 * t.n_items - 1 - w);
-        const int ft = layer_ftilde(t, v, bias, S, i, gen);
-        if constexpr (C::kB == 8 || C::kB == 16 || C::kB == 32)
-            quant_consume_direct<C::kB, C, true>(t, c, v, stage, ft, 1, avg);
-        else
-            quant_consume_tile<C, true>(t, c, v, stage, ft, 1, avg);
+        if (w < t.n_items)
+            return absmax_chunk(t, view(t, w), reinterpret_cast<const float4 *>(stage), warp, lane);
+        quant_chunk<C, true>(t, c, view(t, item_b(w)), stage, stage + kF32Bytes, scratch, info.ft, avg, warp, lane);
+        return 0u;
+    }
+    __device__ void finish(int w, const uint32_t *part) const
+    {
+        if (w < t.n_items) absmax_finish(t, 1, w, part, gen);
     }
 };
+
+// ------------------------------------------------------------------ the engine
+template <class Op>
+__global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const Op op)
+{
+    using Cfg = StageCfg<Op::kCodeBytes>;
+    using Smem = StreamSmem<Cfg::kStages, Cfg::kStageBytes>;
+    constexpr int NS = Cfg::kStages;
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    Smem &S = *reinterpret_cast<Smem *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(&S.full[s], 1);
+            mbar_init(&S.done[s], kConsWarps);
+            mbar_init(&S.empty[s], 1);
+        }
+        fence_mbarrier_init();
+    }
+    __syncthreads();
+    const int nw = op.n_work();
+    if (warp == kConsWarps) {  // ---------------- producer
+        if (lane == 0) {
+            const uint64_t keep = policy_evict_last(), stream = policy_evict_first();
+            int i = 0;
+            for (int w = blockIdx.x; w < nw; w += gridDim.x, ++i) {
+                const int s = i % NS;
+                const uint32_t ph = (uint32_t)(i / NS) & 1u;
+                mbar_wait(&S.empty[s], ph ^ 1u);
+                const Load ld = op.produce(w, S.info[s]);
+                mbar_arrive_expect_tx(&S.full[s], ld.bytes);
+                if (ld.bytes)
+                    bulk_g2s(S.stage[s] + ld.dst_off, ld.src, ld.bytes, &S.full[s], ld.keep ? keep : stream);
+            }
+        }
+        return;
+    }
+    if (warp == kConsWarps + 1) {  // ---------------- finisher
+        if (lane == 0) {
+            int i = 0;
+            for (int w = blockIdx.x; w < nw; w += gridDim.x, ++i) {
+                const int s = i % NS;
+                const uint32_t ph = (uint32_t)(i / NS) & 1u;
+                mbar_wait(&S.done[s], ph);
+                op.finish(w, S.part[s]);
+                mbar_arrive(&S.empty[s]);
+            }
+        }
+        return;
+    }
+    // ---------------- consumers
+    int i = 0;
+    for (int w = blockIdx.x; w < nw; w += gridDim.x, ++i) {
+        const int s = i % NS;
+        const uint32_t ph = (uint32_t)(i / NS) & 1u;
+        mbar_wait(&S.full[s], ph);
+        const uint32_t part = op.consume(w, S.stage[s], S.info[s], S.scratch[warp], warp, lane);
+        if (lane == 0) {
+            bulk_commit();
+            bulk_wait_read();  // the stage may be refilled once the bulk stores have read it
+            S.part[s][warp] = part;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.done[s]);
+    }
+    if (lane == 0) bulk_wait_all();
+}
 
 // ------------------------------------------------------------------ launch
 template <class Op>
 static cudaError_t launch_stream(const Op &op, int n_work, bool cooperative, cudaStream_t s)
 {
+    using Cfg = StageCfg<Op::kCodeBytes>;
+    using Smem = StreamSmem<Cfg::kStages, Cfg::kStageBytes>;
     static bool configured = false;
     static int blocks_per_sm = 1;
-    const size_t smem = sizeof(StreamSmem);
+    const size_t smem = sizeof(Smem) + 1024;  // + alignment slack
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(stream_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
