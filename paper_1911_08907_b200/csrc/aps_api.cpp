@@ -190,9 +190,13 @@ aps_status aps_init(aps_ctx **out, int exp_bits, int man_bits, int world_size, i
             it.layer = l;
             it.tile_begin = (int32_t)t0;
             it.n_tiles = (int32_t)std::min<int64_t>(aps::kItemTiles, T - t0);
+            it.cnt = (int32_t)std::min<int64_t>((int64_t)it.n_tiles * aps::kTile, numels[l] - t0 * aps::kTile);
+            it.tile_pos = toff + t0;
             c->items.push_back(it);
             ++L.n_items;
         }
+        for (size_t k = c->items.size() - (size_t)L.n_items; k < c->items.size(); ++k)
+            c->items[k].layer_items = L.n_items;
         c->layers.push_back(L);
         toff += T;
     }

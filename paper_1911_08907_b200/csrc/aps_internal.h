@@ -10,11 +10,17 @@ constexpr int kTile = 128;        // codes per tile (layout rule, aps.h)
 constexpr int kItemTiles = 64;    // tiles per work item (one CTA): 8192 elements
 constexpr int kThreads = 256;
 
-// One work item = a tile-aligned slice of one layer, processed by one CTA.
+// One work item = a tile-aligned slice of one layer (<= kItemTiles tiles).
+// Flat descriptor, precomputed on the host, so a kernel needs one load (no
+// dependent item -> layer chain) to know everything but the per-call
+// pointers.
 struct Item {
     int32_t layer;
-    int32_t tile_begin;  // within the layer
+    int32_t tile_begin;   // within the layer
     int32_t n_tiles;
+    int32_t cnt;          // valid elements: min(n_tiles * 128, numel - tile_begin * 128)
+    int64_t tile_pos;     // first tile of the item in the packed buffer
+    int32_t layer_items;  // work items of the layer
     int32_t pad;
 };
 

@@ -56,8 +56,18 @@ struct StageCfg {
     static constexpr int kStages = std::min(8, kSmemBudget / kStageBytes);
 };
 
+// Everything the consumers and the finisher need about a work item,
+// resolved by the producer (so no consumer touches a global table).
 struct StageInfo {
-    int ft;  // f~ of the item's layer (quantise / fused phase B)
+    const float *src;     // gradient at the item's first element
+    float *dst;           // output at the item's first element
+    int64_t tile_pos;     // first tile of the item in the packed buffer
+    int32_t cnt;          // valid elements
+    int32_t n_tiles;
+    int32_t layer;
+    int32_t layer_items;
+    int32_t ft;           // f~ of the layer (quantise paths)
+    int32_t pending;      // fused phase B: E of the layer not yet seen final
 };
 
 template <int Stages, int StageBytes>
@@ -67,6 +77,7 @@ struct StreamSmem {
     uint64_t full[Stages], done[Stages], empty[Stages];
     uint32_t part[Stages][kConsWarps];
     StageInfo info[Stages];
+    StageInfo batch[32];  // producer: prefetched descriptors of the next 32 items
 };
 
 // ------------------------------------------------------------------ PTX wrappers
@@ -159,27 +170,41 @@ struct Load {
 };
 
 // ------------------------------------------------------------------ item helpers
-struct ItemView {
-    Item it;
-    LayerDev L;
-    int64_t begin;  // first element of the item within the layer
-    int cnt;        // valid elements in the item
-};
-
-__device__ __forceinline__ ItemView view(const DevTables &t, int k)
+// Producer-side descriptor fetch (one lane per item, 32 items at a time).
+__device__ __forceinline__ StageInfo fetch_info(const DevTables &t, int k)
 {
-    ItemView v;
-    v.it = t.items[k];
-    v.L = t.layers[v.it.layer];
-    v.begin = (int64_t)v.it.tile_begin * kTile;
-    v.cnt = (int)min((int64_t)v.it.n_tiles * kTile, v.L.numel - v.begin);
-    return v;
+    const Item it = t.items[k];
+    StageInfo si;
+    si.layer = it.layer;
+    si.cnt = it.cnt;
+    si.n_tiles = it.n_tiles;
+    si.tile_pos = it.tile_pos;
+    si.layer_items = it.layer_items;
+    const int64_t begin = (int64_t)it.tile_begin * kTile;
+    si.src = t.src[it.layer] + begin;
+    si.dst = t.dst ? t.dst[it.layer] + begin : nullptr;
+    si.ft = 0;
+    si.pending = 0;
+    return si;
 }
 
-__device__ __forceinline__ Load grad_load(const DevTables &t, int k, bool keep)
+__device__ __forceinline__ Load grad_load(const StageInfo &si, bool keep)
 {
-    const ItemView v = view(t, k);
-    return Load{t.src[v.it.layer] + v.begin, (uint32_t)(v.cnt >> 2) * 16u, 0u, keep};
+    return Load{si.src, (uint32_t)(si.cnt >> 2) * 16u, 0u, keep};
+}
+
+// f~ = upper_bound_exp - E (Alg. 1 line 4) for the item's layer; the item
+// holding the layer's first tile records ftilde[] and the non-finite flag.
+__device__ __forceinline__ int resolve_ft(const DevTables &t, int layer, bool first, int bias)
+{
+    const int32_t E = t.E_glob[layer];
+    int ft = (E == INT32_MIN) ? 0 : bias - E;
+    if (E == INT32_MAX) {
+        ft = 0;
+        if (first) atomicOr(t.flag, 1u);
+    }
+    if (first) t.ftilde[layer] = ft;
+    return ft;
 }
 
 // fp32 group j (elements 4j..4j+3) of an item: from the stage when it was
@@ -209,28 +234,19 @@ __device__ __forceinline__ void store_chunk_f32(float *out, const float4 *s4, in
     }
 }
 
-// f~ of the item's layer, resolved by the producer (ftilde[] / flag written
-// by the producer that handles the layer's first item).
-__device__ __forceinline__ int producer_ftilde(const DevTables &t, const ItemView &v, int bias, uint32_t gen)
-{
-    if (gen)
-        while (ld_acquire(&t.ready[v.it.layer]) != gen) __nanosleep(32);
-    return scale_exponent(t, v.it.layer, bias, v.it.tile_begin == 0);
-}
-
 // finisher side of a1: combine the item's abs-max into the layer; the last
 // item of the layer writes E_l (and publishes it when gen != 0).
-__device__ __forceinline__ void absmax_finish(const DevTables &t, int N, int k, const uint32_t *part, uint32_t gen)
+__device__ __forceinline__ void absmax_finish(const DevTables &t, int N, const StageInfo &si, const uint32_t *part,
+                                              uint32_t gen)
 {
-    const Item it = t.items[k];
     uint32_t m = 0;
 #pragma unroll
     for (int w = 0; w < kConsWarps; ++w) m = max(m, part[w]);
-    const int l = it.layer;
+    const int l = si.layer;
     atomicMax(&t.amax[l], m);
     __threadfence();
     const uint32_t done = atomicAdd(&t.count[l], 1u);
-    if (done == (uint32_t)t.layers[l].n_items - 1u) {
+    if (done == (uint32_t)si.layer_items - 1u) {
         __threadfence();
         const uint32_t A = atomicExch(&t.amax[l], 0u);
         t.count[l] = 0u;
@@ -243,19 +259,18 @@ __device__ __forceinline__ void absmax_finish(const DevTables &t, int N, int k, 
 }
 
 // consumer side of a1: the warp's abs-max over its chunk
-__device__ __forceinline__ uint32_t absmax_chunk(const DevTables &t, const ItemView &v, const float4 *s4, int warp,
-                                                 int lane)
+__device__ __forceinline__ uint32_t absmax_chunk(const StageInfo &si, const float4 *s4, int warp, int lane)
 {
     uint32_t mx = 0;
     const int g0 = warp * (kChunk / 4);
-    const int n4 = v.cnt >> 2;
+    const int n4 = si.cnt >> 2;
 #pragma unroll
     for (int k = 0; k < kChunk / 4 / 32; ++k) {
         const int j = g0 + lane + 32 * k;
         if (j < n4) mx = max(mx, absbits4(s4[j]));
     }
-    if (warp == kConsWarps - 1 && lane < (v.cnt & 3))
-        mx = max(mx, __float_as_uint(t.src[v.it.layer][v.begin + 4 * n4 + lane]) & 0x7fffffffu);
+    if (warp == kConsWarps - 1 && lane < (si.cnt & 3))
+        mx = max(mx, __float_as_uint(si.src[4 * n4 + lane]) & 0x7fffffffu);
     return __reduce_max_sync(0xffffffffu, mx);
 }
 
@@ -264,28 +279,41 @@ __device__ __forceinline__ uint32_t absmax_chunk(const DevTables &t, const ItemV
 // buffer); with Fuse the unscaled fp32 result overwrites the stage in place
 // and is bulk-stored to the output.
 template <class C, bool Fuse>
-__device__ __forceinline__ void quant_chunk(const DevTables &t, const C &c, const ItemView &v, uint8_t *stage,
-                                            uint8_t *codes, uint32_t *scratch, int ft, int avg, int warp, int lane)
+__device__ __forceinline__ void quant_chunk(const DevTables &t, const C &c, const StageInfo &si, uint8_t *stage,
+                                            uint8_t *codes, uint32_t *scratch, int avg, int warp, int lane)
 {
     constexpr int B = C::kB;
     float4 *s4 = reinterpret_cast<float4 *>(stage);
-    const float *g = t.src[v.it.layer] + v.begin;
-    const Pow2 s(ft);
-    const Unscale us(ft, 1, avg);
+    const Pow2 s(si.ft);
+    const Unscale us(si.ft, 1, avg);
     const int g0 = warp * (kChunk / 4);
-    const int tiles_w = min(kChunk / kTile, v.it.n_tiles - warp * (kChunk / kTile));  // tiles in this chunk
+    const int tiles_w = min(kChunk / kTile, si.n_tiles - warp * (kChunk / kTile));  // tiles in this chunk
     if (tiles_w <= 0) return;
     if constexpr (B == 8 || B == 16 || B == 32) {
         using W = typename Word4<B>::T;
         W *cw = reinterpret_cast<W *>(codes);
+        const int ng = si.n_tiles * (kTile / 4);
+        if (!s.wide) {
 #pragma unroll
-        for (int k = 0; k < kChunk / 4 / 32; ++k) {
-            const int j = g0 + lane + 32 * k;
-            if (j < v.it.n_tiles * (kTile / 4)) {
-                const float4 x = stage_group(s4, g, j, v.cnt);
-                const W code = pack4<B>(c, s.apply4(x));
-                cw[j] = code;
-                if (Fuse) s4[j] = us.apply4(unpack4<B>(c, code));
+            for (int k = 0; k < kChunk / 4 / 32; ++k) {
+                const int j = g0 + lane + 32 * k;
+                if (j < ng) {
+                    const float4 x = stage_group(s4, si.src, j, si.cnt);
+                    const float4 y = make_float4(__fmul_rn(x.x, s.f), __fmul_rn(x.y, s.f), __fmul_rn(x.z, s.f),
+                                                 __fmul_rn(x.w, s.f));
+                    const W code = pack4<B>(c, y);
+                    cw[j] = code;
+                    if (Fuse) s4[j] = us.apply4(unpack4<B>(c, code));
+                }
+            }
+        } else {
+            for (int k = 0; k < kChunk / 4 / 32; ++k) {
+                const int j = g0 + lane + 32 * k;
+                if (j < ng) {
+                    const W code = pack4<B>(c, s.apply4(stage_group(s4, si.src, j, si.cnt)));
+                    cw[j] = code;
+                    if (Fuse) s4[j] = us.apply4(unpack4<B>(c, code));
+                }
             }
         }
     } else {
@@ -293,7 +321,7 @@ __device__ __forceinline__ void quant_chunk(const DevTables &t, const C &c, cons
         uint32_t *cw = reinterpret_cast<uint32_t *>(codes);
         for (int tt = 0; tt < tiles_w; ++tt) {
             const int j = g0 + tt * (kTile / 4) + lane;
-            const float4 y = s.apply4(stage_group(s4, g, j, v.cnt));
+            const float4 y = s.apply4(stage_group(s4, si.src, j, si.cnt));
             const uint4 cd = make_uint4(c.enc(y.x), c.enc(y.y), c.enc(y.z), c.enc(y.w));
             __syncwarp();
             *reinterpret_cast<uint4 *>(scratch + 4 * lane) = cd;
@@ -305,32 +333,33 @@ __device__ __forceinline__ void quant_chunk(const DevTables &t, const C &c, cons
     }
     fence_proxy_async_smem();
     __syncwarp();
-    const int64_t tile0 = v.L.tile_off + v.it.tile_begin + warp * (kChunk / kTile);
+    const int64_t tile0 = si.tile_pos + warp * (kChunk / kTile);
     if (lane == 0)
         bulk_s2g(t.packed + tile0 * (16 * B), codes + (size_t)warp * (kChunk / kTile) * (16 * B),
                  (uint32_t)(tiles_w * 16 * B));
-    if (Fuse) store_chunk_f32(t.dst[v.it.layer] + v.begin, s4, warp * kChunk, v.cnt, lane);
+    if (Fuse) store_chunk_f32(si.dst, s4, warp * kChunk, si.cnt, lane);
 }
 
 // consumer side of a7 for the warp's chunk: codes (loaded into the stage's
 // code area) -> fp32 in the stage -> bulk store.
 template <class C>
-__device__ __forceinline__ void unpack_chunk(const DevTables &t, const C &c, const ItemView &v, uint8_t *stage,
-                                             const uint8_t *codes, int N, int avg, int warp, int lane)
+__device__ __forceinline__ void unpack_chunk(const C &c, const StageInfo &si, uint8_t *stage, const uint8_t *codes,
+                                             int N, int avg, int warp, int lane)
 {
     constexpr int B = C::kB;
     float4 *s4 = reinterpret_cast<float4 *>(stage);
-    const Unscale us(t.ftilde[v.it.layer], N, avg);
+    const Unscale us(si.ft, N, avg);
     const int g0 = warp * (kChunk / 4);
-    const int tiles_w = min(kChunk / kTile, v.it.n_tiles - warp * (kChunk / kTile));
+    const int tiles_w = min(kChunk / kTile, si.n_tiles - warp * (kChunk / kTile));
     if (tiles_w <= 0) return;
     if constexpr (B == 8 || B == 16 || B == 32) {
         using W = typename Word4<B>::T;
         const W *cw = reinterpret_cast<const W *>(codes);
+        const int ng = si.n_tiles * (kTile / 4);
 #pragma unroll
         for (int k = 0; k < kChunk / 4 / 32; ++k) {
             const int j = g0 + lane + 32 * k;
-            if (j < v.it.n_tiles * (kTile / 4)) s4[j] = us.apply4(unpack4<B>(c, cw[j]));
+            if (j < ng) s4[j] = us.apply4(unpack4<B>(c, cw[j]));
         }
     } else {
         const int b = B;
@@ -345,24 +374,27 @@ __device__ __forceinline__ void unpack_chunk(const DevTables &t, const C &c, con
     }
     fence_proxy_async_smem();
     __syncwarp();
-    store_chunk_f32(t.dst[v.it.layer] + v.begin, s4, warp * kChunk, v.cnt, lane);
+    store_chunk_f32(si.dst, s4, warp * kChunk, si.cnt, lane);
 }
 
 // ------------------------------------------------------------------ ops
-// An Op provides: kCodeBytes (stage code area), n_work(), produce(w, info)
-// -> Load, consume(w, stage, info, scratch, warp, lane) -> partial, and
-// finish(w, partials).
+// An Op provides: kCodeBytes (the stage's code area), n_work(),
+//   fetch(w)              producer lane: descriptor + side info (parallel, 32 items at a time)
+//   resolve(w, si)        producer lane 0: last-moment side info (may wait), -> Load
+//   consume(w, stage, si, scratch, warp, lane) -> per-warp partial
+//   finish(w, si, parts)  finisher lane
 struct AbsmaxOp {
     static constexpr int kCodeBytes = 0;
     DevTables t;
     int N;
     __device__ int n_work() const { return t.n_items; }
-    __device__ Load produce(int w, StageInfo &) const { return grad_load(t, w, true); }
-    __device__ uint32_t consume(int w, uint8_t *stage, const StageInfo &, uint32_t *, int warp, int lane) const
+    __device__ StageInfo fetch(int w) const { return fetch_info(t, w); }
+    __device__ Load resolve(int, StageInfo &si) const { return grad_load(si, true); }
+    __device__ uint32_t consume(int, uint8_t *stage, const StageInfo &si, uint32_t *, int warp, int lane) const
     {
-        return absmax_chunk(t, view(t, w), reinterpret_cast<const float4 *>(stage), warp, lane);
+        return absmax_chunk(si, reinterpret_cast<const float4 *>(stage), warp, lane);
     }
-    __device__ void finish(int w, const uint32_t *part) const { absmax_finish(t, N, w, part, 0u); }
+    __device__ void finish(int, const StageInfo &si, const uint32_t *part) const { absmax_finish(t, N, si, part, 0u); }
 };
 
 template <class C>
@@ -373,19 +405,20 @@ struct QuantOp {
     int bias;
     // reverse order: the items a1 read last are still in L2
     __device__ int n_work() const { return t.n_items; }
-    __device__ int item(int w) const { return t.n_items - 1 - w; }
-    __device__ Load produce(int w, StageInfo &info) const
+    __device__ StageInfo fetch(int w) const
     {
-        info.ft = producer_ftilde(t, view(t, item(w)), bias, 0u);
-        return grad_load(t, item(w), false);
+        const int k = t.n_items - 1 - w;
+        StageInfo si = fetch_info(t, k);
+        si.ft = resolve_ft(t, si.layer, t.items[k].tile_begin == 0, bias);
+        return si;
     }
-    __device__ uint32_t consume(int w, uint8_t *stage, const StageInfo &info, uint32_t *scratch, int warp,
-                                int lane) const
+    __device__ Load resolve(int, StageInfo &si) const { return grad_load(si, false); }
+    __device__ uint32_t consume(int, uint8_t *stage, const StageInfo &si, uint32_t *scratch, int warp, int lane) const
     {
-        quant_chunk<C, false>(t, c, view(t, item(w)), stage, stage + kF32Bytes, scratch, info.ft, 0, warp, lane);
+        quant_chunk<C, false>(t, c, si, stage, stage + kF32Bytes, scratch, 0, warp, lane);
         return 0u;
     }
-    __device__ void finish(int, const uint32_t *) const {}
+    __device__ void finish(int, const StageInfo &, const uint32_t *) const {}
 };
 
 template <class C>
@@ -395,19 +428,23 @@ struct UnpackOp {
     C c;
     int N, avg;
     __device__ int n_work() const { return t.n_items; }
-    __device__ Load produce(int w, StageInfo &) const
+    __device__ StageInfo fetch(int w) const
     {
-        const Item it = t.items[w];
-        const LayerDev L = t.layers[it.layer];
-        return Load{t.packed + (L.tile_off + it.tile_begin) * (16 * C::kB), (uint32_t)(16 * C::kB * it.n_tiles),
-                    (uint32_t)kF32Bytes, false};
+        StageInfo si = fetch_info(t, w);
+        si.ft = t.ftilde[si.layer];
+        return si;
     }
-    __device__ uint32_t consume(int w, uint8_t *stage, const StageInfo &, uint32_t *, int warp, int lane) const
+    __device__ Load resolve(int, StageInfo &si) const
     {
-        unpack_chunk<C>(t, c, view(t, w), stage, stage + kF32Bytes, N, avg, warp, lane);
+        return Load{t.packed + si.tile_pos * (16 * C::kB), (uint32_t)(16 * C::kB * si.n_tiles), (uint32_t)kF32Bytes,
+                    false};
+    }
+    __device__ uint32_t consume(int, uint8_t *stage, const StageInfo &si, uint32_t *, int warp, int lane) const
+    {
+        unpack_chunk<C>(c, si, stage, stage + kF32Bytes, N, avg, warp, lane);
         return 0u;
     }
-    __device__ void finish(int, const uint32_t *) const {}
+    __device__ void finish(int, const StageInfo &, const uint32_t *) const {}
 };
 
 template <class C>
@@ -418,24 +455,37 @@ struct FusedP1Op {
     int bias, avg;
     uint32_t gen;
     __device__ int n_work() const { return 2 * t.n_items; }
-    __device__ int item_b(int w) const { return 2 * t.n_items - 1 - w; }
-    __device__ Load produce(int w, StageInfo &info) const
+    __device__ StageInfo fetch(int w) const
     {
-        if (w < t.n_items) return grad_load(t, w, true);
-        info.ft = producer_ftilde(t, view(t, item_b(w)), bias, gen);
-        return grad_load(t, item_b(w), false);
+        if (w < t.n_items) return fetch_info(t, w);
+        const int k = 2 * t.n_items - 1 - w;
+        StageInfo si = fetch_info(t, k);
+        if (ld_acquire(&t.ready[si.layer]) == gen)
+            si.ft = resolve_ft(t, si.layer, t.items[k].tile_begin == 0, bias);
+        else
+            si.pending = 1;
+        return si;
     }
-    __device__ uint32_t consume(int w, uint8_t *stage, const StageInfo &info, uint32_t *scratch, int warp,
-                                int lane) const
+    __device__ Load resolve(int w, StageInfo &si) const
     {
-        if (w < t.n_items)
-            return absmax_chunk(t, view(t, w), reinterpret_cast<const float4 *>(stage), warp, lane);
-        quant_chunk<C, true>(t, c, view(t, item_b(w)), stage, stage + kF32Bytes, scratch, info.ft, avg, warp, lane);
+        if (w < t.n_items) return grad_load(si, true);
+        if (si.pending) {  // E of the layer not final at prefetch time: wait for it now
+            while (ld_acquire(&t.ready[si.layer]) != gen) __nanosleep(32);
+            const int k = 2 * t.n_items - 1 - w;
+            si.ft = resolve_ft(t, si.layer, t.items[k].tile_begin == 0, bias);
+            si.pending = 0;
+        }
+        return grad_load(si, false);
+    }
+    __device__ uint32_t consume(int w, uint8_t *stage, const StageInfo &si, uint32_t *scratch, int warp, int lane) const
+    {
+        if (w < t.n_items) return absmax_chunk(si, reinterpret_cast<const float4 *>(stage), warp, lane);
+        quant_chunk<C, true>(t, c, si, stage, stage + kF32Bytes, scratch, avg, warp, lane);
         return 0u;
     }
-    __device__ void finish(int w, const uint32_t *part) const
+    __device__ void finish(int w, const StageInfo &si, const uint32_t *part) const
     {
-        if (w < t.n_items) absmax_finish(t, 1, w, part, gen);
+        if (w < t.n_items) absmax_finish(t, 1, si, part, gen);
     }
 };
 
@@ -459,42 +509,57 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const Op op)
     }
     __syncthreads();
     const int nw = op.n_work();
-    if (warp == kConsWarps) {  // ---------------- producer
-        if (lane == 0) {
-            const uint64_t keep = policy_evict_last(), stream = policy_evict_first();
-            int i = 0;
-            for (int w = blockIdx.x; w < nw; w += gridDim.x, ++i) {
-                const int s = i % NS;
-                const uint32_t ph = (uint32_t)(i / NS) & 1u;
-                mbar_wait(&S.empty[s], ph ^ 1u);
-                const Load ld = op.produce(w, S.info[s]);
-                mbar_arrive_expect_tx(&S.full[s], ld.bytes);
-                if (ld.bytes)
-                    bulk_g2s(S.stage[s] + ld.dst_off, ld.src, ld.bytes, &S.full[s], ld.keep ? keep : stream);
+    const int G = gridDim.x;
+    const int my_items = nw > (int)blockIdx.x ? (nw - 1 - (int)blockIdx.x) / G + 1 : 0;
+    if (warp == kConsWarps) {  // ---------------- producer warp
+        const uint64_t keep = policy_evict_last(), stream = policy_evict_first();
+        // batch b covers this CTA's items 32b .. 32b+31; lane j fetches item 32b+j.
+        StageInfo next;
+        if (lane < my_items) next = op.fetch(blockIdx.x + lane * G);
+        for (int b0 = 0; b0 < my_items; b0 += 32) {
+            __syncwarp();
+            S.batch[lane] = next;
+            __syncwarp();
+            const int n_in = min(32, my_items - b0);
+            const int nb = b0 + 32 + lane;
+            if (nb < my_items) next = op.fetch(blockIdx.x + nb * G);  // overlaps the issue loop below
+            if (lane == 0) {
+                for (int j = 0; j < n_in; ++j) {
+                    const int i = b0 + j;
+                    const int w = blockIdx.x + i * G;
+                    const int s = i % NS;
+                    const uint32_t ph = (uint32_t)(i / NS) & 1u;
+                    StageInfo si = S.batch[j];
+                    mbar_wait(&S.empty[s], ph ^ 1u);
+                    const Load ld = op.resolve(w, si);
+                    S.info[s] = si;
+                    mbar_arrive_expect_tx(&S.full[s], ld.bytes);
+                    if (ld.bytes)
+                        bulk_g2s(S.stage[s] + ld.dst_off, ld.src, ld.bytes, &S.full[s], ld.keep ? keep : stream);
+                }
             }
         }
         return;
     }
     if (warp == kConsWarps + 1) {  // ---------------- finisher
         if (lane == 0) {
-            int i = 0;
-            for (int w = blockIdx.x; w < nw; w += gridDim.x, ++i) {
+            for (int i = 0; i < my_items; ++i) {
                 const int s = i % NS;
                 const uint32_t ph = (uint32_t)(i / NS) & 1u;
                 mbar_wait(&S.done[s], ph);
-                op.finish(w, S.part[s]);
+                op.finish(blockIdx.x + i * G, S.info[s], S.part[s]);
                 mbar_arrive(&S.empty[s]);
             }
         }
         return;
     }
     // ---------------- consumers
-    int i = 0;
-    for (int w = blockIdx.x; w < nw; w += gridDim.x, ++i) {
+    for (int i = 0; i < my_items; ++i) {
         const int s = i % NS;
         const uint32_t ph = (uint32_t)(i / NS) & 1u;
         mbar_wait(&S.full[s], ph);
-        const uint32_t part = op.consume(w, S.stage[s], S.info[s], S.scratch[warp], warp, lane);
+        const StageInfo &si = S.info[s];
+        const uint32_t part = op.consume(blockIdx.x + i * G, S.stage[s], si, S.scratch[warp], warp, lane);
         if (lane == 0) {
             bulk_commit();
             bulk_wait_read();  // the stage may be refilled once the bulk stores have read it
