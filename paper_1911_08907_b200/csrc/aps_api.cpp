@@ -42,13 +42,14 @@ struct aps_ctx {
     uint8_t *ws = nullptr;
     size_t ws_bytes = 0, need = 0;
     size_t off_packed = 0, off_recv = 0, off_items = 0, off_layers = 0, off_src = 0, off_dst = 0,
-           off_amax = 0, off_count = 0, off_eloc = 0, off_eglob = 0, off_ft = 0, off_flag = 0, off_ready = 0;
+           off_amax = 0, off_count = 0, off_eloc = 0, off_eglob = 0, off_ft = 0, off_flag = 0, off_amax2 = 0, off_done = 0;
     aps::DevTables t{};
     std::vector<const float *> src_cache;
     std::vector<float *> dst_cache;
     int phase = kNone;
     bool stream_engine = true;  // persistent TMA-bulk kernels (aps_stream.cu) vs simple grid kernels
-    uint32_t gen = 0;           // generation stamp of the fused p = 1 launch
+    uint32_t gen = 0;           // abs-max-pass launches so far (selects the accumulator parity)
+    uint32_t done_target = 0;   // value the CTA-done counter reaches at the end of the current pass
     std::string err;
 };
 
@@ -221,7 +222,8 @@ aps_status aps_init(aps_ctx **out, int exp_bits, int man_bits, int world_size, i
     c->off_eglob = o;  o = align_up(o + 4 * (size_t)n_layers);
     c->off_ft = o;     o = align_up(o + 4 * (size_t)n_layers);
     c->off_flag = o;   o = align_up(o + 4);
-    c->off_ready = o;  o = align_up(o + 4 * (size_t)n_layers);
+    c->off_amax2 = o;  o = align_up(o + 8 * (size_t)n_layers);
+    c->off_done = o;   o = align_up(o + 4);
     c->need = o;
     *out = c;
     return APS_OK;
@@ -253,8 +255,10 @@ aps_status aps_set_workspace(aps_ctx *c, void *dev, size_t bytes)
     t.E_glob = reinterpret_cast<int32_t *>(c->ws + (c->world == 1 ? c->off_eloc : c->off_eglob));
     t.ftilde = reinterpret_cast<int32_t *>(c->ws + c->off_ft);
     t.flag = reinterpret_cast<uint32_t *>(c->ws + c->off_flag);
-    t.ready = reinterpret_cast<uint32_t *>(c->ws + c->off_ready);
+    t.amax2 = reinterpret_cast<uint32_t *>(c->ws + c->off_amax2);
+    t.done = reinterpret_cast<uint32_t *>(c->ws + c->off_done);
     c->gen = 0;
+    c->done_target = 0;
     t.packed = c->ws + c->off_packed;
     t.n_items = (int)c->items.size();
     t.n_layers = c->n_layers;
@@ -276,8 +280,16 @@ aps_status aps_layer_scales(aps_ctx *c, const float *const *grads)
     if (aps_status s = need_ws(c)) return s;
     if (!grads) return fail(c, APS_ERR_ARG, "grads is NULL");
     if (aps_status s = upload_ptrs<const float *>(c, c->src_cache, grads, c->off_src)) return s;
-    APS_CUDA(c, c->stream_engine ? aps::launch_stream_absmax(c->t, c->world, c->stream)
-                                 : aps::launch_absmax_exp(c->t, c->world, c->stream));
+    if (c->stream_engine) {
+        // commit the counter target only if the launch was accepted (a skipped
+        // increment would make a later pass wait forever)
+        const uint32_t tgt = c->done_target + (uint32_t)aps::stream_grid(c->t.n_items);
+        APS_CUDA(c, aps::launch_stream_absmax(c->t, c->world, c->gen, tgt, c->stream));
+        c->done_target = tgt;
+        ++c->gen;
+    } else {
+        APS_CUDA(c, aps::launch_absmax_exp(c->t, c->world, c->stream));
+    }
     if (c->world == 1) {
         c->phase = kScales;
     } else if (c->sim) {
@@ -356,17 +368,16 @@ aps_status aps_sync_out(aps_ctx *c, const float *const *grads, float *const *out
 {
     if (aps_status s = need_ws(c)) return s;
     if (!grads || !out) return fail(c, APS_ERR_ARG, "NULL pointer array");
-    if (c->world == 1 && c->stream_engine) {
+    if (c->world == 1 && c->stream_engine && aps::stream_fused_supported(c->e, c->m, c->hw)) {
         // one rank: FindMaxExp -> f~ -> Cast -> pack -> Cast back -> unscale in one launch
         if (aps_status s = upload_ptrs<const float *>(c, c->src_cache, grads, c->off_src)) return s;
         if (aps_status s = upload_ptrs<float *>(c, c->dst_cache, out, c->off_dst)) return s;
-        if (++c->gen == 0) c->gen = 1;
-        cudaError_t e = aps::launch_stream_fused_p1(c->t, c->e, c->m, c->hw, average, c->gen, c->stream);
-        if (e != cudaErrorNotSupported) {
-            APS_CUDA(c, e);
-            c->phase = kReduced;
-            return APS_OK;
-        }
+        const uint32_t tgt = c->done_target + (uint32_t)aps::stream_grid(2 * c->t.n_items);
+        APS_CUDA(c, aps::launch_stream_fused_p1(c->t, c->e, c->m, c->hw, average, c->gen, tgt, c->stream));
+        c->done_target = tgt;
+        ++c->gen;
+        c->phase = kReduced;
+        return APS_OK;
     }
     if (aps_status s = aps_layer_scales(c, grads)) return s;
     if (aps_status s = aps_quantize_pack(c, grads)) return s;

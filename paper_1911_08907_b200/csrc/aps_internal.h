@@ -43,7 +43,8 @@ struct DevTables {
     int32_t *E_glob;          // [n_layers]
     int32_t *ftilde;          // [n_layers]
     uint32_t *flag;           // non-finite flag
-    uint32_t *ready;          // [n_layers] generation stamp: E of the layer is final (fused p=1 path)
+    uint32_t *amax2;          // [2][n_layers] abs-max accumulators of the stream engine (call parity)
+    uint32_t *done;           // CTAs that finished the abs-max pass (monotone counter)
     uint8_t *packed;          // packed codes
     int n_items;
     int n_layers;
@@ -67,15 +68,17 @@ int sm_count();
 // Persistent TMA-bulk streaming engine (aps_stream.cu): one CTA per SM, a
 // producer warp feeding a multi-stage shared-memory ring with
 // cp.async.bulk, eight consumer warps.
-cudaError_t launch_stream_absmax(const DevTables &t, int world, cudaStream_t s);
+int stream_grid(int n_work);  // CTAs a stream kernel launches for n_work items
+cudaError_t launch_stream_absmax(const DevTables &t, int world, uint32_t gen, uint32_t target, cudaStream_t s);
 cudaError_t launch_stream_quant(const DevTables &t, int e, int m, bool hw, cudaStream_t s);
 cudaError_t launch_stream_unpack(const DevTables &t, int e, int m, bool hw, int world, int average,
                                  cudaStream_t s);
 // p = 1: FindMaxExp -> f~ -> Cast -> pack -> Cast back -> unscale in ONE
 // launch (phase A: abs-max of every work item, forward; phase B: quantise +
 // unscale, reverse order so the second read of the gradients hits L2).
+bool stream_fused_supported(int e, int m, bool hw);
 cudaError_t launch_stream_fused_p1(const DevTables &t, int e, int m, bool hw, int average, uint32_t gen,
-                                   cudaStream_t s);
+                                   uint32_t target, cudaStream_t s);
 
 // true when (e,m) has a hardware converter that is exact on the APS path
 inline bool hw_available(int e, int m) { return (e == 5 && m == 2) || (e == 4 && m == 3); }

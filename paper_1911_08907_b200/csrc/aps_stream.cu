@@ -4,38 +4,38 @@
 // Every hot kernel of the path streams each gradient element through the SM
 // once per pass, so it is bound by HBM bandwidth, and short (~20 us at
 // ResNet-50 size): CTA launch ramp and tail matter as much as steady-state
-// bandwidth.  The engine runs ONE persistent CTA per SM with three roles:
+// bandwidth.  The engine runs ONE persistent CTA per SM:
 //
-//   producer (warp 8, one lane): per work item (static round-robin over the
-//     CTAs) waits for a free stage, resolves the item's side information
-//     (f~ of its layer -- the global/acquire loads happen here, kStages
-//     items ahead of the consumers), arms the stage's `full` mbarrier with
-//     the byte count and issues one cp.async.bulk global->shared copy (TMA
-//     bulk engine, <= 32 KB, L2 eviction-priority hint);
+//   producer (warp 8): its 32 lanes prefetch the flat descriptors (and side
+//     information: layer pointers, f~) of the CTA's next 32 work items in
+//     parallel; lane 0 then, per item, waits for a free stage, arms the
+//     stage's `full` mbarrier with the byte count and issues ONE
+//     cp.async.bulk global->shared copy of up to 32 KB (the TMA bulk engine
+//     sustains ~7 TB/s chip-wide only with >= 16-32 KB requests:
+//     profiles/r01_microbench_stream.txt), with an L2 eviction-priority
+//     hint.  `full` needs two arrivals: the load's, and "side info final".
 //   consumers (warps 0..7): wait `full`, each warp transforms a contiguous
-//     1024-element chunk in shared memory (results written in place or into
-//     the stage's code area), then its lane 0 writes the chunk back with
-//     cp.async.bulk shared->global stores, waits until the stage has been
-//     read, and arrives on `done`;
-//   finisher (warp 9, one lane): waits `done`, does the per-item global
-//     bookkeeping that needs fences/atomics (abs-max combine, last-item
-//     detection, publishing E_l) and frees the stage (`empty`).
-// No register is tied up in loads or stores, the per-item latency of fences
-// and atomics is off the consumers' path, and loads/stores are issued by the
-// bulk-copy engine.
+//     1024-element chunk in shared memory (results in place or into the
+//     stage's code area), writes it back with one cp.async.bulk
+//     shared->global store, waits until the stage has been read, and frees
+//     it (`empty`).
+// FindMaxExp needs no per-item fence or returning atomic: each warp folds its
+// chunk's abs-max into the layer with a fire-and-forget red.max, and each CTA
+// publishes "my abs-max pass is done" once (fence + one counter add).
 //
 // Fused p = 1 path (launch_stream_fused_p1): with one rank there is no
 // collective between FindMaxExp and Cast, so a single launch does
-//   phase A  abs-max of every work item (forward order; L2 evict_last hint);
-//            the finisher of a layer's last item publishes E_l with a
-//            release store of the call's generation stamp;
-//   phase B  per item, in REVERSE order: the producer waits (acquire) for
-//            E_l, then the consumers scale, Cast, pack (codes -> packed
+//   phase A  abs-max of every work item (forward order; L2 evict_last);
+//   phase B  per item, in REVERSE order: scale, Cast, pack (codes -> packed
 //            buffer) and Cast back, unscale, average (fp32 -> output).
-// Reverse order makes the second read of the gradients hit the data phase A
-// left in the 126 MB L2 most recently.  Every producer issues all of its
-// phase A items before its first phase B wait, and phase A items never wait,
-// so with a co-resident grid (cooperative launch) the waits cannot deadlock.
+// The producer issues phase-B loads immediately (the gradients are read-
+// only) and supplies f~ -- the second `full` arrival -- once every CTA has
+// finished phase A (acquire on the counter).  Reverse order makes the second
+// read of the gradients hit the data phase A left in the 126 MB L2 most
+// recently.  Phase-A items never wait, so with a co-resident grid
+// (cooperative launch) the waits cannot deadlock.  The abs-max accumulators
+// are double-buffered by call parity (buffer g&1 in use, buffer (g+1)&1
+// cleared for the next call), so no extra pass resets them.
 #include <cstdint>
 #include <algorithm>
 #include <climits>
@@ -46,18 +46,19 @@ namespace aps {
 
 constexpr int kF32Bytes = kItemTiles * kTile * 4;  // 32 KB: one work item of fp32
 constexpr int kConsWarps = 8;
+constexpr int kConsThreads = kConsWarps * 32;
 constexpr int kChunk = kItemTiles * kTile / kConsWarps;  // 1024 elements per consumer warp
-constexpr int kStreamThreads = (kConsWarps + 2) * 32;
+constexpr int kStreamThreads = kConsThreads + 32;
 constexpr int kSmemBudget = 200 * 1024;
 
 template <int CodeBytes>
 struct StageCfg {
     static constexpr int kStageBytes = kF32Bytes + CodeBytes;
-    static constexpr int kStages = std::min(8, kSmemBudget / kStageBytes);
+    static constexpr int kStages = std::min(6, kSmemBudget / kStageBytes);
 };
 
-// Everything the consumers and the finisher need about a work item,
-// resolved by the producer (so no consumer touches a global table).
+// Everything the consumers need about a work item, resolved by the
+// producer (no consumer touches a global table).
 struct StageInfo {
     const float *src;     // gradient at the item's first element
     float *dst;           // output at the item's first element
@@ -65,19 +66,20 @@ struct StageInfo {
     int32_t cnt;          // valid elements
     int32_t n_tiles;
     int32_t layer;
-    int32_t layer_items;
+    int32_t first;        // the item holds the layer's first tile
     int32_t ft;           // f~ of the layer (quantise paths)
-    int32_t pending;      // fused phase B: E of the layer not yet seen final
+    int32_t phase_b;      // fused: a quantise item (needs f~ from the finished abs-max)
+    int32_t ft_ok;        // ft is final
 };
 
 template <int Stages, int StageBytes>
 struct StreamSmem {
     alignas(1024) uint8_t stage[Stages][StageBytes];
     uint32_t scratch[kConsWarps][kTile];  // per-warp code tile (generic widths)
-    uint64_t full[Stages], done[Stages], empty[Stages];
-    uint32_t part[Stages][kConsWarps];
+    uint64_t full[Stages], empty[Stages];
     StageInfo info[Stages];
     StageInfo batch[32];  // producer: prefetched descriptors of the next 32 items
+    int32_t flag;
 };
 
 // ------------------------------------------------------------------ PTX wrappers
@@ -169,9 +171,24 @@ struct Load {
     bool keep;          // L2 evict_last (data will be read again) vs evict_first
 };
 
+__device__ __forceinline__ void red_max_u32(uint32_t *p, uint32_t v)
+{
+    asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t *p, uint32_t v)
+{
+    uint32_t old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ void bar_consumers()
+{
+    asm volatile("bar.sync 1, %0;" ::"n"(kConsThreads) : "memory");
+}
+
 // ------------------------------------------------------------------ item helpers
 // Producer-side descriptor fetch (one lane per item, 32 items at a time).
-__device__ __forceinline__ StageInfo fetch_info(const DevTables &t, int k)
+__device__ __forceinline__ StageInfo fetch_info(const DevTables &t, int k, bool want_dst)
 {
     const Item it = t.items[k];
     StageInfo si;
@@ -179,12 +196,13 @@ __device__ __forceinline__ StageInfo fetch_info(const DevTables &t, int k)
     si.cnt = it.cnt;
     si.n_tiles = it.n_tiles;
     si.tile_pos = it.tile_pos;
-    si.layer_items = it.layer_items;
+    si.first = it.tile_begin == 0;
     const int64_t begin = (int64_t)it.tile_begin * kTile;
     si.src = t.src[it.layer] + begin;
-    si.dst = t.dst ? t.dst[it.layer] + begin : nullptr;
+    si.dst = want_dst ? t.dst[it.layer] + begin : nullptr;
     si.ft = 0;
-    si.pending = 0;
+    si.phase_b = 0;
+    si.ft_ok = 1;
     return si;
 }
 
@@ -193,11 +211,10 @@ __device__ __forceinline__ Load grad_load(const StageInfo &si, bool keep)
     return Load{si.src, (uint32_t)(si.cnt >> 2) * 16u, 0u, keep};
 }
 
-// f~ = upper_bound_exp - E (Alg. 1 line 4) for the item's layer; the item
-// holding the layer's first tile records ftilde[] and the non-finite flag.
-__device__ __forceinline__ int resolve_ft(const DevTables &t, int layer, bool first, int bias)
+// f~ = upper_bound_exp - E (Alg. 1 line 4) for the layer; the item holding
+// the layer's first tile records ftilde[] and the non-finite flag.
+__device__ __forceinline__ int ft_from_E(const DevTables &t, int32_t E, int layer, bool first, int bias)
 {
-    const int32_t E = t.E_glob[layer];
     int ft = (E == INT32_MIN) ? 0 : bias - E;
     if (E == INT32_MAX) {
         ft = 0;
@@ -234,32 +251,11 @@ __device__ __forceinline__ void store_chunk_f32(float *out, const float4 *s4, in
     }
 }
 
-// finisher side of a1: combine the item's abs-max into the layer; the last
-// item of the layer writes E_l (and publishes it when gen != 0).
-__device__ __forceinline__ void absmax_finish(const DevTables &t, int N, const StageInfo &si, const uint32_t *part,
-                                              uint32_t gen)
-{
-    uint32_t m = 0;
-#pragma unroll
-    for (int w = 0; w < kConsWarps; ++w) m = max(m, part[w]);
-    const int l = si.layer;
-    atomicMax(&t.amax[l], m);
-    __threadfence();
-    const uint32_t done = atomicAdd(&t.count[l], 1u);
-    if (done == (uint32_t)si.layer_items - 1u) {
-        __threadfence();
-        const uint32_t A = atomicExch(&t.amax[l], 0u);
-        t.count[l] = 0u;
-        t.E_local[l] = exponent_of(A, N);
-        if (gen) {
-            __threadfence();
-            st_release(&t.ready[l], gen);
-        }
-    }
-}
-
-// consumer side of a1: the warp's abs-max over its chunk
-__device__ __forceinline__ uint32_t absmax_chunk(const StageInfo &si, const float4 *s4, int warp, int lane)
+// a1, consumer side: the warp's abs-max over its chunk, folded into the
+// layer's accumulator with a fire-and-forget red.max (bits of |x| are
+// monotone in |x|: order-independent, bit-exact).
+__device__ __forceinline__ void absmax_chunk(const StageInfo &si, const float4 *s4, uint32_t *amax, int warp,
+                                             int lane)
 {
     uint32_t mx = 0;
     const int g0 = warp * (kChunk / 4);
@@ -271,13 +267,14 @@ __device__ __forceinline__ uint32_t absmax_chunk(const StageInfo &si, const floa
     }
     if (warp == kConsWarps - 1 && lane < (si.cnt & 3))
         mx = max(mx, __float_as_uint(si.src[4 * n4 + lane]) & 0x7fffffffu);
-    return __reduce_max_sync(0xffffffffu, mx);
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    if (lane == 0 && g0 < 4 * n4 + 4) red_max_u32(&amax[si.layer], mx);
 }
 
-// consumer side of a3/a4 (+ a7 when Fuse) for the warp's chunk.
-// Codes go to `codes` (the stage's code area, bulk-stored to the packed
-// buffer); with Fuse the unscaled fp32 result overwrites the stage in place
-// and is bulk-stored to the output.
+// a3/a4 (+ a7 when Fuse), consumer side, for the warp's chunk.  Codes go to
+// `codes` (the stage's code area) and are bulk-stored to the packed buffer;
+// with Fuse the unscaled fp32 result overwrites the stage in place and is
+// bulk-stored to the output.
 template <class C, bool Fuse>
 __device__ __forceinline__ void quant_chunk(const DevTables &t, const C &c, const StageInfo &si, uint8_t *stage,
                                             uint8_t *codes, uint32_t *scratch, int avg, int warp, int lane)
@@ -340,7 +337,7 @@ __device__ __forceinline__ void quant_chunk(const DevTables &t, const C &c, cons
     if (Fuse) store_chunk_f32(si.dst, s4, warp * kChunk, si.cnt, lane);
 }
 
-// consumer side of a7 for the warp's chunk: codes (loaded into the stage's
+// a7, consumer side, for the warp's chunk: codes (loaded into the stage's
 // code area) -> fp32 in the stage -> bulk store.
 template <class C>
 __device__ __forceinline__ void unpack_chunk(const C &c, const StageInfo &si, uint8_t *stage, const uint8_t *codes,
@@ -378,23 +375,41 @@ __device__ __forceinline__ void unpack_chunk(const C &c, const StageInfo &si, ui
 }
 
 // ------------------------------------------------------------------ ops
-// An Op provides: kCodeBytes (the stage's code area), n_work(),
-//   fetch(w)              producer lane: descriptor + side info (parallel, 32 items at a time)
-//   resolve(w, si)        producer lane 0: last-moment side info (may wait), -> Load
-//   consume(w, stage, si, scratch, warp, lane) -> per-warp partial
-//   finish(w, si, parts)  finisher lane
+// An Op provides
+//   kCodeBytes               size of the stage's code area
+//   n_work(), n_phase_a()    work items, and how many of them are abs-max items (first)
+//   fetch(w, ready)          producer lane: descriptor and side info of item w
+//                            (f~ only when `ready`, i.e. the abs-max pass is complete)
+//   late_ft(si)              producer lane: f~ of a phase-B item once ready
+//   load(w, si)              the TMA load of item w
+//   consume(...)             consumer warp's share of item w
+//   absmax buffer, the done-counter target and whether phase B waits on it.
 struct AbsmaxOp {
     static constexpr int kCodeBytes = 0;
     DevTables t;
+    uint32_t *amax;  // accumulator buffer of this call
+    uint32_t *amax_other;
+    uint32_t target;
     int N;
     __device__ int n_work() const { return t.n_items; }
-    __device__ StageInfo fetch(int w) const { return fetch_info(t, w); }
-    __device__ Load resolve(int, StageInfo &si) const { return grad_load(si, true); }
-    __device__ uint32_t consume(int, uint8_t *stage, const StageInfo &si, uint32_t *, int warp, int lane) const
+    __device__ int n_phase_a() const { return t.n_items; }
+    __device__ bool waits() const { return false; }
+    __device__ StageInfo fetch(int w, bool) const { return fetch_info(t, w, false); }
+    __device__ int late_ft(const StageInfo &) const { return 0; }
+    __device__ Load load(int, const StageInfo &si) const { return grad_load(si, true); }
+    __device__ void consume(int, uint8_t *stage, const StageInfo &si, uint32_t *, int warp, int lane) const
     {
-        return absmax_chunk(si, reinterpret_cast<const float4 *>(stage), warp, lane);
+        absmax_chunk(si, reinterpret_cast<const float4 *>(stage), amax, warp, lane);
     }
-    __device__ void finish(int, const StageInfo &si, const uint32_t *part) const { absmax_finish(t, N, si, part, 0u); }
+    // the last CTA to finish turns the accumulators into E and clears both buffers
+    __device__ void after_phase_a_last(int tid) const
+    {
+        for (int l = tid; l < t.n_layers; l += kConsThreads) {
+            t.E_local[l] = exponent_of(amax[l], N);
+            amax[l] = 0u;
+            amax_other[l] = 0u;
+        }
+    }
 };
 
 template <class C>
@@ -405,20 +420,21 @@ struct QuantOp {
     int bias;
     // reverse order: the items a1 read last are still in L2
     __device__ int n_work() const { return t.n_items; }
-    __device__ StageInfo fetch(int w) const
+    __device__ int n_phase_a() const { return 0; }
+    __device__ bool waits() const { return false; }
+    __device__ StageInfo fetch(int w, bool) const
     {
-        const int k = t.n_items - 1 - w;
-        StageInfo si = fetch_info(t, k);
-        si.ft = resolve_ft(t, si.layer, t.items[k].tile_begin == 0, bias);
+        StageInfo si = fetch_info(t, t.n_items - 1 - w, false);
+        si.ft = ft_from_E(t, t.E_glob[si.layer], si.layer, si.first, bias);
         return si;
     }
-    __device__ Load resolve(int, StageInfo &si) const { return grad_load(si, false); }
-    __device__ uint32_t consume(int, uint8_t *stage, const StageInfo &si, uint32_t *scratch, int warp, int lane) const
+    __device__ int late_ft(const StageInfo &si) const { return si.ft; }
+    __device__ Load load(int, const StageInfo &si) const { return grad_load(si, false); }
+    __device__ void consume(int, uint8_t *stage, const StageInfo &si, uint32_t *scratch, int warp, int lane) const
     {
         quant_chunk<C, false>(t, c, si, stage, stage + kF32Bytes, scratch, 0, warp, lane);
-        return 0u;
     }
-    __device__ void finish(int, const StageInfo &, const uint32_t *) const {}
+    __device__ void after_phase_a_last(int) const {}
 };
 
 template <class C>
@@ -428,23 +444,25 @@ struct UnpackOp {
     C c;
     int N, avg;
     __device__ int n_work() const { return t.n_items; }
-    __device__ StageInfo fetch(int w) const
+    __device__ int n_phase_a() const { return 0; }
+    __device__ bool waits() const { return false; }
+    __device__ StageInfo fetch(int w, bool) const
     {
-        StageInfo si = fetch_info(t, w);
+        StageInfo si = fetch_info(t, w, true);
         si.ft = t.ftilde[si.layer];
         return si;
     }
-    __device__ Load resolve(int, StageInfo &si) const
+    __device__ int late_ft(const StageInfo &si) const { return si.ft; }
+    __device__ Load load(int, const StageInfo &si) const
     {
         return Load{t.packed + si.tile_pos * (16 * C::kB), (uint32_t)(16 * C::kB * si.n_tiles), (uint32_t)kF32Bytes,
                     false};
     }
-    __device__ uint32_t consume(int, uint8_t *stage, const StageInfo &si, uint32_t *, int warp, int lane) const
+    __device__ void consume(int, uint8_t *stage, const StageInfo &si, uint32_t *, int warp, int lane) const
     {
         unpack_chunk<C>(c, si, stage, stage + kF32Bytes, N, avg, warp, lane);
-        return 0u;
     }
-    __device__ void finish(int, const StageInfo &, const uint32_t *) const {}
+    __device__ void after_phase_a_last(int) const {}
 };
 
 template <class C>
@@ -452,46 +470,47 @@ struct FusedP1Op {
     static constexpr int kCodeBytes = kItemTiles * 16 * C::kB;
     DevTables t;
     C c;
+    uint32_t *amax;        // accumulator buffer of this call (parity g & 1)
+    uint32_t *amax_next;   // the other buffer, cleared here for the next call
+    uint32_t target;
     int bias, avg;
-    uint32_t gen;
     __device__ int n_work() const { return 2 * t.n_items; }
-    __device__ StageInfo fetch(int w) const
+    __device__ int n_phase_a() const { return t.n_items; }
+    __device__ bool waits() const { return true; }
+    __device__ StageInfo fetch(int w, bool ready) const
     {
-        if (w < t.n_items) return fetch_info(t, w);
-        const int k = 2 * t.n_items - 1 - w;
-        StageInfo si = fetch_info(t, k);
-        if (ld_acquire(&t.ready[si.layer]) == gen)
-            si.ft = resolve_ft(t, si.layer, t.items[k].tile_begin == 0, bias);
-        else
-            si.pending = 1;
+        if (w < t.n_items) return fetch_info(t, w, false);
+        StageInfo si = fetch_info(t, 2 * t.n_items - 1 - w, true);
+        si.phase_b = 1;
+        si.ft_ok = ready;
+        if (ready) si.ft = late_ft(si);
         return si;
     }
-    __device__ Load resolve(int w, StageInfo &si) const
+    // E_l from the finished abs-max (N = 1); the layer's first item also
+    // records E and clears the other parity buffer.
+    __device__ int late_ft(const StageInfo &si) const
     {
-        if (w < t.n_items) return grad_load(si, true);
-        if (si.pending) {  // E of the layer not final at prefetch time: wait for it now
-            while (ld_acquire(&t.ready[si.layer]) != gen) __nanosleep(32);
-            const int k = 2 * t.n_items - 1 - w;
-            si.ft = resolve_ft(t, si.layer, t.items[k].tile_begin == 0, bias);
-            si.pending = 0;
+        const int32_t E = exponent_of(amax[si.layer], 1);
+        if (si.first) {
+            t.E_local[si.layer] = E;
+            amax_next[si.layer] = 0u;
         }
-        return grad_load(si, false);
+        return ft_from_E(t, E, si.layer, si.first, bias);
     }
-    __device__ uint32_t consume(int w, uint8_t *stage, const StageInfo &si, uint32_t *scratch, int warp, int lane) const
+    __device__ Load load(int w, const StageInfo &si) const { return grad_load(si, w < t.n_items); }
+    __device__ void consume(int w, uint8_t *stage, const StageInfo &si, uint32_t *scratch, int warp, int lane) const
     {
-        if (w < t.n_items) return absmax_chunk(si, reinterpret_cast<const float4 *>(stage), warp, lane);
-        quant_chunk<C, true>(t, c, si, stage, stage + kF32Bytes, scratch, avg, warp, lane);
-        return 0u;
+        if (w < t.n_items)
+            absmax_chunk(si, reinterpret_cast<const float4 *>(stage), amax, warp, lane);
+        else
+            quant_chunk<C, true>(t, c, si, stage, stage + kF32Bytes, scratch, avg, warp, lane);
     }
-    __device__ void finish(int w, const StageInfo &si, const uint32_t *part) const
-    {
-        if (w < t.n_items) absmax_finish(t, 1, si, part, gen);
-    }
+    __device__ void after_phase_a_last(int) const {}
 };
 
 // ------------------------------------------------------------------ the engine
 template <class Op>
-__global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const Op op)
+__global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const Op op, uint32_t *done_ctr, uint32_t target)
 {
     using Cfg = StageCfg<Op::kCodeBytes>;
     using Smem = StreamSmem<Cfg::kStages, Cfg::kStageBytes>;
@@ -501,9 +520,8 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const Op op)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int s = 0; s < NS; ++s) {
-            mbar_init(&S.full[s], 1);
-            mbar_init(&S.done[s], kConsWarps);
-            mbar_init(&S.empty[s], 1);
+            mbar_init(&S.full[s], 2);  // load arrival + "side info final" arrival
+            mbar_init(&S.empty[s], kConsWarps);
         }
         fence_mbarrier_init();
     }
@@ -511,97 +529,140 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const Op op)
     const int nw = op.n_work();
     const int G = gridDim.x;
     const int my_items = nw > (int)blockIdx.x ? (nw - 1 - (int)blockIdx.x) / G + 1 : 0;
+    const int na = op.n_phase_a();
+    const int my_a = na > (int)blockIdx.x ? (na - 1 - (int)blockIdx.x) / G + 1 : 0;  // my phase-A items (first)
+
     if (warp == kConsWarps) {  // ---------------- producer warp
         const uint64_t keep = policy_evict_last(), stream = policy_evict_first();
-        // batch b covers this CTA's items 32b .. 32b+31; lane j fetches item 32b+j.
+        bool ready = !op.waits();
+        int pend_lo = 0, pend_hi = 0;  // my items [pend_lo, pend_hi) issued, f~ still owed
+        // finalize: wait for the abs-max pass, then supply f~ to the owed stages
+        // and to the not-yet-issued entries of the current batch.
+        auto finalize = [&](int b0, int n_in) {
+            if (!ready) {
+                if (lane == 0)
+                    while ((int)(ld_acquire(done_ctr) - target) < 0) __nanosleep(64);
+                __syncwarp();
+                ready = true;
+                for (int i = pend_lo + lane; i < pend_hi; i += 32) {
+                    StageInfo &si = S.info[i % NS];
+                    si.ft = op.late_ft(si);
+                    si.ft_ok = 1;
+                }
+                for (int j = lane; j < n_in; j += 32)
+                    if (b0 + j >= pend_hi && !S.batch[j].ft_ok) {
+                        S.batch[j].ft = op.late_ft(S.batch[j]);
+                        S.batch[j].ft_ok = 1;
+                    }
+                __syncwarp();
+            }
+            if (lane == 0)
+                for (int i = pend_lo; i < pend_hi; ++i) mbar_arrive(&S.full[i % NS]);
+            pend_lo = pend_hi;
+        };
         StageInfo next;
-        if (lane < my_items) next = op.fetch(blockIdx.x + lane * G);
+        if (lane < my_items) next = op.fetch(blockIdx.x + lane * G, ready);
         for (int b0 = 0; b0 < my_items; b0 += 32) {
+            if (ready && lane < my_items - b0 && !next.ft_ok) {  // fetched before the abs-max pass ended
+                next.ft = op.late_ft(next);
+                next.ft_ok = 1;
+            }
             __syncwarp();
             S.batch[lane] = next;
             __syncwarp();
             const int n_in = min(32, my_items - b0);
-            const int nb = b0 + 32 + lane;
-            if (nb < my_items) next = op.fetch(blockIdx.x + nb * G);  // overlaps the issue loop below
-            if (lane == 0) {
-                for (int j = 0; j < n_in; ++j) {
-                    const int i = b0 + j;
-                    const int w = blockIdx.x + i * G;
-                    const int s = i % NS;
-                    const uint32_t ph = (uint32_t)(i / NS) & 1u;
-                    StageInfo si = S.batch[j];
-                    mbar_wait(&S.empty[s], ph ^ 1u);
-                    const Load ld = op.resolve(w, si);
+            if (b0 + 32 + lane < my_items) next = op.fetch(blockIdx.x + (b0 + 32 + lane) * G, ready);
+            for (int j = 0; j < n_in; ++j) {
+                const int i = b0 + j;
+                const int s = i % NS;
+                // the stage's previous occupant may still owe its f~: supply it first
+                if (pend_lo < pend_hi && pend_lo <= i - NS) finalize(b0, n_in);
+                if (lane == 0) {
+                    mbar_wait(&S.empty[s], ((uint32_t)(i / NS) & 1u) ^ 1u);
+                    const StageInfo si = S.batch[j];
                     S.info[s] = si;
+                    const Load ld = op.load(blockIdx.x + i * G, si);
                     mbar_arrive_expect_tx(&S.full[s], ld.bytes);
                     if (ld.bytes)
                         bulk_g2s(S.stage[s] + ld.dst_off, ld.src, ld.bytes, &S.full[s], ld.keep ? keep : stream);
                 }
+                __syncwarp();
+                if (!S.batch[j].ft_ok) {
+                    ++pend_hi;  // f~ owed: the second arrival comes from finalize
+                    int done = 0;
+                    if (lane == 0) done = (int)(ld_acquire(done_ctr) - target) >= 0;
+                    if (__shfl_sync(0xffffffffu, done, 0)) finalize(b0, n_in);
+                } else {
+                    if (pend_lo < pend_hi) finalize(b0, n_in);  // keep arrivals in order
+                    if (lane == 0) mbar_arrive(&S.full[s]);
+                    pend_lo = pend_hi = i + 1;
+                }
             }
         }
+        if (pend_lo < pend_hi) finalize(my_items, 0);
         return;
     }
-    if (warp == kConsWarps + 1) {  // ---------------- finisher
-        if (lane == 0) {
-            for (int i = 0; i < my_items; ++i) {
-                const int s = i % NS;
-                const uint32_t ph = (uint32_t)(i / NS) & 1u;
-                mbar_wait(&S.done[s], ph);
-                op.finish(blockIdx.x + i * G, S.info[s], S.part[s]);
-                mbar_arrive(&S.empty[s]);
-            }
-        }
-        return;
-    }
+
     // ---------------- consumers
     for (int i = 0; i < my_items; ++i) {
         const int s = i % NS;
-        const uint32_t ph = (uint32_t)(i / NS) & 1u;
-        mbar_wait(&S.full[s], ph);
-        const StageInfo &si = S.info[s];
-        const uint32_t part = op.consume(blockIdx.x + i * G, S.stage[s], si, S.scratch[warp], warp, lane);
+        mbar_wait(&S.full[s], (uint32_t)(i / NS) & 1u);
+        op.consume(blockIdx.x + i * G, S.stage[s], S.info[s], S.scratch[warp], warp, lane);
         if (lane == 0) {
             bulk_commit();
             bulk_wait_read();  // the stage may be refilled once the bulk stores have read it
-            S.part[s][warp] = part;
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&S.done[s]);
+        if (lane == 0) mbar_arrive(&S.empty[s]);
+        if (i == my_a - 1 || (my_a == 0 && i == -1)) {
+            // end of my abs-max pass: make my red.max visible, count the CTA done
+            if (lane == 0) __threadfence();
+            bar_consumers();
+            if (threadIdx.x == 0) S.flag = (int)(atom_add_acq_rel(done_ctr, 1u) == target - 1u);
+            bar_consumers();
+            if (S.flag) op.after_phase_a_last(threadIdx.x);
+        }
+    }
+    if (my_a == 0 && na > 0) {  // a CTA with no abs-max items still counts as done
+        bar_consumers();
+        if (threadIdx.x == 0) S.flag = (int)(atom_add_acq_rel(done_ctr, 1u) == target - 1u);
+        bar_consumers();
+        if (S.flag) op.after_phase_a_last(threadIdx.x);
     }
     if (lane == 0) bulk_wait_all();
 }
 
 // ------------------------------------------------------------------ launch
+int stream_grid(int n_work) { return std::max(1, std::min(n_work, sm_count())); }
+
 template <class Op>
-static cudaError_t launch_stream(const Op &op, int n_work, bool cooperative, cudaStream_t s)
+static cudaError_t launch_stream(const Op &op, int n_work, bool cooperative, uint32_t *done_ctr, uint32_t target,
+                                 cudaStream_t s)
 {
     using Cfg = StageCfg<Op::kCodeBytes>;
     using Smem = StreamSmem<Cfg::kStages, Cfg::kStageBytes>;
     static bool configured = false;
-    static int blocks_per_sm = 1;
     const size_t smem = sizeof(Smem) + 1024;  // + alignment slack
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(stream_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, stream_kernel<Op>, kStreamThreads, smem);
-        if (e != cudaSuccess) return e;
-        if (blocks_per_sm < 1) return cudaErrorInvalidConfiguration;
         configured = true;
     }
     if (n_work <= 0) return cudaSuccess;
-    const int grid = std::min(n_work, sm_count() * blocks_per_sm);
+    const int grid = stream_grid(n_work);  // one CTA per SM (the stages take most of shared memory)
     if (cooperative) {
-        void *args[] = {const_cast<Op *>(&op)};
+        void *args[] = {const_cast<Op *>(&op), &done_ctr, &target};
         return cudaLaunchCooperativeKernel((const void *)stream_kernel<Op>, dim3(grid), dim3(kStreamThreads), args,
                                            smem, s);
     }
-    stream_kernel<Op><<<grid, kStreamThreads, smem, s>>>(op);
+    stream_kernel<Op><<<grid, kStreamThreads, smem, s>>>(op, done_ctr, target);
     return cudaGetLastError();
 }
 
-cudaError_t launch_stream_absmax(const DevTables &t, int world, cudaStream_t s)
+cudaError_t launch_stream_absmax(const DevTables &t, int world, uint32_t gen, uint32_t target, cudaStream_t s)
 {
-    return launch_stream(AbsmaxOp{t, world}, t.n_items, false, s);
+    uint32_t *cur = t.amax2 + (size_t)(gen & 1u) * t.n_layers, *other = t.amax2 + (size_t)((gen + 1u) & 1u) * t.n_layers;
+    return launch_stream(AbsmaxOp{t, cur, other, target, world}, t.n_items, false, t.done, target, s);
 }
 
 cudaError_t launch_stream_quant(const DevTables &t, int e, int m, bool hw, cudaStream_t s)
@@ -612,7 +673,7 @@ cudaError_t launch_stream_quant(const DevTables &t, int e, int m, bool hw, cudaS
         if constexpr (C::kB == 0) {
             return cudaErrorNotSupported;  // runtime formats use the simple kernels
         } else {
-            return launch_stream(QuantOp<C>{t, c, bias}, t.n_items, false, s);
+            return launch_stream(QuantOp<C>{t, c, bias}, t.n_items, false, t.done, 0u, s);
         }
     });
 }
@@ -624,21 +685,31 @@ cudaError_t launch_stream_unpack(const DevTables &t, int e, int m, bool hw, int 
         if constexpr (C::kB == 0) {
             return cudaErrorNotSupported;
         } else {
-            return launch_stream(UnpackOp<C>{t, c, world, average}, t.n_items, false, s);
+            return launch_stream(UnpackOp<C>{t, c, world, average}, t.n_items, false, t.done, 0u, s);
         }
     });
 }
 
+bool stream_fused_supported(int e, int m, bool hw)
+{
+    return with_codec(e, m, hw, [&](auto c) -> cudaError_t {
+               using C = decltype(c);
+               return C::kB == 0 ? cudaErrorNotSupported : cudaSuccess;
+           }) == cudaSuccess;
+}
+
 cudaError_t launch_stream_fused_p1(const DevTables &t, int e, int m, bool hw, int average, uint32_t gen,
-                                   cudaStream_t s)
+                                   uint32_t target, cudaStream_t s)
 {
     const int bias = (1 << (e - 1)) - 1;
+    uint32_t *cur = t.amax2 + (size_t)(gen & 1u) * t.n_layers, *other = t.amax2 + (size_t)((gen + 1u) & 1u) * t.n_layers;
     return with_codec(e, m, hw, [&](auto c) -> cudaError_t {
         using C = decltype(c);
         if constexpr (C::kB == 0) {
             return cudaErrorNotSupported;
         } else {
-            return launch_stream(FusedP1Op<C>{t, c, bias, average, gen}, 2 * t.n_items, true, s);
+            return launch_stream(FusedP1Op<C>{t, c, cur, other, target, bias, average}, 2 * t.n_items, true, t.done,
+                                 target, s);
         }
     });
 }
