@@ -332,7 +332,9 @@ def main():
                      "frac": round(gbs / ref_peak, 4)}
     if world == 1:
         # one fused launch per step: FindMaxExp read (4 B) + Cast read (4 B) + codes (b/8 B) + fp32 out (4 B)
-        dom, dms, dbytes = "fused_p1 (stream_kernel<FusedP1Op>)", ms_per_step, (12 + b / 8) * L
+        kname = ("stream_kernel<FusedP1Op>" if os.environ.get("APS_ENGINE") in ("tma", "stream")
+                 else "fused_p1_ldg_kernel")
+        dom, dms, dbytes = f"fused_p1 ({kname})", ms_per_step, (12 + b / 8) * L
         phases["fused_p1"] = {"us": round(ms_per_step * 1e3, 2), "algorithmic_bytes": int(dbytes)}
     else:
         dom = max(kern, key=lambda k: kern[k][0])
@@ -379,7 +381,7 @@ def main():
         "scaling": "weak", "vs_baseline": None, "dtype": "f32->u8 codes" if b == 8 else f"f32->{b}-bit codes",
         "data": "synthetic (seeded normal per layer, binade spread 2^-24..2^-4, 0.5% zeros)",
         "config": {"workload": name, "format": f"1/{e}/{m}", "n_layers": len(numels), "elements": L,
-                   "ranks": world, "hw_convert": ctx_hw(ctx, args), "l2": "flushed (256 MiB write + 256 MiB read) between timed steps"
+                   "ranks": world, "hw_convert": ctx_hw(ctx, args), "engine": os.environ.get("APS_ENGINE", "ldg"), "l2": "flushed (256 MiB write + 256 MiB read) between timed steps"
                    if not args.no_flush else "not flushed", "parallelism": f"dp{world}",
                    "packed_bytes": packed_bytes},
         "roofline": roof, "phases": phases, "gpu_launches": launches_per_step * K,

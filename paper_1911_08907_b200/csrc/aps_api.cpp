@@ -47,7 +47,10 @@ struct aps_ctx {
     std::vector<const float *> src_cache;
     std::vector<float *> dst_cache;
     int phase = kNone;
-    bool stream_engine = true;  // persistent TMA-bulk kernels (aps_stream.cu) vs simple grid kernels
+    // kernel engine: "ldg" (default: grid kernels + the fused p = 1 LDG kernel),
+    // "tma" (persistent TMA-bulk kernels, aps_stream.cu), "simple" (grid kernels only)
+    enum Engine { kLdg = 0, kTma = 1, kSimple = 2 } engine = kLdg;
+    bool stream_engine = false;
     uint32_t gen = 0;           // abs-max-pass launches so far (selects the accumulator parity)
     uint32_t done_target = 0;   // value the CTA-done counter reaches at the end of the current pass
     std::string err;
@@ -162,7 +165,12 @@ aps_status aps_init(aps_ctx **out, int exp_bits, int man_bits, int world_size, i
     c->stream = static_cast<cudaStream_t>(cuda_stream);
     c->hw = aps::hw_available(exp_bits, man_bits);
     if (const char *env = std::getenv("APS_HW_CVT")) c->hw = c->hw && std::atoi(env) != 0;
-    if (const char *env = std::getenv("APS_ENGINE")) c->stream_engine = std::strcmp(env, "simple") != 0;
+    if (const char *env = std::getenv("APS_ENGINE")) {
+        if (!std::strcmp(env, "tma") || !std::strcmp(env, "stream")) c->engine = aps_ctx::kTma;
+        else if (!std::strcmp(env, "simple")) c->engine = aps_ctx::kSimple;
+        else c->engine = aps_ctx::kLdg;
+    }
+    c->stream_engine = c->engine == aps_ctx::kTma;
     if (c->comm) {
         int nr = 0;
         if (ncclCommCount(c->comm, &nr) != ncclSuccess || nr != world_size) {
@@ -368,6 +376,18 @@ aps_status aps_sync_out(aps_ctx *c, const float *const *grads, float *const *out
 {
     if (aps_status s = need_ws(c)) return s;
     if (!grads || !out) return fail(c, APS_ERR_ARG, "NULL pointer array");
+    if (c->world == 1 && c->engine == aps_ctx::kLdg) {
+        // one rank: FindMaxExp -> f~ -> Cast -> pack -> Cast back -> unscale in one launch
+        if (aps_status s = upload_ptrs<const float *>(c, c->src_cache, grads, c->off_src)) return s;
+        if (aps_status s = upload_ptrs<float *>(c, c->dst_cache, out, c->off_dst)) return s;
+        const int grid = aps::fused_p1_ldg_grid(c->e, c->m, c->hw, c->t.n_items);
+        const uint32_t tgt = c->done_target + (uint32_t)grid;
+        APS_CUDA(c, aps::launch_fused_p1_ldg(c->t, c->e, c->m, c->hw, average, c->gen, tgt, grid, c->stream));
+        c->done_target = tgt;
+        ++c->gen;
+        c->phase = kReduced;
+        return APS_OK;
+    }
     if (c->world == 1 && c->stream_engine && aps::stream_fused_supported(c->e, c->m, c->hw)) {
         // one rank: FindMaxExp -> f~ -> Cast -> pack -> Cast back -> unscale in one launch
         if (aps_status s = upload_ptrs<const float *>(c, c->src_cache, grads, c->off_src)) return s;

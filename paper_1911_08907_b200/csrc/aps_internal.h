@@ -9,6 +9,7 @@ namespace aps {
 constexpr int kTile = 128;        // codes per tile (layout rule, aps.h)
 constexpr int kItemTiles = 64;    // tiles per work item (one CTA): 8192 elements
 constexpr int kThreads = 256;
+constexpr int kFusedCtasPerSm = 4;  // fused p = 1 LDG kernel: 4 x 256 threads per SM (64 regs each)
 
 // One work item = a tile-aligned slice of one layer (<= kItemTiles tiles).
 // Flat descriptor, precomputed on the host, so a kernel needs one load (no
@@ -79,6 +80,12 @@ cudaError_t launch_stream_unpack(const DevTables &t, int e, int m, bool hw, int 
 bool stream_fused_supported(int e, int m, bool hw);
 cudaError_t launch_stream_fused_p1(const DevTables &t, int e, int m, bool hw, int average, uint32_t gen,
                                    uint32_t target, cudaStream_t s);
+
+// fused p = 1 on the LDG engine (aps_kernels.cu): cooperative grid of
+// fused_p1_ldg_grid(...) CTAs; `target` = done counter after the call.
+int fused_p1_ldg_grid(int e, int m, bool hw, int n_items);
+cudaError_t launch_fused_p1_ldg(const DevTables &t, int e, int m, bool hw, int average, uint32_t gen,
+                                uint32_t target, int grid, cudaStream_t s);
 
 // true when (e,m) has a hardware converter that is exact on the APS path
 inline bool hw_available(int e, int m) { return (e == 5 && m == 2) || (e == 4 && m == 3); }

@@ -236,6 +236,138 @@ __global__ void __launch_bounds__(NT) ring_reduce_tile_kernel(uint8_t *own, cons
     }
 }
 
+// ------------------------------------------------------------------ fused p = 1 (LDG engine)
+// One rank: no collective separates FindMaxExp from Cast, so ONE persistent
+// cooperative launch (kFusedCtasPerSm CTAs per SM) does
+//   phase A  abs-max of every work item (forward order, L2 evict_last hint):
+//            each warp folds its max into the layer with red.max;
+//   barrier  each CTA fences once and bumps the done counter; all CTAs wait
+//            for the call's target (acquire);
+//   phase B  per item in REVERSE order (the most recently read data is still
+//            in the 126 MB L2): E_l from the accumulator, f~, scale, Cast,
+//            pack (codes -> packed buffer), Cast back, unscale -> output.
+// Accumulators are double-buffered by call parity: buffer g&1 is used,
+// buffer (g+1)&1 is cleared by the layer's first item for the next call.
+__device__ __forceinline__ float4 ld_hint4(const float4 *p, uint64_t pol)
+{
+    float4 r;
+    asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+                 : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t *p)
+{
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+template <class C, int NT>
+__global__ void __launch_bounds__(NT, kFusedCtasPerSm)
+    fused_p1_ldg_kernel(DevTables t, C c, uint32_t *amax, uint32_t *amax_next, uint32_t target, int bias, int avg)
+{
+    __shared__ __align__(16) uint32_t s_codes[NT / 32][kTile];
+    const int G = gridDim.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint64_t keep, strm;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(strm));
+    constexpr int kPer = kItemTiles * kTile / 4 / NT;  // float4 groups per thread in a full item
+
+    // ---------------- phase A: abs-max
+    for (int w = blockIdx.x; w < t.n_items; w += G) {
+        const Item it = t.items[w];
+        const float *g = t.src[it.layer] + (int64_t)it.tile_begin * kTile;
+        const float4 *g4 = reinterpret_cast<const float4 *>(g);
+        uint32_t mx = 0;
+        if (it.cnt == kItemTiles * kTile) {
+            float4 v[kPer];
+#pragma unroll
+            for (int j = 0; j < kPer; ++j) v[j] = ld_hint4(g4 + threadIdx.x + j * NT, keep);
+#pragma unroll
+            for (int j = 0; j < kPer; ++j) mx = max(mx, absbits4(v[j]));
+        } else {
+            const int n4 = it.cnt >> 2;
+            for (int j = threadIdx.x; j < n4; j += NT) mx = max(mx, absbits4(ld_hint4(g4 + j, keep)));
+            if ((int)threadIdx.x < (it.cnt & 3)) mx = max(mx, __float_as_uint(g[4 * n4 + threadIdx.x]) & 0x7fffffffu);
+        }
+        mx = __reduce_max_sync(0xffffffffu, mx);
+        if (lane == 0) asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(&amax[it.layer]), "r"(mx) : "memory");
+    }
+    // ---------------- grid barrier: every abs-max folded in
+    if (lane == 0) __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        atomicAdd(t.done, 1u);
+        while ((int)(ld_relaxed_u32(t.done) - target) < 0) __nanosleep(64);
+        __threadfence();
+    }
+    __syncthreads();
+
+    // ---------------- phase B: quantise + unscale, reverse order
+    constexpr int B = C::kB;
+    for (int w = blockIdx.x; w < t.n_items; w += G) {
+        const Item it = t.items[t.n_items - 1 - w];
+        const int l = it.layer;
+        const int32_t E = exponent_of(ld_relaxed_u32(&amax[l]), 1);
+        int ft = (E == INT32_MIN) ? 0 : bias - E;  // f~ = upper_bound_exp - E (Alg. 1 line 4)
+        if (E == INT32_MAX) ft = 0;
+        if (it.tile_begin == 0 && threadIdx.x == 0) {
+            t.E_local[l] = E;
+            t.ftilde[l] = ft;
+            if (E == INT32_MAX) atomicOr(t.flag, 1u);
+            amax_next[l] = 0u;
+        }
+        const int64_t begin = (int64_t)it.tile_begin * kTile;
+        const float *g = t.src[l] + begin;
+        float *o = t.dst[l] + begin;
+        const float4 *g4 = reinterpret_cast<const float4 *>(g);
+        const Pow2 s(ft);
+        const Unscale us(ft, 1, avg);
+        if constexpr (B == 8 || B == 16 || B == 32) {
+            using W = typename Word4<B>::T;
+            W *out = reinterpret_cast<W *>(t.packed + it.tile_pos * (16 * B));
+            if (it.cnt == kItemTiles * kTile && !s.wide) {
+                float4 v[kPer];
+#pragma unroll
+                for (int j = 0; j < kPer; ++j) v[j] = ld_hint4(g4 + threadIdx.x + j * NT, strm);
+                float4 *o4 = reinterpret_cast<float4 *>(o);
+#pragma unroll
+                for (int j = 0; j < kPer; ++j) {
+                    const float4 y = make_float4(__fmul_rn(v[j].x, s.f), __fmul_rn(v[j].y, s.f), __fmul_rn(v[j].z, s.f),
+                                                 __fmul_rn(v[j].w, s.f));
+                    const W code = pack4<B>(c, y);
+                    out[threadIdx.x + j * NT] = code;
+                    o4[threadIdx.x + j * NT] = us.apply4(unpack4<B>(c, code));
+                }
+            } else {
+                const int ng = it.n_tiles * (kTile / 4);
+                for (int j = threadIdx.x; j < ng; j += NT) {
+                    const W code = pack4<B>(c, s.apply4(load_group(g, 4 * (int64_t)j, it.cnt)));
+                    out[j] = code;
+                    store_group(o, 4 * (int64_t)j, it.cnt, us.apply4(unpack4<B>(c, code)));
+                }
+            }
+        } else {
+            const int b = c.b();
+            uint32_t *codes = s_codes[warp];
+            uint32_t *outw = reinterpret_cast<uint32_t *>(t.packed) + it.tile_pos * (4 * b);
+            for (int tt = warp; tt < it.n_tiles; tt += NT / 32) {
+                const int64_t e0 = (int64_t)tt * kTile + lane * 4;
+                const float4 y = s.apply4(load_group(g, e0, it.cnt));
+                const uint4 cd = make_uint4(c.enc(y.x), c.enc(y.y), c.enc(y.z), c.enc(y.w));
+                *reinterpret_cast<uint4 *>(codes + lane * 4) = cd;
+                __syncwarp();
+                uint32_t *ow = outw + (int64_t)tt * (4 * b);
+                for (int w2 = lane; w2 < 4 * b; w2 += 32) ow[w2] = assemble_word(codes, w2, b);
+                store_group(o, e0, it.cnt, us.apply4(make_float4(c.dec(cd.x), c.dec(cd.y), c.dec(cd.z), c.dec(cd.w))));
+                __syncwarp();
+            }
+        }
+    }
+}
+
 // ------------------------------------------------------------------ sim: MAX exchange of E
 struct PtrArr {
     const int32_t *src[64];
@@ -347,6 +479,31 @@ cudaError_t launch_ring_reduce(uint8_t *own, const uint8_t *recv, int64_t n_tile
         }
         return cudaGetLastError();
     });
+}
+
+cudaError_t launch_fused_p1_ldg(const DevTables &t, int e, int m, bool hw, int average, uint32_t gen,
+                                uint32_t target, int grid, cudaStream_t s)
+{
+    const int bias = (1 << (e - 1)) - 1;
+    uint32_t *cur = t.amax2 + (size_t)(gen & 1u) * t.n_layers;
+    uint32_t *other = t.amax2 + (size_t)((gen + 1u) & 1u) * t.n_layers;
+    return with_codec(e, m, hw, [&](auto c) -> cudaError_t {
+        using C = decltype(c);
+        auto kern = fused_p1_ldg_kernel<C, kThreads>;
+        void *args[] = {const_cast<DevTables *>(&t), &c, &cur, &other, &target, const_cast<int *>(&bias), &average};
+        return cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(kThreads), args, 0, s);
+    });
+}
+
+int fused_p1_ldg_grid(int e, int m, bool hw, int n_items)
+{
+    int per_sm = 0;
+    with_codec(e, m, hw, [&](auto c) -> cudaError_t {
+        using C = decltype(c);
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_p1_ldg_kernel<C, kThreads>, kThreads, 0);
+    });
+    per_sm = std::max(1, std::min(per_sm, kFusedCtasPerSm));
+    return std::max(1, std::min(n_items, sm_count() * per_sm));
 }
 
 cudaError_t launch_sim_max(int32_t *const *E_glob, const int32_t *const *E_local, int p, int n_layers,

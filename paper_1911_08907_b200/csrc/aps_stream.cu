@@ -604,6 +604,17 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const Op op, 
     }
 
     // ---------------- consumers
+    // end of my abs-max pass: make my red.max visible, count the CTA done
+    // (a CTA with no abs-max item counts itself done before anything else:
+    // its quantise items wait for the count)
+    auto count_done = [&]() {
+        if (lane == 0) __threadfence();
+        bar_consumers();
+        if (threadIdx.x == 0) S.flag = (int)(atom_add_acq_rel(done_ctr, 1u) == target - 1u);
+        bar_consumers();
+        if (S.flag) op.after_phase_a_last(threadIdx.x);
+    };
+    if (na > 0 && my_a == 0) count_done();
     for (int i = 0; i < my_items; ++i) {
         const int s = i % NS;
         mbar_wait(&S.full[s], (uint32_t)(i / NS) & 1u);
@@ -614,20 +625,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const Op op, 
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&S.empty[s]);
-        if (i == my_a - 1 || (my_a == 0 && i == -1)) {
-            // end of my abs-max pass: make my red.max visible, count the CTA done
-            if (lane == 0) __threadfence();
-            bar_consumers();
-            if (threadIdx.x == 0) S.flag = (int)(atom_add_acq_rel(done_ctr, 1u) == target - 1u);
-            bar_consumers();
-            if (S.flag) op.after_phase_a_last(threadIdx.x);
-        }
-    }
-    if (my_a == 0 && na > 0) {  // a CTA with no abs-max items still counts as done
-        bar_consumers();
-        if (threadIdx.x == 0) S.flag = (int)(atom_add_acq_rel(done_ctr, 1u) == target - 1u);
-        bar_consumers();
-        if (S.flag) op.after_phase_a_last(threadIdx.x);
+        if (i == my_a - 1) count_done();
     }
     if (lane == 0) bulk_wait_all();
 }

@@ -130,9 +130,34 @@ __global__ void __launch_bounds__(256, 1) k_tmast(uint8_t *outp, size_t nbytes, 
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// persistent LDG stream: grid = SMs * k, each thread keeps 8 float4 in flight, items of R bytes
+__global__ void k_ldg_items(const uint8_t *in, size_t nbytes, int R, uint32_t *out)
+{
+    const size_t nitems = nbytes / R;
+    uint32_t mx = 0;
+    for (size_t w = blockIdx.x; w < nitems; w += gridDim.x) {
+        const float4 *p = reinterpret_cast<const float4 *>(in + w * R);
+        for (int base = 0; base < R / 16; base += 8 * blockDim.x) {
+            float4 v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                int j = base + threadIdx.x + k * blockDim.x;
+                if (j < R / 16) asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v[k].x), "=f"(v[k].y), "=f"(v[k].z), "=f"(v[k].w) : "l"(p + j));
+                else v[k] = make_float4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) mx = max(mx, max(max(__float_as_uint(v[k].x), __float_as_uint(v[k].y)), max(__float_as_uint(v[k].z), __float_as_uint(v[k].w))) & 0x7fffffffu);
+        }
+    }
+    mx = __reduce_max_sync(~0u, mx);
+    if ((threadIdx.x & 31) == 0 && mx == 0x12345678u) out[0] = mx;
+}
+
 int main(int argc, char **argv)
 {
-    const size_t nbytes = (size_t)1 << 30;  // 1 GiB per pass (>> L2)
+    const size_t nbytes = argc > 1 ? (size_t)atoll(argv[1]) : (size_t)1 << 30;
+    const bool quick = argc > 2;
+    printf("=== %zu bytes per pass\n", nbytes);
     uint8_t *a, *b;
     uint32_t *o;
     CK(cudaMalloc(&a, nbytes));
@@ -165,13 +190,20 @@ int main(int argc, char **argv)
         snprintf(nm, sizeof nm, "ldg v4x8 grid=%d x256", ctas);
         timeit([&] { k_ldg<<<ctas, 256>>>((const float4 *)a, nbytes / 16, o); }, nm, (double)nbytes);
     }
+    for (int k : {1, 2, 4, 8}) {
+        for (int R : {8192, 32768}) {
+            snprintf(nm, sizeof nm, "ldg persistent items R=%dK grid=%dxSM x256", R / 1024, k);
+            timeit([&] { k_ldg_items<<<k * sms, 256>>>(a, nbytes, R, o); }, nm, (double)nbytes);
+        }
+    }
     for (int ctas : {sms, 4 * sms, 16 * sms}) {
         snprintf(nm, sizeof nm, "stg v4 grid=%d x256", ctas);
         timeit([&] { k_stg<<<ctas, 256>>>((float4 *)b, nbytes / 16); }, nm, (double)nbytes);
     }
-    for (int pol = 0; pol < 3; ++pol) {
+    for (int pol = 0; pol < (quick ? 1 : 3); ++pol) {
         for (int R : {4096, 8192, 16384, 32768}) {
             for (int S : {2, 4, 6, 12, 24, 48}) {
+                if (quick && !(S == 4 || S == 6)) continue;
                 size_t smem = (size_t)S * R + 2 * S * 8 + 64;
                 if (smem > 220 * 1024) continue;
                 auto kern = pol == 0 ? k_tma<0> : pol == 1 ? k_tma<1> : k_tma<2>;

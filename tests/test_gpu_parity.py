@@ -94,9 +94,10 @@ def check(aps, orc, grads, e, m, hw, average=1, fused=False, ref=None):
 
 # ----------------------------------------------------------------- p = 1
 
-@pytest.fixture(params=["stream", "simple"])
+@pytest.fixture(params=["ldg", "tma", "simple"])
 def engine(request, monkeypatch):
-    """libaps kernel engine: persistent TMA-bulk kernels, or the simple grid kernels."""
+    """libaps kernel engine: grid kernels + fused LDG p = 1 kernel (default),
+    persistent TMA-bulk kernels, or grid kernels only."""
     monkeypatch.setenv("APS_ENGINE", request.param)
     return request.param
 
