@@ -268,7 +268,7 @@ __device__ __forceinline__ void absmax_chunk(const StageInfo &si, const float4 *
     if (warp == kConsWarps - 1 && lane < (si.cnt & 3))
         mx = max(mx, __float_as_uint(si.src[4 * n4 + lane]) & 0x7fffffffu);
     mx = __reduce_max_sync(0xffffffffu, mx);
-    if (lane == 0 && g0 < 4 * n4 + 4) red_max_u32(&amax[si.layer], mx);
+    if (lane == 0 && mx != 0u) red_max_u32(&amax[si.layer], mx);  // (0 never raises the max)
 }
 
 // a3/a4 (+ a7 when Fuse), consumer side, for the warp's chunk.  Codes go to
