@@ -42,7 +42,8 @@ struct aps_ctx {
     uint8_t *ws = nullptr;
     size_t ws_bytes = 0, need = 0;
     size_t off_packed = 0, off_recv = 0, off_items = 0, off_layers = 0, off_src = 0, off_dst = 0,
-           off_amax = 0, off_count = 0, off_eloc = 0, off_eglob = 0, off_ft = 0, off_flag = 0, off_amax2 = 0, off_done = 0;
+           off_amax = 0, off_count = 0, off_eloc = 0, off_eglob = 0, off_ft = 0, off_flag = 0, off_amax2 = 0, off_done = 0, off_iptr = 0;
+    bool iptr_valid = false;
     aps::DevTables t{};
     std::vector<const float *> src_cache;
     std::vector<float *> dst_cache;
@@ -95,6 +96,7 @@ aps_status upload_ptrs(aps_ctx *c, std::vector<P> &cache, P const *ptrs, size_t 
         if (same && cache[l] != ptrs[l]) same = false;
     }
     if (same) return APS_OK;
+    c->iptr_valid = false;
     cache.assign(ptrs, ptrs + c->n_layers);
     APS_CUDA(c, cudaMemcpyAsync(c->ws + off, cache.data(), sizeof(P) * (size_t)c->n_layers,
                                 cudaMemcpyHostToDevice, c->stream));
@@ -232,6 +234,7 @@ aps_status aps_init(aps_ctx **out, int exp_bits, int man_bits, int world_size, i
     c->off_flag = o;   o = align_up(o + 4);
     c->off_amax2 = o;  o = align_up(o + 8 * (size_t)n_layers);
     c->off_done = o;   o = align_up(o + 4);
+    c->off_iptr = o;   o = align_up(o + sizeof(aps::ItemPtr) * c->items.size());
     c->need = o;
     *out = c;
     return APS_OK;
@@ -265,6 +268,8 @@ aps_status aps_set_workspace(aps_ctx *c, void *dev, size_t bytes)
     t.flag = reinterpret_cast<uint32_t *>(c->ws + c->off_flag);
     t.amax2 = reinterpret_cast<uint32_t *>(c->ws + c->off_amax2);
     t.done = reinterpret_cast<uint32_t *>(c->ws + c->off_done);
+    t.iptr = reinterpret_cast<aps::ItemPtr *>(c->ws + c->off_iptr);
+    c->iptr_valid = false;
     c->gen = 0;
     c->done_target = 0;
     t.packed = c->ws + c->off_packed;
@@ -380,8 +385,12 @@ aps_status aps_sync_out(aps_ctx *c, const float *const *grads, float *const *out
         // one rank: FindMaxExp -> f~ -> Cast -> pack -> Cast back -> unscale in one launch
         if (aps_status s = upload_ptrs<const float *>(c, c->src_cache, grads, c->off_src)) return s;
         if (aps_status s = upload_ptrs<float *>(c, c->dst_cache, out, c->off_dst)) return s;
+        if (!c->iptr_valid) {
+            APS_CUDA(c, aps::launch_build_item_ptrs(c->t, c->stream));
+            c->iptr_valid = true;
+        }
         const int grid = aps::fused_p1_ldg_grid(c->e, c->m, c->hw, c->t.n_items);
-        const uint32_t tgt = c->done_target + (uint32_t)grid;
+        const uint32_t tgt = c->done_target + (uint32_t)grid * (uint32_t)aps::kFusedWarps;
         APS_CUDA(c, aps::launch_fused_p1_ldg(c->t, c->e, c->m, c->hw, average, c->gen, tgt, grid, c->stream));
         c->done_target = tgt;
         ++c->gen;

@@ -33,6 +33,13 @@ struct LayerDev {
     int64_t pad1;
 };
 
+// Per-call gradient / output address of every work item (rebuilt on the
+// device only when the caller's layer pointers change).
+struct ItemPtr {
+    const float *src;
+    float *dst;
+};
+
 struct DevTables {
     const Item *items;
     const LayerDev *layers;
@@ -46,6 +53,7 @@ struct DevTables {
     uint32_t *flag;           // non-finite flag
     uint32_t *amax2;          // [2][n_layers] abs-max accumulators of the stream engine (call parity)
     uint32_t *done;           // CTAs that finished the abs-max pass (monotone counter)
+    ItemPtr *iptr;            // [n_items] per-item addresses (fused LDG kernel)
     uint8_t *packed;          // packed codes
     int n_items;
     int n_layers;
@@ -84,6 +92,9 @@ cudaError_t launch_stream_fused_p1(const DevTables &t, int e, int m, bool hw, in
 // fused p = 1 on the LDG engine (aps_kernels.cu): cooperative grid of
 // fused_p1_ldg_grid(...) CTAs; `target` = done counter after the call.
 int fused_p1_ldg_grid(int e, int m, bool hw, int n_items);
+constexpr int kFusedWarps = kThreads / 32;  // the done counter advances by grid * kFusedWarps per call
+constexpr int kFusedSmemLayers = 8192;      // f~ table in shared memory up to this many layers
+cudaError_t launch_build_item_ptrs(const DevTables &t, cudaStream_t s);
 cudaError_t launch_fused_p1_ldg(const DevTables &t, int e, int m, bool hw, int average, uint32_t gen,
                                 uint32_t target, int grid, cudaStream_t s);
 

@@ -263,23 +263,52 @@ __device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t *p)
     return v;
 }
 
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t *p)
+{
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__global__ void build_item_ptrs_kernel(DevTables t)
+{
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < t.n_items; k += gridDim.x * blockDim.x) {
+        const Item it = t.items[k];
+        const int64_t begin = (int64_t)it.tile_begin * kTile;
+        t.iptr[k] = ItemPtr{t.src[it.layer] + begin, t.dst[it.layer] + begin};
+    }
+}
+
 template <class C, int NT>
 __global__ void __launch_bounds__(NT, kFusedCtasPerSm)
     fused_p1_ldg_kernel(DevTables t, C c, uint32_t *amax, uint32_t *amax_next, uint32_t target, int bias, int avg)
 {
+    extern __shared__ int32_t s_ft[];  // f~ per layer (when n_layers <= kFusedSmemLayers)
     __shared__ __align__(16) uint32_t s_codes[NT / 32][kTile];
     const int G = gridDim.x;
+    const int n = t.n_items;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint64_t keep, strm;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(strm));
     constexpr int kPer = kItemTiles * kTile / 4 / NT;  // float4 groups per thread in a full item
 
-    // ---------------- phase A: abs-max
-    for (int w = blockIdx.x; w < t.n_items; w += G) {
-        const Item it = t.items[w];
-        const float *g = t.src[it.layer] + (int64_t)it.tile_begin * kTile;
-        const float4 *g4 = reinterpret_cast<const float4 *>(g);
+    // ---------------- phase A: abs-max (descriptors prefetched one item ahead)
+    int w = blockIdx.x;
+    Item it{};
+    const float *src = nullptr;
+    if (w < n) {
+        it = t.items[w];
+        src = t.iptr[w].src;
+    }
+    for (; w < n; w += G) {
+        Item itn{};
+        const float *srcn = nullptr;
+        if (w + G < n) {
+            itn = t.items[w + G];
+            srcn = t.iptr[w + G].src;
+        }
+        const float4 *g4 = reinterpret_cast<const float4 *>(src);
         uint32_t mx = 0;
         if (it.cnt == kItemTiles * kTile) {
             float4 v[kPer];
@@ -290,48 +319,82 @@ __global__ void __launch_bounds__(NT, kFusedCtasPerSm)
         } else {
             const int n4 = it.cnt >> 2;
             for (int j = threadIdx.x; j < n4; j += NT) mx = max(mx, absbits4(ld_hint4(g4 + j, keep)));
-            if ((int)threadIdx.x < (it.cnt & 3)) mx = max(mx, __float_as_uint(g[4 * n4 + threadIdx.x]) & 0x7fffffffu);
+            if ((int)threadIdx.x < (it.cnt & 3)) mx = max(mx, __float_as_uint(src[4 * n4 + threadIdx.x]) & 0x7fffffffu);
         }
         mx = __reduce_max_sync(0xffffffffu, mx);
-        if (lane == 0) asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(&amax[it.layer]), "r"(mx) : "memory");
+        if (lane == 0 && mx) asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(&amax[it.layer]), "r"(mx) : "memory");
+        it = itn;
+        src = srcn;
     }
-    // ---------------- grid barrier: every abs-max folded in
-    if (lane == 0) __threadfence();
+
+    // ---------------- first phase-B item: descriptor and data in flight before the barrier
+    constexpr int B = C::kB;
+    int wb = blockIdx.x;
+    Item ib{};
+    ItemPtr pb{};
+    float4 v[kPer];
+    bool preloaded = false;
+    if (wb < n) {
+        ib = t.items[n - 1 - wb];
+        pb = t.iptr[n - 1 - wb];
+        if (ib.cnt == kItemTiles * kTile) {
+            const float4 *g4 = reinterpret_cast<const float4 *>(pb.src);
+#pragma unroll
+            for (int j = 0; j < kPer; ++j) v[j] = ld_hint4(g4 + threadIdx.x + j * NT, strm);
+            preloaded = true;
+        }
+    }
+
+    // ---------------- grid barrier: every warp's red.max ordered before its count
+    if (lane == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(t.done) : "memory");
+    if (threadIdx.x == 0)
+        while ((int)(ld_acquire_u32(t.done) - target) < 0) __nanosleep(32);
     __syncthreads();
-    if (threadIdx.x == 0) {
-        atomicAdd(t.done, 1u);
-        while ((int)(ld_relaxed_u32(t.done) - target) < 0) __nanosleep(64);
-        __threadfence();
+    const bool table = t.n_layers <= kFusedSmemLayers;
+    if (table || blockIdx.x == 0) {
+        for (int l = threadIdx.x; l < t.n_layers; l += NT) {
+            const int32_t E = exponent_of(ld_relaxed_u32(&amax[l]), 1);
+            const int ft = (E == INT32_MIN || E == INT32_MAX) ? 0 : bias - E;  // f~ (Alg. 1 line 4)
+            if (table) s_ft[l] = ft;
+            if (blockIdx.x == 0) {  // record E, f~, the non-finite flag; clear the next call's buffer
+                t.E_local[l] = E;
+                t.ftilde[l] = ft;
+                if (E == INT32_MAX) atomicOr(t.flag, 1u);
+                amax_next[l] = 0u;
+            }
+        }
     }
     __syncthreads();
 
     // ---------------- phase B: quantise + unscale, reverse order
-    constexpr int B = C::kB;
-    for (int w = blockIdx.x; w < t.n_items; w += G) {
-        const Item it = t.items[t.n_items - 1 - w];
-        const int l = it.layer;
-        const int32_t E = exponent_of(ld_relaxed_u32(&amax[l]), 1);
-        int ft = (E == INT32_MIN) ? 0 : bias - E;  // f~ = upper_bound_exp - E (Alg. 1 line 4)
-        if (E == INT32_MAX) ft = 0;
-        if (it.tile_begin == 0 && threadIdx.x == 0) {
-            t.E_local[l] = E;
-            t.ftilde[l] = ft;
-            if (E == INT32_MAX) atomicOr(t.flag, 1u);
-            amax_next[l] = 0u;
+    for (; wb < n; wb += G) {
+        Item ibn{};
+        ItemPtr pbn{};
+        if (wb + G < n) {
+            ibn = t.items[n - 1 - (wb + G)];
+            pbn = t.iptr[n - 1 - (wb + G)];
         }
-        const int64_t begin = (int64_t)it.tile_begin * kTile;
-        const float *g = t.src[l] + begin;
-        float *o = t.dst[l] + begin;
+        const int l = ib.layer;
+        int ft;
+        if (table) {
+            ft = s_ft[l];
+        } else {
+            const int32_t E = exponent_of(ld_relaxed_u32(&amax[l]), 1);
+            ft = (E == INT32_MIN || E == INT32_MAX) ? 0 : bias - E;
+        }
+        const float *g = pb.src;
+        float *o = pb.dst;
         const float4 *g4 = reinterpret_cast<const float4 *>(g);
         const Pow2 s(ft);
         const Unscale us(ft, 1, avg);
         if constexpr (B == 8 || B == 16 || B == 32) {
             using W = typename Word4<B>::T;
-            W *out = reinterpret_cast<W *>(t.packed + it.tile_pos * (16 * B));
-            if (it.cnt == kItemTiles * kTile && !s.wide) {
-                float4 v[kPer];
+            W *out = reinterpret_cast<W *>(t.packed + ib.tile_pos * (16 * B));
+            if (ib.cnt == kItemTiles * kTile && !s.wide) {
+                if (!preloaded) {
 #pragma unroll
-                for (int j = 0; j < kPer; ++j) v[j] = ld_hint4(g4 + threadIdx.x + j * NT, strm);
+                    for (int j = 0; j < kPer; ++j) v[j] = ld_hint4(g4 + threadIdx.x + j * NT, strm);
+                }
                 float4 *o4 = reinterpret_cast<float4 *>(o);
 #pragma unroll
                 for (int j = 0; j < kPer; ++j) {
@@ -342,29 +405,32 @@ __global__ void __launch_bounds__(NT, kFusedCtasPerSm)
                     o4[threadIdx.x + j * NT] = us.apply4(unpack4<B>(c, code));
                 }
             } else {
-                const int ng = it.n_tiles * (kTile / 4);
+                const int ng = ib.n_tiles * (kTile / 4);
                 for (int j = threadIdx.x; j < ng; j += NT) {
-                    const W code = pack4<B>(c, s.apply4(load_group(g, 4 * (int64_t)j, it.cnt)));
+                    const W code = pack4<B>(c, s.apply4(load_group(g, 4 * (int64_t)j, ib.cnt)));
                     out[j] = code;
-                    store_group(o, 4 * (int64_t)j, it.cnt, us.apply4(unpack4<B>(c, code)));
+                    store_group(o, 4 * (int64_t)j, ib.cnt, us.apply4(unpack4<B>(c, code)));
                 }
             }
         } else {
             const int b = c.b();
             uint32_t *codes = s_codes[warp];
-            uint32_t *outw = reinterpret_cast<uint32_t *>(t.packed) + it.tile_pos * (4 * b);
-            for (int tt = warp; tt < it.n_tiles; tt += NT / 32) {
+            uint32_t *outw = reinterpret_cast<uint32_t *>(t.packed) + ib.tile_pos * (4 * b);
+            for (int tt = warp; tt < ib.n_tiles; tt += NT / 32) {
                 const int64_t e0 = (int64_t)tt * kTile + lane * 4;
-                const float4 y = s.apply4(load_group(g, e0, it.cnt));
+                const float4 y = s.apply4(load_group(g, e0, ib.cnt));
                 const uint4 cd = make_uint4(c.enc(y.x), c.enc(y.y), c.enc(y.z), c.enc(y.w));
                 *reinterpret_cast<uint4 *>(codes + lane * 4) = cd;
                 __syncwarp();
                 uint32_t *ow = outw + (int64_t)tt * (4 * b);
                 for (int w2 = lane; w2 < 4 * b; w2 += 32) ow[w2] = assemble_word(codes, w2, b);
-                store_group(o, e0, it.cnt, us.apply4(make_float4(c.dec(cd.x), c.dec(cd.y), c.dec(cd.z), c.dec(cd.w))));
+                store_group(o, e0, ib.cnt, us.apply4(make_float4(c.dec(cd.x), c.dec(cd.y), c.dec(cd.z), c.dec(cd.w))));
                 __syncwarp();
             }
         }
+        preloaded = false;
+        ib = ibn;
+        pb = pbn;
     }
 }
 
@@ -481,17 +547,27 @@ cudaError_t launch_ring_reduce(uint8_t *own, const uint8_t *recv, int64_t n_tile
     });
 }
 
+static size_t fused_smem(const DevTables &t)
+{
+    return t.n_layers <= kFusedSmemLayers ? sizeof(int32_t) * (size_t)t.n_layers : 0;
+}
+
 cudaError_t launch_fused_p1_ldg(const DevTables &t, int e, int m, bool hw, int average, uint32_t gen,
                                 uint32_t target, int grid, cudaStream_t s)
 {
     const int bias = (1 << (e - 1)) - 1;
     uint32_t *cur = t.amax2 + (size_t)(gen & 1u) * t.n_layers;
     uint32_t *other = t.amax2 + (size_t)((gen + 1u) & 1u) * t.n_layers;
+    const size_t smem = fused_smem(t);
     return with_codec(e, m, hw, [&](auto c) -> cudaError_t {
         using C = decltype(c);
         auto kern = fused_p1_ldg_kernel<C, kThreads>;
+        if (smem > 48 * 1024) {
+            cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (err != cudaSuccess) return err;
+        }
         void *args[] = {const_cast<DevTables *>(&t), &c, &cur, &other, &target, const_cast<int *>(&bias), &average};
-        return cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(kThreads), args, 0, s);
+        return cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(kThreads), args, smem, s);
     });
 }
 
@@ -500,10 +576,17 @@ int fused_p1_ldg_grid(int e, int m, bool hw, int n_items)
     int per_sm = 0;
     with_codec(e, m, hw, [&](auto c) -> cudaError_t {
         using C = decltype(c);
-        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_p1_ldg_kernel<C, kThreads>, kThreads, 0);
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_p1_ldg_kernel<C, kThreads>, kThreads,
+                                                             sizeof(int32_t) * kFusedSmemLayers);
     });
     per_sm = std::max(1, std::min(per_sm, kFusedCtasPerSm));
     return std::max(1, std::min(n_items, sm_count() * per_sm));
+}
+
+cudaError_t launch_build_item_ptrs(const DevTables &t, cudaStream_t s)
+{
+    build_item_ptrs_kernel<<<(t.n_items + 255) / 256, 256, 0, s>>>(t);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_sim_max(int32_t *const *E_glob, const int32_t *const *E_local, int p, int n_layers,
