@@ -200,6 +200,10 @@ aps_status aps_debug_cast(const float *in, uint32_t *codes, int64_t n, int exp_b
                           int man_bits, int hw, void *cuda_stream);
 aps_status aps_debug_decode(const uint32_t *codes, float *out, int64_t n, int exp_bits,
                             int man_bits, int hw, void *cuda_stream);
+/* [sync] Per-CTA %globaltimer stamps (start, end of abs-max pass, after the
+ * grid barrier, end; 4 x uint64 per CTA, ns) of the last fused p = 1 launch
+ * run with APS_FUSED_FLAGS bit 16 set (profiling aid). */
+aps_status aps_debug_timeline(aps_ctx *ctx, uint64_t *host_out, int max_slots);
 /* Reduce step on its own: own[i] <- Cast(fl32(dec(recv[i]) + dec(own[i]))),
  * over n_tiles tiles of packed codes. */
 aps_status aps_debug_ring_reduce(uint8_t *own, const uint8_t *recv, int64_t n_tiles,

@@ -27,7 +27,7 @@ EXPORTS = [
     "aps_sync_host", "aps_status_sync", "aps_get_scales", "aps_get_packed", "aps_layout",
     "aps_ring_step", "aps_last_error", "aps_destroy", "aps_version", "aps_nccl_unique_id",
     "aps_nccl_comm_init", "aps_nccl_comm_destroy", "aps_sim_layer_scales", "aps_sim_allreduce",
-    "aps_debug_cast", "aps_debug_decode", "aps_debug_ring_reduce",
+    "aps_debug_cast", "aps_debug_decode", "aps_debug_ring_reduce", "aps_debug_timeline",
 ]
 
 
@@ -45,7 +45,8 @@ def load(path: Path | str | None = None):
     global _lib
     if _lib is not None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    import os
+    p = Path(path or os.environ.get("APS_LIB") or LIB_PATH)  # APS_LIB: A/B another build
     if not p.exists():
         raise ImportError(f"libaps.so not built at {p}; run __graft_entry__.build()")
     L = ctypes.CDLL(str(p))
@@ -79,6 +80,7 @@ def load(path: Path | str | None = None):
         "aps_debug_cast": ([vp, vp, i64, i32, i32, i32, vp], i32),
         "aps_debug_decode": ([vp, vp, i64, i32, i32, i32, vp], i32),
         "aps_debug_ring_reduce": ([vp, vp, i64, i32, i32, i32, vp], i32),
+        "aps_debug_timeline": ([vp, vp, i32], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -227,6 +229,13 @@ class ApsContext:
         self._check(self.L.aps_get_packed(self.h, ctypes.byref(ptr), ctypes.byref(nb)), "aps_get_packed")
         off = ptr.value - self.workspace.data_ptr()
         return self.workspace[off:off + nb.value]
+
+    def timeline(self):
+        """Per-CTA globaltimer stamps of the last fused launch (APS_FUSED_FLAGS & 16)."""
+        import numpy as np
+        out = np.zeros(4 * 2048, dtype=np.uint64)
+        self._check(self.L.aps_debug_timeline(self.h, out.ctypes.data, out.size), "aps_debug_timeline")
+        return out.reshape(-1, 4)
 
     def set_hw_convert(self, enable: bool):
         self._check(self.L.aps_set_hw_convert(self.h, int(enable)), "aps_set_hw_convert")

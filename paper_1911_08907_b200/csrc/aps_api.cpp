@@ -42,7 +42,8 @@ struct aps_ctx {
     uint8_t *ws = nullptr;
     size_t ws_bytes = 0, need = 0;
     size_t off_packed = 0, off_recv = 0, off_items = 0, off_layers = 0, off_src = 0, off_dst = 0,
-           off_amax = 0, off_count = 0, off_eloc = 0, off_eglob = 0, off_ft = 0, off_flag = 0, off_amax2 = 0, off_done = 0, off_iptr = 0;
+           off_amax = 0, off_count = 0, off_eloc = 0, off_eglob = 0, off_ft = 0, off_flag = 0, off_amax2 = 0, off_done = 0, off_iptr = 0, off_tl = 0, off_claim = 0;
+    uint32_t claim_base = 0;   // value of the fused kernel's claim counters at the next launch
     bool iptr_valid = false;
     aps::DevTables t{};
     std::vector<const float *> src_cache;
@@ -235,6 +236,8 @@ aps_status aps_init(aps_ctx **out, int exp_bits, int man_bits, int world_size, i
     c->off_amax2 = o;  o = align_up(o + 8 * (size_t)n_layers);
     c->off_done = o;   o = align_up(o + 4);
     c->off_iptr = o;   o = align_up(o + sizeof(aps::ItemPtr) * c->items.size());
+    c->off_tl = o;     o = align_up(o + sizeof(uint64_t) * aps::kTimelineSlots);
+    c->off_claim = o;  o = align_up(o + 2 * sizeof(uint32_t));
     c->need = o;
     *out = c;
     return APS_OK;
@@ -269,6 +272,9 @@ aps_status aps_set_workspace(aps_ctx *c, void *dev, size_t bytes)
     t.amax2 = reinterpret_cast<uint32_t *>(c->ws + c->off_amax2);
     t.done = reinterpret_cast<uint32_t *>(c->ws + c->off_done);
     t.iptr = reinterpret_cast<aps::ItemPtr *>(c->ws + c->off_iptr);
+    t.timeline = reinterpret_cast<uint64_t *>(c->ws + c->off_tl);
+    t.claim = reinterpret_cast<uint32_t *>(c->ws + c->off_claim);
+    c->claim_base = 0;
     c->iptr_valid = false;
     c->gen = 0;
     c->done_target = 0;
@@ -391,8 +397,10 @@ aps_status aps_sync_out(aps_ctx *c, const float *const *grads, float *const *out
         }
         const int grid = aps::fused_p1_ldg_grid(c->e, c->m, c->hw, c->t.n_items);
         const uint32_t tgt = c->done_target + (uint32_t)grid * (uint32_t)aps::kFusedWarps;
-        APS_CUDA(c, aps::launch_fused_p1_ldg(c->t, c->e, c->m, c->hw, average, c->gen, tgt, grid, c->stream));
+        APS_CUDA(c, aps::launch_fused_p1_ldg(c->t, c->e, c->m, c->hw, average, c->gen, tgt, c->claim_base, grid,
+                                             c->stream));
         c->done_target = tgt;
+        c->claim_base += (uint32_t)(c->t.n_items + grid);  // every CTA's last claim overshoots once
         ++c->gen;
         c->phase = kReduced;
         return APS_OK;
@@ -582,6 +590,16 @@ aps_status aps_debug_decode(const uint32_t *codes, float *out, int64_t n, int e,
     if (hw && !aps::hw_available(e, m)) return APS_ERR_FORMAT;
     return aps::launch_debug_decode(codes, out, n, e, m, hw != 0, static_cast<cudaStream_t>(stream)) == cudaSuccess
                ? APS_OK : APS_ERR_CUDA;
+}
+
+aps_status aps_debug_timeline(aps_ctx *c, uint64_t *host_out, int max_slots)
+{
+    if (aps_status s = need_ws(c)) return s;
+    if (!host_out || max_slots < 0) return APS_ERR_ARG;
+    const size_t n = (size_t)std::min(max_slots, aps::kTimelineSlots);
+    APS_CUDA(c, cudaMemcpyAsync(host_out, c->t.timeline, n * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
+    APS_CUDA(c, cudaStreamSynchronize(c->stream));
+    return APS_OK;
 }
 
 aps_status aps_debug_ring_reduce(uint8_t *own, const uint8_t *recv, int64_t n_tiles, int e, int m, int hw,

@@ -54,6 +54,8 @@ struct DevTables {
     uint32_t *amax2;          // [2][n_layers] abs-max accumulators of the stream engine (call parity)
     uint32_t *done;           // CTAs that finished the abs-max pass (monotone counter)
     ItemPtr *iptr;            // [n_items] per-item addresses (fused LDG kernel)
+    uint64_t *timeline;       // [kTimelineSlots] per-CTA phase stamps (flag 16)
+    uint32_t *claim;          // [2] monotone work-claim counters of the fused kernel (phase A, phase B)
     uint8_t *packed;          // packed codes
     int n_items;
     int n_layers;
@@ -93,10 +95,14 @@ cudaError_t launch_stream_fused_p1(const DevTables &t, int e, int m, bool hw, in
 // fused_p1_ldg_grid(...) CTAs; `target` = done counter after the call.
 int fused_p1_ldg_grid(int e, int m, bool hw, int n_items);
 constexpr int kFusedWarps = kThreads / 32;  // the done counter advances by grid * kFusedWarps per call
+constexpr int kFusedDefaultFlags = 2 | 32;       // fused kernel tuning flags (aps_kernels.cu; measured in DESIGN.md)
+constexpr int kTimelineSlots = 4 * 2048;     // globaltimer stamps (4 per CTA) of the last fused launch
 constexpr int kFusedSmemLayers = 8192;      // f~ table in shared memory up to this many layers
 cudaError_t launch_build_item_ptrs(const DevTables &t, cudaStream_t s);
+// claim_base: value of both claim counters at launch (each call advances
+// them by n_items + grid: every CTA's last claim overshoots once).
 cudaError_t launch_fused_p1_ldg(const DevTables &t, int e, int m, bool hw, int average, uint32_t gen,
-                                uint32_t target, int grid, cudaStream_t s);
+                                uint32_t target, uint32_t claim_base, int grid, cudaStream_t s);
 
 // true when (e,m) has a hardware converter that is exact on the APS path
 inline bool hw_available(int e, int m) { return (e == 5 && m == 2) || (e == 4 && m == 3); }

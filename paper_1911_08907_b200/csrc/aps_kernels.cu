@@ -12,6 +12,7 @@
 #include <cstdint>
 #include <climits>
 #include <algorithm>
+#include <cstdlib>
 
 #include "aps_device.cuh"
 
@@ -281,8 +282,26 @@ __global__ void build_item_ptrs_kernel(DevTables t)
 
 template <class C, int NT>
 __global__ void __launch_bounds__(NT, kFusedCtasPerSm)
-    fused_p1_ldg_kernel(DevTables t, C c, uint32_t *amax, uint32_t *amax_next, uint32_t target, int bias, int avg)
+    fused_p1_ldg_kernel(DevTables t, C c, uint32_t *amax, uint32_t *amax_next, uint32_t target, uint32_t claim_base,
+                        int bias, int avg, int flags)
 {
+    // flags (tuning; measured in DESIGN.md "fused p = 1 kernel"):
+    //   2  f~ table in shared memory (else one abs-max load per item)
+    //   16 record %globaltimer at start / end of phase A / after the barrier / end (per CTA)
+    //   32 dynamic work claiming (atomic counters, claim prefetched one item ahead) instead of
+    //      static round-robin: the items are equal, but CTAs sharing an SM and HBM do not
+    //      progress equally (static: phase-A finish times spread 14-26 us)
+    const bool f_table = flags & 2, f_dynamic = flags & 32;
+    __shared__ int s_claim[2];
+    const bool f_timeline = (flags & 16) && blockIdx.x * 4 + 3 < kTimelineSlots;
+    auto stamp = [&](int k) {
+        if (f_timeline && threadIdx.x == 0) {
+            uint64_t ns;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+            t.timeline[blockIdx.x * 4 + k] = ns;
+        }
+    };
+    stamp(0);
     extern __shared__ int32_t s_ft[];  // f~ per layer (when n_layers <= kFusedSmemLayers)
     __shared__ __align__(16) uint32_t s_codes[NT / 32][kTile];
     const int G = gridDim.x;
@@ -293,21 +312,28 @@ __global__ void __launch_bounds__(NT, kFusedCtasPerSm)
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(strm));
     constexpr int kPer = kItemTiles * kTile / 4 / NT;  // float4 groups per thread in a full item
 
-    // ---------------- phase A: abs-max (descriptors prefetched one item ahead)
-    int w = blockIdx.x;
-    Item it{};
-    const float *src = nullptr;
-    if (w < n) {
-        it = t.items[w];
-        src = t.iptr[w].src;
-    }
-    for (; w < n; w += G) {
-        Item itn{};
-        const float *srcn = nullptr;
-        if (w + G < n) {
-            itn = t.items[w + G];
-            srcn = t.iptr[w + G].src;
-        }
+    // ---------------- phase A: abs-max
+    // next work item: static round-robin, or claimed from counter `which`
+    auto first_item = [&](int which) -> int {
+        if (!f_dynamic) return blockIdx.x;
+        if (threadIdx.x == 0) s_claim[0] = (int)(atomicAdd(&t.claim[which], 1u) - claim_base);
+        __syncthreads();
+        return s_claim[0];
+    };
+    int slot = 0;
+    auto prefetch_claim = [&](int which) {
+        if (f_dynamic && threadIdx.x == 0) s_claim[slot ^ 1] = (int)(atomicAdd(&t.claim[which], 1u) - claim_base);
+    };
+    auto next_item = [&](int w) -> int {
+        if (!f_dynamic) return w + G;
+        __syncthreads();
+        slot ^= 1;
+        return s_claim[slot];
+    };
+    for (int w = first_item(0); w < n; w = next_item(w)) {
+        prefetch_claim(0);
+        const Item it = t.items[w];
+        const float *src = t.iptr[w].src;
         const float4 *g4 = reinterpret_cast<const float4 *>(src);
         uint32_t mx = 0;
         if (it.cnt == kItemTiles * kTile) {
@@ -323,35 +349,20 @@ __global__ void __launch_bounds__(NT, kFusedCtasPerSm)
         }
         mx = __reduce_max_sync(0xffffffffu, mx);
         if (lane == 0 && mx) asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(&amax[it.layer]), "r"(mx) : "memory");
-        it = itn;
-        src = srcn;
     }
-
-    // ---------------- first phase-B item: descriptor and data in flight before the barrier
+    stamp(1);
     constexpr int B = C::kB;
-    int wb = blockIdx.x;
-    Item ib{};
-    ItemPtr pb{};
-    float4 v[kPer];
-    bool preloaded = false;
-    if (wb < n) {
-        ib = t.items[n - 1 - wb];
-        pb = t.iptr[n - 1 - wb];
-        if (ib.cnt == kItemTiles * kTile) {
-            const float4 *g4 = reinterpret_cast<const float4 *>(pb.src);
-#pragma unroll
-            for (int j = 0; j < kPer; ++j) v[j] = ld_hint4(g4 + threadIdx.x + j * NT, strm);
-            preloaded = true;
-        }
-    }
 
     // ---------------- grid barrier: every warp's red.max ordered before its count
-    if (lane == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(t.done) : "memory");
+    if (lane == 0) __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) atomicAdd(t.done, (uint32_t)(NT / 32));
     if (threadIdx.x == 0)
         while ((int)(ld_acquire_u32(t.done) - target) < 0) __nanosleep(32);
     __syncthreads();
-    const bool table = t.n_layers <= kFusedSmemLayers;
-    if (table || blockIdx.x == 0) {
+    stamp(2);
+    const bool table = f_table && t.n_layers <= kFusedSmemLayers;
+    if (table || blockIdx.x == 0) {  // (without the table, CTA 0 still records E / f~ for every layer)
         for (int l = threadIdx.x; l < t.n_layers; l += NT) {
             const int32_t E = exponent_of(ld_relaxed_u32(&amax[l]), 1);
             const int ft = (E == INT32_MIN || E == INT32_MAX) ? 0 : bias - E;  // f~ (Alg. 1 line 4)
@@ -367,13 +378,11 @@ __global__ void __launch_bounds__(NT, kFusedCtasPerSm)
     __syncthreads();
 
     // ---------------- phase B: quantise + unscale, reverse order
-    for (; wb < n; wb += G) {
-        Item ibn{};
-        ItemPtr pbn{};
-        if (wb + G < n) {
-            ibn = t.items[n - 1 - (wb + G)];
-            pbn = t.iptr[n - 1 - (wb + G)];
-        }
+    slot = 0;
+    for (int wb = first_item(1); wb < n; wb = next_item(wb)) {
+        prefetch_claim(1);
+        const Item ib = t.items[n - 1 - wb];
+        const ItemPtr pb = t.iptr[n - 1 - wb];
         const int l = ib.layer;
         int ft;
         if (table) {
@@ -391,10 +400,9 @@ __global__ void __launch_bounds__(NT, kFusedCtasPerSm)
             using W = typename Word4<B>::T;
             W *out = reinterpret_cast<W *>(t.packed + ib.tile_pos * (16 * B));
             if (ib.cnt == kItemTiles * kTile && !s.wide) {
-                if (!preloaded) {
+                float4 v[kPer];
 #pragma unroll
-                    for (int j = 0; j < kPer; ++j) v[j] = ld_hint4(g4 + threadIdx.x + j * NT, strm);
-                }
+                for (int j = 0; j < kPer; ++j) v[j] = ld_hint4(g4 + threadIdx.x + j * NT, strm);
                 float4 *o4 = reinterpret_cast<float4 *>(o);
 #pragma unroll
                 for (int j = 0; j < kPer; ++j) {
@@ -428,10 +436,8 @@ __global__ void __launch_bounds__(NT, kFusedCtasPerSm)
                 __syncwarp();
             }
         }
-        preloaded = false;
-        ib = ibn;
-        pb = pbn;
     }
+    stamp(3);
 }
 
 // ------------------------------------------------------------------ sim: MAX exchange of E
@@ -553,7 +559,7 @@ static size_t fused_smem(const DevTables &t)
 }
 
 cudaError_t launch_fused_p1_ldg(const DevTables &t, int e, int m, bool hw, int average, uint32_t gen,
-                                uint32_t target, int grid, cudaStream_t s)
+                                uint32_t target, uint32_t claim_base, int grid, cudaStream_t s)
 {
     const int bias = (1 << (e - 1)) - 1;
     uint32_t *cur = t.amax2 + (size_t)(gen & 1u) * t.n_layers;
@@ -566,7 +572,10 @@ cudaError_t launch_fused_p1_ldg(const DevTables &t, int e, int m, bool hw, int a
             cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (err != cudaSuccess) return err;
         }
-        void *args[] = {const_cast<DevTables *>(&t), &c, &cur, &other, &target, const_cast<int *>(&bias), &average};
+        int flags = kFusedDefaultFlags;
+        if (const char *env = std::getenv("APS_FUSED_FLAGS")) flags = std::atoi(env);
+        void *args[] = {const_cast<DevTables *>(&t), &c, &cur, &other, &target, &claim_base, const_cast<int *>(&bias),
+                        &average, &flags};
         return cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(kThreads), args, smem, s);
     });
 }
