@@ -400,7 +400,8 @@ aps_status aps_sync_out(aps_ctx *c, const float *const *grads, float *const *out
         APS_CUDA(c, aps::launch_fused_p1_ldg(c->t, c->e, c->m, c->hw, average, c->gen, tgt, c->claim_base, grid,
                                              c->stream));
         c->done_target = tgt;
-        c->claim_base += (uint32_t)(c->t.n_items + grid);  // every CTA's last claim overshoots once
+        // each call claims every unit once and every CTA overshoots once
+        c->claim_base += (uint32_t)(c->t.n_items * (aps::kItemTiles / aps::kFusedUnitTiles) + grid);
         ++c->gen;
         c->phase = kReduced;
         return APS_OK;

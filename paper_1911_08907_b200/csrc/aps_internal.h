@@ -95,8 +95,9 @@ cudaError_t launch_stream_fused_p1(const DevTables &t, int e, int m, bool hw, in
 // fused_p1_ldg_grid(...) CTAs; `target` = done counter after the call.
 int fused_p1_ldg_grid(int e, int m, bool hw, int n_items);
 constexpr int kFusedWarps = kThreads / 32;  // the done counter advances by grid * kFusedWarps per call
-constexpr int kFusedDefaultFlags = 2 | 32;       // fused kernel tuning flags (aps_kernels.cu; measured in DESIGN.md)
+constexpr int kFusedDefaultFlags = 2 | 32 | 64;       // fused kernel tuning flags (aps_kernels.cu; measured in DESIGN.md)
 constexpr int kTimelineSlots = 4 * 2048;     // globaltimer stamps (4 per CTA) of the last fused launch
+constexpr int kFusedUnitTiles = 64;        // fused kernel claim unit (tiles): a whole item (16 KB units measured slower)
 constexpr int kFusedSmemLayers = 8192;      // f~ table in shared memory up to this many layers
 cudaError_t launch_build_item_ptrs(const DevTables &t, cudaStream_t s);
 // claim_base: value of both claim counters at launch (each call advances

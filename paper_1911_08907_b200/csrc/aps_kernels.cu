@@ -271,6 +271,29 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t *p)
     return v;
 }
 
+__device__ __forceinline__ void st_hint4(float4 *p, float4 v, uint64_t pol)
+{
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(v.x),
+                 "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ void st_hint(uint32_t *p, uint32_t v, uint64_t pol)
+{
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_hint(uint2 *p, uint2 v, uint64_t pol)
+{
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.u32 [%0], {%1, %2}, %3;" ::"l"(p), "r"(v.x), "r"(v.y),
+                 "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ void st_hint(uint4 *p, uint4 v, uint64_t pol)
+{
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(v.x),
+                 "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol)
+                 : "memory");
+}
+
 __global__ void build_item_ptrs_kernel(DevTables t)
 {
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < t.n_items; k += gridDim.x * blockDim.x) {
@@ -291,7 +314,11 @@ __global__ void __launch_bounds__(NT, kFusedCtasPerSm)
     //   32 dynamic work claiming (atomic counters, claim prefetched one item ahead) instead of
     //      static round-robin: the items are equal, but CTAs sharing an SM and HBM do not
     //      progress equally (static: phase-A finish times spread 14-26 us)
-    const bool f_table = flags & 2, f_dynamic = flags & 32;
+    //   64 output and code stores with an L2 evict_first hint (keep the gradients phase A left
+    //      in L2 for phase B's second read)
+    // (measured and dropped: per-warp release counting, loading the first phase-B item before the
+    //  barrier, descriptor prefetch, 16 KB claim units, L2 bulk prefetch of the next claim)
+    const bool f_table = flags & 2, f_dynamic = flags & 32, f_st_hint = flags & 64;
     __shared__ int s_claim[2];
     const bool f_timeline = (flags & 16) && blockIdx.x * 4 + 3 < kTimelineSlots;
     auto stamp = [&](int k) {
@@ -310,7 +337,30 @@ __global__ void __launch_bounds__(NT, kFusedCtasPerSm)
     uint64_t keep, strm;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(strm));
-    constexpr int kPer = kItemTiles * kTile / 4 / NT;  // float4 groups per thread in a full item
+    constexpr int kPer = kFusedUnitTiles * kTile / 4 / NT;  // float4 groups per thread in a full unit
+    constexpr int kSub = kItemTiles / kFusedUnitTiles;       // claim units per work item
+    const int nu = n * kSub;                                 // claim units (some empty: short items)
+    // unit u = tiles [sub * kFusedUnitTiles, ...) of item u / kSub
+    struct Unit {
+        int layer, cnt, n_tiles;
+        int64_t tile_pos;
+        const float *src;
+        float *dst;
+    };
+    auto unit = [&](int u) -> Unit {
+        const int k = u / kSub, sub = u - k * kSub;
+        const Item it = t.items[k];
+        const ItemPtr p = t.iptr[k];
+        Unit x;
+        const int t0 = sub * kFusedUnitTiles;
+        x.layer = it.layer;
+        x.n_tiles = min(kFusedUnitTiles, it.n_tiles - t0);
+        x.cnt = min(kFusedUnitTiles * kTile, it.cnt - t0 * kTile);
+        x.tile_pos = it.tile_pos + t0;
+        x.src = p.src + (int64_t)t0 * kTile;
+        x.dst = p.dst + (int64_t)t0 * kTile;
+        return x;
+    };
 
     // ---------------- phase A: abs-max
     // next work item: static round-robin, or claimed from counter `which`
@@ -322,7 +372,10 @@ __global__ void __launch_bounds__(NT, kFusedCtasPerSm)
     };
     int slot = 0;
     auto prefetch_claim = [&](int which) {
-        if (f_dynamic && threadIdx.x == 0) s_claim[slot ^ 1] = (int)(atomicAdd(&t.claim[which], 1u) - claim_base);
+        if (f_dynamic && threadIdx.x == 0) {
+            const int u = (int)(atomicAdd(&t.claim[which], 1u) - claim_base);
+            s_claim[slot ^ 1] = u;
+        }
     };
     auto next_item = [&](int w) -> int {
         if (!f_dynamic) return w + G;
@@ -330,13 +383,14 @@ __global__ void __launch_bounds__(NT, kFusedCtasPerSm)
         slot ^= 1;
         return s_claim[slot];
     };
-    for (int w = first_item(0); w < n; w = next_item(w)) {
+    for (int w = first_item(0); w < nu; w = next_item(w)) {
         prefetch_claim(0);
-        const Item it = t.items[w];
-        const float *src = t.iptr[w].src;
+        const Unit it = unit(w);
+        if (it.cnt <= 0) continue;  // past the end of a short item (uniform across the CTA)
+        const float *src = it.src;
         const float4 *g4 = reinterpret_cast<const float4 *>(src);
         uint32_t mx = 0;
-        if (it.cnt == kItemTiles * kTile) {
+        if (it.cnt == kFusedUnitTiles * kTile) {
             float4 v[kPer];
 #pragma unroll
             for (int j = 0; j < kPer; ++j) v[j] = ld_hint4(g4 + threadIdx.x + j * NT, keep);
@@ -379,10 +433,11 @@ __global__ void __launch_bounds__(NT, kFusedCtasPerSm)
 
     // ---------------- phase B: quantise + unscale, reverse order
     slot = 0;
-    for (int wb = first_item(1); wb < n; wb = next_item(wb)) {
+    for (int wb = first_item(1); wb < nu; wb = next_item(wb)) {
         prefetch_claim(1);
-        const Item ib = t.items[n - 1 - wb];
-        const ItemPtr pb = t.iptr[n - 1 - wb];
+        const Unit ib = unit(nu - 1 - wb);
+        if (ib.cnt <= 0) continue;
+        const Unit &pb = ib;
         const int l = ib.layer;
         int ft;
         if (table) {
@@ -399,7 +454,7 @@ __global__ void __launch_bounds__(NT, kFusedCtasPerSm)
         if constexpr (B == 8 || B == 16 || B == 32) {
             using W = typename Word4<B>::T;
             W *out = reinterpret_cast<W *>(t.packed + ib.tile_pos * (16 * B));
-            if (ib.cnt == kItemTiles * kTile && !s.wide) {
+            if (ib.cnt == kFusedUnitTiles * kTile && !s.wide) {
                 float4 v[kPer];
 #pragma unroll
                 for (int j = 0; j < kPer; ++j) v[j] = ld_hint4(g4 + threadIdx.x + j * NT, strm);
@@ -409,8 +464,14 @@ __global__ void __launch_bounds__(NT, kFusedCtasPerSm)
                     const float4 y = make_float4(__fmul_rn(v[j].x, s.f), __fmul_rn(v[j].y, s.f), __fmul_rn(v[j].z, s.f),
                                                  __fmul_rn(v[j].w, s.f));
                     const W code = pack4<B>(c, y);
-                    out[threadIdx.x + j * NT] = code;
-                    o4[threadIdx.x + j * NT] = us.apply4(unpack4<B>(c, code));
+                    const float4 r = us.apply4(unpack4<B>(c, code));
+                    if (f_st_hint) {
+                        st_hint(out + threadIdx.x + j * NT, code, strm);
+                        st_hint4(o4 + threadIdx.x + j * NT, r, strm);
+                    } else {
+                        out[threadIdx.x + j * NT] = code;
+                        o4[threadIdx.x + j * NT] = r;
+                    }
                 }
             } else {
                 const int ng = ib.n_tiles * (kTile / 4);
