@@ -207,7 +207,7 @@ def run_reference(args):
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32->u8 codes",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64/f32 (oracle)",
         "data": "synthetic", "config": {"workload": name, "format": f"1/{e}/{m}", "ranks": p,
                                         "sample": sample_desc},
         "cpu_baseline": {"value": round(value, 6), "unit": UNIT, "cores": 1, "kind": "oracle",
@@ -348,7 +348,11 @@ def main():
         tr = traffic.get(dom.split(" ")[0])
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": tr, "kernel": dom,
-                "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)"}
+                "algorithmic_bytes_per_launch": int(dbytes),
+                "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
+                "traffic_note": "ncu dram read+write per launch (profiles/ncu_traffic.json); below the "
+                                "algorithmic bytes because phase B re-reads part of the gradients from L2 "
+                                "and dirty output lines are still in L2 when the kernel ends"}
 
     # -------- e2e through aps_sync_host (pinned host buffers, copies inside)
     hin = [torch.from_numpy(a).pin_memory() for a in host]
@@ -378,7 +382,8 @@ def main():
     result = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": max(args.warmup, 3), "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32->u8 codes" if b == 8 else f"f32->{b}-bit codes",
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "wire_dtype": f"{b}-bit 1/{e}/{m} codes",
         "data": "synthetic (seeded normal per layer, binade spread 2^-24..2^-4, 0.5% zeros)",
         "config": {"workload": name, "format": f"1/{e}/{m}", "n_layers": len(numels), "elements": L,
                    "ranks": world, "hw_convert": ctx_hw(ctx, args), "engine": os.environ.get("APS_ENGINE", "ldg"), "l2": "flushed (256 MiB write + 256 MiB read) between timed steps"
