@@ -42,7 +42,10 @@ struct aps_ctx {
     uint8_t *ws = nullptr;
     size_t ws_bytes = 0, need = 0;
     size_t off_packed = 0, off_recv = 0, off_items = 0, off_layers = 0, off_src = 0, off_dst = 0,
-           off_amax = 0, off_count = 0, off_eloc = 0, off_eglob = 0, off_ft = 0, off_flag = 0, off_amax2 = 0, off_done = 0, off_iptr = 0, off_tl = 0, off_claim = 0;
+           off_amax = 0, off_count = 0, off_eloc = 0, off_eglob = 0, off_ft = 0, off_flag = 0, off_amax2 = 0, off_done = 0, off_iptr = 0, off_tl = 0, off_claim = 0, off_ldone = 0;
+    uint32_t wave_calls = 0;    // wavefront launches so far (per-layer counter targets)
+    uint32_t wave_claim_base = 0;
+    int max_layer_items = 0;
     uint32_t claim_base = 0;   // value of the fused kernel's claim counters at the next launch
     bool iptr_valid = false;
     aps::DevTables t{};
@@ -237,7 +240,9 @@ aps_status aps_init(aps_ctx **out, int exp_bits, int man_bits, int world_size, i
     c->off_done = o;   o = align_up(o + 4);
     c->off_iptr = o;   o = align_up(o + sizeof(aps::ItemPtr) * c->items.size());
     c->off_tl = o;     o = align_up(o + sizeof(uint64_t) * aps::kTimelineSlots);
-    c->off_claim = o;  o = align_up(o + 2 * sizeof(uint32_t));
+    c->off_claim = o;  o = align_up(o + 3 * sizeof(uint32_t));
+    c->off_ldone = o;  o = align_up(o + 4 * (size_t)n_layers);
+    for (const auto &L : c->layers) c->max_layer_items = std::max(c->max_layer_items, (int)L.n_items);
     c->need = o;
     *out = c;
     return APS_OK;
@@ -274,6 +279,9 @@ aps_status aps_set_workspace(aps_ctx *c, void *dev, size_t bytes)
     t.iptr = reinterpret_cast<aps::ItemPtr *>(c->ws + c->off_iptr);
     t.timeline = reinterpret_cast<uint64_t *>(c->ws + c->off_tl);
     t.claim = reinterpret_cast<uint32_t *>(c->ws + c->off_claim);
+    t.layer_done = reinterpret_cast<uint32_t *>(c->ws + c->off_ldone);
+    c->wave_calls = 0;
+    c->wave_claim_base = 0;
     c->claim_base = 0;
     c->iptr_valid = false;
     c->gen = 0;
@@ -396,6 +404,21 @@ aps_status aps_sync_out(aps_ctx *c, const float *const *grads, float *const *out
             c->iptr_valid = true;
         }
         const int grid = aps::fused_p1_ldg_grid(c->e, c->m, c->hw, c->t.n_items);
+        const char *sched = std::getenv("APS_FUSED_SCHEDULE");
+        if (!sched || std::strcmp(sched, "barrier") != 0) {
+            // wavefront: quantise items trail their abs-max items by D positions
+            const int lag = std::min(c->t.n_items, c->max_layer_items + grid);
+            int split = 0;  // quarter-split tail units: measured slower
+            if (const char *env = std::getenv("APS_FUSED_SPLIT")) split = std::min(lag, std::max(0, std::atoi(env)));
+            APS_CUDA(c, aps::launch_fused_p1_wave(c->t, c->e, c->m, c->hw, average, c->gen, c->wave_claim_base,
+                                                  c->wave_calls, lag, split, grid, c->stream));
+            // every unit is claimed once and every CTA's last claim overshoots once
+            c->wave_claim_base += (uint32_t)(2 * c->t.n_items + 3 * split + grid);
+            ++c->wave_calls;
+            ++c->gen;
+            c->phase = kReduced;
+            return APS_OK;
+        }
         const uint32_t tgt = c->done_target + (uint32_t)grid * (uint32_t)aps::kFusedWarps;
         APS_CUDA(c, aps::launch_fused_p1_ldg(c->t, c->e, c->m, c->hw, average, c->gen, tgt, c->claim_base, grid,
                                              c->stream));

@@ -55,7 +55,8 @@ struct DevTables {
     uint32_t *done;           // CTAs that finished the abs-max pass (monotone counter)
     ItemPtr *iptr;            // [n_items] per-item addresses (fused LDG kernel)
     uint64_t *timeline;       // [kTimelineSlots] per-CTA phase stamps (flag 16)
-    uint32_t *claim;          // [2] monotone work-claim counters of the fused kernel (phase A, phase B)
+    uint32_t *claim;          // [3] monotone work-claim counters: barrier kernel phase A, phase B; wavefront
+    uint32_t *layer_done;     // [n_layers] monotone per-layer abs-max completion counters (wavefront kernel)
     uint8_t *packed;          // packed codes
     int n_items;
     int n_layers;
@@ -100,6 +101,12 @@ constexpr int kTimelineSlots = 4 * 2048;     // globaltimer stamps (4 per CTA) o
 constexpr int kFusedUnitTiles = 64;        // fused kernel claim unit (tiles): a whole item (16 KB units measured slower)
 constexpr int kFusedSmemLayers = 8192;      // f~ table in shared memory up to this many layers
 cudaError_t launch_build_item_ptrs(const DevTables &t, cudaStream_t s);
+// wavefront variant (no grid barrier): claim_base advances by 2 * n_items + grid per call;
+// call_no = wavefront calls before this one on these counters; lag = D positions.
+// split = the last `split` quantise items are claimed as 4 quarter units each
+// (claim_base then advances by 2 * n_items + 3 * split + grid).
+cudaError_t launch_fused_p1_wave(const DevTables &t, int e, int m, bool hw, int average, uint32_t gen,
+                                 uint32_t claim_base, uint32_t call_no, int lag, int split, int grid, cudaStream_t s);
 // claim_base: value of both claim counters at launch (each call advances
 // them by n_items + grid: every CTA's last claim overshoots once).
 cudaError_t launch_fused_p1_ldg(const DevTables &t, int e, int m, bool hw, int average, uint32_t gen,

@@ -614,6 +614,217 @@ cudaError_t launch_ring_reduce(uint8_t *own, const uint8_t *recv, int64_t n_tile
     });
 }
 
+// ------------------------------------------------------------------ fused p = 1, wavefront schedule
+// No grid barrier: ONE claim counter walks a merged sequence of 2n items in
+// which quantise item B(i) trails abs-max item A(i) by `lag` positions:
+//   A(0..D-1), then A(D) B(0) A(D+1) B(1) ..., then B(n-D..n-1).
+// Every warp of an A item counts itself into the layer's completion counter
+// with a fire-and-forget red.release (after its red.max); B(i) waits
+// (acquire) until its layer's counter reaches 8 x layer_items for this call.
+// With D >= (items of the largest layer) + grid, every A item of B(i)'s layer
+// sits earlier in the sequence and is normally finished when B(i) is
+// claimed, and B(i) re-reads data read only ~D items (~D x 32 KB) ago: it is
+// still in L2.  Progress: a waiting B depends only on A items at earlier
+// positions, and each CTA holds at most its current and next claim, so the
+// earliest waiting B always completes (induction on position).
+template <class C, int NT>
+__global__ void __launch_bounds__(NT, kFusedCtasPerSm)
+    fused_p1_wave_kernel(DevTables t, C c, uint32_t *amax, uint32_t *amax_next, uint32_t claim_base, uint32_t call_no,
+                         int lag, int split, int bias, int avg, int flags)
+{
+    __shared__ __align__(16) uint32_t s_codes[NT / 32][kTile];
+    __shared__ int s_claim[2], s_ft[2], s_ok[2];
+    // positions: A(0..D-1), A(D) B(0) A(D+1) B(1) ..., B(n-D..n-1-S), then the last S quantise
+    // items as 4 quarter units each (a finer tail: the last claims finish closer together)
+    const int n = t.n_items, D = lag, S = split;
+    const int body = 2 * n - S;            // whole-item positions
+    const int total = body + 4 * S;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const bool f_st_hint = flags & 64;
+    const bool f_timeline = (flags & 16) && blockIdx.x * 4 + 3 < kTimelineSlots;
+    auto stamp = [&](int k) {
+        if (f_timeline && threadIdx.x == 0) {
+            uint64_t ns;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+            t.timeline[blockIdx.x * 4 + k] = ns;
+        }
+    };
+    stamp(0);
+    uint64_t keep, strm;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(strm));
+    constexpr int kPer = kItemTiles * kTile / 4 / NT;
+    constexpr int kQTiles = kItemTiles / 4;  // tiles per quarter unit
+    constexpr int B = C::kB;
+    // position -> (is quantise, item, quarter (-1: whole item))
+    auto decode = [&](int j, bool &isB, int &quarter) -> int {
+        quarter = -1;
+        if (j < D) { isB = false; return j; }
+        if (j < 2 * n - D) {
+            const int k = j - D;
+            isB = k & 1;
+            return isB ? (k >> 1) : D + (k >> 1);
+        }
+        isB = true;
+        if (j < body) return n - D + (j - (2 * n - D));
+        quarter = (j - body) & 3;
+        return n - S + ((j - body) >> 2);
+    };
+    auto ft_of = [&](int l) -> int {
+        const int32_t E = exponent_of(ld_relaxed_u32(&amax[l]), 1);
+        return (E == INT32_MIN || E == INT32_MAX) ? 0 : bias - E;  // f~ (Alg. 1 line 4)
+    };
+    auto layer_target = [&](const Item &it) -> uint32_t { return (call_no + 1u) * (uint32_t)(8 * it.layer_items); };
+    // thread 0: claim the next position; if it is a quantise unit whose layer
+    // is already complete, resolve its f~ now (off the critical path)
+    auto claim_next = [&](int sl) {
+        const int j = (int)(atomicAdd(&t.claim[2], 1u) - claim_base);  // the wavefront's own counter
+        s_claim[sl] = j;
+        s_ok[sl] = 0;
+        if (j < total) {
+            bool isB;
+            int qq;
+            const int k = decode(j, isB, qq);
+            if (isB) {
+                const Item it = t.items[k];
+                if ((int)(ld_acquire_u32(&t.layer_done[it.layer]) - layer_target(it)) >= 0) {
+                    s_ft[sl] = ft_of(it.layer);
+                    s_ok[sl] = 1;
+                }
+            }
+        }
+    };
+    int slot = 0;
+    if (threadIdx.x == 0) claim_next(0);
+    __syncthreads();
+    for (int j = s_claim[0]; j < total;) {
+        bool isB;
+        int quarter;
+        const int k = decode(j, isB, quarter);
+        Item it = t.items[k];
+        ItemPtr p = t.iptr[k];
+        bool whole = it.cnt == kItemTiles * kTile;  // a full 32 KB item: preloaded, fully unrolled
+        if (quarter >= 0) {  // restrict the item to its quarter
+            const int t0 = quarter * kQTiles;
+            it.n_tiles = max(0, min(kQTiles, it.n_tiles - t0));
+            it.cnt = max(0, min(kQTiles * kTile, it.cnt - t0 * kTile));
+            it.tile_pos += t0;
+            it.tile_begin += t0;
+            p.src += (int64_t)t0 * kTile;
+            p.dst += (int64_t)t0 * kTile;
+            whole = false;
+        }
+        const float4 *g4 = reinterpret_cast<const float4 *>(p.src);
+        float4 v[kPer];
+        if (whole) {
+#pragma unroll
+            for (int q = 0; q < kPer; ++q) v[q] = ld_hint4(g4 + threadIdx.x + q * NT, isB ? strm : keep);
+        }
+        if (threadIdx.x == 0) claim_next(slot ^ 1);
+        if (!isB) {
+            // ---------------- abs-max item
+            uint32_t mx = 0;
+            if (whole) {
+#pragma unroll
+                for (int q = 0; q < kPer; ++q) mx = max(mx, absbits4(v[q]));
+            } else {
+                const int n4 = it.cnt >> 2;
+                for (int q = threadIdx.x; q < n4; q += NT) mx = max(mx, absbits4(ld_hint4(g4 + q, keep)));
+                if ((int)threadIdx.x < (it.cnt & 3)) mx = max(mx, __float_as_uint(p.src[4 * n4 + threadIdx.x]) & 0x7fffffffu);
+            }
+            mx = __reduce_max_sync(0xffffffffu, mx);
+            if (lane == 0) {
+                if (mx) asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(&amax[it.layer]), "r"(mx) : "memory");
+                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&t.layer_done[it.layer]) : "memory");
+            }
+        } else if (it.n_tiles > 0) {
+            // ---------------- quantise + unscale unit
+            if (!s_ok[slot]) {  // (uniform) layer not seen complete at claim time: wait now
+                if (threadIdx.x == 0) {
+                    while ((int)(ld_acquire_u32(&t.layer_done[it.layer]) - layer_target(it)) < 0) __nanosleep(32);
+                    s_ft[slot] = ft_of(it.layer);
+                }
+                __syncthreads();
+            }
+            const int ft = s_ft[slot];
+            if (it.tile_begin == 0 && threadIdx.x == 0) {  // record E, f~, flag; clear the next call's accumulator
+                const int32_t E = exponent_of(ld_relaxed_u32(&amax[it.layer]), 1);
+                t.E_local[it.layer] = E;
+                t.ftilde[it.layer] = ft;
+                if (E == INT32_MAX) atomicOr(t.flag, 1u);
+                amax_next[it.layer] = 0u;
+            }
+            const Pow2 s(ft);
+            const Unscale us(ft, 1, avg);
+            if constexpr (B == 8 || B == 16 || B == 32) {
+                using W = typename Word4<B>::T;
+                W *out = reinterpret_cast<W *>(t.packed + it.tile_pos * (16 * B));
+                if (whole && !s.wide) {
+                    float4 *o4 = reinterpret_cast<float4 *>(p.dst);
+#pragma unroll
+                    for (int q = 0; q < kPer; ++q) {
+                        const float4 y = make_float4(__fmul_rn(v[q].x, s.f), __fmul_rn(v[q].y, s.f),
+                                                     __fmul_rn(v[q].z, s.f), __fmul_rn(v[q].w, s.f));
+                        const W code = pack4<B>(c, y);
+                        const float4 r = us.apply4(unpack4<B>(c, code));
+                        if (f_st_hint) {
+                            st_hint(out + threadIdx.x + q * NT, code, strm);
+                            st_hint4(o4 + threadIdx.x + q * NT, r, strm);
+                        } else {
+                            out[threadIdx.x + q * NT] = code;
+                            o4[threadIdx.x + q * NT] = r;
+                        }
+                    }
+                } else {
+                    const int ng = it.n_tiles * (kTile / 4);
+                    for (int q = threadIdx.x; q < ng; q += NT) {
+                        const W code = pack4<B>(c, s.apply4(load_group(p.src, 4 * (int64_t)q, it.cnt)));
+                        out[q] = code;
+                        store_group(p.dst, 4 * (int64_t)q, it.cnt, us.apply4(unpack4<B>(c, code)));
+                    }
+                }
+            } else {
+                const int b = c.b();
+                uint32_t *codes = s_codes[warp];
+                uint32_t *outw = reinterpret_cast<uint32_t *>(t.packed) + it.tile_pos * (4 * b);
+                for (int tt = warp; tt < it.n_tiles; tt += NT / 32) {
+                    const int64_t e0 = (int64_t)tt * kTile + lane * 4;
+                    const float4 y = s.apply4(load_group(p.src, e0, it.cnt));
+                    const uint4 cd = make_uint4(c.enc(y.x), c.enc(y.y), c.enc(y.z), c.enc(y.w));
+                    *reinterpret_cast<uint4 *>(codes + lane * 4) = cd;
+                    __syncwarp();
+                    uint32_t *ow = outw + (int64_t)tt * (4 * b);
+                    for (int w2 = lane; w2 < 4 * b; w2 += 32) ow[w2] = assemble_word(codes, w2, b);
+                    store_group(p.dst, e0, it.cnt,
+                                us.apply4(make_float4(c.dec(cd.x), c.dec(cd.y), c.dec(cd.z), c.dec(cd.w))));
+                    __syncwarp();
+                }
+            }
+        }
+        __syncthreads();
+        slot ^= 1;
+        j = s_claim[slot];
+    }
+    stamp(3);
+}
+
+cudaError_t launch_fused_p1_wave(const DevTables &t, int e, int m, bool hw, int average, uint32_t gen,
+                                 uint32_t claim_base, uint32_t call_no, int lag, int split, int grid, cudaStream_t s)
+{
+    const int bias = (1 << (e - 1)) - 1;
+    uint32_t *cur = t.amax2 + (size_t)(gen & 1u) * t.n_layers;
+    uint32_t *other = t.amax2 + (size_t)((gen + 1u) & 1u) * t.n_layers;
+    return with_codec(e, m, hw, [&](auto c) -> cudaError_t {
+        using C = decltype(c);
+        auto kern = fused_p1_wave_kernel<C, kThreads>;
+        int flags = kFusedDefaultFlags;
+        if (const char *env = std::getenv("APS_FUSED_FLAGS")) flags = std::atoi(env);
+        void *args[] = {const_cast<DevTables *>(&t), &c, &cur, &other, &claim_base, &call_no, &lag, &split,
+                        const_cast<int *>(&bias), &average, &flags};
+        return cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(kThreads), args, 0, s);
+    });
+}
+
 static size_t fused_smem(const DevTables &t)
 {
     return t.n_layers <= kFusedSmemLayers ? sizeof(int32_t) * (size_t)t.n_layers : 0;
