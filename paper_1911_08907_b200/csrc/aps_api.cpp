@@ -17,6 +17,10 @@
 
 #include "aps_internal.h"
 
+namespace aps {
+constexpr uint32_t kFlagWaitTimeout = 2u;  // (mirrors aps_device.cuh)
+}
+
 namespace {
 
 enum Phase { kNone = 0, kLocalScales = 1, kScales = 2, kPacked = 3, kReduced = 4 };
@@ -412,8 +416,9 @@ aps_status aps_sync_out(aps_ctx *c, const float *const *grads, float *const *out
             if (const char *env = std::getenv("APS_FUSED_SPLIT")) split = std::min(lag, std::max(0, std::atoi(env)));
             APS_CUDA(c, aps::launch_fused_p1_wave(c->t, c->e, c->m, c->hw, average, c->gen, c->wave_claim_base,
                                                   c->wave_calls, lag, split, grid, c->stream));
-            // every unit is claimed once and every CTA's last claim overshoots once
-            c->wave_claim_base += (uint32_t)(2 * c->t.n_items + 3 * split + grid);
+            // every position is claimed once and every CTA's last TWO claims overshoot
+            // (it holds its current, next and next-but-one claims)
+            c->wave_claim_base += (uint32_t)(2 * c->t.n_items + 3 * split + aps::kWaveOvershoot * grid);
             ++c->wave_calls;
             ++c->gen;
             c->phase = kReduced;
@@ -474,6 +479,8 @@ aps_status aps_status_sync(aps_ctx *c)
     APS_CUDA(c, cudaStreamSynchronize(c->stream));
     if (flag) {
         APS_CUDA(c, cudaMemsetAsync(c->t.flag, 0, 4, c->stream));
+        if (flag & aps::kFlagWaitTimeout)
+            return fail(c, APS_ERR_STATE, "a device-side wait timed out (work counters out of step); outputs invalid");
         return fail(c, APS_ERR_NONFINITE, "non-finite gradient seen (outputs unspecified)");
     }
     return APS_OK;

@@ -274,6 +274,31 @@ struct Unscale {
     }
 };
 
+// ------------------------------------------------------------------ bounded spin
+// Device-side waits (grid barrier, per-layer completion) give up after 2 s of
+// %globaltimer and raise flag bit 2 (reported by aps_status_sync as
+// APS_ERR_STATE): a bookkeeping bug must never hang the GPU.
+constexpr uint32_t kFlagNonfinite = 1u, kFlagWaitTimeout = 2u;
+__device__ __forceinline__ uint64_t global_ns()
+{
+    uint64_t ns;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+    return ns;
+}
+template <class Ready>
+__device__ __forceinline__ void spin_until(Ready ready, uint32_t *flag)
+{
+    if (ready()) return;
+    const uint64_t t0 = global_ns();
+    while (!ready()) {
+        __nanosleep(32);
+        if (global_ns() - t0 > 2000000000ull) {
+            atomicOr(flag, kFlagWaitTimeout);
+            return;
+        }
+    }
+}
+
 // ------------------------------------------------------------------ dispatch
 // Calls f(codec) with the compiled specialisation for the config formats,
 // the hardware fp8 codec when requested, else the runtime codec.

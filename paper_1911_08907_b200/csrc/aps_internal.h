@@ -103,6 +103,7 @@ constexpr int kFusedSmemLayers = 8192;      // f~ table in shared memory up to t
 cudaError_t launch_build_item_ptrs(const DevTables &t, cudaStream_t s);
 // wavefront variant (no grid barrier): claim_base advances by 2 * n_items + grid per call;
 // call_no = wavefront calls before this one on these counters; lag = D positions.
+constexpr int kWaveOvershoot = 1;  // claims past the end per CTA and call (wavefront kernel: current + next)
 // split = the last `split` quantise items are claimed as 4 quarter units each
 // (claim_base then advances by 2 * n_items + 3 * split + grid).
 cudaError_t launch_fused_p1_wave(const DevTables &t, int e, int m, bool hw, int average, uint32_t gen,

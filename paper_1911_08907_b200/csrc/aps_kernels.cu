@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(NT, kFusedCtasPerSm)
     __syncthreads();
     if (threadIdx.x == 0) atomicAdd(t.done, (uint32_t)(NT / 32));
     if (threadIdx.x == 0)
-        while ((int)(ld_acquire_u32(t.done) - target) < 0) __nanosleep(32);
+        spin_until([&] { return (int)(ld_acquire_u32(t.done) - target) >= 0; }, t.flag);
     __syncthreads();
     stamp(2);
     const bool table = f_table && t.n_layers <= kFusedSmemLayers;
@@ -741,7 +741,8 @@ __global__ void __launch_bounds__(NT, kFusedCtasPerSm)
             // ---------------- quantise + unscale unit
             if (!s_ok[slot]) {  // (uniform) layer not seen complete at claim time: wait now
                 if (threadIdx.x == 0) {
-                    while ((int)(ld_acquire_u32(&t.layer_done[it.layer]) - layer_target(it)) < 0) __nanosleep(32);
+                    spin_until([&] { return (int)(ld_acquire_u32(&t.layer_done[it.layer]) - layer_target(it)) >= 0; },
+                               t.flag);
                     s_ft[slot] = ft_of(it.layer);
                 }
                 __syncthreads();

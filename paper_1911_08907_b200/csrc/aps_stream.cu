@@ -541,7 +541,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const Op op, 
         auto finalize = [&](int b0, int n_in) {
             if (!ready) {
                 if (lane == 0)
-                    while ((int)(ld_acquire(done_ctr) - target) < 0) __nanosleep(64);
+                    spin_until([&] { return (int)(ld_acquire(done_ctr) - target) >= 0; }, op.t.flag);
                 __syncwarp();
                 ready = true;
                 for (int i = pend_lo + lane; i < pend_hi; i += 32) {

@@ -22,6 +22,7 @@ for _ in range(5):
 for rep in range(3):
     flush.zero_()
     torch.cuda.synchronize()
+    ctx.timeline()[:] = 0
     ctx.sync_out(g, out)
     torch.cuda.synchronize()
     tl = ctx.timeline().astype(np.int64)
@@ -29,5 +30,8 @@ for rep in range(3):
     t0 = tl[:, 0].min()
     rel = (tl - t0) / 1e3
     q = lambda a: f"min {a.min():6.2f} med {np.median(a):6.2f} max {a.max():6.2f}"
-    print(f"rep {rep}: CTAs {len(tl)}  start [{q(rel[:, 0])}]  endA [{q(rel[:, 1])}]  barrier-out [{q(rel[:, 2])}]  end [{q(rel[:, 3])}] us")
-    print(f"        phaseA dur [{q(rel[:, 1] - rel[:, 0])}]  wait [{q(rel[:, 2] - rel[:, 1])}]  phaseB dur [{q(rel[:, 3] - rel[:, 2])}]")
+    if (tl[:, 1] > 0).all():   # barrier schedule: 4 stamps
+        print(f"rep {rep}: CTAs {len(tl)}  start [{q(rel[:, 0])}]  endA [{q(rel[:, 1])}]  barrier-out [{q(rel[:, 2])}]  end [{q(rel[:, 3])}] us")
+        print(f"        phaseA dur [{q(rel[:, 1] - rel[:, 0])}]  wait [{q(rel[:, 2] - rel[:, 1])}]  phaseB dur [{q(rel[:, 3] - rel[:, 2])}]")
+    else:                      # wavefront schedule: start / end only
+        print(f"rep {rep}: CTAs {len(tl)}  start [{q(rel[:, 0])}]  end [{q(rel[:, 3])}] us")

@@ -124,6 +124,25 @@ def test_p1_resnet50_full(aps, orc, fmt, hw):
     check(aps, orc, grads, e, m, hw, fused=False, ref=ref)
 
 
+@pytest.mark.timeout(300)
+def test_p1_fused_repeated_resnet50(aps, orc):
+    """Many fused syncs on one context at bench scale: the monotone claim /
+    completion counters must stay in step across calls (a drift hangs or
+    corrupts); every 5th result is compared with the oracle."""
+    numels = synthetic.RESNET50_NUMELS
+    grads = synthetic.make_grads(numels, 1)
+    ref = orc.aps_sync(grads, 5, 2, average=1)
+    g = [torch.from_numpy(a).cuda() for a in grads[0]]
+    out = [torch.empty_like(x) for x in g]
+    ctx = aps.ApsContext(5, 2, numels)
+    for it in range(25):
+        ctx.sync_out(g, out)
+        if it % 5 == 4:
+            assert ctx.status_sync() == 0
+            for a, b in zip(out, ref.out):
+                assert np.array_equal(a.cpu().numpy().view(np.uint32), b.view(np.uint32)), it
+
+
 def test_p1_fused_repeated_and_inplace(aps, orc):
     """The generation-stamped fused launch: many syncs in a row (fresh data
     each time, alternating in-place and out-of-place) stay bit-exact."""
