@@ -70,7 +70,7 @@ def peaks():
 
 def ncu_traffic():
     """Per-launch DRAM bytes of each kernel from the committed ncu summary."""
-    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")  # written by scripts/ncu_summary.py
     try:
         return json.load(open(p))
     except Exception:
@@ -333,7 +333,8 @@ def main():
     if world == 1:
         # one fused launch per step: FindMaxExp read (4 B) + Cast read (4 B) + codes (b/8 B) + fp32 out (4 B)
         kname = ("stream_kernel<FusedP1Op>" if os.environ.get("APS_ENGINE") in ("tma", "stream")
-                 else "fused_p1_ldg_kernel")
+                 else "fused_p1_ldg_kernel" if os.environ.get("APS_FUSED_SCHEDULE") == "barrier"
+                 else "fused_p1_wave_kernel")
         dom, dms, dbytes = f"fused_p1 ({kname})", ms_per_step, (12 + b / 8) * L
         phases["fused_p1"] = {"us": round(ms_per_step * 1e3, 2), "algorithmic_bytes": int(dbytes)}
     else:

@@ -318,6 +318,10 @@ aps_status aps_layer_scales(aps_ctx *c, const float *const *grads)
         APS_CUDA(c, aps::launch_stream_absmax(c->t, c->world, c->gen, tgt, c->stream));
         c->done_target = tgt;
         ++c->gen;
+    } else if (c->engine == aps_ctx::kLdg) {
+        const uint32_t tgt = c->done_target + (uint32_t)aps::absmax_ranges_grid(c->t.n_items);
+        APS_CUDA(c, aps::launch_absmax_ranges(c->t, c->world, tgt, c->stream));
+        c->done_target = tgt;
     } else {
         APS_CUDA(c, aps::launch_absmax_exp(c->t, c->world, c->stream));
     }

@@ -65,10 +65,82 @@ __global__ void __launch_bounds__(NT) absmax_exp_kernel(DevTables t, int N)
 }
 
 // direct widths 8/16/32: group of 4 fp32 -> one 4-code word group
+// a1 for the separate-call path (N > 1): each CTA takes kAbsItemsPerCta
+// consecutive work items (mostly one layer), keeps a per-warp running max,
+// flushes it with a fire-and-forget red.max when the layer changes, and
+// counts itself done once (fence + atomic); the last CTA turns the
+// accumulators into E_l = ceil(log2(N * A_l)) and clears them.  Compared with
+// one CTA per item and a fence per CTA, the fence latency is paid 4x less
+// often and the block scheduler still balances the load.
+constexpr int kAbsItemsPerCta = 4;
+
+__device__ __forceinline__ float4 ld_keep4(const float4 *p, uint64_t pol)
+{
+    float4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+                 : "l"(p), "l"(pol));
+    return r;
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT, 6) absmax_ranges_kernel(DevTables t, int N, uint32_t target)
+{
+    __shared__ int s_last;
+    const int lane = threadIdx.x & 31;
+    uint64_t keep;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
+    constexpr int kPer = kItemTiles * kTile / 4 / NT;
+    const int lo = blockIdx.x * kAbsItemsPerCta, hi = min(t.n_items, lo + kAbsItemsPerCta);
+    uint32_t run = 0;
+    int run_layer = -1;
+    for (int w = lo; w < hi; ++w) {
+        const Item it = t.items[w];
+        if (it.layer != run_layer) {
+            if (lane == 0 && run)
+                asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(&t.amax[run_layer]), "r"(run) : "memory");
+            run = 0;
+            run_layer = it.layer;
+        }
+        const float *g = t.src[it.layer] + (int64_t)it.tile_begin * kTile;
+        const float4 *g4 = reinterpret_cast<const float4 *>(g);
+        uint32_t mx = 0;
+        if (it.cnt == kItemTiles * kTile) {
+            float4 v[kPer];
+#pragma unroll
+            for (int j = 0; j < kPer; ++j) v[j] = ld_keep4(g4 + threadIdx.x + j * NT, keep);
+#pragma unroll
+            for (int j = 0; j < kPer; ++j) mx = max(mx, absbits4(v[j]));
+        } else {
+            const int n4 = it.cnt >> 2;
+            for (int j = threadIdx.x; j < n4; j += NT) mx = max(mx, absbits4(ld_keep4(g4 + j, keep)));
+            if ((int)threadIdx.x < (it.cnt & 3)) mx = max(mx, __float_as_uint(g[4 * n4 + threadIdx.x]) & 0x7fffffffu);
+        }
+        run = max(run, __reduce_max_sync(0xffffffffu, mx));
+    }
+    if (lane == 0) {
+        if (run && run_layer >= 0)
+            asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(&t.amax[run_layer]), "r"(run) : "memory");
+        __threadfence();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(t.done, 1u) == target - 1u;
+    __syncthreads();
+    if (s_last) {
+        __threadfence();
+        for (int l = threadIdx.x; l < t.n_layers; l += NT) {
+            uint32_t a_;
+            asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(a_) : "l"(&t.amax[l]) : "memory");
+            t.E_local[l] = exponent_of(a_, N);
+            t.amax[l] = 0u;
+        }
+    }
+}
+
 template <int B, class C, int NT>
 __global__ void __launch_bounds__(NT) quant_pack_direct_kernel(DevTables t, C c, int bias)
 {
-    const Item it = t.items[blockIdx.x];
+    const Item it = t.items[t.n_items - 1 - blockIdx.x];  // reverse: a1 read these last (L2)
     const LayerDev L = t.layers[it.layer];
     const float *g = t.src[it.layer];
     const int ft = scale_exponent(t, it.layer, bias, it.tile_begin == 0 && threadIdx.x == 0);
@@ -105,7 +177,7 @@ template <class C, int NT>
 __global__ void __launch_bounds__(NT) quant_pack_tile_kernel(DevTables t, C c, int bias)
 {
     __shared__ __align__(16) uint32_t s_codes[NT / 32][kTile];
-    const Item it = t.items[blockIdx.x];
+    const Item it = t.items[t.n_items - 1 - blockIdx.x];  // reverse: a1 read these last (L2)
     const LayerDev L = t.layers[it.layer];
     const float *g = t.src[it.layer];
     const int ft = scale_exponent(t, it.layer, bias, it.tile_begin == 0 && threadIdx.x == 0);
@@ -547,6 +619,15 @@ cudaError_t launch_absmax_exp(const DevTables &t, int world, cudaStream_t s)
 {
     if (t.n_items == 0) return cudaSuccess;
     absmax_exp_kernel<kThreads><<<t.n_items, kThreads, 0, s>>>(t, world);
+    return cudaGetLastError();
+}
+
+int absmax_ranges_grid(int n_items) { return (n_items + kAbsItemsPerCta - 1) / kAbsItemsPerCta; }
+
+cudaError_t launch_absmax_ranges(const DevTables &t, int world, uint32_t target, cudaStream_t s)
+{
+    if (t.n_items == 0) return cudaSuccess;
+    absmax_ranges_kernel<kThreads><<<absmax_ranges_grid(t.n_items), kThreads, 0, s>>>(t, world, target);
     return cudaGetLastError();
 }
 
