@@ -325,7 +325,7 @@ aps_status aps_layer_scales(aps_ctx *c, const float *const *grads)
     } else {
         APS_CUDA(c, aps::launch_absmax_exp(c->t, c->world, c->stream));
     }
-    if (c->world == 1) {
+    if (c->world == 1 && !c->comm) {
         c->phase = kScales;
     } else if (c->sim) {
         c->phase = kLocalScales;  // aps_sim_layer_scales completes the exchange
@@ -356,7 +356,7 @@ aps_status aps_allreduce(aps_ctx *c)
 {
     if (aps_status s = need_ws(c)) return s;
     if (c->phase != kPacked) return fail(c, APS_ERR_STATE, "aps_allreduce before aps_quantize_pack");
-    if (c->world == 1) {
+    if (c->world == 1 && !c->comm) {  // (a 1-rank communicator still goes through NCCL)
         c->phase = kReduced;
         return APS_OK;
     }
@@ -403,7 +403,7 @@ aps_status aps_sync_out(aps_ctx *c, const float *const *grads, float *const *out
 {
     if (aps_status s = need_ws(c)) return s;
     if (!grads || !out) return fail(c, APS_ERR_ARG, "NULL pointer array");
-    if (c->world == 1 && c->engine == aps_ctx::kLdg) {
+    if (c->world == 1 && !c->comm && c->engine == aps_ctx::kLdg) {
         // one rank: FindMaxExp -> f~ -> Cast -> pack -> Cast back -> unscale in one launch
         if (aps_status s = upload_ptrs<const float *>(c, c->src_cache, grads, c->off_src)) return s;
         if (aps_status s = upload_ptrs<float *>(c, c->dst_cache, out, c->off_dst)) return s;
@@ -438,7 +438,7 @@ aps_status aps_sync_out(aps_ctx *c, const float *const *grads, float *const *out
         c->phase = kReduced;
         return APS_OK;
     }
-    if (c->world == 1 && c->stream_engine && aps::stream_fused_supported(c->e, c->m, c->hw)) {
+    if (c->world == 1 && !c->comm && c->stream_engine && aps::stream_fused_supported(c->e, c->m, c->hw)) {
         // one rank: FindMaxExp -> f~ -> Cast -> pack -> Cast back -> unscale in one launch
         if (aps_status s = upload_ptrs<const float *>(c, c->src_cache, grads, c->off_src)) return s;
         if (aps_status s = upload_ptrs<float *>(c, c->dst_cache, out, c->off_dst)) return s;

@@ -92,17 +92,28 @@ __global__ void __launch_bounds__(NT, 6) absmax_ranges_kernel(DevTables t, int N
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
     constexpr int kPer = kItemTiles * kTile / 4 / NT;
     const int lo = blockIdx.x * kAbsItemsPerCta, hi = min(t.n_items, lo + kAbsItemsPerCta);
+    // all descriptors and layer pointers of the range up front (independent loads)
+    Item its[kAbsItemsPerCta];
+    const float *srcs[kAbsItemsPerCta];
+#pragma unroll
+    for (int k = 0; k < kAbsItemsPerCta; ++k)
+        if (lo + k < hi) its[k] = t.items[lo + k];
+#pragma unroll
+    for (int k = 0; k < kAbsItemsPerCta; ++k)
+        if (lo + k < hi) srcs[k] = t.src[its[k].layer] + (int64_t)its[k].tile_begin * kTile;
     uint32_t run = 0;
     int run_layer = -1;
-    for (int w = lo; w < hi; ++w) {
-        const Item it = t.items[w];
+#pragma unroll
+    for (int k = 0; k < kAbsItemsPerCta; ++k) {
+        if (lo + k >= hi) break;
+        const Item it = its[k];
         if (it.layer != run_layer) {
             if (lane == 0 && run)
                 asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(&t.amax[run_layer]), "r"(run) : "memory");
             run = 0;
             run_layer = it.layer;
         }
-        const float *g = t.src[it.layer] + (int64_t)it.tile_begin * kTile;
+        const float *g = srcs[k];
         const float4 *g4 = reinterpret_cast<const float4 *>(g);
         uint32_t mx = 0;
         if (it.cnt == kItemTiles * kTile) {

@@ -303,3 +303,28 @@ def test_repeated_syncs_self_reset(aps, orc):
         assert np.array_equal(ctx.scales(), ref.ftilde)
         for a, b in zip(g, ref.out):
             assert np.array_equal(a.cpu().numpy().view(np.uint32), b.view(np.uint32))
+
+
+def test_nccl_world1_path(aps, orc):
+    """A 1-rank NCCL communicator routes the sync through the real NCCL calls
+    (unique id, ncclCommInitRank, int32 MAX all-reduce of E, in-place
+    all-gather of the packed chunks) -- the plumbing of the N > 1 ring,
+    checked bit-exactly on one GPU."""
+    numels = synthetic.C1_NUMELS + [1000, 1]
+    grads = synthetic.make_grads(numels, 1)
+    ref = orc.aps_sync(grads, 5, 2, average=1)
+    comm = aps.nccl_comm_init(aps.nccl_unique_id(), 1, 0)
+    try:
+        ctx = aps.ApsContext(5, 2, numels, world_size=1, rank=0, nccl_comm=comm)
+        g = [torch.from_numpy(a).cuda() for a in grads[0]]
+        for _ in range(3):
+            out = [torch.empty_like(x) for x in g]
+            ctx.sync_out(g, out)
+            assert ctx.status_sync() == 0
+            assert np.array_equal(ctx.scales(), ref.ftilde)
+            assert np.array_equal(ctx.packed().cpu().numpy(), ref.reduced)
+            for a, b in zip(out, ref.out):
+                assert np.array_equal(a.cpu().numpy().view(np.uint32), b.view(np.uint32))
+        ctx.close()
+    finally:
+        aps.nccl_comm_destroy(comm)
