@@ -826,8 +826,22 @@ __global__ void __launch_bounds__(NT, kFusedCtasPerSm)
             }
             mx = __reduce_max_sync(0xffffffffu, mx);
             if (lane == 0) {
-                if (mx) asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(&amax[it.layer]), "r"(mx) : "memory");
-                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&t.layer_done[it.layer]) : "memory");
+                // Count this warp into the layer only after its max has been PERFORMED at
+                // L2 (the returning atomic), without a release fence: a release here is a
+                // MEMBAR that would also wait for this lane's pending stores of the
+                // previous quantise item (measured: 20% of all stall samples).
+                uint32_t old = 0;
+                if (flags & 128)
+                    asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(&amax[it.layer]), "r"(mx) : "memory");
+                else
+                    asm volatile("atom.relaxed.gpu.global.max.u32 %0, [%1], %2;" : "=r"(old) : "l"(&amax[it.layer]), "r"(mx) : "memory");
+                // the increment depends on the atomic's return value (abs bits are <= 0x7fffffff,
+                // so it is always 1), which makes the add wait for the max to be performed
+                const uint32_t inc = (old == 0xffffffffu) ? 0u : 1u;
+                if (flags & 128)
+                    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&t.layer_done[it.layer]) : "memory");
+                else
+                    asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(&t.layer_done[it.layer]), "r"(inc) : "memory");
             }
         } else if (it.n_tiles > 0) {
             // ---------------- quantise + unscale unit
