@@ -415,14 +415,12 @@ aps_status aps_sync_out(aps_ctx *c, const float *const *grads, float *const *out
         const char *sched = std::getenv("APS_FUSED_SCHEDULE");
         if (!sched || std::strcmp(sched, "barrier") != 0) {
             // wavefront: quantise items trail their abs-max items by D positions
-            const int lag = std::min(c->t.n_items, c->max_layer_items + grid);
-            int split = 0;  // quarter-split tail units: measured slower
-            if (const char *env = std::getenv("APS_FUSED_SPLIT")) split = std::min(lag, std::max(0, std::atoi(env)));
+            const int wgrid = aps::fused_p1_wave_grid(c->e, c->m, c->hw, c->t.n_items);
+            const int lag = std::min(c->t.n_items, c->max_layer_items + wgrid);
             APS_CUDA(c, aps::launch_fused_p1_wave(c->t, c->e, c->m, c->hw, average, c->gen, c->wave_claim_base,
-                                                  c->wave_calls, lag, split, grid, c->stream));
-            // every position is claimed once and every CTA's last TWO claims overshoot
-            // (it holds its current, next and next-but-one claims)
-            c->wave_claim_base += (uint32_t)(2 * c->t.n_items + 3 * split + aps::kWaveOvershoot * grid);
+                                                  c->wave_calls, lag, wgrid, c->stream));
+            // every position is claimed once and every CTA overshoots kWaveOvershoot times
+            c->wave_claim_base += (uint32_t)(2 * c->t.n_items + aps::kWaveOvershoot * wgrid);
             ++c->wave_calls;
             ++c->gen;
             c->phase = kReduced;

@@ -106,11 +106,15 @@ constexpr int kFusedSmemLayers = 8192;      // f~ table in shared memory up to t
 cudaError_t launch_build_item_ptrs(const DevTables &t, cudaStream_t s);
 // wavefront variant (no grid barrier): claim_base advances by 2 * n_items + grid per call;
 // call_no = wavefront calls before this one on these counters; lag = D positions.
-constexpr int kWaveOvershoot = 1;  // claims past the end per CTA and call (wavefront kernel: current + next)
-// split = the last `split` quantise items are claimed as 4 quarter units each
-// (claim_base then advances by 2 * n_items + 3 * split + grid).
+#ifndef APS_WAVE_CTAS_PER_SM
+#define APS_WAVE_CTAS_PER_SM 4
+#endif
+constexpr int kWaveCtasPerSm = APS_WAVE_CTAS_PER_SM;  // wavefront kernel occupancy (register budget)
+int fused_p1_wave_grid(int e, int m, bool hw, int n_items);
+constexpr int kWaveOvershoot = 2;  // claims past the end per CTA and call (wavefront kernel claims 2 ahead)
+// claim_base advances by 2 * n_items + kWaveOvershoot * grid per call.
 cudaError_t launch_fused_p1_wave(const DevTables &t, int e, int m, bool hw, int average, uint32_t gen,
-                                 uint32_t claim_base, uint32_t call_no, int lag, int split, int grid, cudaStream_t s);
+                                 uint32_t claim_base, uint32_t call_no, int lag, int grid, cudaStream_t s);
 // claim_base: value of both claim counters at launch (each call advances
 // them by n_items + grid: every CTA's last claim overshoots once).
 cudaError_t launch_fused_p1_ldg(const DevTables &t, int e, int m, bool hw, int average, uint32_t gen,

@@ -720,17 +720,16 @@ cudaError_t launch_ring_reduce(uint8_t *own, const uint8_t *recv, int64_t n_tile
 // positions, and each CTA holds at most its current and next claim, so the
 // earliest waiting B always completes (induction on position).
 template <class C, int NT>
-__global__ void __launch_bounds__(NT, kFusedCtasPerSm)
+__global__ void __launch_bounds__(NT, kWaveCtasPerSm)
     fused_p1_wave_kernel(DevTables t, C c, uint32_t *amax, uint32_t *amax_next, uint32_t claim_base, uint32_t call_no,
-                         int lag, int split, int bias, int avg, int flags)
+                         int lag, int bias, int avg, int flags)
 {
     __shared__ __align__(16) uint32_t s_codes[NT / 32][kTile];
-    __shared__ int s_claim[2], s_ft[2], s_ok[2];
-    // positions: A(0..D-1), A(D) B(0) A(D+1) B(1) ..., B(n-D..n-1-S), then the last S quantise
-    // items as 4 quarter units each (a finer tail: the last claims finish closer together)
-    const int n = t.n_items, D = lag, S = split;
-    const int body = 2 * n - S;            // whole-item positions
-    const int total = body + 4 * S;
+    __shared__ int s_claim[3], s_ft[3], s_ok[3];  // claims run two items ahead (3 slots)
+    __shared__ uint32_t s_part[2][NT / 32];       // per-warp maxima of the last two items
+    __shared__ int s_part_layer[2];               // their layer (-1: a quantise item)
+    // positions: A(0..D-1), A(D) B(0) A(D+1) B(1) ..., B(n-D..n-1)
+    const int n = t.n_items, D = lag, total = 2 * n;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const bool f_st_hint = flags & 64;
     const bool f_timeline = (flags & 16) && blockIdx.x * 4 + 3 < kTimelineSlots;
@@ -746,37 +745,31 @@ __global__ void __launch_bounds__(NT, kFusedCtasPerSm)
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(strm));
     constexpr int kPer = kItemTiles * kTile / 4 / NT;
-    constexpr int kQTiles = kItemTiles / 4;  // tiles per quarter unit
     constexpr int B = C::kB;
-    // position -> (is quantise, item, quarter (-1: whole item))
-    auto decode = [&](int j, bool &isB, int &quarter) -> int {
-        quarter = -1;
+    constexpr int kFlushThread = 32;  // lane 0 of warp 1 folds finished abs-max items into the layer
+    auto decode = [&](int j, bool &isB) -> int {
         if (j < D) { isB = false; return j; }
-        if (j < 2 * n - D) {
+        if (j < total - D) {
             const int k = j - D;
             isB = k & 1;
             return isB ? (k >> 1) : D + (k >> 1);
         }
         isB = true;
-        if (j < body) return n - D + (j - (2 * n - D));
-        quarter = (j - body) & 3;
-        return n - S + ((j - body) >> 2);
+        return n - D + (j - (total - D));
     };
     auto ft_of = [&](int l) -> int {
         const int32_t E = exponent_of(ld_relaxed_u32(&amax[l]), 1);
         return (E == INT32_MIN || E == INT32_MAX) ? 0 : bias - E;  // f~ (Alg. 1 line 4)
     };
     auto layer_target = [&](const Item &it) -> uint32_t { return (call_no + 1u) * (uint32_t)(8 * it.layer_items); };
-    // thread 0: claim the next position; if it is a quantise unit whose layer
-    // is already complete, resolve its f~ now (off the critical path)
-    auto claim_next = [&](int sl) {
+    // thread 0: claim a position into slot sl; resolve f~ now if it is a quantise item of a complete layer
+    auto claim_into = [&](int sl) {
         const int j = (int)(atomicAdd(&t.claim[2], 1u) - claim_base);  // the wavefront's own counter
         s_claim[sl] = j;
         s_ok[sl] = 0;
         if (j < total) {
             bool isB;
-            int qq;
-            const int k = decode(j, isB, qq);
+            const int k = decode(j, isB);
             if (isB) {
                 const Item it = t.items[k];
                 if ((int)(ld_acquire_u32(&t.layer_done[it.layer]) - layer_target(it)) >= 0) {
@@ -786,37 +779,52 @@ __global__ void __launch_bounds__(NT, kFusedCtasPerSm)
             }
         }
     };
-    int slot = 0;
-    if (threadIdx.x == 0) claim_next(0);
+    // flush pipeline (kFlushThread): an item's max is folded in (returning atomic) one
+    // iteration after the item, and counted (add dependent on the atomic's result, so
+    // only after the max is performed at L2) one iteration after that
+    int pend_layer = -1;  // layer whose max was folded last iteration and is not yet counted
+    uint32_t pend_old = 0;
+    auto flush = [&](int pp) {
+        if (pend_layer >= 0) {
+            const uint32_t inc = (pend_old == 0xffffffffu) ? 0u : 8u;  // always 8: abs bits <= 0x7fffffff
+            asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(&t.layer_done[pend_layer]), "r"(inc)
+                         : "memory");
+            pend_layer = -1;
+        }
+        const int l = pp >= 0 ? s_part_layer[pp] : -1;
+        if (l >= 0) {
+            uint32_t m = 0;
+#pragma unroll
+            for (int w = 0; w < NT / 32; ++w) m = max(m, s_part[pp][w]);
+            asm volatile("atom.relaxed.gpu.global.max.u32 %0, [%1], %2;" : "=r"(pend_old) : "l"(&amax[l]), "r"(m) : "memory");
+            pend_layer = l;
+        }
+    };
+    if (threadIdx.x == 0) {
+        claim_into(0);
+        claim_into(1);
+        s_part_layer[0] = s_part_layer[1] = -1;
+    }
     __syncthreads();
+    int slot = 0, par = 0;
     for (int j = s_claim[0]; j < total;) {
         bool isB;
-        int quarter;
-        const int k = decode(j, isB, quarter);
-        Item it = t.items[k];
-        ItemPtr p = t.iptr[k];
-        bool whole = it.cnt == kItemTiles * kTile;  // a full 32 KB item: preloaded, fully unrolled
-        if (quarter >= 0) {  // restrict the item to its quarter
-            const int t0 = quarter * kQTiles;
-            it.n_tiles = max(0, min(kQTiles, it.n_tiles - t0));
-            it.cnt = max(0, min(kQTiles * kTile, it.cnt - t0 * kTile));
-            it.tile_pos += t0;
-            it.tile_begin += t0;
-            p.src += (int64_t)t0 * kTile;
-            p.dst += (int64_t)t0 * kTile;
-            whole = false;
-        }
+        const int k = decode(j, isB);
+        const Item it = t.items[k];
+        const ItemPtr p = t.iptr[k];
         const float4 *g4 = reinterpret_cast<const float4 *>(p.src);
+        const bool full = it.cnt == kItemTiles * kTile;
         float4 v[kPer];
-        if (whole) {
+        if (full) {
 #pragma unroll
             for (int q = 0; q < kPer; ++q) v[q] = ld_hint4(g4 + threadIdx.x + q * NT, isB ? strm : keep);
         }
-        if (threadIdx.x == 0) claim_next(slot ^ 1);
+        if (threadIdx.x == 0) claim_into((slot + 2) % 3);
+        if (threadIdx.x == kFlushThread) flush(par ^ 1);
         if (!isB) {
             // ---------------- abs-max item
             uint32_t mx = 0;
-            if (whole) {
+            if (full) {
 #pragma unroll
                 for (int q = 0; q < kPer; ++q) mx = max(mx, absbits4(v[q]));
             } else {
@@ -825,27 +833,15 @@ __global__ void __launch_bounds__(NT, kFusedCtasPerSm)
                 if ((int)threadIdx.x < (it.cnt & 3)) mx = max(mx, __float_as_uint(p.src[4 * n4 + threadIdx.x]) & 0x7fffffffu);
             }
             mx = __reduce_max_sync(0xffffffffu, mx);
-            if (lane == 0) {
-                // Count this warp into the layer only after its max has been PERFORMED at
-                // L2 (the returning atomic), without a release fence: a release here is a
-                // MEMBAR that would also wait for this lane's pending stores of the
-                // previous quantise item (measured: 20% of all stall samples).
-                uint32_t old = 0;
-                if (flags & 128)
-                    asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(&amax[it.layer]), "r"(mx) : "memory");
-                else
-                    asm volatile("atom.relaxed.gpu.global.max.u32 %0, [%1], %2;" : "=r"(old) : "l"(&amax[it.layer]), "r"(mx) : "memory");
-                // the increment depends on the atomic's return value (abs bits are <= 0x7fffffff,
-                // so it is always 1), which makes the add wait for the max to be performed
-                const uint32_t inc = (old == 0xffffffffu) ? 0u : 1u;
-                if (flags & 128)
-                    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&t.layer_done[it.layer]) : "memory");
-                else
-                    asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(&t.layer_done[it.layer]), "r"(inc) : "memory");
-            }
-        } else if (it.n_tiles > 0) {
-            // ---------------- quantise + unscale unit
+            if (lane == 0) s_part[par][warp] = mx;
+            if (threadIdx.x == 0) s_part_layer[par] = it.layer;
+        } else {
+            if (threadIdx.x == 0) s_part_layer[par] = -1;
+            // ---------------- quantise + unscale item
             if (!s_ok[slot]) {  // (uniform) layer not seen complete at claim time: wait now
+                // this CTA's own not-yet-counted abs-max item may be one the wait needs:
+                // count it first (deadlock otherwise)
+                if (threadIdx.x == kFlushThread) flush(-1);
                 if (threadIdx.x == 0) {
                     spin_until([&] { return (int)(ld_acquire_u32(&t.layer_done[it.layer]) - layer_target(it)) >= 0; },
                                t.flag);
@@ -866,7 +862,7 @@ __global__ void __launch_bounds__(NT, kFusedCtasPerSm)
             if constexpr (B == 8 || B == 16 || B == 32) {
                 using W = typename Word4<B>::T;
                 W *out = reinterpret_cast<W *>(t.packed + it.tile_pos * (16 * B));
-                if (whole && !s.wide) {
+                if (full && !s.wide) {
                     float4 *o4 = reinterpret_cast<float4 *>(p.dst);
 #pragma unroll
                     for (int q = 0; q < kPer; ++q) {
@@ -909,14 +905,19 @@ __global__ void __launch_bounds__(NT, kFusedCtasPerSm)
             }
         }
         __syncthreads();
-        slot ^= 1;
+        slot = (slot + 1) % 3;
+        par ^= 1;
         j = s_claim[slot];
+    }
+    if (threadIdx.x == kFlushThread) {  // drain: the last item's max, then its count
+        flush(par ^ 1);
+        flush(-1);
     }
     stamp(3);
 }
 
 cudaError_t launch_fused_p1_wave(const DevTables &t, int e, int m, bool hw, int average, uint32_t gen,
-                                 uint32_t claim_base, uint32_t call_no, int lag, int split, int grid, cudaStream_t s)
+                                 uint32_t claim_base, uint32_t call_no, int lag, int grid, cudaStream_t s)
 {
     const int bias = (1 << (e - 1)) - 1;
     uint32_t *cur = t.amax2 + (size_t)(gen & 1u) * t.n_layers;
@@ -926,7 +927,7 @@ cudaError_t launch_fused_p1_wave(const DevTables &t, int e, int m, bool hw, int 
         auto kern = fused_p1_wave_kernel<C, kThreads>;
         int flags = kFusedDefaultFlags;
         if (const char *env = std::getenv("APS_FUSED_FLAGS")) flags = std::atoi(env);
-        void *args[] = {const_cast<DevTables *>(&t), &c, &cur, &other, &claim_base, &call_no, &lag, &split,
+        void *args[] = {const_cast<DevTables *>(&t), &c, &cur, &other, &claim_base, &call_no, &lag,
                         const_cast<int *>(&bias), &average, &flags};
         return cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(kThreads), args, 0, s);
     });
@@ -968,6 +969,17 @@ int fused_p1_ldg_grid(int e, int m, bool hw, int n_items)
                                                              sizeof(int32_t) * kFusedSmemLayers);
     });
     per_sm = std::max(1, std::min(per_sm, kFusedCtasPerSm));
+    return std::max(1, std::min(n_items, sm_count() * per_sm));
+}
+
+int fused_p1_wave_grid(int e, int m, bool hw, int n_items)
+{
+    int per_sm = 0;
+    with_codec(e, m, hw, [&](auto c) -> cudaError_t {
+        using C = decltype(c);
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_p1_wave_kernel<C, kThreads>, kThreads, 0);
+    });
+    per_sm = std::max(1, std::min(per_sm, kWaveCtasPerSm));
     return std::max(1, std::min(n_items, sm_count() * per_sm));
 }
 
