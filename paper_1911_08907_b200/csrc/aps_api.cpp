@@ -216,6 +216,7 @@ aps_status aps_init(aps_ctx **out, int exp_bits, int man_bits, int world_size, i
         }
         for (size_t k = c->items.size() - (size_t)L.n_items; k < c->items.size(); ++k)
             c->items[k].layer_items = L.n_items;
+
         c->layers.push_back(L);
         toff += T;
     }
@@ -246,6 +247,7 @@ aps_status aps_init(aps_ctx **out, int exp_bits, int man_bits, int world_size, i
     c->off_tl = o;     o = align_up(o + sizeof(uint64_t) * aps::kTimelineSlots);
     c->off_claim = o;  o = align_up(o + 3 * sizeof(uint32_t));
     c->off_ldone = o;  o = align_up(o + 4 * (size_t)n_layers);
+
     for (const auto &L : c->layers) c->max_layer_items = std::max(c->max_layer_items, (int)L.n_items);
     c->need = o;
     *out = c;
@@ -284,6 +286,7 @@ aps_status aps_set_workspace(aps_ctx *c, void *dev, size_t bytes)
     t.timeline = reinterpret_cast<uint64_t *>(c->ws + c->off_tl);
     t.claim = reinterpret_cast<uint32_t *>(c->ws + c->off_claim);
     t.layer_done = reinterpret_cast<uint32_t *>(c->ws + c->off_ldone);
+
     c->wave_calls = 0;
     c->wave_claim_base = 0;
     c->claim_base = 0;

@@ -111,6 +111,7 @@ cudaError_t launch_build_item_ptrs(const DevTables &t, cudaStream_t s);
 #endif
 constexpr int kWaveCtasPerSm = APS_WAVE_CTAS_PER_SM;  // wavefront kernel occupancy (register budget)
 int fused_p1_wave_grid(int e, int m, bool hw, int n_items);
+
 constexpr int kWaveOvershoot = 2;  // claims past the end per CTA and call (wavefront kernel claims 2 ahead)
 // claim_base advances by 2 * n_items + kWaveOvershoot * grid per call.
 cudaError_t launch_fused_p1_wave(const DevTables &t, int e, int m, bool hw, int average, uint32_t gen,

@@ -328,3 +328,27 @@ def test_nccl_world1_path(aps, orc):
         ctx.close()
     finally:
         aps.nccl_comm_destroy(comm)
+
+
+@pytest.mark.parametrize("schedule", ["wave", "barrier"])
+@pytest.mark.timeout(300)
+def test_p1_fused_schedules(aps, orc, schedule, monkeypatch):
+    """Every fused N = 1 schedule (wavefront, grid barrier) is bit-exact: edge cases and ResNet-50 at full size, in
+    several formats, with repeated calls on one context."""
+    monkeypatch.setenv("APS_FUSED_SCHEDULE", schedule)
+    for (e, m), hw in [((5, 2), True), ((5, 2), False), ((3, 0), False), ((5, 6), False), ((5, 10), False)]:
+        check(aps, orc, synthetic.edge_case_layers(1), e, m, hw, average=0, fused=True)
+        grads = synthetic.make_grads(synthetic.C1_NUMELS + [1000, 1, 130, 8195, 16387], 1)
+        check(aps, orc, grads, e, m, hw, fused=True)
+    numels = synthetic.RESNET50_NUMELS
+    grads = synthetic.make_grads(numels, 1)
+    ref = orc.aps_sync(grads, 5, 2, average=1)
+    g = [torch.from_numpy(a).cuda() for a in grads[0]]
+    ctx = aps.ApsContext(5, 2, numels)
+    for it in range(12):
+        out = [torch.empty_like(x) for x in g]
+        ctx.sync_out(g, out)
+        if it % 4 == 3:
+            assert ctx.status_sync() == 0
+            for a, b in zip(out, ref.out):
+                assert np.array_equal(a.cpu().numpy().view(np.uint32), b.view(np.uint32)), (schedule, it)
