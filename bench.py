@@ -313,6 +313,23 @@ def main():
     torch.cuda.synchronize()
     phase_ms = [[pev[k][i].elapsed_time(pev[k][i + 1]) for k in range(KP)] for i in range(4)]
 
+    # -------- the ring's reduce step on one device: one p = 8 chunk (unpack, fp32 add,
+    # re-quantise, repack), the kernel each rank runs between ring steps
+    T8, pb8 = aps.layout(8, e, m, numels)
+    chunk_tiles = T8 // 8
+    own = torch.zeros(pb8 // 8, dtype=torch.uint8, device=dev)
+    rcv = torch.zeros(pb8 // 8, dtype=torch.uint8, device=dev)
+    hw = ctx_hw(ctx, args)
+    for _ in range(3):
+        aps.debug_ring_reduce(own, rcv, chunk_tiles, e, m, hw=hw)
+    rr = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    rr[0].record(stream)
+    for _ in range(50):
+        aps.debug_ring_reduce(own, rcv, chunk_tiles, e, m, hw=hw)
+    rr[1].record(stream)
+    torch.cuda.synchronize()
+    rr_ms = rr[0].elapsed_time(rr[1]) / 50
+
     # -------- roofline of the dominant kernel (algorithmic bytes / launch time)
     T, packed_bytes = aps.layout(world, e, m, numels)
     kern = {
@@ -331,6 +348,11 @@ def main():
         ref_peak = 900.0 if k == "ring_allreduce" else peak
         phases[k] = {"us": round(ms * 1e3, 2), "algorithmic_bytes": int(byts), "GB/s": round(gbs, 1),
                      "frac": round(gbs / ref_peak, 4)}
+    rr_bytes = 3 * (pb8 // 8)   # read recv + read own + write own, b/8 bytes per element each
+    phases["ring_reduce_step_p8"] = {"us": round(rr_ms * 1e3, 2), "algorithmic_bytes": int(rr_bytes),
+                                     "GB/s": round(rr_bytes / (rr_ms * 1e-3) / 1e9, 1),
+                                     "frac": round(rr_bytes / (rr_ms * 1e-3) / 1e9 / peak, 4),
+                                     "note": "one reduce-scatter step's kernel for a p = 8 chunk (launch-bound at this size)"}
     if world == 1:
         # one fused launch per step: FindMaxExp read (4 B) + Cast read (4 B) + codes (b/8 B) + fp32 out (4 B)
         kname = ("stream_kernel<FusedP1Op>" if os.environ.get("APS_ENGINE") in ("tma", "stream")

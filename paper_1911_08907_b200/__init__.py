@@ -5,6 +5,8 @@ from .aps import (ApsContext, ApsError, debug_cast, debug_decode, debug_ring_red
                   nccl_comm_destroy, nccl_comm_init, nccl_unique_id, ring_step, sim_allreduce,
                   sim_layer_scales)
 
-__all__ = ["ApsContext", "ApsError", "debug_cast", "debug_decode", "debug_ring_reduce", "layout", "load",
+from .ddp import ApsHookState, aps_hook
+
+__all__ = ["ApsHookState", "aps_hook", "ApsContext", "ApsError", "debug_cast", "debug_decode", "debug_ring_reduce", "layout", "load",
            "nccl_comm_destroy", "nccl_comm_init", "nccl_unique_id", "ring_step", "sim_allreduce",
            "sim_layer_scales"]

@@ -1,0 +1,91 @@
+"""DDP communication hook running APS on every gradient bucket (SURVEY 8(f)
+NEXT-1): DistributedDataParallel hands each bucket to `aps_hook` as soon as
+backward() has produced it, so the low-precision synchronisation of early
+buckets overlaps the backward pass of later layers.
+
+Per bucket: the flat fp32 buffer is split at the parameter boundaries into
+APS layers (Alg. 1's per-layer exponents); a parameter whose view
+does not start 16-byte aligned is merged into the preceding layer (so the
+bucket may have fewer exponents than parameters -- P:230 allows several
+consecutive layers "as a whole tensor").  The buffer is synchronised in place
+by libaps (scale, Cast, packed ring over NCCL, unscale, average) on the
+current stream and returned.
+
+Usage:
+    state = ApsHookState(process_group=None, exp_bits=5, man_bits=2)
+    ddp_model.register_comm_hook(state, aps_hook)
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+from .aps import ApsContext, nccl_comm_destroy, nccl_comm_init, nccl_unique_id
+
+
+class ApsHookState:
+    """Per-process hook state: the format, the NCCL communicator libaps uses
+    for its ring (created here, collectively, outside backward), and one
+    ApsContext per bucket (created on the bucket's first call)."""
+
+    def __init__(self, process_group=None, exp_bits: int = 5, man_bits: int = 2, average: bool = True):
+        self.pg = process_group if process_group is not None else dist.group.WORLD
+        self.exp_bits, self.man_bits, self.average = exp_bits, man_bits, average
+        self.world = dist.get_world_size(self.pg)
+        self.rank = dist.get_rank(self.pg)
+        self.comm = None
+        if self.world > 1:
+            uid = [nccl_unique_id() if self.rank == 0 else None]
+            dist.broadcast_object_list(uid, src=dist.get_global_rank(self.pg, 0), group=self.pg)
+            self.comm = nccl_comm_init(uid[0], self.world, self.rank)
+        self.contexts: dict[int, tuple[ApsContext, list[tuple[int, int]]]] = {}
+        self.groups: dict[int, list[list[int]]] = {}  # bucket index -> parameter indices per APS layer
+        self.bucket_params: dict[int, list[torch.nn.Parameter]] = {}
+
+    def close(self):
+        for ctx, _ in self.contexts.values():
+            ctx.close()
+        self.contexts.clear()
+        if self.comm:
+            nccl_comm_destroy(self.comm)
+            self.comm = None
+
+
+def layer_spans(buffer: torch.Tensor, numels: list[int]) -> tuple[list[tuple[int, int]], list[list[int]]]:
+    """Split a flat bucket into APS layers at 16-byte-aligned parameter starts.
+    Returns [(offset, numel)] per layer and the parameter indices of each."""
+    base = buffer.data_ptr()
+    spans, groups, off = [], [], 0
+    for i, n in enumerate(numels):
+        if not spans or (base + 4 * off) % 16 == 0:
+            spans.append([off, n])
+            groups.append([i])
+        else:
+            spans[-1][1] += n
+            groups[-1].append(i)
+        off += n
+    return [tuple(s) for s in spans], groups
+
+
+def aps_hook(state: ApsHookState, bucket: "dist.GradBucket") -> torch.futures.Future:
+    buf = bucket.buffer()
+    if buf.dtype != torch.float32:
+        raise TypeError("aps_hook needs fp32 gradients")
+    idx = bucket.index()
+    numels = [p.numel() for p in bucket.parameters()]
+    entry = state.contexts.get(idx)
+    spans, groups = layer_spans(buf, numels)
+    if entry is None or entry[1] != spans:
+        if entry is not None:
+            entry[0].close()
+        ctx = ApsContext(state.exp_bits, state.man_bits, [n for _, n in spans], world_size=state.world,
+                         rank=state.rank, nccl_comm=state.comm, device=buf.device)
+        state.contexts[idx] = (ctx, spans)
+        state.groups[idx] = groups
+        state.bucket_params[idx] = list(bucket.parameters())
+    ctx = state.contexts[idx][0]
+    views = [buf[o:o + n] for o, n in spans]
+    ctx.sync(views, average=state.average)
+    fut = torch.futures.Future()
+    fut.set_result(buf)
+    return fut
