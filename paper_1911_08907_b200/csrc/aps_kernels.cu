@@ -13,6 +13,7 @@
 #include <climits>
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 #include "aps_device.cuh"
 
@@ -270,17 +271,27 @@ __global__ void __launch_bounds__(NT) unpack_unscale_tile_kernel(DevTables t, C 
 // own[i] <- Cast(fl32(dec(recv[i]) + dec(own[i])))   (re-quantise after the add, A13)
 template <int B, class C, int NT>
 __global__ void __launch_bounds__(NT) ring_reduce_direct_kernel(uint8_t *own, const uint8_t *recv,
-                                                                 int64_t n_groups, C c)
+                                                                 int64_t n_vec, C c)
 {
+    // one 16-byte vector of codes per thread and iteration (16 codes at b = 8)
     using W = typename Word4<B>::T;
-    W *o = reinterpret_cast<W *>(own);
-    const W *r = reinterpret_cast<const W *>(recv);
-    for (int64_t gi = blockIdx.x * (int64_t)NT + threadIdx.x; gi < n_groups; gi += (int64_t)gridDim.x * NT) {
-        const float4 a = unpack4<B>(c, r[gi]);
-        const float4 b = unpack4<B>(c, o[gi]);
-        const float4 s = make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z),
-                                     __fadd_rn(a.w, b.w));
-        o[gi] = pack4<B>(c, s);
+    constexpr int G = 16 / sizeof(W);  // 4-code groups per vector
+    uint4 *o = reinterpret_cast<uint4 *>(own);
+    const uint4 *r = reinterpret_cast<const uint4 *>(recv);
+    for (int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x; i < n_vec; i += (int64_t)gridDim.x * NT) {
+        uint4 va = r[i], vb = o[i];
+        W wa[G], wb[G];
+        memcpy(wa, &va, 16);
+        memcpy(wb, &vb, 16);
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            const float4 a = unpack4<B>(c, wa[g]);
+            const float4 b = unpack4<B>(c, wb[g]);
+            wb[g] = pack4<B>(c, make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z),
+                                            __fadd_rn(a.w, b.w)));
+        }
+        memcpy(&vb, wb, 16);
+        o[i] = vb;
     }
 }
 
@@ -689,15 +700,15 @@ cudaError_t launch_ring_reduce(uint8_t *own, const uint8_t *recv, int64_t n_tile
     return with_codec(e, m, hw, [&](auto c) -> cudaError_t {
         using C = decltype(c);
         const int b = 1 + e + m;
-        const int64_t n_groups = n_tiles * (kTile / 4);
-        const int grid_direct = (int)std::min<int64_t>((n_groups + kThreads - 1) / kThreads, (int64_t)sm_count() * 8);
+        const int64_t n_vec = n_tiles * 16 * b / 16;  // 16-byte vectors (a tile is 16 b bytes)
+        const int grid_direct = (int)std::min<int64_t>((n_vec + kThreads - 1) / kThreads, (int64_t)sm_count() * 8);
         const int grid_tile = (int)std::min<int64_t>((n_tiles + kThreads / 32 - 1) / (kThreads / 32), (int64_t)sm_count() * 8);
         if constexpr (C::kB == 8 || C::kB == 16 || C::kB == 32) {
-            ring_reduce_direct_kernel<C::kB, C, kThreads><<<grid_direct, kThreads, 0, s>>>(own, recv, n_groups, c);
+            ring_reduce_direct_kernel<C::kB, C, kThreads><<<grid_direct, kThreads, 0, s>>>(own, recv, n_vec, c);
         } else if constexpr (C::kB == 0) {
-            if (b == 8) ring_reduce_direct_kernel<8, C, kThreads><<<grid_direct, kThreads, 0, s>>>(own, recv, n_groups, c);
-            else if (b == 16) ring_reduce_direct_kernel<16, C, kThreads><<<grid_direct, kThreads, 0, s>>>(own, recv, n_groups, c);
-            else if (b == 32) ring_reduce_direct_kernel<32, C, kThreads><<<grid_direct, kThreads, 0, s>>>(own, recv, n_groups, c);
+            if (b == 8) ring_reduce_direct_kernel<8, C, kThreads><<<grid_direct, kThreads, 0, s>>>(own, recv, n_vec, c);
+            else if (b == 16) ring_reduce_direct_kernel<16, C, kThreads><<<grid_direct, kThreads, 0, s>>>(own, recv, n_vec, c);
+            else if (b == 32) ring_reduce_direct_kernel<32, C, kThreads><<<grid_direct, kThreads, 0, s>>>(own, recv, n_vec, c);
             else ring_reduce_tile_kernel<C, kThreads><<<grid_tile, kThreads, 0, s>>>(own, recv, n_tiles, c);
         } else {
             ring_reduce_tile_kernel<C, kThreads><<<grid_tile, kThreads, 0, s>>>(own, recv, n_tiles, c);

@@ -15,8 +15,6 @@ Usage:
     state = ApsHookState(process_group=None, exp_bits=5, man_bits=2)
     ddp_model.register_comm_hook(state, aps_hook)
 """
-from __future__ import annotations
-
 import torch
 import torch.distributed as dist
 
@@ -38,9 +36,9 @@ class ApsHookState:
             uid = [nccl_unique_id() if self.rank == 0 else None]
             dist.broadcast_object_list(uid, src=dist.get_global_rank(self.pg, 0), group=self.pg)
             self.comm = nccl_comm_init(uid[0], self.world, self.rank)
-        self.contexts: dict[int, tuple[ApsContext, list[tuple[int, int]]]] = {}
-        self.groups: dict[int, list[list[int]]] = {}  # bucket index -> parameter indices per APS layer
-        self.bucket_params: dict[int, list[torch.nn.Parameter]] = {}
+        self.contexts: dict = {}  # bucket index -> (ApsContext, layer spans)
+        self.groups: dict = {}  # bucket index -> parameter indices per APS layer
+        self.bucket_params: dict = {}  # bucket index -> its parameters
 
     def close(self):
         for ctx, _ in self.contexts.values():
@@ -51,7 +49,7 @@ class ApsHookState:
             self.comm = None
 
 
-def layer_spans(buffer: torch.Tensor, numels: list[int]) -> tuple[list[tuple[int, int]], list[list[int]]]:
+def layer_spans(buffer: torch.Tensor, numels):
     """Split a flat bucket into APS layers at 16-byte-aligned parameter starts.
     Returns [(offset, numel)] per layer and the parameter indices of each."""
     base = buffer.data_ptr()
@@ -67,7 +65,7 @@ def layer_spans(buffer: torch.Tensor, numels: list[int]) -> tuple[list[tuple[int
     return [tuple(s) for s in spans], groups
 
 
-def aps_hook(state: ApsHookState, bucket: "dist.GradBucket") -> torch.futures.Future:
+def aps_hook(state: ApsHookState, bucket: dist.GradBucket) -> torch.futures.Future[torch.Tensor]:
     buf = bucket.buffer()
     if buf.dtype != torch.float32:
         raise TypeError("aps_hook needs fp32 gradients")
