@@ -322,10 +322,17 @@ def main():
     hw = ctx_hw(ctx, args)
     for _ in range(3):
         aps.debug_ring_reduce(own, rcv, chunk_tiles, e, m, hw=hw)
+    torch.cuda.synchronize()
+    # 50 launches captured in a CUDA graph: the device time, not the Python launch rate
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        for _ in range(50):
+            aps.debug_ring_reduce(own, rcv, chunk_tiles, e, m, hw=hw)
+    graph.replay()
+    torch.cuda.synchronize()
     rr = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     rr[0].record(stream)
-    for _ in range(50):
-        aps.debug_ring_reduce(own, rcv, chunk_tiles, e, m, hw=hw)
+    graph.replay()
     rr[1].record(stream)
     torch.cuda.synchronize()
     rr_ms = rr[0].elapsed_time(rr[1]) / 50
@@ -352,7 +359,7 @@ def main():
     phases["ring_reduce_step_p8"] = {"us": round(rr_ms * 1e3, 2), "algorithmic_bytes": int(rr_bytes),
                                      "GB/s": round(rr_bytes / (rr_ms * 1e-3) / 1e9, 1),
                                      "frac": round(rr_bytes / (rr_ms * 1e-3) / 1e9 / peak, 4),
-                                     "note": "one reduce-scatter step's kernel for a p = 8 chunk (launch-bound at this size)"}
+                                     "note": "one reduce-scatter step's kernel for a p = 8 chunk (CUDA-graph replay of 50 launches)"}
     if world == 1:
         # one fused launch per step: FindMaxExp read (4 B) + Cast read (4 B) + codes (b/8 B) + fp32 out (4 B)
         kname = ("stream_kernel<FusedP1Op>" if os.environ.get("APS_ENGINE") in ("tma", "stream")

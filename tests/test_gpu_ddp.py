@@ -42,14 +42,15 @@ def test_ddp_hook_matches_oracle(pg, orc):
     state = aps.ApsHookState(exp_bits=5, man_bits=2)
     ddp.register_comm_hook(state, aps.aps_hook)
     x = torch.randn(64, 37, device="cuda")
-    for it in range(2):
+    seen_buckets = set()
+    for it in range(3):
         for p in list(model.parameters()) + list(ref.parameters()):
             p.grad = None
         (ddp(x * (it + 1)).square().sum() * 1e-3).backward()
         (ref(x * (it + 1)).square().sum() * 1e-3).backward()
         torch.cuda.synchronize()
         assert state.contexts, "hook never ran"
-        assert len(state.contexts) >= 2, "expected several buckets"
+        seen_buckets |= set(state.contexts)
         raw = {id(p): q.grad.detach().cpu().numpy().ravel() for p, q in zip(model.parameters(), ref.parameters())}
         got = {id(p): p.grad.detach().cpu().numpy().ravel() for p in model.parameters()}
         merged = 0
@@ -67,4 +68,5 @@ def test_ddp_hook_matches_oracle(pg, orc):
                         (idx, i)
                     off += n
         assert merged >= 1, "the misaligned parameter sizes should force at least one merged layer"
+    assert len(seen_buckets) >= 2, "DDP's rebuilt buckets (bucket_cap_mb=0.1) should give several buckets"
     state.close()
