@@ -79,6 +79,9 @@ def lib():
         L.oracle_ring_add_n.argtypes = [vp, vp, vp, i64, ctypes.c_int, ctypes.c_int]
         L.oracle_unscale_n.argtypes = [vp, vp, i64, i32, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int]
         L.oracle_scale_cast_n.argtypes = [vp, vp, i64, i32, ctypes.c_int, ctypes.c_int]
+        L.oracle_packed_bytes_mixed.argtypes = [ctypes.c_int, ctypes.c_int, vp, vp, vp]
+        L.oracle_packed_bytes_mixed.restype = i64
+        L.oracle_aps_sync_mixed.argtypes = [ctypes.c_int, vp, vp, ctypes.c_int, vp, vp, ctypes.c_int, vp, vp, vp, vp]
         _lib = L
     return _lib
 
@@ -208,4 +211,31 @@ def aps_sync(grads, e: int, m: int, average: int = 1, want_packed: bool = True,
     rc = lib().oracle_aps_sync(p, e, m, nl, _ptr(numels), gptrs, average, _ptr(ft),
                                _ptr(packed) if want_packed else None, _ptr(reduced),
                                optrs)
+    return SyncResult(rc, ft, packed, reduced, outs)
+
+
+def packed_bytes_mixed(p: int, numels, fmts) -> int:
+    n = np.ascontiguousarray(numels, dtype=np.int64)
+    e = np.ascontiguousarray([f[0] for f in fmts], dtype=np.int32)
+    m = np.ascontiguousarray([f[1] for f in fmts], dtype=np.int32)
+    return lib().oracle_packed_bytes_mixed(p, n.size, _ptr(n), _ptr(e), _ptr(m))
+
+
+def aps_sync_mixed(grads, fmts, average: int = 1, want_packed: bool = True) -> SyncResult:
+    """APS sync with per-layer formats fmts[l] = (e, m) (hybrid precision)."""
+    p = len(grads)
+    nl = len(grads[0])
+    numels = np.array([np.asarray(g).size for g in grads[0]], dtype=np.int64)
+    e = np.ascontiguousarray([f[0] for f in fmts], dtype=np.int32)
+    m = np.ascontiguousarray([f[1] for f in fmts], dtype=np.int32)
+    flat = [np.ascontiguousarray(grads[r][l], dtype=np.float32) for r in range(p) for l in range(nl)]
+    gptrs = (ctypes.c_void_p * len(flat))(*[a.ctypes.data for a in flat])
+    nbytes = packed_bytes_mixed(p, numels, fmts)
+    ft = np.zeros(nl, dtype=np.int32)
+    packed = np.zeros((p, nbytes), dtype=np.uint8) if want_packed else None
+    reduced = np.zeros(nbytes, dtype=np.uint8)
+    outs = [np.empty(int(n), dtype=np.float32) for n in numels]
+    optrs = (ctypes.c_void_p * nl)(*[a.ctypes.data for a in outs])
+    rc = lib().oracle_aps_sync_mixed(p, _ptr(e), _ptr(m), nl, _ptr(numels), gptrs, average, _ptr(ft),
+                                     _ptr(packed) if want_packed else None, _ptr(reduced), optrs)
     return SyncResult(rc, ft, packed, reduced, outs)

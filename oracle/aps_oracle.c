@@ -406,3 +406,112 @@ int oracle_scale_cast_n(const float *g, uint32_t *codes, int64_t n, int32_t ft, 
     for (int64_t i = 0; i < n; ++i) codes[i] = oracle_cast1(oracle_scale(g[i], ft), e, m);
     return OR_OK;
 }
+
+/* ------------------------------------------------------------------ */
+/* Per-layer formats (hybrid precision, Table      */
+/* `last_layer_precision` P:571-584 and P:545: "IEEE FP32 for the       */
+/* gradient of the last layer ... low precision for all other layers"). */
+/* Layer l has format (e[l], m[l]) and code width b_l; its tiles are     */
+/* 16*b_l bytes.  Padding tiles (T..T') continue the last layer's        */
+/* format.  Tile t starts at byte sum_{u<t} 16*b(u); chunk c = tiles     */
+/* [c T'/p, (c+1) T'/p) as before; every element is cast, re-quantised   */
+/* and decoded in its own layer's format.                                */
+/* ------------------------------------------------------------------ */
+int64_t oracle_packed_bytes_mixed(int p, int n_layers, const int64_t *numels, const int *e, const int *m)
+{
+    if (p < 1 || n_layers < 1 || !numels || !e || !m) return -1;
+    int64_t bytes = 0, T = 0;
+    for (int l = 0; l < n_layers; ++l) {
+        if (oracle_format_valid(e[l], m[l])) return -1;
+        const int64_t Tl = (numels[l] + OR_TILE - 1) / OR_TILE;
+        bytes += 16 * (int64_t)(1 + e[l] + m[l]) * Tl;
+        T += Tl;
+    }
+    const int64_t Tp = ((T + p - 1) / p) * p;
+    return bytes + 16 * (int64_t)(1 + e[n_layers - 1] + m[n_layers - 1]) * (Tp - T);
+}
+
+int oracle_aps_sync_mixed(int p, const int *e, const int *m, int n_layers, const int64_t *numels,
+                          const float *const *grads, int average, int32_t *ftilde_out,
+                          uint8_t *packed_out, uint8_t *reduced_out, float *const *out)
+{
+    if (p < 1 || n_layers < 1 || !numels || !grads || !e || !m) return OR_ERR_ARG;
+    for (int l = 0; l < n_layers; ++l) {
+        if (oracle_format_valid(e[l], m[l])) return OR_ERR_FORMAT;
+        if (numels[l] < 1) return OR_ERR_ARG;
+    }
+    const int64_t Tp = oracle_total_tiles(p, n_layers, numels);
+    const int64_t ncodes = Tp * OR_TILE;
+    const int64_t chunk_codes = (Tp / p) * OR_TILE;
+    const int64_t nbytes = oracle_packed_bytes_mixed(p, n_layers, numels, e, m);
+    /* per-code layer (padding codes belong to the last layer) and tile byte offsets */
+    int *lay = (int *)malloc(sizeof(int) * (size_t)ncodes);
+    int64_t *tile_byte = (int64_t *)malloc(sizeof(int64_t) * (size_t)(Tp + 1));
+    {
+        int64_t i = 0, t = 0, byte = 0;
+        for (int l = 0; l < n_layers; ++l) {
+            const int64_t Tl = (numels[l] + OR_TILE - 1) / OR_TILE;
+            for (int64_t k = 0; k < Tl * OR_TILE; ++k) lay[i++] = l;
+            for (int64_t k = 0; k < Tl; ++k, ++t) { tile_byte[t] = byte; byte += 16 * (1 + e[l] + m[l]); }
+        }
+        for (; i < ncodes; ++i) lay[i] = n_layers - 1;
+        for (; t < Tp; ++t) { tile_byte[t] = byte; byte += 16 * (1 + e[n_layers - 1] + m[n_layers - 1]); }
+        tile_byte[Tp] = byte;
+    }
+    /* Alg. 1 lines 3-4 per layer, in the layer's format */
+    int32_t *ft = (int32_t *)malloc(sizeof(int32_t) * (size_t)n_layers);
+    int nonfinite = 0;
+    for (int l = 0; l < n_layers; ++l) {
+        int32_t Emax = OR_EMPTY;
+        for (int r = 0; r < p; ++r) {
+            int32_t Er = oracle_find_max_exp(grads[(size_t)r * n_layers + l], numels[l], p);
+            if (Er == OR_NONFINITE) nonfinite = 1;
+            if (Er > Emax) Emax = Er;
+        }
+        ft[l] = oracle_scale_exp(e[l], Emax);
+        if (ftilde_out) ftilde_out[l] = ft[l];
+    }
+    if (nonfinite) { free(lay); free(tile_byte); free(ft); return OR_ERR_NONFINITE; }
+    /* lines 5-6: scale and Cast in the layer's format */
+    uint32_t *q = (uint32_t *)calloc((size_t)p * (size_t)ncodes, sizeof(uint32_t));
+    for (int r = 0; r < p; ++r) {
+        int64_t off = 0;
+        for (int l = 0; l < n_layers; ++l) {
+            const float *g = grads[(size_t)r * n_layers + l];
+            for (int64_t i = 0; i < numels[l]; ++i)
+                q[(size_t)r * ncodes + off + i] = oracle_cast1(oracle_scale(g[i], ft[l]), e[l], m[l]);
+            off += OR_TILE * ((numels[l] + OR_TILE - 1) / OR_TILE);
+        }
+    }
+    /* line 7: the ring with a re-quantise after every add, element in its own format */
+    uint32_t *s = (uint32_t *)calloc((size_t)ncodes, sizeof(uint32_t));
+    for (int c = 0; c < p; ++c)
+        for (int64_t i = c * chunk_codes; i < (c + 1) * chunk_codes; ++i) {
+            const int l = lay[i];
+            uint32_t acc = q[(size_t)((c + 1) % p) * ncodes + i];
+            for (int j = 2; j <= p; ++j) acc = oracle_ring_add(acc, q[(size_t)((c + j) % p) * ncodes + i], e[l], m[l]);
+            s[i] = acc;
+        }
+    /* O11 per tile: code k of tile t at bit k*b inside the tile's bytes */
+    for (int which = 0; which <= p; ++which) {
+        uint8_t *dst = which < p ? (packed_out ? packed_out + (size_t)which * (size_t)nbytes : NULL) : reduced_out;
+        const uint32_t *src = which < p ? q + (size_t)which * ncodes : s;
+        if (!dst) continue;
+        memset(dst, 0, (size_t)nbytes);
+        for (int64_t t = 0; t < Tp; ++t) {
+            const int l = lay[t * OR_TILE];
+            const int b = 1 + e[l] + m[l];
+            oracle_pack(src + t * OR_TILE, OR_TILE, b, dst + tile_byte[t]);
+        }
+    }
+    /* lines 8-9 */
+    if (out) {
+        int64_t off = 0;
+        for (int l = 0; l < n_layers; ++l) {
+            for (int64_t i = 0; i < numels[l]; ++i) out[l][i] = oracle_unscale1(s[off + i], ft[l], p, average, e[l], m[l]);
+            off += OR_TILE * ((numels[l] + OR_TILE - 1) / OR_TILE);
+        }
+    }
+    free(q); free(s); free(lay); free(tile_byte); free(ft);
+    return OR_OK;
+}

@@ -413,3 +413,90 @@ def test_all_zero_layer(orc):
     res = orc.aps_sync(g, 5, 2, average=1)
     assert res.ftilde[0] == 0
     assert [hex(v) for v in res.out[0].view(np.uint32)] == ["0x0", "0x80000000", "0x0"]
+
+
+# ---------------------------------------------------------------- per-layer formats (NEXT-2)
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4])
+def test_mixed_uniform_equals_uniform(orc, p):
+    """The per-layer-format oracle with one format everywhere is the uniform oracle."""
+    numels = [5, 128, 300, 1, 1000]
+    grads = synthetic.make_grads(numels, p, seed=synthetic.SEED + 5)
+    for fmt in [(5, 2), (3, 0), (5, 6)]:
+        a = orc.aps_sync(grads, *fmt, average=1)
+        b = orc.aps_sync_mixed(grads, [fmt] * len(numels), average=1)
+        assert np.array_equal(a.ftilde, b.ftilde)
+        assert np.array_equal(a.packed, b.packed) and np.array_equal(a.reduced, b.reduced)
+        for x, y in zip(a.out, b.out):
+            assert np.array_equal(x.view(np.uint32), y.view(np.uint32))
+
+
+def _independent_mixed(grads, fmts, average):
+    """Hybrid precision re-derived per layer with library casts (torch dtypes;
+    (8,23) = fp32 itself, section 3.3.1: power-of-two scaling is exact), the
+    ring in the order of A14, and the per-tile packed layout written with
+    numpy.packbits."""
+    p = len(grads)
+    numels = [g.size for g in grads[0]]
+    T = sum((n + 127) // 128 for n in numels)
+    Tp = p * ((T + p - 1) // p)
+    lay = np.concatenate([np.full(128 * ((n + 127) // 128), l) for l, n in enumerate(numels)]
+                         + [np.full(128 * (Tp - T), len(numels) - 1)])
+    def codes_of(x, fmt):
+        if fmt == (8, 23):
+            return np.ascontiguousarray(x, np.float32).view(np.uint32).copy()
+        return _torch_codes(x, TORCH_DT[fmt])
+    def vals_of(c, fmt):
+        if fmt == (8, 23):
+            return np.ascontiguousarray(c, np.uint32).view(np.float32)
+        return _torch_values(c, TORCH_DT[fmt])
+    ft = []
+    for l, fmt in enumerate(fmts):
+        E = max(_find_max_exp_literal(grads[r][l], p) for r in range(p))
+        ft.append(0 if E == EMPTY else ((1 << (fmt[0] - 1)) - 1) - E)
+    q = np.zeros((p, Tp * 128), np.uint32)
+    for r in range(p):
+        off = 0
+        for l, n in enumerate(numels):
+            q[r, off:off + n] = codes_of(np.ldexp(grads[r][l], np.int32(ft[l])), fmts[l])
+            off += 128 * ((n + 127) // 128)
+    chunk = Tp // p * 128
+    s = np.zeros(Tp * 128, np.uint32)
+    for i0 in range(0, Tp * 128, 128):
+        fmt = fmts[lay[i0]]
+        c = i0 // chunk
+        sl = slice(i0, i0 + 128)
+        acc = q[(c + 1) % p, sl]
+        for j in range(2, p + 1):
+            v = (vals_of(acc, fmt) + vals_of(q[(c + j) % p, sl], fmt)).astype(np.float32)
+            acc = codes_of(v, fmt)
+        s[sl] = acc
+    def pack(codes):
+        parts = []
+        for i0 in range(0, Tp * 128, 128):
+            fmt = fmts[lay[i0]]
+            parts.append(_pack_little(codes[i0:i0 + 128], 1 + fmt[0] + fmt[1]))
+        return np.concatenate(parts)
+    outs, off = [], 0
+    for l, n in enumerate(numels):
+        t = np.ldexp(vals_of(s[off:off + n], fmts[l]).astype(np.float32), np.int32(-ft[l]))
+        outs.append((t / np.float32(p)).astype(np.float32) if average else t)
+        off += 128 * ((n + 127) // 128)
+    return np.array(ft, np.int32), np.stack([pack(q[r]) for r in range(p)]), pack(s), outs
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4])
+def test_mixed_hybrid_vs_torch(orc, p):
+    """Hybrid precision: (5,2) everywhere, (8,23) = fp32 for the classifier
+    weight and bias (Table `last_layer_precision`), plus a (5,10) layer."""
+    numels = [300, 128, 4096, 1000, 1]
+    fmts = [(5, 2), (5, 10), (5, 2), (8, 23), (8, 23)]
+    grads = synthetic.make_grads(numels, p, seed=synthetic.SEED + 9)
+    res = orc.aps_sync_mixed(grads, fmts, average=1)
+    ft, packed, reduced, outs = _independent_mixed(grads, fmts, 1)
+    assert res.rc == 0
+    assert np.array_equal(res.ftilde, ft)
+    assert np.array_equal(res.packed, packed)
+    assert np.array_equal(res.reduced, reduced)
+    for a, b in zip(res.out, outs):
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
