@@ -95,6 +95,20 @@ typedef enum {
 aps_status aps_init(aps_ctx **out, int exp_bits, int man_bits, int world_size, int rank,
                     int n_layers, const int64_t *numels, void *nccl_comm, void *cuda_stream);
 
+/* As aps_init with a format PER LAYER (hybrid precision):
+ * layer l uses (exp_bits[l], man_bits[l]) -- the paper's per-layer precision
+ * choice ("the last layer's gradients ... in higher precision",
+ * Table last_layer_precision).  f~_l uses layer l's upper_bound_exp.
+ * Packed layout: layer l's tiles are 16*b_l bytes each, in layer order; the
+ * padding tiles up to T' continue the LAST layer's format (reading A22).  Ring
+ * chunk c is still tiles [c T'/p, (c+1) T'/p); its byte size then differs per
+ * chunk, its reduction runs per format run, and the all-gather forwards the
+ * chunks around the ring (send/recv) instead of ncclAllGather.  Arrays are
+ * host [n_layers]; everything else as aps_init.  Equal formats everywhere
+ * behave exactly like aps_init. */
+aps_status aps_init_mixed(aps_ctx **out, const int *exp_bits, const int *man_bits, int world_size, int rank,
+                          int n_layers, const int64_t *numels, void *nccl_comm, void *cuda_stream);
+
 /* Bytes of device workspace the context needs (packed buffer, one ring
  * receive chunk, layer and work tables, exponent vectors). */
 size_t aps_workspace_bytes(const aps_ctx *ctx);
@@ -165,6 +179,11 @@ aps_status aps_get_packed(aps_ctx *ctx, const void **dev, size_t *bytes);
 /* Layout queries (host only, no device): tiles T' and packed bytes 16*b*T'. */
 aps_status aps_layout(int world_size, int exp_bits, int man_bits, int n_layers,
                       const int64_t *numels, int64_t *total_tiles, int64_t *packed_bytes);
+
+/* aps_layout for per-layer formats (host only): T' and the packed bytes
+ * sum_l 16 b_l T_l + (T' - T) 16 b_last (aps_init_mixed's layout). */
+aps_status aps_layout_mixed(int world_size, int n_layers, const int64_t *numels, const int *exp_bits,
+                            const int *man_bits, int64_t *total_tiles, int64_t *packed_bytes);
 
 /* Ring schedule (host only): at reduce-scatter step `step` (0..p-2) rank
  * `rank` sends chunk (rank-1-step) mod p to rank+1 and receives chunk

@@ -28,6 +28,7 @@ EXPORTS = [
     "aps_ring_step", "aps_last_error", "aps_destroy", "aps_version", "aps_nccl_unique_id",
     "aps_nccl_comm_init", "aps_nccl_comm_destroy", "aps_sim_layer_scales", "aps_sim_allreduce",
     "aps_debug_cast", "aps_debug_decode", "aps_debug_ring_reduce", "aps_debug_timeline",
+    "aps_init_mixed", "aps_layout_mixed",
 ]
 
 
@@ -81,6 +82,8 @@ def load(path: Path | str | None = None):
         "aps_debug_decode": ([vp, vp, i64, i32, i32, i32, vp], i32),
         "aps_debug_ring_reduce": ([vp, vp, i64, i32, i32, i32, vp], i32),
         "aps_debug_timeline": ([vp, vp, i32], i32),
+        "aps_init_mixed": ([ctypes.POINTER(vp), vp, vp, i32, i32, i32, vp, vp, vp], i32),
+        "aps_layout_mixed": ([i32, i32, vp, vp, vp, ctypes.POINTER(i64), ctypes.POINTER(i64)], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -105,6 +108,21 @@ def layout(world_size: int, exp_bits: int, man_bits: int, numels: Sequence[int])
                       ctypes.byref(T), ctypes.byref(nb))
     if st:
         raise ApsError(st, "aps_layout")
+    return T.value, nb.value
+
+
+def _i32_array(vals: Sequence[int]):
+    return (ctypes.c_int32 * len(vals))(*vals)
+
+
+def layout_mixed(world_size: int, numels: Sequence[int], formats: Sequence[tuple[int, int]]) -> tuple[int, int]:
+    """(T', packed_bytes) with a format (exp_bits, man_bits) per layer -- host only."""
+    L = load()
+    T, nb = ctypes.c_int64(), ctypes.c_int64()
+    st = L.aps_layout_mixed(world_size, len(numels), _i64_array(numels), _i32_array([f[0] for f in formats]),
+                            _i32_array([f[1] for f in formats]), ctypes.byref(T), ctypes.byref(nb))
+    if st:
+        raise ApsError(st, "aps_layout_mixed")
     return T.value, nb.value
 
 
@@ -141,12 +159,14 @@ class ApsContext:
     """One aps_ctx plus its torch-owned workspace.
 
     grads are lists of torch fp32 CUDA tensors (one per layer, contiguous,
-    16-byte aligned); the order fixes the packed layout.
+    16-byte aligned); the order fixes the packed layout.  `formats`, if
+    given, is one (exp_bits, man_bits) per layer (hybrid precision,
+    aps_init_mixed) and overrides exp_bits/man_bits.
     """
 
     def __init__(self, exp_bits: int, man_bits: int, numels: Sequence[int], world_size: int = 1,
                  rank: int = 0, nccl_comm: int | None = None, stream=None, device=None,
-                 hw_convert: bool | None = None):
+                 hw_convert: bool | None = None, formats: Sequence[tuple[int, int]] | None = None):
         import torch
         self.L = load()
         self.exp_bits, self.man_bits = exp_bits, man_bits
@@ -155,8 +175,17 @@ class ApsContext:
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
         h = ctypes.c_void_p()
-        st = self.L.aps_init(ctypes.byref(h), exp_bits, man_bits, world_size, rank, len(self.numels),
-                             _i64_array(self.numels), nccl_comm, self.stream.cuda_stream)
+        self.formats = [tuple(f) for f in formats] if formats is not None else None
+        if self.formats is not None:
+            if len(self.formats) != len(self.numels):
+                raise ValueError("formats needs one (exp_bits, man_bits) per layer")
+            st = self.L.aps_init_mixed(ctypes.byref(h), _i32_array([f[0] for f in self.formats]),
+                                       _i32_array([f[1] for f in self.formats]), world_size, rank,
+                                       len(self.numels), _i64_array(self.numels), nccl_comm,
+                                       self.stream.cuda_stream)
+        else:
+            st = self.L.aps_init(ctypes.byref(h), exp_bits, man_bits, world_size, rank, len(self.numels),
+                                 _i64_array(self.numels), nccl_comm, self.stream.cuda_stream)
         if st:
             raise ApsError(st, "aps_init")
         self.h = h

@@ -40,8 +40,27 @@ struct aps_ctx {
     std::vector<aps::Item> items;
     std::vector<aps::LayerDev> layers;
     int64_t tiles = 0;        // T' (padded to a multiple of world)
-    int64_t packed_bytes = 0; // 16 * b * T'
-    int64_t chunk_bytes = 0;  // packed_bytes / world
+    int64_t packed_bytes = 0; // sum over tiles of 16 * b(tile)
+    int64_t chunk_bytes = 0;  // packed_bytes / world (uniform formats)
+    // per-layer formats (NEXT-2, hybrid precision): the layers' (e, m); items are
+    // grouped by format (one launch per group); the ring reduces each chunk by
+    // format segments and all-gathers unequal chunks with send/recv
+    std::vector<int> le, lm;
+    bool uniform = true, hw_enabled = true;
+    struct Group {
+        int e, m;
+        bool hw;
+        int item_begin, item_count, max_layer_items;
+    };
+    std::vector<Group> groups;
+    struct Seg {
+        int64_t byte_off, n_tiles;  // byte offset in the packed buffer, tiles
+        int e, m;
+        bool hw;
+    };
+    std::vector<int64_t> chunk_byte;            // [world + 1]
+    std::vector<std::vector<Seg>> chunk_segs;   // [world]
+    int64_t max_chunk_bytes = 0;
     // workspace carve-up
     uint8_t *ws = nullptr;
     size_t ws_bytes = 0, need = 0;
@@ -154,27 +173,33 @@ aps_status aps_ring_step(int world_size, int rank, int step, int *send_c, int *r
     return APS_OK;
 }
 
-aps_status aps_init(aps_ctx **out, int exp_bits, int man_bits, int world_size, int rank, int n_layers,
-                    const int64_t *numels, void *nccl_comm, void *cuda_stream)
+static aps_status init_common(aps_ctx **out, const int *e_arr, const int *m_arr, int world_size, int rank,
+                              int n_layers, const int64_t *numels, void *nccl_comm, void *cuda_stream)
 {
     if (!out) return APS_ERR_ARG;
     *out = nullptr;
-    if (!format_ok(exp_bits, man_bits)) return APS_ERR_FORMAT;
-    if (world_size < 1 || rank < 0 || rank >= world_size || n_layers < 1 || !numels) return APS_ERR_ARG;
+    if (world_size < 1 || rank < 0 || rank >= world_size || n_layers < 1 || !numels || !e_arr || !m_arr)
+        return APS_ERR_ARG;
     if (n_layers > (1 << 24)) return APS_ERR_ARG;
+    for (int l = 0; l < n_layers; ++l)
+        if (!format_ok(e_arr[l], m_arr[l])) return APS_ERR_FORMAT;
     aps_ctx *c = new (std::nothrow) aps_ctx();
     if (!c) return APS_ERR_ARG;
-    c->e = exp_bits;
-    c->m = man_bits;
-    c->b = 1 + exp_bits + man_bits;
+    c->le.assign(e_arr, e_arr + n_layers);
+    c->lm.assign(m_arr, m_arr + n_layers);
+    for (int l = 1; l < n_layers; ++l)
+        if (c->le[l] != c->le[0] || c->lm[l] != c->lm[0]) c->uniform = false;
+    c->e = e_arr[0];
+    c->m = m_arr[0];
+    c->b = 1 + c->e + c->m;
     c->world = world_size;
     c->rank = rank;
     c->n_layers = n_layers;
     c->comm = static_cast<ncclComm_t>(nccl_comm);
     c->sim = (world_size > 1 && !nccl_comm);
     c->stream = static_cast<cudaStream_t>(cuda_stream);
-    c->hw = aps::hw_available(exp_bits, man_bits);
-    if (const char *env = std::getenv("APS_HW_CVT")) c->hw = c->hw && std::atoi(env) != 0;
+    if (const char *env = std::getenv("APS_HW_CVT")) c->hw_enabled = std::atoi(env) != 0;
+    c->hw = c->hw_enabled && aps::hw_available(c->e, c->m);
     if (const char *env = std::getenv("APS_ENGINE")) {
         if (!std::strcmp(env, "tma") || !std::strcmp(env, "stream")) c->engine = aps_ctx::kTma;
         else if (!std::strcmp(env, "simple")) c->engine = aps_ctx::kSimple;
@@ -189,7 +214,8 @@ aps_status aps_init(aps_ctx **out, int exp_bits, int man_bits, int world_size, i
         }
     }
     c->numels.assign(numels, numels + n_layers);
-    int64_t toff = 0;
+    std::vector<int64_t> layer_byte(n_layers);
+    int64_t toff = 0, boff = 0;
     for (int l = 0; l < n_layers; ++l) {
         if (numels[l] < 1) {
             delete c;
@@ -200,6 +226,8 @@ aps_status aps_init(aps_ctx **out, int exp_bits, int man_bits, int world_size, i
             delete c;
             return APS_ERR_ARG;
         }
+        const int64_t tb = 16 * (int64_t)(1 + c->le[l] + c->lm[l]);  // bytes per tile of this layer
+        layer_byte[l] = boff;
         aps::LayerDev L{};
         L.numel = numels[l];
         L.tile_off = toff;
@@ -211,26 +239,86 @@ aps_status aps_init(aps_ctx **out, int exp_bits, int man_bits, int world_size, i
             it.n_tiles = (int32_t)std::min<int64_t>(aps::kItemTiles, T - t0);
             it.cnt = (int32_t)std::min<int64_t>((int64_t)it.n_tiles * aps::kTile, numels[l] - t0 * aps::kTile);
             it.tile_pos = toff + t0;
+            it.byte_pos = boff + t0 * tb;
             c->items.push_back(it);
             ++L.n_items;
         }
         for (size_t k = c->items.size() - (size_t)L.n_items; k < c->items.size(); ++k)
             c->items[k].layer_items = L.n_items;
-
         c->layers.push_back(L);
         toff += T;
+        boff += T * tb;
     }
     if (c->items.size() > (size_t)INT32_MAX) {
         delete c;
         return APS_ERR_ARG;
     }
-    c->tiles = (toff + world_size - 1) / world_size * world_size;
-    c->packed_bytes = 16 * (int64_t)c->b * c->tiles;
-    c->chunk_bytes = c->packed_bytes / world_size;
+    const int64_t T = toff;
+    c->tiles = (T + world_size - 1) / world_size * world_size;
+    const int64_t tb_last = 16 * (int64_t)(1 + c->le[n_layers - 1] + c->lm[n_layers - 1]);
+    c->packed_bytes = boff + (c->tiles - T) * tb_last;  // padding tiles continue the last layer's format
+    c->chunk_bytes = c->packed_bytes / world_size;     // (uniform formats)
+    // format groups (first-appearance order), items stably grouped by format
+    std::vector<int> layer_group(n_layers);
+    for (int l = 0; l < n_layers; ++l) {
+        int g = 0;
+        while (g < (int)c->groups.size() && (c->groups[g].e != c->le[l] || c->groups[g].m != c->lm[l])) ++g;
+        if (g == (int)c->groups.size())
+            c->groups.push_back({c->le[l], c->lm[l], c->hw_enabled && aps::hw_available(c->le[l], c->lm[l]), 0, 0, 0});
+        layer_group[l] = g;
+    }
+    std::stable_sort(c->items.begin(), c->items.end(), [&](const aps::Item &a, const aps::Item &b) {
+        return layer_group[a.layer] < layer_group[b.layer];
+    });
+    for (size_t k = 0; k < c->items.size(); ++k) {
+        aps_ctx::Group &g = c->groups[layer_group[c->items[k].layer]];
+        if (g.item_count == 0) g.item_begin = (int)k;
+        ++g.item_count;
+        g.max_layer_items = std::max(g.max_layer_items, c->items[k].layer_items);
+    }
+    // ring chunks: byte ranges and per-format segments
+    auto tile_layer_byte = [&](int64_t t, int &layer) -> int64_t {  // byte offset of tile t
+        if (t >= T) {
+            layer = n_layers - 1;
+            return boff + (t - T) * tb_last;
+        }
+        int lo = 0, hi = n_layers - 1;  // last layer with tile_off <= t
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) / 2;
+            if (c->layers[mid].tile_off <= t) lo = mid; else hi = mid - 1;
+        }
+        layer = lo;
+        return layer_byte[lo] + (t - c->layers[lo].tile_off) * 16 * (int64_t)(1 + c->le[lo] + c->lm[lo]);
+    };
+    const int64_t ct = c->tiles / world_size;
+    c->chunk_byte.resize(world_size + 1);
+    c->chunk_segs.assign(world_size, {});
+    for (int ch = 0; ch <= world_size; ++ch) {
+        int lay;
+        c->chunk_byte[ch] = ch == world_size ? c->packed_bytes : tile_layer_byte(ch * ct, lay);
+    }
+    for (int ch = 0; ch < world_size; ++ch) {
+        int64_t t = ch * ct;
+        const int64_t t_end = (ch + 1) * ct;
+        while (t < t_end) {
+            int lay;
+            const int64_t byte = tile_layer_byte(t, lay);
+            int64_t run_end = (t >= T) ? t_end : std::min<int64_t>(t_end, c->layers[lay].tile_off + layer_tiles(numels[lay]));
+            if (run_end == T && lay == n_layers - 1) run_end = t_end;  // padding continues the last layer
+            const int e = c->le[lay], m = c->lm[lay];
+            std::vector<aps_ctx::Seg> &segs = c->chunk_segs[ch];
+            if (!segs.empty() && segs.back().e == e && segs.back().m == m)
+                segs.back().n_tiles += run_end - t;
+            else
+                segs.push_back({byte, run_end - t, e, m, c->hw_enabled && aps::hw_available(e, m)});
+            t = run_end;
+        }
+        c->max_chunk_bytes = std::max(c->max_chunk_bytes, c->chunk_byte[ch + 1] - c->chunk_byte[ch]);
+    }
     // workspace layout
     size_t o = 0;
     c->off_packed = o; o = align_up(o + (size_t)c->packed_bytes);
-    c->off_recv = o;   o = align_up(o + (world_size > 1 ? (size_t)c->chunk_bytes : 0));
+    c->off_recv = o;   o = align_up(o + (world_size > 1 ? (size_t)c->max_chunk_bytes : 0));
     c->off_items = o;  o = align_up(o + sizeof(aps::Item) * c->items.size());
     c->off_layers = o; o = align_up(o + sizeof(aps::LayerDev) * c->layers.size());
     c->off_src = o;    o = align_up(o + sizeof(void *) * (size_t)n_layers);
@@ -251,6 +339,41 @@ aps_status aps_init(aps_ctx **out, int exp_bits, int man_bits, int world_size, i
     for (const auto &L : c->layers) c->max_layer_items = std::max(c->max_layer_items, (int)L.n_items);
     c->need = o;
     *out = c;
+    return APS_OK;
+}
+
+aps_status aps_init(aps_ctx **out, int exp_bits, int man_bits, int world_size, int rank, int n_layers,
+                    const int64_t *numels, void *nccl_comm, void *cuda_stream)
+{
+    if (!out) return APS_ERR_ARG;
+    *out = nullptr;
+    if (!format_ok(exp_bits, man_bits)) return APS_ERR_FORMAT;
+    if (n_layers < 1 || n_layers > (1 << 24)) return APS_ERR_ARG;
+    std::vector<int> e(n_layers, exp_bits), m(n_layers, man_bits);
+    return init_common(out, e.data(), m.data(), world_size, rank, n_layers, numels, nccl_comm, cuda_stream);
+}
+
+aps_status aps_init_mixed(aps_ctx **out, const int *exp_bits, const int *man_bits, int world_size, int rank,
+                          int n_layers, const int64_t *numels, void *nccl_comm, void *cuda_stream)
+{
+    return init_common(out, exp_bits, man_bits, world_size, rank, n_layers, numels, nccl_comm, cuda_stream);
+}
+
+aps_status aps_layout_mixed(int world_size, int n_layers, const int64_t *numels, const int *exp_bits,
+                            const int *man_bits, int64_t *total_tiles, int64_t *packed_bytes)
+{
+    if (world_size < 1 || n_layers < 1 || !numels || !exp_bits || !man_bits) return APS_ERR_ARG;
+    int64_t T = 0, bytes = 0;
+    for (int l = 0; l < n_layers; ++l) {
+        if (!format_ok(exp_bits[l], man_bits[l])) return APS_ERR_FORMAT;
+        if (numels[l] < 1) return APS_ERR_ARG;
+        T += layer_tiles(numels[l]);
+        bytes += 16 * (int64_t)(1 + exp_bits[l] + man_bits[l]) * layer_tiles(numels[l]);
+    }
+    const int64_t Tp = (T + world_size - 1) / world_size * world_size;
+    if (total_tiles) *total_tiles = Tp;
+    if (packed_bytes)
+        *packed_bytes = bytes + (Tp - T) * 16 * (int64_t)(1 + exp_bits[n_layers - 1] + man_bits[n_layers - 1]);
     return APS_OK;
 }
 
@@ -302,10 +425,35 @@ aps_status aps_set_workspace(aps_ctx *c, void *dev, size_t bytes)
     return APS_OK;
 }
 
+// the tables of one format group: its items (contiguous after the grouping in init)
+static aps::DevTables group_tables(const aps_ctx *c, const aps_ctx::Group &g)
+{
+    aps::DevTables t = c->t;
+    t.items += g.item_begin;
+    t.iptr += g.item_begin;
+    t.n_items = g.item_count;
+    return t;
+}
+
+// reduce the received copy of chunk ch into this rank's own copy, one launch per
+// format segment of the chunk (a segment is a run of tiles of one format)
+static aps_status reduce_chunk(aps_ctx *c, const aps_ctx *layout, int ch, const uint8_t *recv, cudaStream_t st)
+{
+    const int64_t base = layout->chunk_byte[ch];
+    for (const auto &sg : layout->chunk_segs[ch])
+        APS_CUDA(c, aps::launch_ring_reduce(c->t.packed + sg.byte_off, recv + (sg.byte_off - base), sg.n_tiles, sg.e,
+                                            sg.m, sg.hw, st));
+    return APS_OK;
+}
+
 aps_status aps_set_hw_convert(aps_ctx *c, int enable)
 {
     if (!c) return APS_ERR_ARG;
-    c->hw = enable && aps::hw_available(c->e, c->m);
+    c->hw_enabled = enable != 0;
+    c->hw = c->hw_enabled && aps::hw_available(c->e, c->m);
+    for (auto &g : c->groups) g.hw = c->hw_enabled && aps::hw_available(g.e, g.m);
+    for (auto &segs : c->chunk_segs)
+        for (auto &sg : segs) sg.hw = c->hw_enabled && aps::hw_available(sg.e, sg.m);
     return APS_OK;
 }
 
@@ -347,10 +495,13 @@ aps_status aps_quantize_pack(aps_ctx *c, const float *const *grads)
     if (c->phase < kScales) return fail(c, APS_ERR_STATE, "aps_quantize_pack before aps_layer_scales");
     if (!grads) return fail(c, APS_ERR_ARG, "grads is NULL");
     if (aps_status s = upload_ptrs<const float *>(c, c->src_cache, grads, c->off_src)) return s;
-    cudaError_t e = c->stream_engine ? aps::launch_stream_quant(c->t, c->e, c->m, c->hw, c->stream)
-                                     : cudaErrorNotSupported;
-    if (e == cudaErrorNotSupported) e = aps::launch_quant_pack(c->t, c->e, c->m, c->hw, c->stream);
-    APS_CUDA(c, e);
+    for (const auto &g : c->groups) {  // one launch per format group (NEXT-2)
+        const aps::DevTables t = group_tables(c, g);
+        cudaError_t e = c->stream_engine ? aps::launch_stream_quant(t, g.e, g.m, g.hw, c->stream)
+                                         : cudaErrorNotSupported;
+        if (e == cudaErrorNotSupported) e = aps::launch_quant_pack(t, g.e, g.m, g.hw, c->stream);
+        APS_CUDA(c, e);
+    }
     c->phase = kPacked;
     return APS_OK;
 }
@@ -367,21 +518,34 @@ aps_status aps_allreduce(aps_ctx *c)
     const int p = c->world, r = c->rank;
     uint8_t *packed = c->t.packed;
     uint8_t *recv = c->ws + c->off_recv;
-    const size_t cb = (size_t)c->chunk_bytes;
-    const int64_t chunk_tiles = c->tiles / p;
     // reduce-scatter: p-1 steps, each a send/recv of packed bytes then the
-    // unpack-add-requantise-repack kernel (same stream: ordered)
+    // unpack-add-requantise-repack kernel per format segment (same stream: ordered)
     for (int s = 0; s < p - 1; ++s) {
         const int sc = send_chunk(p, r, s), rc = recv_chunk(p, r, s);
         APS_NCCL(c, ncclGroupStart());
-        APS_NCCL(c, ncclSend(packed + (size_t)sc * cb, cb, ncclUint8, mod(r + 1, p), c->comm, c->stream));
-        APS_NCCL(c, ncclRecv(recv, cb, ncclUint8, mod(r - 1, p), c->comm, c->stream));
+        APS_NCCL(c, ncclSend(packed + c->chunk_byte[sc], (size_t)(c->chunk_byte[sc + 1] - c->chunk_byte[sc]),
+                             ncclUint8, mod(r + 1, p), c->comm, c->stream));
+        APS_NCCL(c, ncclRecv(recv, (size_t)(c->chunk_byte[rc + 1] - c->chunk_byte[rc]), ncclUint8, mod(r - 1, p),
+                             c->comm, c->stream));
         APS_NCCL(c, ncclGroupEnd());
-        APS_CUDA(c, aps::launch_ring_reduce(packed + (size_t)rc * cb, recv, chunk_tiles, c->e, c->m, c->hw,
-                                            c->stream));
+        if (aps_status st = reduce_chunk(c, c, rc, recv, c->stream)) return st;
     }
     // all-gather of the reduced chunks (pure data movement; rank r owns chunk r)
-    APS_NCCL(c, ncclAllGather(packed + (size_t)r * cb, packed, cb, ncclUint8, c->comm, c->stream));
+    if (c->uniform) {
+        const size_t cb = (size_t)c->chunk_bytes;
+        APS_NCCL(c, ncclAllGather(packed + (size_t)r * cb, packed, cb, ncclUint8, c->comm, c->stream));
+    } else {
+        // chunks of unequal byte size: p-1 ring forwarding steps (step s passes on chunk r-s)
+        for (int s = 0; s < p - 1; ++s) {
+            const int sc = mod(r - s, p), rc = mod(r - s - 1, p);
+            APS_NCCL(c, ncclGroupStart());
+            APS_NCCL(c, ncclSend(packed + c->chunk_byte[sc], (size_t)(c->chunk_byte[sc + 1] - c->chunk_byte[sc]),
+                                 ncclUint8, mod(r + 1, p), c->comm, c->stream));
+            APS_NCCL(c, ncclRecv(packed + c->chunk_byte[rc], (size_t)(c->chunk_byte[rc + 1] - c->chunk_byte[rc]),
+                                 ncclUint8, mod(r - 1, p), c->comm, c->stream));
+            APS_NCCL(c, ncclGroupEnd());
+        }
+    }
     c->phase = kReduced;
     return APS_OK;
 }
@@ -393,12 +557,15 @@ aps_status aps_unscale(aps_ctx *c, float *const *out, int average)
         return fail(c, APS_ERR_STATE, "aps_unscale before aps_allreduce");
     if (!out) return fail(c, APS_ERR_ARG, "out is NULL");
     if (aps_status s = upload_ptrs<float *>(c, c->dst_cache, out, c->off_dst)) return s;
-    cudaError_t e = c->stream_engine
-                        ? aps::launch_stream_unpack(c->t, c->e, c->m, c->hw, c->world, average, c->stream)
-                        : cudaErrorNotSupported;
-    if (e == cudaErrorNotSupported)
-        e = aps::launch_unpack_unscale(c->t, c->e, c->m, c->hw, c->world, average, c->stream);
-    APS_CUDA(c, e);
+    for (const auto &g : c->groups) {
+        const aps::DevTables t = group_tables(c, g);
+        cudaError_t e = c->stream_engine
+                            ? aps::launch_stream_unpack(t, g.e, g.m, g.hw, c->world, average, c->stream)
+                            : cudaErrorNotSupported;
+        if (e == cudaErrorNotSupported)
+            e = aps::launch_unpack_unscale(t, g.e, g.m, g.hw, c->world, average, c->stream);
+        APS_CUDA(c, e);
+    }
     return APS_OK;
 }
 
@@ -414,21 +581,25 @@ aps_status aps_sync_out(aps_ctx *c, const float *const *grads, float *const *out
             APS_CUDA(c, aps::launch_build_item_ptrs(c->t, c->stream));
             c->iptr_valid = true;
         }
-        const int grid = aps::fused_p1_ldg_grid(c->e, c->m, c->hw, c->t.n_items);
         const char *sched = std::getenv("APS_FUSED_SCHEDULE");
-        if (!sched || std::strcmp(sched, "barrier") != 0) {
-            // wavefront: quantise items trail their abs-max items by D positions
-            const int wgrid = aps::fused_p1_wave_grid(c->e, c->m, c->hw, c->t.n_items);
-            const int lag = std::min(c->t.n_items, c->max_layer_items + wgrid);
-            APS_CUDA(c, aps::launch_fused_p1_wave(c->t, c->e, c->m, c->hw, average, c->gen, c->wave_claim_base,
-                                                  c->wave_calls, lag, wgrid, c->stream));
-            // every position is claimed once and every CTA overshoots kWaveOvershoot times
-            c->wave_claim_base += (uint32_t)(2 * c->t.n_items + aps::kWaveOvershoot * wgrid);
+        if (!c->uniform || !sched || std::strcmp(sched, "barrier") != 0) {
+            // wavefront: quantise items trail their abs-max items by D positions;
+            // one launch per format group (a layer's items never straddle groups)
+            for (const auto &g : c->groups) {
+                const aps::DevTables t = group_tables(c, g);
+                const int wgrid = aps::fused_p1_wave_grid(g.e, g.m, g.hw, t.n_items);
+                const int lag = std::min(t.n_items, g.max_layer_items + wgrid);
+                APS_CUDA(c, aps::launch_fused_p1_wave(t, g.e, g.m, g.hw, average, c->gen, c->wave_claim_base,
+                                                      c->wave_calls, lag, wgrid, c->stream));
+                // every position is claimed once and every CTA overshoots kWaveOvershoot times
+                c->wave_claim_base += (uint32_t)(2 * t.n_items + aps::kWaveOvershoot * wgrid);
+            }
             ++c->wave_calls;
             ++c->gen;
             c->phase = kReduced;
             return APS_OK;
         }
+        const int grid = aps::fused_p1_ldg_grid(c->e, c->m, c->hw, c->t.n_items);
         const uint32_t tgt = c->done_target + (uint32_t)grid * (uint32_t)aps::kFusedWarps;
         APS_CUDA(c, aps::launch_fused_p1_ldg(c->t, c->e, c->m, c->hw, average, c->gen, tgt, c->claim_base, grid,
                                              c->stream));
@@ -439,7 +610,7 @@ aps_status aps_sync_out(aps_ctx *c, const float *const *grads, float *const *out
         c->phase = kReduced;
         return APS_OK;
     }
-    if (c->world == 1 && !c->comm && c->stream_engine && aps::stream_fused_supported(c->e, c->m, c->hw)) {
+    if (c->world == 1 && !c->comm && c->stream_engine && c->uniform && aps::stream_fused_supported(c->e, c->m, c->hw)) {
         // one rank: FindMaxExp -> f~ -> Cast -> pack -> Cast back -> unscale in one launch
         if (aps_status s = upload_ptrs<const float *>(c, c->src_cache, grads, c->off_src)) return s;
         if (aps_status s = upload_ptrs<float *>(c, c->dst_cache, out, c->off_dst)) return s;
@@ -551,8 +722,8 @@ static aps_status sim_check(aps_ctx *const *ctxs, int p)
         aps_ctx *c = ctxs[r];
         if (!c || !c->sim || c->world != p || c->rank != r) return APS_ERR_ARG;
         if (!c->ws) return fail(c, APS_ERR_STATE, "no workspace");
-        if (c->stream != ctxs[0]->stream || c->e != ctxs[0]->e || c->m != ctxs[0]->m ||
-            c->packed_bytes != ctxs[0]->packed_bytes || c->hw != ctxs[0]->hw)
+        if (c->stream != ctxs[0]->stream || c->le != ctxs[0]->le || c->lm != ctxs[0]->lm ||
+            c->packed_bytes != ctxs[0]->packed_bytes || c->hw_enabled != ctxs[0]->hw_enabled)
             return fail(c, APS_ERR_ARG, "simulated ranks differ in stream/format/layout");
     }
     return APS_OK;
@@ -581,8 +752,7 @@ aps_status aps_sim_allreduce(aps_ctx *const *ctxs, int p)
     for (int r = 0; r < p; ++r)
         if (ctxs[r]->phase != kPacked) return fail(ctxs[r], APS_ERR_STATE, "sim allreduce before quantize");
     aps_ctx *c0 = ctxs[0];
-    const size_t cb = (size_t)c0->chunk_bytes;
-    const int64_t chunk_tiles = c0->tiles / p;
+    const std::vector<int64_t> &cbyte = c0->chunk_byte;
     cudaStream_t st = c0->stream;
     for (int s = 0; s < p - 1; ++s) {
         // the "send/recv": rank r receives chunk recv_chunk(p, r, s) from rank r-1,
@@ -590,21 +760,19 @@ aps_status aps_sim_allreduce(aps_ctx *const *ctxs, int p)
         for (int r = 0; r < p; ++r) {
             aps_ctx *me = ctxs[r], *prev = ctxs[mod(r - 1, p)];
             const int rc = recv_chunk(p, r, s);
-            APS_CUDA(me, cudaMemcpyAsync(me->ws + me->off_recv, prev->t.packed + (size_t)rc * cb, cb,
-                                         cudaMemcpyDeviceToDevice, st));
+            APS_CUDA(me, cudaMemcpyAsync(me->ws + me->off_recv, prev->t.packed + cbyte[rc],
+                                         (size_t)(cbyte[rc + 1] - cbyte[rc]), cudaMemcpyDeviceToDevice, st));
         }
         for (int r = 0; r < p; ++r) {
             aps_ctx *me = ctxs[r];
-            const int rc = recv_chunk(p, r, s);
-            APS_CUDA(me, aps::launch_ring_reduce(me->t.packed + (size_t)rc * cb, me->ws + me->off_recv,
-                                                 chunk_tiles, me->e, me->m, me->hw, st));
+            if (aps_status sr = reduce_chunk(me, me, recv_chunk(p, r, s), me->ws + me->off_recv, st)) return sr;
         }
     }
     for (int r = 0; r < p; ++r)
         for (int q = 0; q < p; ++q)
             if (q != r)
-                APS_CUDA(ctxs[r], cudaMemcpyAsync(ctxs[r]->t.packed + (size_t)q * cb, ctxs[q]->t.packed + (size_t)q * cb,
-                                                  cb, cudaMemcpyDeviceToDevice, st));
+                APS_CUDA(ctxs[r], cudaMemcpyAsync(ctxs[r]->t.packed + cbyte[q], ctxs[q]->t.packed + cbyte[q],
+                                                  (size_t)(cbyte[q + 1] - cbyte[q]), cudaMemcpyDeviceToDevice, st));
     for (int r = 0; r < p; ++r) ctxs[r]->phase = kReduced;
     return APS_OK;
 }

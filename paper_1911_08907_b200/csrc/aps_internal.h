@@ -23,6 +23,8 @@ struct Item {
     int64_t tile_pos;     // first tile of the item in the packed buffer
     int32_t layer_items;  // work items of the layer
     int32_t pad;
+    int64_t byte_pos;     // byte offset of the item's first tile in the packed buffer
+                          // (tiles are 16 * b bytes, b = the layer's code width)
 };
 
 struct LayerDev {

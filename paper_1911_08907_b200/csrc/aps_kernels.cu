@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(NT) quant_pack_direct_kernel(DevTables t, C c,
     const int64_t begin = (int64_t)it.tile_begin * kTile;
     const int64_t n = min((int64_t)it.n_tiles * kTile, L.numel - begin);
     using W = typename Word4<B>::T;
-    W *out = reinterpret_cast<W *>(t.packed + (L.tile_off + it.tile_begin) * (16 * B));
+    W *out = reinterpret_cast<W *>(t.packed + it.byte_pos);
     const float *gb = g + begin;
     constexpr int kFull4 = kItemTiles * kTile / 4;
     constexpr int kPer = kFull4 / NT;
@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(NT) quant_pack_tile_kernel(DevTables t, C c, i
     const int64_t n = min((int64_t)it.n_tiles * kTile, L.numel - begin);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint32_t *codes = s_codes[warp];
-    uint32_t *out = reinterpret_cast<uint32_t *>(t.packed) + (L.tile_off + it.tile_begin) * (4 * b);
+    uint32_t *out = reinterpret_cast<uint32_t *>(t.packed + it.byte_pos);
     for (int tt = warp; tt < it.n_tiles; tt += NT / 32) {
         const int64_t e0 = (int64_t)tt * kTile + lane * 4;
         const float4 y = s.apply4(load_group(g + begin, e0, n));
@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(NT) unpack_unscale_direct_kernel(DevTables t, 
     const int64_t begin = (int64_t)it.tile_begin * kTile;
     const int64_t n = min((int64_t)it.n_tiles * kTile, L.numel - begin);
     using W = typename Word4<B>::T;
-    const W *in = reinterpret_cast<const W *>(t.packed + (L.tile_off + it.tile_begin) * (16 * B));
+    const W *in = reinterpret_cast<const W *>(t.packed + it.byte_pos);
     float *ob = o + begin;
     constexpr int kFull4 = kItemTiles * kTile / 4;
     constexpr int kPer = kFull4 / NT;
@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(NT) unpack_unscale_tile_kernel(DevTables t, C 
     const int64_t n = min((int64_t)it.n_tiles * kTile, L.numel - begin);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint32_t *words = s_words[warp];
-    const uint32_t *in = reinterpret_cast<const uint32_t *>(t.packed) + (L.tile_off + it.tile_begin) * (4 * b);
+    const uint32_t *in = reinterpret_cast<const uint32_t *>(t.packed + it.byte_pos);
     for (int tt = warp; tt < it.n_tiles; tt += NT / 32) {
         const uint32_t *iw = in + (int64_t)tt * (4 * b);
         for (int w = lane; w < 4 * b; w += 32) words[w] = iw[w];
@@ -437,7 +437,7 @@ __global__ void __launch_bounds__(NT, kFusedCtasPerSm)
     // unit u = tiles [sub * kFusedUnitTiles, ...) of item u / kSub
     struct Unit {
         int layer, cnt, n_tiles;
-        int64_t tile_pos;
+        int64_t tile_pos, byte_pos;
         const float *src;
         float *dst;
     };
@@ -451,6 +451,7 @@ __global__ void __launch_bounds__(NT, kFusedCtasPerSm)
         x.n_tiles = min(kFusedUnitTiles, it.n_tiles - t0);
         x.cnt = min(kFusedUnitTiles * kTile, it.cnt - t0 * kTile);
         x.tile_pos = it.tile_pos + t0;
+        x.byte_pos = it.byte_pos + (int64_t)t0 * 16 * c.b();
         x.src = p.src + (int64_t)t0 * kTile;
         x.dst = p.dst + (int64_t)t0 * kTile;
         return x;
@@ -547,7 +548,7 @@ __global__ void __launch_bounds__(NT, kFusedCtasPerSm)
         const Unscale us(ft, 1, avg);
         if constexpr (B == 8 || B == 16 || B == 32) {
             using W = typename Word4<B>::T;
-            W *out = reinterpret_cast<W *>(t.packed + ib.tile_pos * (16 * B));
+            W *out = reinterpret_cast<W *>(t.packed + ib.byte_pos);
             if (ib.cnt == kFusedUnitTiles * kTile && !s.wide) {
                 float4 v[kPer];
 #pragma unroll
@@ -578,7 +579,7 @@ __global__ void __launch_bounds__(NT, kFusedCtasPerSm)
         } else {
             const int b = c.b();
             uint32_t *codes = s_codes[warp];
-            uint32_t *outw = reinterpret_cast<uint32_t *>(t.packed) + ib.tile_pos * (4 * b);
+            uint32_t *outw = reinterpret_cast<uint32_t *>(t.packed + ib.byte_pos);
             for (int tt = warp; tt < ib.n_tiles; tt += NT / 32) {
                 const int64_t e0 = (int64_t)tt * kTile + lane * 4;
                 const float4 y = s.apply4(load_group(g, e0, ib.cnt));
@@ -872,7 +873,7 @@ __global__ void __launch_bounds__(NT, kWaveCtasPerSm)
             const Unscale us(ft, 1, avg);
             if constexpr (B == 8 || B == 16 || B == 32) {
                 using W = typename Word4<B>::T;
-                W *out = reinterpret_cast<W *>(t.packed + it.tile_pos * (16 * B));
+                W *out = reinterpret_cast<W *>(t.packed + it.byte_pos);
                 if (full && !s.wide) {
                     float4 *o4 = reinterpret_cast<float4 *>(p.dst);
 #pragma unroll
@@ -900,7 +901,7 @@ __global__ void __launch_bounds__(NT, kWaveCtasPerSm)
             } else {
                 const int b = c.b();
                 uint32_t *codes = s_codes[warp];
-                uint32_t *outw = reinterpret_cast<uint32_t *>(t.packed) + it.tile_pos * (4 * b);
+                uint32_t *outw = reinterpret_cast<uint32_t *>(t.packed + it.byte_pos);
                 for (int tt = warp; tt < it.n_tiles; tt += NT / 32) {
                     const int64_t e0 = (int64_t)tt * kTile + lane * 4;
                     const float4 y = s.apply4(load_group(p.src, e0, it.cnt));

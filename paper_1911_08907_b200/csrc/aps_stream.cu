@@ -63,6 +63,7 @@ struct StageInfo {
     const float *src;     // gradient at the item's first element
     float *dst;           // output at the item's first element
     int64_t tile_pos;     // first tile of the item in the packed buffer
+    int64_t byte_pos;     // its byte offset
     int32_t cnt;          // valid elements
     int32_t n_tiles;
     int32_t layer;
@@ -196,6 +197,7 @@ __device__ __forceinline__ StageInfo fetch_info(const DevTables &t, int k, bool 
     si.cnt = it.cnt;
     si.n_tiles = it.n_tiles;
     si.tile_pos = it.tile_pos;
+    si.byte_pos = it.byte_pos;
     si.first = it.tile_begin == 0;
     const int64_t begin = (int64_t)it.tile_begin * kTile;
     si.src = t.src[it.layer] + begin;
@@ -330,9 +332,9 @@ __device__ __forceinline__ void quant_chunk(const DevTables &t, const C &c, cons
     }
     fence_proxy_async_smem();
     __syncwarp();
-    const int64_t tile0 = si.tile_pos + warp * (kChunk / kTile);
     if (lane == 0)
-        bulk_s2g(t.packed + tile0 * (16 * B), codes + (size_t)warp * (kChunk / kTile) * (16 * B),
+        bulk_s2g(t.packed + si.byte_pos + (int64_t)warp * (kChunk / kTile) * (16 * B),
+                 codes + (size_t)warp * (kChunk / kTile) * (16 * B),
                  (uint32_t)(tiles_w * 16 * B));
     if (Fuse) store_chunk_f32(si.dst, s4, warp * kChunk, si.cnt, lane);
 }
@@ -455,7 +457,7 @@ struct UnpackOp {
     __device__ int late_ft(const StageInfo &si) const { return si.ft; }
     __device__ Load load(int, const StageInfo &si) const
     {
-        return Load{t.packed + si.tile_pos * (16 * C::kB), (uint32_t)(16 * C::kB * si.n_tiles), (uint32_t)kF32Bytes,
+        return Load{t.packed + si.byte_pos, (uint32_t)(16 * C::kB * si.n_tiles), (uint32_t)kF32Bytes,
                     false};
     }
     __device__ void consume(int, uint8_t *stage, const StageInfo &si, uint32_t *, int warp, int lane) const

@@ -73,6 +73,15 @@ CONFIGS = {
 }
 
 
+def resnet50_hybrid_formats(low=(5, 2), last=(8, 23)) -> list[tuple[int, int]]:
+    """Per-tensor formats of the paper's hybrid precision on ResNet-50 (P:545,
+    Table last_layer_precision): the last (classification) layer --
+    the fc weight and bias, the final two tensors -- in `last` (FP32 = (8, 23)),
+    every other tensor in `low`."""
+    n = len(RESNET50_NUMELS)
+    return [tuple(low)] * (n - 2) + [tuple(last)] * 2
+
+
 def layer_spread(l: int, seed: int = SEED) -> int:
     return int(np.random.default_rng([seed, 999, l]).integers(-24, -3))
 

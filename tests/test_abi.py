@@ -57,6 +57,22 @@ def test_layout_matches_oracle(aps, orc):
                 assert nb == orc.packed_bytes(p, e, m, numels)
 
 
+def test_layout_mixed_matches_oracle(aps, orc):
+    """Per-layer formats (aps_layout_mixed) against the oracle's mixed layout;
+    uniform formats reduce to aps_layout."""
+    rng = np.random.default_rng(5)
+    fmts_all = [(5, 2), (3, 0), (4, 3), (5, 6), (5, 10), (8, 23), (2, 1)]
+    for numels in (synthetic.C1_NUMELS, synthetic.RESNET50_NUMELS, [1], [127, 129, 1, 5000]):
+        for p in (1, 2, 3, 4, 8):
+            fmts = [fmts_all[i] for i in rng.integers(0, len(fmts_all), len(numels))]
+            assert aps.layout_mixed(p, numels, fmts) == (orc.total_tiles(p, numels),
+                                                        orc.packed_bytes_mixed(p, numels, fmts))
+            assert aps.layout_mixed(p, numels, [(4, 3)] * len(numels)) == aps.layout(p, 4, 3, numels)
+    hyb = synthetic.resnet50_hybrid_formats()
+    assert aps.layout_mixed(8, synthetic.RESNET50_NUMELS, hyb) == (
+        orc.total_tiles(8, synthetic.RESNET50_NUMELS), orc.packed_bytes_mixed(8, synthetic.RESNET50_NUMELS, hyb))
+
+
 def test_ring_schedule_is_a_ring(aps):
     """At every step rank r receives exactly the chunk rank r-1 sends; after
     p-1 steps rank r holds chunk r, accumulated in order c+1, ..., c (A14)."""
