@@ -43,6 +43,9 @@ def parse():
     ap.add_argument("--format", default="5,2")
     ap.add_argument("--config", default="c2", choices=["c2", "c3", "res5c"])
     ap.add_argument("--no-hw", action="store_true", help="generic bit-arithmetic codec instead of cvt")
+    ap.add_argument("--hybrid", action="store_true",
+                    help="hybrid precision (P:545): last layer (final two tensors) in FP32 (8,23), the rest --format")
+    ap.add_argument("--hybrid-last", default="8,23", help="format of the last layer under --hybrid")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--phase-steps", type=int, default=0, help="steps of the per-phase breakdown (0: max(20, K/4))")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -247,8 +250,11 @@ def main():
     grads = [torch.from_numpy(a).to(dev) for a in host]
     outs = [torch.empty_like(g) for g in grads]
     stream = torch.cuda.current_stream(dev)
+    last = tuple(map(int, args.hybrid_last.split(",")))
+    fmts = [(e, m)] * (len(numels) - 2) + [last] * 2 if args.hybrid else None
+    code_bytes = sum(n * (1 + f[0] + f[1]) for n, f in zip(numels, fmts)) / 8 if fmts else L * b / 8
     ctx = aps.ApsContext(e, m, numels, world_size=world, rank=rank, nccl_comm=comm, stream=stream,
-                         device=dev, hw_convert=not args.no_hw)
+                         device=dev, hw_convert=not args.no_hw, formats=fmts)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     flush_rd = torch.zeros(256 << 20, dtype=torch.uint8, device=dev)
 
@@ -338,17 +344,18 @@ def main():
     rr_ms = rr[0].elapsed_time(rr[1]) / 50
 
     # -------- roofline of the dominant kernel (algorithmic bytes / launch time)
-    T, packed_bytes = aps.layout(world, e, m, numels)
+    T, packed_bytes = aps.layout_mixed(world, numels, fmts) if fmts else aps.layout(world, e, m, numels)
     kern = {
         "absmax_exp": (statistics.mean(phase_ms[0]), 4 * L),
-        "quant_pack": (statistics.mean(phase_ms[1]), 4 * L + L * b / 8),
-        "unpack_unscale": (statistics.mean(phase_ms[3]), L * b / 8 + 4 * L),
+        "quant_pack": (statistics.mean(phase_ms[1]), 4 * L + code_bytes),
+        "unpack_unscale": (statistics.mean(phase_ms[3]), code_bytes + 4 * L),
     }
     if world > 1:
         kern["ring_allreduce"] = (statistics.mean(phase_ms[2]), 2 * (world - 1) / world * packed_bytes)
     peak, peak_kind = peaks()
     # the committed ncu capture is of the default workload (config 2, 1/5/2) only
-    traffic = ncu_traffic() if (args.config == "c2" and (e, m) == (5, 2) and not args.no_hw) else {}
+    traffic = ncu_traffic() if (args.config == "c2" and (e, m) == (5, 2) and not args.no_hw
+                                and not fmts) else {}
     phases = {}
     for k, (ms, byts) in kern.items():
         gbs = byts / (ms * 1e-3) / 1e9
@@ -365,7 +372,7 @@ def main():
         kname = ("stream_kernel<FusedP1Op>" if os.environ.get("APS_ENGINE") in ("tma", "stream")
                  else "fused_p1_ldg_kernel" if os.environ.get("APS_FUSED_SCHEDULE") == "barrier"
                  else "fused_p1_wave_kernel")
-        dom, dms, dbytes = f"fused_p1 ({kname})", ms_per_step, (12 + b / 8) * L
+        dom, dms, dbytes = f"fused_p1 ({kname})", ms_per_step, 12 * L + code_bytes
         phases["fused_p1"] = {"us": round(ms_per_step * 1e3, 2), "algorithmic_bytes": int(dbytes)}
     else:
         dom = max(kern, key=lambda k: kern[k][0])
@@ -409,14 +416,18 @@ def main():
            "h2d_bytes_per_step": 4 * L, "d2h_bytes_per_step": 4 * L, "ms_per_step": round(e2e_ms, 4),
            "api": "aps_sync_host"}
 
-    launches_per_step = 1 if world == 1 else 3 + (world - 1)
+    G = len(set(fmts)) if fmts else 1  # one quantise / unscale / fused launch per format group
+    if world == 1:
+        launches_per_step = G
+    else:  # absmax + G quantise + per ring step one reduce launch per format run of the chunk + G unscale
+        launches_per_step = 1 + 2 * G + sum(format_runs(numels, fmts or [(e, m)] * len(numels), world, rank))
     result = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": max(args.warmup, 3), "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "wire_dtype": f"{b}-bit 1/{e}/{m} codes",
+        "wire_dtype": (f"{b}-bit 1/{e}/{m} codes, last layer 1/{last[0]}/{last[1]}" if fmts else f"{b}-bit 1/{e}/{m} codes"),
         "data": "synthetic (seeded normal per layer, binade spread 2^-24..2^-4, 0.5% zeros)",
-        "config": {"workload": name, "format": f"1/{e}/{m}", "n_layers": len(numels), "elements": L,
+        "config": {"workload": name, "format": f"1/{e}/{m}" + (f" + last layer 1/{last[0]}/{last[1]} (hybrid)" if fmts else ""), "n_layers": len(numels), "elements": L,
                    "ranks": world, "hw_convert": ctx_hw(ctx, args), "engine": os.environ.get("APS_ENGINE", "ldg"), "l2": "flushed (256 MiB write + 256 MiB read) between timed steps"
                    if not args.no_flush else "not flushed", "parallelism": f"dp{world}",
                    "packed_bytes": packed_bytes},
@@ -438,8 +449,25 @@ def main():
         dist.destroy_process_group()
 
 
+def format_runs(numels, fmts, p, rank):
+    """Per reduce-scatter step of `rank`: the number of format runs in the chunk
+    it receives (one reduce launch each; padding tiles take the last format)."""
+    tile_fmt = []
+    for n, f in zip(numels, fmts):
+        tile_fmt += [f] * ((n + 127) // 128)
+    Tp = (len(tile_fmt) + p - 1) // p * p
+    tile_fmt += [fmts[-1]] * (Tp - len(tile_fmt))
+    ct = Tp // p
+    out = []
+    for s in range(p - 1):
+        rc = (rank - 2 - s) % p
+        seg = tile_fmt[rc * ct:(rc + 1) * ct]
+        out.append(1 + sum(1 for a, b in zip(seg, seg[1:]) if a != b))
+    return out
+
+
 def ctx_hw(ctx, args):
-    return (not args.no_hw) and (ctx.exp_bits, ctx.man_bits) in ((5, 2), (4, 3))
+    return (not args.no_hw) and (ctx.exp_bits, ctx.man_bits) in ((5, 2), (4, 3), (5, 10), (8, 7), (8, 23))
 
 
 if __name__ == "__main__":

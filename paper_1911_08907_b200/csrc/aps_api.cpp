@@ -51,6 +51,7 @@ struct aps_ctx {
         int e, m;
         bool hw;
         int item_begin, item_count, max_layer_items;
+        uint32_t wave_claim_base;  // this group's wavefront claim counter at its next launch
     };
     std::vector<Group> groups;
     struct Seg {
@@ -67,7 +68,6 @@ struct aps_ctx {
     size_t off_packed = 0, off_recv = 0, off_items = 0, off_layers = 0, off_src = 0, off_dst = 0,
            off_amax = 0, off_count = 0, off_eloc = 0, off_eglob = 0, off_ft = 0, off_flag = 0, off_amax2 = 0, off_done = 0, off_iptr = 0, off_tl = 0, off_claim = 0, off_ldone = 0;
     uint32_t wave_calls = 0;    // wavefront launches so far (per-layer counter targets)
-    uint32_t wave_claim_base = 0;
     int max_layer_items = 0;
     uint32_t claim_base = 0;   // value of the fused kernel's claim counters at the next launch
     bool iptr_valid = false;
@@ -81,7 +81,18 @@ struct aps_ctx {
     bool stream_engine = false;
     uint32_t gen = 0;           // abs-max-pass launches so far (selects the accumulator parity)
     uint32_t done_target = 0;   // value the CTA-done counter reaches at the end of the current pass
+    // format groups after the first run on side streams, concurrently with group 0
+    // (disjoint layers, packed bytes and counters): fork/join through events
+    std::vector<cudaStream_t> side;
+    std::vector<cudaEvent_t> ev_join;
+    cudaEvent_t ev_fork = nullptr;
     std::string err;
+    ~aps_ctx()
+    {
+        for (cudaStream_t s : side) cudaStreamDestroy(s);
+        for (cudaEvent_t e : ev_join) cudaEventDestroy(e);
+        if (ev_fork) cudaEventDestroy(ev_fork);
+    }
 };
 
 namespace {
@@ -264,13 +275,14 @@ static aps_status init_common(aps_ctx **out, const int *e_arr, const int *m_arr,
         int g = 0;
         while (g < (int)c->groups.size() && (c->groups[g].e != c->le[l] || c->groups[g].m != c->lm[l])) ++g;
         if (g == (int)c->groups.size())
-            c->groups.push_back({c->le[l], c->lm[l], c->hw_enabled && aps::hw_available(c->le[l], c->lm[l]), 0, 0, 0});
+            c->groups.push_back({c->le[l], c->lm[l], c->hw_enabled && aps::hw_available(c->le[l], c->lm[l]), 0, 0, 0, 0});
         layer_group[l] = g;
     }
     std::stable_sort(c->items.begin(), c->items.end(), [&](const aps::Item &a, const aps::Item &b) {
         return layer_group[a.layer] < layer_group[b.layer];
     });
     for (size_t k = 0; k < c->items.size(); ++k) {
+        c->items[k].fmt = layer_group[c->items[k].layer];
         aps_ctx::Group &g = c->groups[layer_group[c->items[k].layer]];
         if (g.item_count == 0) g.item_begin = (int)k;
         ++g.item_count;
@@ -333,7 +345,7 @@ static aps_status init_common(aps_ctx **out, const int *e_arr, const int *m_arr,
     c->off_done = o;   o = align_up(o + 4);
     c->off_iptr = o;   o = align_up(o + sizeof(aps::ItemPtr) * c->items.size());
     c->off_tl = o;     o = align_up(o + sizeof(uint64_t) * aps::kTimelineSlots);
-    c->off_claim = o;  o = align_up(o + 3 * sizeof(uint32_t));
+    c->off_claim = o;  o = align_up(o + 3 * sizeof(uint32_t) * c->groups.size());  // 3 per format group
     c->off_ldone = o;  o = align_up(o + 4 * (size_t)n_layers);
 
     for (const auto &L : c->layers) c->max_layer_items = std::max(c->max_layer_items, (int)L.n_items);
@@ -411,7 +423,16 @@ aps_status aps_set_workspace(aps_ctx *c, void *dev, size_t bytes)
     t.layer_done = reinterpret_cast<uint32_t *>(c->ws + c->off_ldone);
 
     c->wave_calls = 0;
-    c->wave_claim_base = 0;
+    for (auto &g : c->groups) g.wave_claim_base = 0;
+    if (c->groups.size() > 1 && c->side.empty()) {
+        c->side.resize(c->groups.size() - 1);
+        c->ev_join.resize(c->groups.size() - 1);
+        for (size_t i = 0; i < c->side.size(); ++i) {
+            APS_CUDA(c, cudaStreamCreateWithFlags(&c->side[i], cudaStreamNonBlocking));
+            APS_CUDA(c, cudaEventCreateWithFlags(&c->ev_join[i], cudaEventDisableTiming));
+        }
+        APS_CUDA(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+    }
     c->claim_base = 0;
     c->iptr_valid = false;
     c->gen = 0;
@@ -432,8 +453,40 @@ static aps::DevTables group_tables(const aps_ctx *c, const aps_ctx::Group &g)
     t.items += g.item_begin;
     t.iptr += g.item_begin;
     t.n_items = g.item_count;
+    t.claim += 3 * (&g - c->groups.data());
     return t;
 }
+
+// Launch `launch(group, tables, stream)` for every format group: group 0 on the
+// context's stream, the others forked onto side streams and joined back (they
+// touch disjoint layers, packed bytes and claim counters), so a small group (the
+// FP32 classifier of the hybrid format) runs in the tail of the big one instead of
+// after it.  The TMA engine's kernels share the CTA-done counter: serialised.
+extern "C++" {
+template <class F>
+static aps_status for_groups(aps_ctx *c, F launch)
+{
+    static const bool serial_env = [] {
+        const char *v = std::getenv("APS_GROUP_STREAMS");
+        return v && std::atoi(v) == 0;
+    }();
+    const bool concurrent = c->groups.size() > 1 && !c->side.empty() && !c->stream_engine && !serial_env;
+    if (concurrent) {
+        APS_CUDA(c, cudaEventRecord(c->ev_fork, c->stream));
+        for (cudaStream_t s : c->side) APS_CUDA(c, cudaStreamWaitEvent(s, c->ev_fork, 0));
+    }
+    for (size_t g = 0; g < c->groups.size(); ++g) {
+        cudaStream_t s = (concurrent && g > 0) ? c->side[g - 1] : c->stream;
+        APS_CUDA(c, launch(c->groups[g], group_tables(c, c->groups[g]), s, !concurrent));
+    }
+    if (concurrent)
+        for (size_t i = 0; i < c->side.size(); ++i) {
+            APS_CUDA(c, cudaEventRecord(c->ev_join[i], c->side[i]));
+            APS_CUDA(c, cudaStreamWaitEvent(c->stream, c->ev_join[i], 0));
+        }
+    return APS_OK;
+}
+}  // extern "C++"
 
 // reduce the received copy of chunk ch into this rank's own copy, one launch per
 // format segment of the chunk (a segment is a run of tiles of one format)
@@ -495,13 +548,13 @@ aps_status aps_quantize_pack(aps_ctx *c, const float *const *grads)
     if (c->phase < kScales) return fail(c, APS_ERR_STATE, "aps_quantize_pack before aps_layer_scales");
     if (!grads) return fail(c, APS_ERR_ARG, "grads is NULL");
     if (aps_status s = upload_ptrs<const float *>(c, c->src_cache, grads, c->off_src)) return s;
-    for (const auto &g : c->groups) {  // one launch per format group (NEXT-2)
-        const aps::DevTables t = group_tables(c, g);
-        cudaError_t e = c->stream_engine ? aps::launch_stream_quant(t, g.e, g.m, g.hw, c->stream)
-                                         : cudaErrorNotSupported;
-        if (e == cudaErrorNotSupported) e = aps::launch_quant_pack(t, g.e, g.m, g.hw, c->stream);
-        APS_CUDA(c, e);
-    }
+    // one launch per format group (NEXT-2)
+    if (aps_status s = for_groups(c, [&](const aps_ctx::Group &g, const aps::DevTables &t, cudaStream_t st, bool) {
+            cudaError_t e = c->stream_engine ? aps::launch_stream_quant(t, g.e, g.m, g.hw, st) : cudaErrorNotSupported;
+            if (e == cudaErrorNotSupported) e = aps::launch_quant_pack(t, g.e, g.m, g.hw, st);
+            return e;
+        }))
+        return s;
     c->phase = kPacked;
     return APS_OK;
 }
@@ -557,15 +610,13 @@ aps_status aps_unscale(aps_ctx *c, float *const *out, int average)
         return fail(c, APS_ERR_STATE, "aps_unscale before aps_allreduce");
     if (!out) return fail(c, APS_ERR_ARG, "out is NULL");
     if (aps_status s = upload_ptrs<float *>(c, c->dst_cache, out, c->off_dst)) return s;
-    for (const auto &g : c->groups) {
-        const aps::DevTables t = group_tables(c, g);
-        cudaError_t e = c->stream_engine
-                            ? aps::launch_stream_unpack(t, g.e, g.m, g.hw, c->world, average, c->stream)
-                            : cudaErrorNotSupported;
-        if (e == cudaErrorNotSupported)
-            e = aps::launch_unpack_unscale(t, g.e, g.m, g.hw, c->world, average, c->stream);
-        APS_CUDA(c, e);
-    }
+    if (aps_status s = for_groups(c, [&](const aps_ctx::Group &g, const aps::DevTables &t, cudaStream_t st, bool) {
+            cudaError_t e = c->stream_engine ? aps::launch_stream_unpack(t, g.e, g.m, g.hw, c->world, average, st)
+                                             : cudaErrorNotSupported;
+            if (e == cudaErrorNotSupported) e = aps::launch_unpack_unscale(t, g.e, g.m, g.hw, c->world, average, st);
+            return e;
+        }))
+        return s;
     return APS_OK;
 }
 
@@ -585,15 +636,45 @@ aps_status aps_sync_out(aps_ctx *c, const float *const *grads, float *const *out
         if (!c->uniform || !sched || std::strcmp(sched, "barrier") != 0) {
             // wavefront: quantise items trail their abs-max items by D positions;
             // one launch per format group (a layer's items never straddle groups)
-            for (const auto &g : c->groups) {
-                const aps::DevTables t = group_tables(c, g);
-                const int wgrid = aps::fused_p1_wave_grid(g.e, g.m, g.hw, t.n_items);
-                const int lag = std::min(t.n_items, g.max_layer_items + wgrid);
-                APS_CUDA(c, aps::launch_fused_p1_wave(t, g.e, g.m, g.hw, average, c->gen, c->wave_claim_base,
-                                                      c->wave_calls, lag, wgrid, c->stream));
-                // every position is claimed once and every CTA overshoots kWaveOvershoot times
-                c->wave_claim_base += (uint32_t)(2 * t.n_items + aps::kWaveOvershoot * wgrid);
+            // the paper's hybrid precision (one low format + the FP32 classifier layer):
+            // ONE launch, binary32 items switch codec inside the kernel
+            static const bool hybrid_fuse = [] {
+                const char *v = std::getenv("APS_HYBRID_FUSE");
+                return !v || std::atoi(v) != 0;
+            }();
+            int fp32_group = -1;
+            if (c->groups.size() == 2 && hybrid_fuse)
+                for (int g = 0; g < 2; ++g)
+                    if (c->groups[g].e == 8 && c->groups[g].m == 23 && c->groups[g].hw &&
+                        !(c->groups[1 - g].e == 8 && c->groups[1 - g].m == 23))
+                        fp32_group = g;
+            if (fp32_group >= 0) {
+                const aps_ctx::Group &lo = c->groups[1 - fp32_group];
+                aps_ctx::Group &g0 = c->groups[0];  // its claim counter serves the single launch
+                const int wgrid = aps::fused_p1_wave_grid(lo.e, lo.m, lo.hw, c->t.n_items);
+                const int lag = std::min(c->t.n_items, c->max_layer_items + wgrid);
+                APS_CUDA(c, aps::launch_fused_p1_wave_hybrid32(c->t, lo.e, lo.m, lo.hw, fp32_group, average, c->gen,
+                                                               g0.wave_claim_base, c->wave_calls, lag, wgrid,
+                                                               c->stream));
+                g0.wave_claim_base += (uint32_t)(2 * c->t.n_items + aps::kWaveOvershoot * wgrid);
+                ++c->wave_calls;
+                ++c->gen;
+                c->phase = kReduced;
+                return APS_OK;
             }
+            // one launch per format group, each with its own claim counter
+            if (aps_status s = for_groups(c, [&](const aps_ctx::Group &gc, const aps::DevTables &t, cudaStream_t st,
+                                                 bool coop) {
+                    aps_ctx::Group &g = const_cast<aps_ctx::Group &>(gc);
+                    const int wgrid = aps::fused_p1_wave_grid(g.e, g.m, g.hw, t.n_items);
+                    const int lag = std::min(t.n_items, g.max_layer_items + wgrid);
+                    cudaError_t e = aps::launch_fused_p1_wave(t, g.e, g.m, g.hw, average, c->gen, g.wave_claim_base,
+                                                              c->wave_calls, lag, wgrid, st, coop);
+                    // every position is claimed once and every CTA overshoots kWaveOvershoot times
+                    if (e == cudaSuccess) g.wave_claim_base += (uint32_t)(2 * t.n_items + aps::kWaveOvershoot * wgrid);
+                    return e;
+                }))
+                return s;
             ++c->wave_calls;
             ++c->gen;
             c->phase = kReduced;

@@ -64,6 +64,48 @@ struct CHw {
     }
 };
 
+// IEEE binary16 = (5,10) and bfloat16 = (8,7) through the hardware converters
+// (cvt.rn.f16x2.f32 / cvt.rn.bf16x2.f32: RNE, gradual underflow, IEEE overflow
+// -- the same Cast on every non-NaN fp32, reading A12), and binary32 = (8,23),
+// where Cast is the identity on every non-NaN fp32.
+template <bool BF16>
+struct CHw16 {
+    static constexpr int kB = 16;
+    static constexpr bool kVec4 = true;
+    __device__ __forceinline__ int b() const { return 16; }
+    __device__ __forceinline__ static uint32_t cvt2(float lo, float hi)
+    {
+        uint32_t d;
+        if constexpr (BF16) asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+        else asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+        return d;
+    }
+    __device__ __forceinline__ static float2 uncvt2(uint32_t w)
+    {
+        if constexpr (BF16) return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
+        __half2 h = *reinterpret_cast<__half2 *>(&w);
+        return __half22float2(h);
+    }
+    __device__ __forceinline__ uint32_t enc(float y) const { return cvt2(y, 0.f) & 0xffffu; }
+    __device__ __forceinline__ float dec(uint32_t c) const { return uncvt2(c & 0xffffu).x; }
+    __device__ __forceinline__ float dec_any(uint32_t c) const { return dec(c); }
+    __device__ __forceinline__ uint2 enc4(float4 v) const { return make_uint2(cvt2(v.x, v.y), cvt2(v.z, v.w)); }
+    __device__ __forceinline__ float4 dec4(uint2 w) const
+    {
+        const float2 a = uncvt2(w.x), c = uncvt2(w.y);
+        return make_float4(a.x, a.y, c.x, c.y);
+    }
+};
+
+struct CF32 {
+    static constexpr int kB = 32;
+    static constexpr bool kVec4 = false;
+    __device__ __forceinline__ int b() const { return 32; }
+    __device__ __forceinline__ uint32_t enc(float y) const { return __float_as_uint(y); }
+    __device__ __forceinline__ float dec(uint32_t c) const { return __uint_as_float(c); }
+    __device__ __forceinline__ float dec_any(uint32_t c) const { return __uint_as_float(c); }
+};
+
 struct CRt {
     static constexpr int kB = 0;  // runtime width
     static constexpr bool kVec4 = false;
@@ -166,7 +208,8 @@ __device__ __forceinline__ typename Word4<B>::T pack4(const C &c, float4 v)
     if constexpr (B == 8) {
         return enc4_bytes(c, v);
     } else if constexpr (B == 16) {
-        return make_uint2(c.enc(v.x) | (c.enc(v.y) << 16), c.enc(v.z) | (c.enc(v.w) << 16));
+        if constexpr (C::kB == 16 && C::kVec4) return c.enc4(v);
+        else return make_uint2(c.enc(v.x) | (c.enc(v.y) << 16), c.enc(v.z) | (c.enc(v.w) << 16));
     } else {
         return make_uint4(c.enc(v.x), c.enc(v.y), c.enc(v.z), c.enc(v.w));
     }
@@ -178,8 +221,9 @@ __device__ __forceinline__ float4 unpack4(const C &c, typename Word4<B>::T w)
     if constexpr (B == 8) {
         return dec4_bytes(c, w);
     } else if constexpr (B == 16) {
-        return make_float4(c.dec(w.x & 0xffffu), c.dec(w.x >> 16), c.dec(w.y & 0xffffu),
-                           c.dec(w.y >> 16));
+        if constexpr (C::kB == 16 && C::kVec4) return c.dec4(w);
+        else return make_float4(c.dec(w.x & 0xffffu), c.dec(w.x >> 16), c.dec(w.y & 0xffffu),
+                                c.dec(w.y >> 16));
     } else {
         return make_float4(c.dec(w.x), c.dec(w.y), c.dec(w.z), c.dec(w.w));
     }
@@ -307,6 +351,9 @@ cudaError_t with_codec(int e, int m, bool hw, F &&f)
 {
     if (hw && e == 5 && m == 2) return f(CHw<false>{});
     if (hw && e == 4 && m == 3) return f(CHw<true>{});
+    if (hw && e == 5 && m == 10) return f(CHw16<false>{});
+    if (hw && e == 8 && m == 7) return f(CHw16<true>{});
+    if (hw && e == 8 && m == 23) return f(CF32{});
     if (e == 5 && m == 2) return f(CGen<5, 2>{});
     if (e == 4 && m == 3) return f(CGen<4, 3>{});
     if (e == 3 && m == 0) return f(CGen<3, 0>{});

@@ -22,7 +22,7 @@ struct Item {
     int32_t cnt;          // valid elements: min(n_tiles * 128, numel - tile_begin * 128)
     int64_t tile_pos;     // first tile of the item in the packed buffer
     int32_t layer_items;  // work items of the layer
-    int32_t pad;
+    int32_t fmt;          // format group of the layer (per-layer formats; 0 when uniform)
     int64_t byte_pos;     // byte offset of the item's first tile in the packed buffer
                           // (tiles are 16 * b bytes, b = the layer's code width)
 };
@@ -117,13 +117,25 @@ int fused_p1_wave_grid(int e, int m, bool hw, int n_items);
 constexpr int kWaveOvershoot = 2;  // claims past the end per CTA and call (wavefront kernel claims 2 ahead)
 // claim_base advances by 2 * n_items + kWaveOvershoot * grid per call.
 cudaError_t launch_fused_p1_wave(const DevTables &t, int e, int m, bool hw, int average, uint32_t gen,
-                                 uint32_t claim_base, uint32_t call_no, int lag, int grid, cudaStream_t s);
+                                 uint32_t claim_base, uint32_t call_no, int lag, int grid, cudaStream_t s,
+                                 bool cooperative = true);
+// One wavefront launch over two format groups: items whose fmt == fmt2 use the
+// binary32 codec (the hybrid FP32 classifier layer), the others (e, m, hw).
+cudaError_t launch_fused_p1_wave_hybrid32(const DevTables &t, int e, int m, bool hw, int fmt2, int average,
+                                          uint32_t gen, uint32_t claim_base, uint32_t call_no, int lag, int grid,
+                                          cudaStream_t s);
 // claim_base: value of both claim counters at launch (each call advances
 // them by n_items + grid: every CTA's last claim overshoots once).
 cudaError_t launch_fused_p1_ldg(const DevTables &t, int e, int m, bool hw, int average, uint32_t gen,
                                 uint32_t target, uint32_t claim_base, int grid, cudaStream_t s);
 
 // true when (e,m) has a hardware converter that is exact on the APS path
-inline bool hw_available(int e, int m) { return (e == 5 && m == 2) || (e == 4 && m == 3); }
+// formats with a hardware / exact fast codec: fp8 e5m2, e4m3 (APS regime only,
+// reading A12), binary16, bfloat16, binary32 (every non-NaN input)
+inline bool hw_available(int e, int m)
+{
+    return (e == 5 && m == 2) || (e == 4 && m == 3) || (e == 5 && m == 10) || (e == 8 && m == 7) ||
+           (e == 8 && m == 23);
+}
 
 }  // namespace aps

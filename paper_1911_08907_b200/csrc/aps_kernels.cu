@@ -9,6 +9,7 @@
 // coalesced loads (ld.global.nc.L1::no_allocate) and coalesced stores;
 // b = 8/16/32 pack directly from registers, other widths go through a
 // per-warp shared-memory tile.
+#include <type_traits>
 #include <cstdint>
 #include <climits>
 #include <algorithm>
@@ -731,11 +732,17 @@ cudaError_t launch_ring_reduce(uint8_t *own, const uint8_t *recv, int64_t n_tile
 // still in L2.  Progress: a waiting B depends only on A items at earlier
 // positions, and each CTA holds at most its current and next claim, so the
 // earliest waiting B always completes (induction on position).
-template <class C, int NT>
+// No second codec (uniform formats, or one launch per format group).
+struct CNone {
+    static constexpr int kB = -1;
+};
+
+template <class C, class C2, int NT>
 __global__ void __launch_bounds__(NT, kWaveCtasPerSm)
-    fused_p1_wave_kernel(DevTables t, C c, uint32_t *amax, uint32_t *amax_next, uint32_t claim_base, uint32_t call_no,
-                         int lag, int bias, int avg, int flags)
+    fused_p1_wave_kernel(DevTables t, C c, C2 c2, uint32_t *amax, uint32_t *amax_next, uint32_t claim_base,
+                         uint32_t call_no, int lag, int bias, int bias2, int fmt2, int avg, int flags)
 {
+    constexpr bool kTwo = C2::kB > 0;  // items with fmt == fmt2 use c2 (bias2)
     __shared__ __align__(16) uint32_t s_codes[NT / 32][kTile];
     __shared__ int s_claim[3], s_ft[3], s_ok[3];  // claims run two items ahead (3 slots)
     __shared__ uint32_t s_part[2][NT / 32];       // per-warp maxima of the last two items
@@ -757,7 +764,6 @@ __global__ void __launch_bounds__(NT, kWaveCtasPerSm)
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(strm));
     constexpr int kPer = kItemTiles * kTile / 4 / NT;
-    constexpr int B = C::kB;
     constexpr int kFlushThread = 32;  // lane 0 of warp 1 folds finished abs-max items into the layer
     auto decode = [&](int j, bool &isB) -> int {
         if (j < D) { isB = false; return j; }
@@ -769,9 +775,10 @@ __global__ void __launch_bounds__(NT, kWaveCtasPerSm)
         isB = true;
         return n - D + (j - (total - D));
     };
-    auto ft_of = [&](int l) -> int {
-        const int32_t E = exponent_of(ld_relaxed_u32(&amax[l]), 1);
-        return (E == INT32_MIN || E == INT32_MAX) ? 0 : bias - E;  // f~ (Alg. 1 line 4)
+    auto ft_of = [&](const Item &it) -> int {
+        const int32_t E = exponent_of(ld_relaxed_u32(&amax[it.layer]), 1);
+        const int bs = (kTwo && it.fmt == fmt2) ? bias2 : bias;  // the layer's upper_bound_exp
+        return (E == INT32_MIN || E == INT32_MAX) ? 0 : bs - E;  // f~ (Alg. 1 line 4)
     };
     auto layer_target = [&](const Item &it) -> uint32_t { return (call_no + 1u) * (uint32_t)(8 * it.layer_items); };
     // thread 0: claim a position into slot sl; resolve f~ now if it is a quantise item of a complete layer
@@ -785,7 +792,7 @@ __global__ void __launch_bounds__(NT, kWaveCtasPerSm)
             if (isB) {
                 const Item it = t.items[k];
                 if ((int)(ld_acquire_u32(&t.layer_done[it.layer]) - layer_target(it)) >= 0) {
-                    s_ft[sl] = ft_of(it.layer);
+                    s_ft[sl] = ft_of(it);
                     s_ok[sl] = 1;
                 }
             }
@@ -857,7 +864,7 @@ __global__ void __launch_bounds__(NT, kWaveCtasPerSm)
                 if (threadIdx.x == 0) {
                     spin_until([&] { return (int)(ld_acquire_u32(&t.layer_done[it.layer]) - layer_target(it)) >= 0; },
                                t.flag);
-                    s_ft[slot] = ft_of(it.layer);
+                    s_ft[slot] = ft_of(it);
                 }
                 __syncthreads();
             }
@@ -871,49 +878,59 @@ __global__ void __launch_bounds__(NT, kWaveCtasPerSm)
             }
             const Pow2 s(ft);
             const Unscale us(ft, 1, avg);
-            if constexpr (B == 8 || B == 16 || B == 32) {
-                using W = typename Word4<B>::T;
-                W *out = reinterpret_cast<W *>(t.packed + it.byte_pos);
-                if (full && !s.wide) {
-                    float4 *o4 = reinterpret_cast<float4 *>(p.dst);
+            auto quantise = [&](const auto &cc) {
+                using CC = std::decay_t<decltype(cc)>;
+                constexpr int B = CC::kB;
+                if constexpr (B == 8 || B == 16 || B == 32) {
+                    using W = typename Word4<B>::T;
+                    W *out = reinterpret_cast<W *>(t.packed + it.byte_pos);
+                    if (full && !s.wide) {
+                        float4 *o4 = reinterpret_cast<float4 *>(p.dst);
 #pragma unroll
-                    for (int q = 0; q < kPer; ++q) {
-                        const float4 y = make_float4(__fmul_rn(v[q].x, s.f), __fmul_rn(v[q].y, s.f),
-                                                     __fmul_rn(v[q].z, s.f), __fmul_rn(v[q].w, s.f));
-                        const W code = pack4<B>(c, y);
-                        const float4 r = us.apply4(unpack4<B>(c, code));
-                        if (f_st_hint) {
-                            st_hint(out + threadIdx.x + q * NT, code, strm);
-                            st_hint4(o4 + threadIdx.x + q * NT, r, strm);
-                        } else {
-                            out[threadIdx.x + q * NT] = code;
-                            o4[threadIdx.x + q * NT] = r;
+                        for (int q = 0; q < kPer; ++q) {
+                            const float4 y = make_float4(__fmul_rn(v[q].x, s.f), __fmul_rn(v[q].y, s.f),
+                                                         __fmul_rn(v[q].z, s.f), __fmul_rn(v[q].w, s.f));
+                            const W code = pack4<B>(cc, y);
+                            const float4 r = us.apply4(unpack4<B>(cc, code));
+                            if (f_st_hint) {
+                                st_hint(out + threadIdx.x + q * NT, code, strm);
+                                st_hint4(o4 + threadIdx.x + q * NT, r, strm);
+                            } else {
+                                out[threadIdx.x + q * NT] = code;
+                                o4[threadIdx.x + q * NT] = r;
+                            }
+                        }
+                    } else {
+                        const int ng = it.n_tiles * (kTile / 4);
+                        for (int q = threadIdx.x; q < ng; q += NT) {
+                            const W code = pack4<B>(cc, s.apply4(load_group(p.src, 4 * (int64_t)q, it.cnt)));
+                            out[q] = code;
+                            store_group(p.dst, 4 * (int64_t)q, it.cnt, us.apply4(unpack4<B>(cc, code)));
                         }
                     }
                 } else {
-                    const int ng = it.n_tiles * (kTile / 4);
-                    for (int q = threadIdx.x; q < ng; q += NT) {
-                        const W code = pack4<B>(c, s.apply4(load_group(p.src, 4 * (int64_t)q, it.cnt)));
-                        out[q] = code;
-                        store_group(p.dst, 4 * (int64_t)q, it.cnt, us.apply4(unpack4<B>(c, code)));
+                    const int b = cc.b();
+                    uint32_t *codes = s_codes[warp];
+                    uint32_t *outw = reinterpret_cast<uint32_t *>(t.packed + it.byte_pos);
+                    for (int tt = warp; tt < it.n_tiles; tt += NT / 32) {
+                        const int64_t e0 = (int64_t)tt * kTile + lane * 4;
+                        const float4 y = s.apply4(load_group(p.src, e0, it.cnt));
+                        const uint4 cd = make_uint4(cc.enc(y.x), cc.enc(y.y), cc.enc(y.z), cc.enc(y.w));
+                        *reinterpret_cast<uint4 *>(codes + lane * 4) = cd;
+                        __syncwarp();
+                        uint32_t *ow = outw + (int64_t)tt * (4 * b);
+                        for (int w2 = lane; w2 < 4 * b; w2 += 32) ow[w2] = assemble_word(codes, w2, b);
+                        store_group(p.dst, e0, it.cnt,
+                                    us.apply4(make_float4(cc.dec(cd.x), cc.dec(cd.y), cc.dec(cd.z), cc.dec(cd.w))));
+                        __syncwarp();
                     }
                 }
+            };
+            if constexpr (kTwo) {
+                if (it.fmt == fmt2) quantise(c2);
+                else quantise(c);
             } else {
-                const int b = c.b();
-                uint32_t *codes = s_codes[warp];
-                uint32_t *outw = reinterpret_cast<uint32_t *>(t.packed + it.byte_pos);
-                for (int tt = warp; tt < it.n_tiles; tt += NT / 32) {
-                    const int64_t e0 = (int64_t)tt * kTile + lane * 4;
-                    const float4 y = s.apply4(load_group(p.src, e0, it.cnt));
-                    const uint4 cd = make_uint4(c.enc(y.x), c.enc(y.y), c.enc(y.z), c.enc(y.w));
-                    *reinterpret_cast<uint4 *>(codes + lane * 4) = cd;
-                    __syncwarp();
-                    uint32_t *ow = outw + (int64_t)tt * (4 * b);
-                    for (int w2 = lane; w2 < 4 * b; w2 += 32) ow[w2] = assemble_word(codes, w2, b);
-                    store_group(p.dst, e0, it.cnt,
-                                us.apply4(make_float4(c.dec(cd.x), c.dec(cd.y), c.dec(cd.z), c.dec(cd.w))));
-                    __syncwarp();
-                }
+                quantise(c);
             }
         }
         __syncthreads();
@@ -928,20 +945,42 @@ __global__ void __launch_bounds__(NT, kWaveCtasPerSm)
     stamp(3);
 }
 
-cudaError_t launch_fused_p1_wave(const DevTables &t, int e, int m, bool hw, int average, uint32_t gen,
-                                 uint32_t claim_base, uint32_t call_no, int lag, int grid, cudaStream_t s)
+template <class C, class C2>
+static cudaError_t launch_wave(const DevTables &t, C c, C2 c2, int bias, int bias2, int fmt2, int average, uint32_t gen,
+                               uint32_t claim_base, uint32_t call_no, int lag, int grid, cudaStream_t s,
+                               bool cooperative)
 {
-    const int bias = (1 << (e - 1)) - 1;
     uint32_t *cur = t.amax2 + (size_t)(gen & 1u) * t.n_layers;
     uint32_t *other = t.amax2 + (size_t)((gen + 1u) & 1u) * t.n_layers;
+    auto kern = fused_p1_wave_kernel<C, C2, kThreads>;
+    int flags = kFusedDefaultFlags;
+    if (const char *env = std::getenv("APS_FUSED_FLAGS")) flags = std::atoi(env);
+    void *args[] = {const_cast<DevTables *>(&t), &c, &c2, &cur, &other, &claim_base, &call_no, &lag, &bias, &bias2,
+                    &fmt2, &average, &flags};
+    // co-residency is not needed for progress (a CTA waits only on positions claimed
+    // earlier, i.e. by running CTAs); a plain launch lets a concurrent group's kernel
+    // fill this one's tail
+    if (!cooperative) return cudaLaunchKernel((const void *)kern, dim3(grid), dim3(kThreads), args, 0, s);
+    return cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(kThreads), args, 0, s);
+}
+
+cudaError_t launch_fused_p1_wave(const DevTables &t, int e, int m, bool hw, int average, uint32_t gen,
+                                 uint32_t claim_base, uint32_t call_no, int lag, int grid, cudaStream_t s,
+                                 bool cooperative)
+{
+    const int bias = (1 << (e - 1)) - 1;
     return with_codec(e, m, hw, [&](auto c) -> cudaError_t {
-        using C = decltype(c);
-        auto kern = fused_p1_wave_kernel<C, kThreads>;
-        int flags = kFusedDefaultFlags;
-        if (const char *env = std::getenv("APS_FUSED_FLAGS")) flags = std::atoi(env);
-        void *args[] = {const_cast<DevTables *>(&t), &c, &cur, &other, &claim_base, &call_no, &lag,
-                        const_cast<int *>(&bias), &average, &flags};
-        return cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(kThreads), args, 0, s);
+        return launch_wave(t, c, CNone{}, bias, 0, -1, average, gen, claim_base, call_no, lag, grid, s, cooperative);
+    });
+}
+
+cudaError_t launch_fused_p1_wave_hybrid32(const DevTables &t, int e, int m, bool hw, int fmt2, int average,
+                                          uint32_t gen, uint32_t claim_base, uint32_t call_no, int lag, int grid,
+                                          cudaStream_t s)
+{
+    const int bias = (1 << (e - 1)) - 1;
+    return with_codec(e, m, hw, [&](auto c) -> cudaError_t {
+        return launch_wave(t, c, CF32{}, bias, 127, fmt2, average, gen, claim_base, call_no, lag, grid, s, true);
     });
 }
 
@@ -989,7 +1028,8 @@ int fused_p1_wave_grid(int e, int m, bool hw, int n_items)
     int per_sm = 0;
     with_codec(e, m, hw, [&](auto c) -> cudaError_t {
         using C = decltype(c);
-        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_p1_wave_kernel<C, kThreads>, kThreads, 0);
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_p1_wave_kernel<C, CNone, kThreads>,
+                                                             kThreads, 0);
     });
     per_sm = std::max(1, std::min(per_sm, kWaveCtasPerSm));
     return std::max(1, std::min(n_items, sm_count() * per_sm));

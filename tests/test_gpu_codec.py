@@ -74,16 +74,21 @@ def test_debug_cast_exhaustive_vs_torch(aps, fmt, dt):
         del bits, x, ours, t, ref, ok
 
 
-@pytest.mark.parametrize("fmt", [(5, 2), (4, 3)])
-def test_hw_codec_equals_generic_in_aps_regime(aps, fmt):
-    """The hardware cvt.rn.satfinite.{e5m2,e4m3}x2 path equals the generic
-    bit-arithmetic cast on every fp32 pattern with |x| <= 1.5 * 2^bias -- the
-    largest magnitude the APS path can present to a cast (scaled values
-    <= 2^bias / N, pre-rounding partial sums <= 2^bias + 2^bias / N,
-    Eq. (1)).  Exhaustive over that range, both signs."""
+@pytest.mark.parametrize("fmt", [(5, 2), (4, 3), (5, 10), (8, 7), (8, 23)], ids=lambda f: f"e{f[0]}m{f[1]}")
+def test_hw_codec_equals_generic(aps, fmt):
+    """The fast codecs equal the generic bit-arithmetic cast.  fp8
+    (cvt.rn.satfinite.{e5m2,e4m3}x2): on every fp32 pattern with
+    |x| <= 1.5 * 2^bias -- the largest magnitude the APS path can present to a
+    cast (scaled values <= 2^bias / N, pre-rounding partial sums <= 2^bias +
+    2^bias / N, Eq. (1)), reading A12.  binary16 / bfloat16
+    (cvt.rn.{f16,bf16}x2.f32) and binary32 (identity): on EVERY non-NaN fp32
+    pattern, +-Inf included.  Exhaustive, both signs; decode on every finite
+    code (sampled 2^26 + specials for the 32-bit format)."""
     e, m = fmt
     bias = (1 << (e - 1)) - 1
-    limit = int(np.float32(1.5 * 2.0 ** bias).view(np.uint32))
+    b = 1 + e + m
+    fp8 = b == 8
+    limit = int(np.float32(1.5 * 2.0 ** bias).view(np.uint32)) if fp8 else 0x7F800000
     chunk = 1 << 28
     for start in range(0, limit + 1, chunk):
         stop = min(start + chunk, limit + 1)
@@ -91,14 +96,21 @@ def test_hw_codec_equals_generic_in_aps_regime(aps, fmt):
         for sign in (0, -(1 << 31)):
             x = (bits | sign).view(torch.float32)
             a = aps.debug_cast(x, e, m, hw=False)
-            b = aps.debug_cast(x, e, m, hw=True)
-            assert torch.equal(a, b), f"hw/generic differ in chunk {start:#x} sign {sign}"
-    # decode: every finite code
-    codes = torch.arange(0, 256, dtype=torch.int32, device="cuda")
+            c = aps.debug_cast(x, e, m, hw=True)
+            assert torch.equal(a, c), f"hw/generic differ in chunk {start:#x} sign {sign}"
+            del x, a, c
+        del bits
+    if b <= 16:
+        codes = torch.arange(0, 1 << b, dtype=torch.int32, device="cuda")
+    else:
+        g = torch.Generator(device="cuda").manual_seed(synthetic.SEED)
+        codes = torch.randint(-(1 << 31), (1 << 31) - 1, (1 << 26,), generator=g, device="cuda", dtype=torch.int64)
+        special = torch.tensor([0, 1, 0x7FFFFF, 0x800000, 0x7F7FFFFF, 0x3F800000], dtype=torch.int64, device="cuda")
+        codes = torch.cat([codes, special, special | (1 << 31)]).to(torch.int32)
     fin = ((codes >> m) & ((1 << e) - 1)) != (1 << e) - 1
     a = aps.debug_decode(codes, e, m, hw=False)
-    b = aps.debug_decode(codes, e, m, hw=True)
-    assert torch.equal(a[fin].view(torch.int32), b[fin].view(torch.int32))
+    c = aps.debug_decode(codes, e, m, hw=True)
+    assert torch.equal(a[fin].view(torch.int32), c[fin].view(torch.int32))
 
 
 def _finite_codes(e, m):
@@ -109,7 +121,8 @@ def _finite_codes(e, m):
 
 @pytest.mark.parametrize("fmt,hw", [((5, 2), False), ((5, 2), True), ((4, 3), False), ((4, 3), True),
                                     ((3, 0), False), ((2, 1), False), ((5, 6), False), ((5, 10), False),
-                                    ((8, 7), False), ((4, 6), False), ((8, 23), False)],
+                                    ((8, 7), False), ((4, 6), False), ((8, 23), False), ((5, 10), True),
+                                    ((8, 7), True), ((8, 23), True)],
                          ids=lambda x: str(x))
 def test_ring_reduce_vs_oracle(aps, orc, fmt, hw):
     """s <- Cast(fl32(dec(recv) + dec(own))) on packed tiles (a5), against the
@@ -125,7 +138,7 @@ def test_ring_reduce_vs_oracle(aps, orc, fmt, hw):
     else:
         A = fin[rng.integers(0, fin.size, 1 << 21)]
         B = fin[rng.integers(0, fin.size, 1 << 21)]
-    if hw:   # APS regime only (reading A12): |a| + |b| <= 1.5 * 2^bias
+    if hw and b == 8:   # fp8 converters: APS regime only (reading A12): |a| + |b| <= 1.5 * 2^bias
         va, vb = orc.decode(A, e, m), orc.decode(B, e, m)
         keep = np.abs(va.astype(np.float64)) + np.abs(vb.astype(np.float64)) <= 1.5 * 2.0 ** bias
         A, B = A[keep], B[keep]

@@ -14,7 +14,7 @@ pytestmark = pytest.mark.gpu
 
 FORMATS = [((5, 2), True), ((5, 2), False), ((4, 3), True), ((4, 3), False), ((3, 0), False),
            ((5, 6), False), ((5, 10), False), ((8, 7), False), ((8, 23), False), ((4, 6), False),
-           ((6, 9), False), ((2, 1), False)]
+           ((6, 9), False), ((2, 1), False), ((5, 10), True), ((8, 7), True), ((8, 23), True)]
 FMT_IDS = [f"e{e}m{m}{'hw' if hw else ''}" for (e, m), hw in FORMATS]
 
 
@@ -112,7 +112,7 @@ def test_p1_c1_and_edges(aps, orc, fmt, hw, fused, engine):
 
 
 @pytest.mark.parametrize("fmt,hw", [((5, 2), True), ((5, 2), False), ((3, 0), False), ((5, 6), False),
-                                    ((5, 10), False), ((4, 3), True)], ids=lambda x: str(x))
+                                    ((5, 10), False), ((4, 3), True), ((5, 10), True), ((8, 23), True)], ids=lambda x: str(x))
 def test_p1_resnet50_full(aps, orc, fmt, hw):
     """Config 2 at N = 1 (the bench workload, bench's launch configuration:
     the fused single launch), 161 tensors, 25,557,032 elements; also the
