@@ -82,6 +82,12 @@ def lib():
         L.oracle_packed_bytes_mixed.argtypes = [ctypes.c_int, ctypes.c_int, vp, vp, vp]
         L.oracle_packed_bytes_mixed.restype = i64
         L.oracle_aps_sync_mixed.argtypes = [ctypes.c_int, vp, vp, ctypes.c_int, vp, vp, ctypes.c_int, vp, vp, vp, vp]
+        ci = ctypes.c_int
+        L.oracle_aps_sync_ex.argtypes = [ci, ci, ci, ci, vp, vp, ci, ci, ci, ci, ci, vp, vp, vp, vp]
+        L.oracle_reduce1.argtypes = [vp, ci, i64, i64, ci, ci, ci, ci, ci, ci]
+        L.oracle_reduce1.restype = u32
+        L.oracle_round_off_error.argtypes = [vp, vp, i64, vp]
+        L.oracle_round_off_error.restype = ctypes.c_double
         _lib = L
     return _lib
 
@@ -239,3 +245,43 @@ def aps_sync_mixed(grads, fmts, average: int = 1, want_packed: bool = True) -> S
     rc = lib().oracle_aps_sync_mixed(p, _ptr(e), _ptr(m), nl, _ptr(numels), gptrs, average, _ptr(ft),
                                      _ptr(packed) if want_packed else None, _ptr(reduced), optrs)
     return SyncResult(rc, ft, packed, reduced, outs)
+
+
+def aps_sync_ex(grads, e: int, m: int, average: int = 1, group_k: int = 1, acc=None, kahan: int = 0,
+                want_packed: bool = True) -> SyncResult:
+    """APS sync with a reduction order and accumulator:
+    ``group_k`` = hierarchical group size (1 or p: the flat ring, reading A23),
+    ``acc`` = accumulator format (default: the wire format), ``kahan`` =
+    compensated accumulation (reading A24)."""
+    p = len(grads)
+    nl = len(grads[0])
+    ae, am = acc if acc is not None else (e, m)
+    numels = np.array([np.asarray(g).size for g in grads[0]], dtype=np.int64)
+    flat = [np.ascontiguousarray(grads[r][l], dtype=np.float32) for r in range(p) for l in range(nl)]
+    gptrs = (ctypes.c_void_p * len(flat))(*[a.ctypes.data for a in flat])
+    nbytes = packed_bytes(p, e, m, numels)
+    ft = np.zeros(nl, dtype=np.int32)
+    packed = np.zeros((p, nbytes), dtype=np.uint8) if want_packed else None
+    reduced = np.zeros(nbytes, dtype=np.uint8)
+    outs = [np.empty(int(n), dtype=np.float32) for n in numels]
+    optrs = (ctypes.c_void_p * nl)(*[a.ctypes.data for a in outs])
+    rc = lib().oracle_aps_sync_ex(p, e, m, nl, _ptr(numels), gptrs, average, group_k, ae, am, kahan, _ptr(ft),
+                                  _ptr(packed) if want_packed else None, _ptr(reduced), optrs)
+    return SyncResult(rc, ft, packed, reduced, outs)
+
+
+def reduce1(codes, tile: int, tiles: int, group_k: int, e: int, m: int, acc=None, kahan: int = 0) -> int:
+    """One element's all-reduce: codes[r] = rank r's wire code, ``tile`` its tile, ``tiles`` = T'."""
+    c = np.ascontiguousarray(codes, dtype=np.uint32)
+    ae, am = acc if acc is not None else (e, m)
+    return lib().oracle_reduce1(_ptr(c), c.size, tile, tiles, group_k, e, m, ae, am, kahan)
+
+
+def round_off_error(grad_h, grad_l):
+    """Eq. (5), reading A25: mean of |(h - l) / h| over h != 0.
+    Returns (error, count)."""
+    h = np.ascontiguousarray(grad_h, dtype=np.float32)
+    l_ = np.ascontiguousarray(grad_l, dtype=np.float32)
+    cnt = ctypes.c_int64(0)
+    err = lib().oracle_round_off_error(_ptr(h), _ptr(l_), h.size, ctypes.byref(cnt))
+    return err, cnt.value

@@ -515,3 +515,157 @@ int oracle_aps_sync_mixed(int p, const int *e, const int *m, int n_layers, const
     free(q); free(s); free(lay); free(tile_byte); free(ft);
     return OR_OK;
 }
+
+/* ------------------------------------------------------------------ */
+/* Reduction order and accumulator.    */
+/*                                                                     */
+/* NEXT-3, hierarchical all-reduce: "partition the nodes   */
+/* into groups ... (1) within each group, all worker nodes send their  */
+/* local gradients to the master node; (2) ring all-reduce across all  */
+/* the master nodes; (3) within each group, the master node broadcasts */
+/* the global gradients".  Reading A23: p ranks form G =   */
+/* p/k groups of k consecutive ranks; step (1) is the ring reduce of   */
+/* the group (its step count 2(k-1) of the paper's 4(k-1)+2(p/k-1),    */
+/* P:528), i.e. O7/O8 applied inside the group: tile t lies in group   */
+/* chunk c1 = t / (T'/k) and is accumulated over group members in      */
+/* local order c1+1, ..., c1; step (2) is O8 over the G group sums:    */
+/* tile t lies in master chunk c2 = t / (T'/G), accumulated over groups*/
+/* c2+1, ..., c2; step (3) moves codes only.  k = 1 and k = p are the  */
+/* flat ring of O8.                                                    */
+/*                                                                     */
+/* NEXT-4, CPD accumulator: "use a higher precision to     */
+/* store the accumulator", "arbitrary low precision (<= 32 bits) for   */
+/* the accumulator", "the Kahan summation algorithm".  Reading A24:    */
+/* the running sum is held in the accumulator format (ae, am); every   */
+/* arithmetic result is an fp32 operation re-quantised to (ae, am)     */
+/* (CPD's emulation, as in O8); the first addend is cast into the      */
+/* accumulator; the final sum is cast to the wire format once.  Kahan  */
+/* (Higham's compensated summation): y = x - c; t = s + y;             */
+/* c = (t - s) - y; s = t, each result re-quantised; c starts at 0 in  */
+/* every fold (a group's compensation is not sent to its master).      */
+/* ------------------------------------------------------------------ */
+static float acc_q(float x, int ae, int am) { return oracle_decode1(oracle_cast1(x, ae, am), ae, am); }
+
+/* Sum x[0..n-1] in the given order in accumulator format (ae, am). */
+static float oracle_fold(const float *x, int n, int ae, int am, int kahan)
+{
+    float s = acc_q(x[0], ae, am);
+    float c = 0.0f;
+    for (int j = 1; j < n; ++j) {
+        if (!kahan) {
+            s = acc_q(s + x[j], ae, am);                 /* fl32 add, re-quantise */
+        } else {
+            const float y = acc_q(x[j] - c, ae, am);
+            const float t = acc_q(s + y, ae, am);
+            c = acc_q(acc_q(t - s, ae, am) - y, ae, am);
+            s = t;
+        }
+    }
+    return s;
+}
+
+/* One element's all-reduce: q[r] = rank r's wire code of the element
+ * (r = 0..p-1), t = its tile, Tp = T'.  Returns the reduced wire code. */
+uint32_t oracle_reduce1(const uint32_t *q, int p, int64_t t, int64_t Tp, int group_k, int e, int m,
+                        int ae, int am, int kahan)
+{
+    const int k = group_k, G = p / group_k;
+    const int64_t c1 = t / (Tp / k), c2 = t / (Tp / G);
+    float gs[256], xs[256];
+    for (int gi = 0; gi < G; ++gi) {
+        const int g = (int)((c2 + 1 + gi) % G);          /* masters in ring order c2+1, ..., c2 */
+        for (int j = 0; j < k; ++j)                      /* members in ring order c1+1, ..., c1 */
+            xs[j] = oracle_decode1(q[g * k + (int)((c1 + 1 + j) % k)], e, m);
+        gs[gi] = oracle_fold(xs, k, ae, am, kahan);
+    }
+    return oracle_cast1(oracle_fold(gs, G, ae, am, kahan), e, m);
+}
+
+/* oracle_aps_sync with a reduction order (group_k: 1 <= k <= p, k | p,
+ * p <= 256) and an accumulator format (ae, am) with optional Kahan
+ * compensation.  group_k = 1 (or p), (ae, am) = (e, m), kahan = 0 is
+ * oracle_aps_sync. */
+int oracle_aps_sync_ex(int p, int e, int m, int n_layers, const int64_t *numels, const float *const *grads,
+                       int average, int group_k, int ae, int am, int kahan, int32_t *ftilde_out,
+                       uint8_t *packed_out, uint8_t *reduced_out, float *const *out)
+{
+    if (oracle_format_valid(e, m) || oracle_format_valid(ae, am)) return OR_ERR_FORMAT;
+    if (p < 1 || p > 256 || n_layers < 1 || !numels || !grads) return OR_ERR_ARG;
+    if (group_k < 1 || group_k > p || p % group_k) return OR_ERR_ARG;
+    for (int l = 0; l < n_layers; ++l)
+        if (numels[l] < 1) return OR_ERR_ARG;
+    const int b = 1 + e + m;
+    const int64_t Tp = oracle_total_tiles(p, n_layers, numels);
+    const int64_t ncodes = Tp * OR_TILE;
+    const int64_t nbytes = 16 * (int64_t)b * Tp;
+
+    /* Alg. 1 lines 3-4 */
+    int32_t *ft = (int32_t *)malloc(sizeof(int32_t) * (size_t)n_layers);
+    int nonfinite = 0;
+    for (int l = 0; l < n_layers; ++l) {
+        int32_t Emax = OR_EMPTY;
+        for (int r = 0; r < p; ++r) {
+            int32_t Er = oracle_find_max_exp(grads[(size_t)r * n_layers + l], numels[l], p);
+            if (Er == OR_NONFINITE) nonfinite = 1;
+            if (Er > Emax) Emax = Er;
+        }
+        ft[l] = oracle_scale_exp(e, Emax);
+        if (ftilde_out) ftilde_out[l] = ft[l];
+    }
+    if (nonfinite) { free(ft); return OR_ERR_NONFINITE; }
+    /* lines 5-6 */
+    uint32_t *q = (uint32_t *)calloc((size_t)p * (size_t)ncodes, sizeof(uint32_t));
+    for (int r = 0; r < p; ++r) {
+        int64_t off = 0;
+        for (int l = 0; l < n_layers; ++l) {
+            const float *g = grads[(size_t)r * n_layers + l];
+            for (int64_t i = 0; i < numels[l]; ++i)
+                q[(size_t)r * ncodes + off + i] = oracle_cast1(oracle_scale(g[i], ft[l]), e, m);
+            off += OR_TILE * ((numels[l] + OR_TILE - 1) / OR_TILE);
+        }
+        if (packed_out) {
+            uint8_t *pk = packed_out + (size_t)r * (size_t)nbytes;
+            memset(pk, 0, (size_t)nbytes);
+            oracle_pack(q + (size_t)r * ncodes, ncodes, b, pk);
+        }
+    }
+    /* line 7 in the chosen order and accumulator */
+    uint32_t *s = (uint32_t *)calloc((size_t)ncodes, sizeof(uint32_t));
+    uint32_t col[256];
+    for (int64_t i = 0; i < ncodes; ++i) {
+        for (int r = 0; r < p; ++r) col[r] = q[(size_t)r * ncodes + i];
+        s[i] = oracle_reduce1(col, p, i / OR_TILE, Tp, group_k, e, m, ae, am, kahan);
+    }
+    if (reduced_out) {
+        memset(reduced_out, 0, (size_t)nbytes);
+        oracle_pack(s, ncodes, b, reduced_out);
+    }
+    /* lines 8-9 */
+    if (out) {
+        int64_t off = 0;
+        for (int l = 0; l < n_layers; ++l) {
+            for (int64_t i = 0; i < numels[l]; ++i) out[l][i] = oracle_unscale1(s[off + i], ft[l], p, average, e, m);
+            off += OR_TILE * ((numels[l] + OR_TILE - 1) / OR_TILE);
+        }
+    }
+    free(q); free(s); free(ft);
+    return OR_OK;
+}
+
+/* Eq. (5) `equation:round_off_error`:
+ *   average_round_off_error = sum_i |(grad_h_i - grad_l_i) / grad_h_i| / N.
+ * Reading A25: terms with grad_h_i = 0 are undefined and are left out of
+ * both the sum and N ("N elements" counts the defined terms); the sum is
+ * taken in binary64, in index order.  *count_out receives that N. */
+double oracle_round_off_error(const float *h, const float *l, int64_t n, int64_t *count_out)
+{
+    double sum = 0.0;
+    int64_t cnt = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        if (h[i] == 0.0f) continue;
+        sum += fabs(((double)h[i] - (double)l[i]) / (double)h[i]);
+        ++cnt;
+    }
+    if (count_out) *count_out = cnt;
+    return cnt ? sum / (double)cnt : 0.0;
+}
