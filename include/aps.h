@@ -190,6 +190,58 @@ aps_status aps_layout_mixed(int world_size, int n_layers, const int64_t *numels,
  * (rank-2-step) mod p from rank-1, which it reduces into its own copy. */
 aps_status aps_ring_step(int world_size, int rank, int step, int *send_chunk, int *recv_chunk);
 
+/* ---- reduction order and accumulator ------
+ * group_k: hierarchical all-reduce with groups of group_k consecutive ranks
+ *   (intra-group reduce to a master, ring all-reduce across the
+ *   masters, broadcast; the paper's round-off argument P:531-541).  Reading
+ *   A23: tile t is accumulated over the members of each group in ring order
+ *   c1+1, ..., c1 of its group chunk c1 = t / (T'/group_k), then over the
+ *   p/group_k group sums in ring order c2+1, ..., c2 of its master chunk
+ *   c2 = t / (T' group_k / p).  group_k = 1 or world_size: the flat ring (A14).
+ *   Must divide world_size.
+ * acc_exp_bits, acc_man_bits: accumulator format (CPD: "use a
+ *   higher precision to store the accumulator"; reading A24): the running sum
+ *   is re-quantised to it after every fp32 add and cast to the wire format
+ *   once at the end.  Must hold every wire value (>= the wire's exp and man
+ *   bits); equal to the wire format by default.
+ * kahan: Kahan-compensated accumulation (reading A24): y = x - c,
+ *   t = s + y, c = (t - s) - y, s = t, every result re-quantised.
+ * Anything but the default (flat ring, wire accumulator, no compensation)
+ * needs the peer transport (aps_peer_import / aps_sim_connect): the NCCL ring
+ * moves partial sums in the wire format.  Accumulator variants need one
+ * format for every layer (aps_init).  Errors: APS_ERR_ARG, APS_ERR_FORMAT. */
+aps_status aps_set_reduction(aps_ctx *ctx, int group_k, int acc_exp_bits, int acc_man_bits, int kahan);
+
+/* ---- peer-memory transport (NVLink / NVSwitch load-store) ----------------
+ * Alg. 1 line 7's all-reduce without NCCL: rank r loads the p ranks' packed
+ * codes of ring chunk r straight from their workspaces (CUDA IPC mappings),
+ * folds them in the reduction order above, and stores the reduced codes into
+ * every rank's packed buffer (the all-gather, fused).  NVLink bytes per rank
+ * equal the ring's.  The exponent MAX (Alg. 1 line 4) goes through peer
+ * memory too.  Cross-rank ordering uses monotone epoch flags (system-scope
+ * release/acquire); every device wait gives up after 2 s (APS_ERR_STATE from
+ * aps_status_sync).  Bit-identical to the NCCL ring for the flat order.
+ * Protocol: every rank calls aps_peer_export [sync] after aps_set_workspace,
+ * the host gathers the world_size (handle, offset) pairs (e.g. over
+ * torch.distributed), then every rank calls aps_peer_import.  All ranks must
+ * then issue the same sequence of syncs.
+ *   host_handle : APS_PEER_HANDLE_BYTES bytes (a cudaIpcMemHandle_t of the
+ *                 allocation holding the workspace)
+ *   host_offset : the workspace's byte offset in that allocation
+ *   host_handles: [world_size * APS_PEER_HANDLE_BYTES], rank-major; host_offsets: [world_size]
+ * aps_destroy unmaps the peers (every rank must have finished its last sync). */
+#define APS_PEER_HANDLE_BYTES 64
+aps_status aps_peer_export(aps_ctx *ctx, void *host_handle, uint64_t *host_offset);
+aps_status aps_peer_import(aps_ctx *ctx, const void *host_handles, const uint64_t *host_offsets);
+
+/* Eq. (5) `equation:round_off_error`, reading A25: adds
+ * sum over i with h[i] != 0 of |(h[i] - l[i]) / h[i]| (binary64) to *dev_sum and
+ * the number of such i to *dev_count (device scalars the caller zeroes);
+ * the average round-off error is sum / count.  h, l: device fp32 [n].
+ * The binary64 sum is accumulated in a device-dependent order. */
+aps_status aps_round_off_error(const float *h, const float *l, int64_t n, double *dev_sum,
+                               unsigned long long *dev_count, void *cuda_stream);
+
 const char *aps_last_error(const aps_ctx *ctx);
 aps_status aps_destroy(aps_ctx *ctx);
 const char *aps_version(void);
@@ -209,6 +261,10 @@ aps_status aps_nccl_comm_destroy(void *comm);
  * aps_allreduce with device-to-device copies in place of send/recv. */
 aps_status aps_sim_layer_scales(aps_ctx *const *ctxs, int p, const float *const *grads);
 aps_status aps_sim_allreduce(aps_ctx *const *ctxs, int p);
+/* Connect p simulated ranks through the peer transport (each context's
+ * "peer" pointers are the other contexts' workspaces on the same device);
+ * aps_sim_layer_scales / aps_sim_allreduce then run the peer kernels. */
+aps_status aps_sim_connect(aps_ctx *const *ctxs, int p);
 
 /* ---- test only: the device cast on arbitrary inputs ------------------ */
 /* codes[i] = Cast(in[i]) (uint32 per code, unpacked); exercises Inf/NaN and

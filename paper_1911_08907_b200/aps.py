@@ -28,8 +28,10 @@ EXPORTS = [
     "aps_ring_step", "aps_last_error", "aps_destroy", "aps_version", "aps_nccl_unique_id",
     "aps_nccl_comm_init", "aps_nccl_comm_destroy", "aps_sim_layer_scales", "aps_sim_allreduce",
     "aps_debug_cast", "aps_debug_decode", "aps_debug_ring_reduce", "aps_debug_timeline",
-    "aps_init_mixed", "aps_layout_mixed",
+    "aps_init_mixed", "aps_layout_mixed", "aps_set_reduction", "aps_peer_export", "aps_peer_import",
+    "aps_sim_connect", "aps_round_off_error",
 ]
+PEER_HANDLE_BYTES = 64
 
 
 class ApsError(RuntimeError):
@@ -84,6 +86,11 @@ def load(path: Path | str | None = None):
         "aps_debug_timeline": ([vp, vp, i32], i32),
         "aps_init_mixed": ([ctypes.POINTER(vp), vp, vp, i32, i32, i32, vp, vp, vp], i32),
         "aps_layout_mixed": ([i32, i32, vp, vp, vp, ctypes.POINTER(i64), ctypes.POINTER(i64)], i32),
+        "aps_set_reduction": ([vp, i32, i32, i32, i32], i32),
+        "aps_peer_export": ([vp, vp, ctypes.POINTER(ctypes.c_uint64)], i32),
+        "aps_peer_import": ([vp, vp, vp], i32),
+        "aps_sim_connect": ([vp, i32], i32),
+        "aps_round_off_error": ([vp, vp, i64, vp, vp, vp], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -269,6 +276,35 @@ class ApsContext:
     def set_hw_convert(self, enable: bool):
         self._check(self.L.aps_set_hw_convert(self.h, int(enable)), "aps_set_hw_convert")
 
+    def set_reduction(self, group_k: int = 1, acc: tuple[int, int] | None = None, kahan: bool = False):
+        """Reduction order (hierarchical group size, 1 = flat ring) and accumulator
+        (format, Kahan) of the all-reduce (aps_set_reduction)."""
+        wire = self.formats[0] if self.formats is not None else (self.exp_bits, self.man_bits)
+        ae, am = acc if acc is not None else wire
+        self._check(self.L.aps_set_reduction(self.h, group_k, ae, am, int(kahan)), "aps_set_reduction")
+
+    # -------------------------------------------------------------- peer transport
+    def peer_export(self) -> tuple[bytes, int]:
+        buf = ctypes.create_string_buffer(PEER_HANDLE_BYTES)
+        off = ctypes.c_uint64()
+        self._check(self.L.aps_peer_export(self.h, buf, ctypes.byref(off)), "aps_peer_export")
+        return buf.raw, off.value
+
+    def peer_import(self, handles: Sequence[bytes], offsets: Sequence[int]):
+        blob = b"".join(handles)
+        offs = (ctypes.c_uint64 * len(offsets))(*offsets)
+        self._check(self.L.aps_peer_import(self.h, blob, offs), "aps_peer_import")
+
+    def connect_peers(self, group=None):
+        """Map every rank's workspace (CUDA IPC) and switch the all-reduce to the
+        peer-memory transport.  Collective over the torch.distributed group."""
+        import torch.distributed as dist
+        mine = self.peer_export()
+        allv = [None] * self.world_size
+        dist.all_gather_object(allv, mine, group=group)
+        self.peer_import([h for h, _ in allv], [o for _, o in allv])
+        dist.barrier(group=group)
+
 
 def sim_layer_scales(ctxs: Sequence[ApsContext], grads_per_rank):
     L = load()
@@ -277,6 +313,29 @@ def sim_layer_scales(ctxs: Sequence[ApsContext], grads_per_rank):
     st = L.aps_sim_layer_scales(hs, len(ctxs), _ptr_array([t.data_ptr() for t in flat]))
     if st:
         raise ApsError(st, "aps_sim_layer_scales: " + L.aps_last_error(ctxs[0].h).decode())
+
+
+def sim_connect(ctxs: Sequence[ApsContext]):
+    """Connect simulated ranks through the peer-memory transport (aps_sim_connect)."""
+    L = load()
+    hs = _ptr_array([c.h.value for c in ctxs])
+    st = L.aps_sim_connect(hs, len(ctxs))
+    if st:
+        raise ApsError(st, "aps_sim_connect: " + L.aps_last_error(ctxs[0].h).decode())
+
+
+def round_off_error(grad_h, grad_l) -> tuple[float, int]:
+    """Eq. (5) on the device: mean of |(h - l) / h| over h != 0
+    (binary64 sum on the GPU).  Returns (error, count)."""
+    import torch
+    acc = torch.zeros(2, dtype=torch.float64, device=grad_h.device)
+    st = load().aps_round_off_error(grad_h.data_ptr(), grad_l.data_ptr(), grad_h.numel(), acc.data_ptr(),
+                                    acc.data_ptr() + 8, torch.cuda.current_stream(grad_h.device).cuda_stream)
+    if st:
+        raise ApsError(st, "aps_round_off_error")
+    s = float(acc[0].item())
+    n = int(acc[1:].view(torch.int64).item())
+    return (s / n if n else 0.0), n
 
 
 def sim_allreduce(ctxs: Sequence[ApsContext]):

@@ -1,19 +1,23 @@
 """Build libaps.so in-tree with nvcc for sm_100a (no JIT, no torch extension
-machinery): the .so travels with the repo to the GPU box."""
+machinery): the .so travels with the repo to the GPU box.  Each source is
+compiled to an object in parallel, then linked."""
 from __future__ import annotations
 
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libaps.so"
-SOURCES = [CSRC / "aps_kernels.cu", CSRC / "aps_stream.cu", CSRC / "aps_api.cpp"]
-HEADERS = [CSRC / "aps_numerics.cuh", CSRC / "aps_device.cuh", CSRC / "aps_internal.h", ROOT / "include" / "aps.h"]
+SOURCES = [CSRC / "aps_kernels.cu", CSRC / "aps_stream.cu", CSRC / "aps_peer.cu", CSRC / "aps_api.cpp"]
+HEADERS = [CSRC / "aps_numerics.cuh", CSRC / "aps_device.cuh", CSRC / "aps_internal.h", CSRC / "aps_peer.h",
+           ROOT / "include" / "aps.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
 def nccl_dirs() -> tuple[Path, Path]:
@@ -23,21 +27,36 @@ def nccl_dirs() -> tuple[Path, Path]:
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
-    newest = max(p.stat().st_mtime for p in SOURCES + HEADERS)
+    newest = max(p.stat().st_mtime for p in SOURCES + HEADERS + [Path(__file__)])
     if not force and LIB.exists() and LIB.stat().st_mtime >= newest:
         return LIB
     inc, lib = nccl_dirs()
+    objdir = PKG / "build"
+    objdir.mkdir(exist_ok=True)
+    common = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
+              "-Xptxas", "-v" if verbose else "-O3", f"-I{ROOT / 'include'}", f"-I{inc}"]
+
+    def compile_one(src: Path):
+        obj = objdir / (src.name + f".{os.getpid()}.o")
+        return obj, subprocess.run(common + ["-c", str(src), "-o", str(obj)], capture_output=True, text=True)
+
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        results = list(ex.map(compile_one, SOURCES))
+    for (obj, r), src in zip(results, SOURCES):
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError(f"nvcc failed on {src.name}")
+        if verbose:
+            sys.stderr.write(r.stderr)
     tmp = LIB.with_suffix(f".so.tmp{os.getpid()}")
-    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-           "-Xcompiler", "-fPIC,-O2", "-shared", "-Xptxas", "-v" if verbose else "-O3",
-           f"-I{ROOT / 'include'}", f"-I{inc}", *map(str, SOURCES), "-o", str(tmp),
-           f"-L{lib}", "-l:libnccl.so.2", f"-Xlinker", f"-rpath={lib}"]
+    cmd = [NVCC, *ARCH, "-shared", *[str(o) for o, _ in results], "-o", str(tmp),
+           f"-L{lib}", "-l:libnccl.so.2", "-Xlinker", f"-rpath={lib}"]
     r = subprocess.run(cmd, capture_output=True, text=True)
+    for o, _ in results:
+        o.unlink(missing_ok=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc failed building libaps.so")
-    if verbose:
-        sys.stderr.write(r.stderr)
+        raise RuntimeError("nvcc failed linking libaps.so")
     os.replace(tmp, LIB)
     return LIB
 

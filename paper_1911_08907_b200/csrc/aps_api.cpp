@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "aps_internal.h"
+#include "aps_peer.h"
 
 namespace aps {
 constexpr uint32_t kFlagWaitTimeout = 2u;  // (mirrors aps_device.cuh)
@@ -56,6 +57,7 @@ struct aps_ctx {
     std::vector<Group> groups;
     struct Seg {
         int64_t byte_off, n_tiles;  // byte offset in the packed buffer, tiles
+        int64_t tile0;              // first tile (global index: selects the reduction schedule)
         int e, m;
         bool hw;
     };
@@ -86,9 +88,20 @@ struct aps_ctx {
     std::vector<cudaStream_t> side;
     std::vector<cudaEvent_t> ev_join;
     cudaEvent_t ev_fork = nullptr;
+    // reduction order and accumulator: hierarchical
+    // group size (1 = flat ring), accumulator format, Kahan compensation
+    int group_k = 1, acc_e = 0, acc_m = 0;
+    bool kahan = false;
+    // peer-memory transport (aps_peer.cu): every rank's workspace mapped here
+    bool peer = false;
+    aps::PeerArgs pa{};
+    uint32_t e_epoch = 0, r_epoch = 0;  // AllReduce(E, MAX) calls / all-reduce calls so far
+    std::vector<void *> ipc_mapped;     // cudaIpcOpenMemHandle mappings (closed by aps_destroy)
+    size_t off_pflags = 0, off_eslots = 0;
     std::string err;
     ~aps_ctx()
     {
+        for (void *p : ipc_mapped) cudaIpcCloseMemHandle(p);
         for (cudaStream_t s : side) cudaStreamDestroy(s);
         for (cudaEvent_t e : ev_join) cudaEventDestroy(e);
         if (ev_fork) cudaEventDestroy(ev_fork);
@@ -322,7 +335,7 @@ static aps_status init_common(aps_ctx **out, const int *e_arr, const int *m_arr,
             if (!segs.empty() && segs.back().e == e && segs.back().m == m)
                 segs.back().n_tiles += run_end - t;
             else
-                segs.push_back({byte, run_end - t, e, m, c->hw_enabled && aps::hw_available(e, m)});
+                segs.push_back({byte, run_end - t, t, e, m, c->hw_enabled && aps::hw_available(e, m)});
             t = run_end;
         }
         c->max_chunk_bytes = std::max(c->max_chunk_bytes, c->chunk_byte[ch + 1] - c->chunk_byte[ch]);
@@ -347,6 +360,11 @@ static aps_status init_common(aps_ctx **out, const int *e_arr, const int *m_arr,
     c->off_tl = o;     o = align_up(o + sizeof(uint64_t) * aps::kTimelineSlots);
     c->off_claim = o;  o = align_up(o + 3 * sizeof(uint32_t) * c->groups.size());  // 3 per format group
     c->off_ldone = o;  o = align_up(o + 4 * (size_t)n_layers);
+    // peer transport: flag block and E slots [2][world][n_layers] (world > 1 only)
+    c->off_pflags = o; o = align_up(o + (world_size > 1 ? 4 * (size_t)aps::kFlagWords : 0));
+    c->off_eslots = o; o = align_up(o + (world_size > 1 ? 2 * 4 * (size_t)world_size * (size_t)n_layers : 0));
+    c->acc_e = c->e;
+    c->acc_m = c->m;
 
     for (const auto &L : c->layers) c->max_layer_items = std::max(c->max_layer_items, (int)L.n_items);
     c->need = o;
@@ -499,6 +517,30 @@ static aps_status reduce_chunk(aps_ctx *c, const aps_ctx *layout, int ch, const 
     return APS_OK;
 }
 
+static bool flat_reduction(const aps_ctx *c)
+{
+    return (c->group_k == 1 || c->group_k == c->world) && !c->kahan && c->acc_e == c->e && c->acc_m == c->m;
+}
+
+// peer transport: announce this rank's packed codes, wait for every rank's
+static aps_status peer_ready(aps_ctx *c)
+{
+    APS_CUDA(c, aps::launch_peer_signal(c->pa, aps::kSlotReady, c->r_epoch, c->stream));
+    APS_CUDA(c, aps::launch_peer_wait(c->pa, aps::kSlotReady, c->r_epoch, c->t.flag, c->stream));
+    return APS_OK;
+}
+
+// peer transport: reduce this rank's chunk from every rank's codes, store it into every rank
+static aps_status peer_reduce_own(aps_ctx *c)
+{
+    c->pa.group_k = c->group_k;
+    for (const auto &sg : c->chunk_segs[c->rank])
+        APS_CUDA(c, aps::launch_peer_reduce(c->pa, sg.byte_off, sg.tile0, sg.n_tiles, sg.e, sg.m, sg.hw,
+                                            c->uniform ? c->acc_e : sg.e, c->uniform ? c->acc_m : sg.m, c->kahan,
+                                            c->stream));
+    return APS_OK;
+}
+
 aps_status aps_set_hw_convert(aps_ctx *c, int enable)
 {
     if (!c) return APS_ERR_ARG;
@@ -531,6 +573,16 @@ aps_status aps_layer_scales(aps_ctx *c, const float *const *grads)
     }
     if (c->world == 1 && !c->comm) {
         c->phase = kScales;
+    } else if (c->peer) {
+        // AllReduce(max_grad_exp, MAX) over peer memory: post E to every rank, collect
+        ++c->e_epoch;
+        APS_CUDA(c, aps::launch_peer_post_E(c->pa, c->t.E_local, c->n_layers, c->e_epoch, c->stream));
+        if (c->sim) {
+            c->phase = kLocalScales;  // aps_sim_layer_scales collects after every rank posted
+        } else {
+            APS_CUDA(c, aps::launch_peer_collect_E(c->pa, c->t.E_glob, c->n_layers, c->e_epoch, c->t.flag, c->stream));
+            c->phase = kScales;
+        }
     } else if (c->sim) {
         c->phase = kLocalScales;  // aps_sim_layer_scales completes the exchange
     } else {
@@ -568,6 +620,17 @@ aps_status aps_allreduce(aps_ctx *c)
         return APS_OK;
     }
     if (c->sim) return fail(c, APS_ERR_STATE, "simulated rank: use aps_sim_allreduce");
+    if (c->peer) {
+        ++c->r_epoch;
+        if (aps_status s = peer_ready(c)) return s;
+        if (aps_status s = peer_reduce_own(c)) return s;
+        APS_CUDA(c, aps::launch_peer_signal(c->pa, aps::kSlotDone, c->r_epoch, c->stream));
+        APS_CUDA(c, aps::launch_peer_wait(c->pa, aps::kSlotDone, c->r_epoch, c->t.flag, c->stream));
+        c->phase = kReduced;
+        return APS_OK;
+    }
+    if (!flat_reduction(c))
+        return fail(c, APS_ERR_STATE, "hierarchical order / accumulator variants need the peer transport");
     const int p = c->world, r = c->rank;
     uint8_t *packed = c->t.packed;
     uint8_t *recv = c->ws + c->off_recv;
@@ -762,6 +825,110 @@ aps_status aps_get_packed(aps_ctx *c, const void **dev, size_t *bytes)
 
 const char *aps_last_error(const aps_ctx *c) { return c ? c->err.c_str() : "NULL context"; }
 
+aps_status aps_set_reduction(aps_ctx *c, int group_k, int acc_exp_bits, int acc_man_bits, int kahan)
+{
+    if (!c) return APS_ERR_ARG;
+    if (group_k < 1 || group_k > c->world || c->world % group_k)
+        return fail(c, APS_ERR_ARG, "group_k must divide world_size");
+    if (!format_ok(acc_exp_bits, acc_man_bits)) return fail(c, APS_ERR_FORMAT, "invalid accumulator format");
+    const bool ext = kahan || acc_exp_bits != c->e || acc_man_bits != c->m;
+    if (ext && !c->uniform) return fail(c, APS_ERR_ARG, "accumulator variants need one format for every layer");
+    if (acc_exp_bits < c->e || acc_man_bits < c->m)
+        return fail(c, APS_ERR_FORMAT, "the accumulator must hold every wire value (exp and man bits >= the wire's)");
+    c->group_k = group_k;
+    c->acc_e = acc_exp_bits;
+    c->acc_m = acc_man_bits;
+    c->kahan = kahan != 0;
+    return APS_OK;
+}
+
+// base of the device allocation holding p (cuMemGetAddressRange through the runtime's
+// driver entry point: libaps does not link libcuda)
+static cudaError_t alloc_base(void *p, uint8_t **base)
+{
+    typedef int (*Fn)(unsigned long long *, size_t *, unsigned long long);
+    static Fn fn = nullptr;
+    if (!fn) {
+        void *f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        cudaError_t e = cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q);
+        if (e != cudaSuccess) return e;
+        if (q != cudaDriverEntryPointSuccess || !f) return cudaErrorNotSupported;
+        fn = reinterpret_cast<Fn>(f);
+    }
+    unsigned long long b = 0;
+    size_t sz = 0;
+    if (fn(&b, &sz, reinterpret_cast<unsigned long long>(p)) != 0) return cudaErrorInvalidValue;
+    *base = reinterpret_cast<uint8_t *>(b);
+    return cudaSuccess;
+}
+
+static void peer_set(aps_ctx *c, int q, uint8_t *ws)
+{
+    c->pa.packed[q] = ws + c->off_packed;
+    c->pa.flags[q] = reinterpret_cast<uint32_t *>(ws + c->off_pflags);
+    c->pa.eslots[q] = reinterpret_cast<int32_t *>(ws + c->off_eslots);
+}
+
+static void peer_common(aps_ctx *c)
+{
+    c->pa.p = c->world;
+    c->pa.rank = c->rank;
+    c->pa.tiles = c->tiles;
+    c->pa.group_k = c->group_k;
+    c->e_epoch = c->r_epoch = 0;
+    c->peer = true;
+}
+
+aps_status aps_peer_export(aps_ctx *c, void *host_handle, uint64_t *host_offset)
+{
+    if (aps_status s = need_ws(c)) return s;
+    if (!host_handle || !host_offset) return APS_ERR_ARG;
+    if (c->world < 2 || c->world > aps::kMaxPeers || c->sim)
+        return fail(c, APS_ERR_STATE, "peer transport needs 2..64 real ranks");
+    uint8_t *base = nullptr;
+    APS_CUDA(c, alloc_base(c->ws, &base));
+    cudaIpcMemHandle_t h;
+    APS_CUDA(c, cudaIpcGetMemHandle(&h, base));
+    static_assert(sizeof(h) <= APS_PEER_HANDLE_BYTES, "IPC handle size");
+    std::memset(host_handle, 0, APS_PEER_HANDLE_BYTES);
+    std::memcpy(host_handle, &h, sizeof(h));
+    *host_offset = (uint64_t)(c->ws - base);
+    APS_CUDA(c, cudaStreamSynchronize(c->stream));  // the workspace zero-fill is done before any peer writes
+    return APS_OK;
+}
+
+aps_status aps_peer_import(aps_ctx *c, const void *host_handles, const uint64_t *host_offsets)
+{
+    if (aps_status s = need_ws(c)) return s;
+    if (!host_handles || !host_offsets) return APS_ERR_ARG;
+    if (c->world < 2 || c->world > aps::kMaxPeers || c->sim)
+        return fail(c, APS_ERR_STATE, "peer transport needs 2..64 real ranks");
+    if (c->peer) return fail(c, APS_ERR_STATE, "peers already imported");
+    for (int q = 0; q < c->world; ++q) {
+        if (q == c->rank) {
+            peer_set(c, q, c->ws);
+            continue;
+        }
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, static_cast<const uint8_t *>(host_handles) + (size_t)q * APS_PEER_HANDLE_BYTES, sizeof(h));
+        void *p = nullptr;
+        APS_CUDA(c, cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+        c->ipc_mapped.push_back(p);
+        peer_set(c, q, static_cast<uint8_t *>(p) + host_offsets[q]);
+    }
+    peer_common(c);
+    return APS_OK;
+}
+
+aps_status aps_round_off_error(const float *h, const float *l, int64_t n, double *dev_sum,
+                               unsigned long long *dev_count, void *stream)
+{
+    if (n < 0 || (n > 0 && (!h || !l)) || !dev_sum || !dev_count) return APS_ERR_ARG;
+    return aps::launch_round_off(h, l, n, dev_sum, dev_count, static_cast<cudaStream_t>(stream)) == cudaSuccess
+               ? APS_OK : APS_ERR_CUDA;
+}
+
 aps_status aps_destroy(aps_ctx *c)
 {
     delete c;
@@ -810,12 +977,30 @@ static aps_status sim_check(aps_ctx *const *ctxs, int p)
     return APS_OK;
 }
 
+aps_status aps_sim_connect(aps_ctx *const *ctxs, int p)
+{
+    if (aps_status s = sim_check(ctxs, p)) return s;
+    for (int r = 0; r < p; ++r) {
+        for (int q = 0; q < p; ++q) peer_set(ctxs[r], q, ctxs[q]->ws);
+        peer_common(ctxs[r]);
+    }
+    return APS_OK;
+}
+
 aps_status aps_sim_layer_scales(aps_ctx *const *ctxs, int p, const float *const *grads)
 {
     if (aps_status s = sim_check(ctxs, p)) return s;
     if (!grads) return APS_ERR_ARG;
     for (int r = 0; r < p; ++r)
         if (aps_status s = aps_layer_scales(ctxs[r], grads + (size_t)r * ctxs[r]->n_layers)) return s;
+    if (ctxs[0]->peer) {  // every rank posted its E; now every rank collects
+        for (int r = 0; r < p; ++r) {
+            aps_ctx *c = ctxs[r];
+            APS_CUDA(c, aps::launch_peer_collect_E(c->pa, c->t.E_glob, c->n_layers, c->e_epoch, c->t.flag, c->stream));
+            c->phase = kScales;
+        }
+        return APS_OK;
+    }
     std::vector<int32_t *> dst(p);
     std::vector<const int32_t *> src(p);
     for (int r = 0; r < p; ++r) {
@@ -832,6 +1017,28 @@ aps_status aps_sim_allreduce(aps_ctx *const *ctxs, int p)
     if (aps_status s = sim_check(ctxs, p)) return s;
     for (int r = 0; r < p; ++r)
         if (ctxs[r]->phase != kPacked) return fail(ctxs[r], APS_ERR_STATE, "sim allreduce before quantize");
+    if (ctxs[0]->peer) {  // same kernels as aps_allreduce, phase by phase over the ranks
+        for (int r = 0; r < p; ++r) {
+            ++ctxs[r]->r_epoch;
+            APS_CUDA(ctxs[r], aps::launch_peer_signal(ctxs[r]->pa, aps::kSlotReady, ctxs[r]->r_epoch, ctxs[r]->stream));
+        }
+        for (int r = 0; r < p; ++r) {
+            aps_ctx *c = ctxs[r];
+            APS_CUDA(c, aps::launch_peer_wait(c->pa, aps::kSlotReady, c->r_epoch, c->t.flag, c->stream));
+            if (aps_status s = peer_reduce_own(c)) return s;
+        }
+        for (int r = 0; r < p; ++r)
+            APS_CUDA(ctxs[r], aps::launch_peer_signal(ctxs[r]->pa, aps::kSlotDone, ctxs[r]->r_epoch, ctxs[r]->stream));
+        for (int r = 0; r < p; ++r) {
+            APS_CUDA(ctxs[r], aps::launch_peer_wait(ctxs[r]->pa, aps::kSlotDone, ctxs[r]->r_epoch, ctxs[r]->t.flag,
+                                                    ctxs[r]->stream));
+            ctxs[r]->phase = kReduced;
+        }
+        return APS_OK;
+    }
+    for (int r = 0; r < p; ++r)
+        if (!flat_reduction(ctxs[r]))
+            return fail(ctxs[r], APS_ERR_STATE, "hierarchical order / accumulator variants need aps_sim_connect");
     aps_ctx *c0 = ctxs[0];
     const std::vector<int64_t> &cbyte = c0->chunk_byte;
     cudaStream_t st = c0->stream;

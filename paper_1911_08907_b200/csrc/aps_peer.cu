@@ -1,0 +1,410 @@
+// aps_peer.cu -- the all-reduce of Alg. 1 line 7 over PEER MEMORY
+// (NVLink / NVSwitch load-store through CUDA IPC mappings) instead of NCCL
+// send/recv, with any reduction order and accumulator:
+//
+//   * owner-computes: rank r reduces ring chunk r (tiles [r T'/p, (r+1) T'/p))
+//     by loading the p ranks' packed codes of the chunk directly (p-1 of them
+//     over NVLink), folding them in the order the reduction schedule fixes,
+//     and STORING the reduced codes into every rank's packed buffer (the
+//     all-gather, fused into the same pass).  NVLink bytes per rank equal the
+//     ring's: (p-1)/p of the packed buffer in, (p-1)/p out.  No partial sum
+//     ever travels, so the order of the additions is a free parameter:
+//       - flat ring (reading A14): chunk c accumulated over ranks c+1, ..., c;
+//       - hierarchical (reading A23): groups of k consecutive
+//         ranks; group chunk c1 = t / (T'/k) accumulated over members
+//         c1+1, ..., c1; master chunk c2 = t / (T'/G) over groups c2+1, ..., c2;
+//     and the accumulator may be wider than the wire format, or Kahan-
+//     compensated (CPD, reading A24) at no wire cost.
+//   * cross-rank synchronisation by monotone epoch flags in each rank's
+//     workspace, written remotely with st.release.sys after a system fence
+//     and polled locally with ld.acquire.sys; every wait is bounded (2 s
+//     watchdog -> flag bit 2 -> APS_ERR_STATE), so a missing peer cannot hang
+//     the GPU.
+//   * AllReduce(max_grad_exp, MAX) (Alg. 1 line 4) the same way: every
+//     rank stores its E vector into every rank's slot [rank] (double-buffered
+//     by epoch parity), flags, and each rank takes the max of the p slots.
+//
+// The same kernels serve p simulated ranks on one device (the "peer" pointers
+// are then the other contexts' workspaces): the parity tests drive them there.
+#include <cstdint>
+#include <climits>
+#include <algorithm>
+#include <cstring>
+
+#include "aps_device.cuh"
+#include "aps_peer.h"
+
+namespace aps {
+
+// ------------------------------------------------------------------ system-scope flag helpers
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t *p)
+{
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(uint32_t *p, uint32_t v)
+{
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// 16-byte peer load that bypasses L1 (the line may have been written by a
+// peer since this SM last saw it).
+__device__ __forceinline__ uint4 ld_peer16(const void *p)
+{
+    uint4 r;
+    asm volatile("ld.relaxed.sys.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p)
+                 : "memory");
+    return r;
+}
+__device__ __forceinline__ uint32_t ld_peer4(const void *p)
+{
+    uint32_t r;
+    asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(r) : "l"(p) : "memory");
+    return r;
+}
+
+__device__ __forceinline__ int32_t ld_relaxed_i32(const int32_t *p)
+{
+    int32_t v;
+    asm volatile("ld.relaxed.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// wait until flags[slot + q] >= epoch for every rank q (bounded)
+__device__ void wait_all(const PeerArgs &a, int slot, uint32_t epoch, uint32_t *err_flag)
+{
+    const uint32_t *f = a.flags[a.rank] + slot;
+    for (int q = 0; q < a.p; ++q)
+        spin_until([&] { return (int32_t)(ld_acquire_sys(f + q) - epoch) >= 0; }, err_flag);
+}
+
+// ------------------------------------------------------------------ AllReduce(E, MAX)
+// post: E_local -> slot [epoch & 1][rank] of every rank, then flag kSlotE.
+__global__ void peer_post_E_kernel(PeerArgs a, const int32_t *E_local, int n_layers, uint32_t epoch)
+{
+    const size_t par = (size_t)(epoch & 1u) * (size_t)a.p + (size_t)a.rank;
+    for (int q = 0; q < a.p; ++q) {
+        int32_t *dst = a.eslots[q] + par * (size_t)n_layers;
+        for (int l = threadIdx.x; l < n_layers; l += blockDim.x) dst[l] = E_local[l];
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int q = 0; q < a.p; ++q) st_release_sys(a.flags[q] + kSlotE + a.rank, epoch);
+}
+
+// collect: wait for every rank's post, E_glob = max over the slots.
+__global__ void peer_collect_E_kernel(PeerArgs a, int32_t *E_glob, int n_layers, uint32_t epoch, uint32_t *err_flag)
+{
+    if (threadIdx.x == 0) wait_all(a, kSlotE, epoch, err_flag);
+    __syncthreads();
+    const int32_t *base = a.eslots[a.rank] + (size_t)(epoch & 1u) * (size_t)a.p * (size_t)n_layers;
+    for (int l = threadIdx.x; l < n_layers; l += blockDim.x) {
+        int32_t mx = INT32_MIN;
+        for (int q = 0; q < a.p; ++q) mx = max(mx, ld_relaxed_i32(base + (size_t)q * n_layers + l));
+        E_glob[l] = mx;
+    }
+}
+
+// ------------------------------------------------------------------ signal / wait
+__global__ void peer_signal_kernel(PeerArgs a, int slot, uint32_t epoch)
+{
+    __threadfence_system();
+    for (int q = threadIdx.x; q < a.p; q += blockDim.x) st_release_sys(a.flags[q] + slot + a.rank, epoch);
+}
+
+__global__ void peer_wait_kernel(PeerArgs a, int slot, uint32_t epoch, uint32_t *err_flag)
+{
+    if (threadIdx.x == 0) wait_all(a, slot, epoch, err_flag);
+}
+
+// ------------------------------------------------------------------ the fold
+// Reduction schedule of one tile: rank of the j-th addend of group gi.
+struct Order {
+    int k, G, c1, c2;
+    __device__ __forceinline__ Order(const PeerArgs &a, int64_t t)
+    {
+        k = a.group_k;
+        G = a.p / a.group_k;
+        c1 = (int)(t / (a.tiles / k));
+        c2 = (int)(t / (a.tiles / G));
+    }
+    __device__ __forceinline__ int rank_of(int gi, int j) const
+    {
+        const int g = (c2 + 1 + gi) % G;
+        return g * k + (c1 + 1 + j) % k;
+    }
+};
+
+// Rounding of the accumulator.  EXT = false: the wire format itself (s <- Cast(fl32(s + x)),
+// reading A13); EXT = true: the accumulator format A, optionally Kahan-compensated
+// (reading A24).  Values are carried as fp32 (every format value is exact in fp32).
+template <class C, class A, bool EXT>
+__device__ __forceinline__ float rnd(const C &cw, const A &ca, float x)
+{
+    if constexpr (EXT) return ca.dec(ca.enc(x));
+    else return cw.dec(cw.enc(x));
+}
+
+template <class C, class A, bool EXT, bool KAHAN>
+__device__ __forceinline__ void fold_add(const C &cw, const A &ca, float &s, float &c, float x)
+{
+    if constexpr (KAHAN) {
+        const float y = rnd<C, A, EXT>(cw, ca, __fsub_rn(x, c));
+        const float t = rnd<C, A, EXT>(cw, ca, __fadd_rn(s, y));
+        c = rnd<C, A, EXT>(cw, ca, __fsub_rn(rnd<C, A, EXT>(cw, ca, __fsub_rn(t, s)), y));
+        s = t;
+    } else {
+        s = rnd<C, A, EXT>(cw, ca, __fadd_rn(s, x));
+    }
+}
+
+// ------------------------------------------------------------------ reduce, direct widths (b = 8, 16, 32)
+// One 16-byte vector (16 / 8 / 4 codes) per thread and iteration; all codes of
+// a vector share a tile, hence one reduction schedule.
+template <int B, class C, class A, bool EXT, bool KAHAN, int NT>
+__global__ void __launch_bounds__(NT) peer_reduce_direct_kernel(PeerArgs a, int64_t byte_off, int64_t tile0,
+                                                                int64_t n_vec, C cw, A ca)
+{
+    using W = typename Word4<B>::T;
+    constexpr int G4 = 16 / sizeof(W);  // 4-code groups per vector
+    constexpr int NC = 4 * G4;
+    constexpr int kBatch = 8;
+    for (int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x; i < n_vec; i += (int64_t)gridDim.x * NT) {
+        const int64_t off = byte_off + i * 16;
+        const Order o(a, tile0 + (i * 16) / (16 * B));
+        float S[NC], Sc[NC];
+        for (int gi = 0; gi < o.G; ++gi) {
+            float s[NC], c[NC];
+            for (int j0 = 0; j0 < o.k; j0 += kBatch) {
+                uint4 v[kBatch];
+                const int nb = min(kBatch, o.k - j0);
+#pragma unroll
+                for (int u = 0; u < kBatch; ++u)
+                    if (u < nb) v[u] = ld_peer16(a.packed[o.rank_of(gi, j0 + u)] + off);
+#pragma unroll
+                for (int u = 0; u < kBatch; ++u) {
+                    if (u >= nb) break;
+                    W w[G4];
+                    memcpy(w, &v[u], 16);
+#pragma unroll
+                    for (int g = 0; g < G4; ++g) {
+                        const float4 x = unpack4<B>(cw, w[g]);
+                        const float xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+                        for (int h = 0; h < 4; ++h) {
+                            const int n = 4 * g + h;
+                            if (j0 + u == 0) {
+                                s[n] = EXT ? rnd<C, A, EXT>(cw, ca, xs[h]) : xs[h];
+                                c[n] = 0.f;
+                            } else {
+                                fold_add<C, A, EXT, KAHAN>(cw, ca, s[n], c[n], xs[h]);
+                            }
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int n = 0; n < NC; ++n) {
+                if (gi == 0) {
+                    S[n] = s[n];
+                    Sc[n] = 0.f;
+                } else {
+                    fold_add<C, A, EXT, KAHAN>(cw, ca, S[n], Sc[n], s[n]);
+                }
+            }
+        }
+        W w[G4];
+#pragma unroll
+        for (int g = 0; g < G4; ++g) w[g] = pack4<B>(cw, make_float4(S[4 * g], S[4 * g + 1], S[4 * g + 2], S[4 * g + 3]));
+        uint4 r;
+        memcpy(&r, w, 16);
+        for (int q = 0; q < a.p; ++q) *reinterpret_cast<uint4 *>(a.packed[q] + off) = r;
+    }
+    __threadfence_system();
+}
+
+// ------------------------------------------------------------------ reduce, any width (per-warp tile)
+template <class C, class A, bool EXT, bool KAHAN, int NT>
+__global__ void __launch_bounds__(NT) peer_reduce_tile_kernel(PeerArgs a, int64_t byte_off, int64_t tile0,
+                                                              int64_t n_tiles, C cw, A ca)
+{
+    __shared__ __align__(16) uint32_t s_w[NT / 32][kTile + 1];
+    const int b = cw.b();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t *wa = s_w[warp];
+    const int64_t warps = (int64_t)gridDim.x * (NT / 32);
+    for (int64_t tt = blockIdx.x * (int64_t)(NT / 32) + warp; tt < n_tiles; tt += warps) {
+        const int64_t off = byte_off + tt * 16 * b;
+        const Order o(a, tile0 + tt);
+        float S[4], Sc[4], s[4], c[4];
+        for (int gi = 0; gi < o.G; ++gi) {
+            for (int j = 0; j < o.k; ++j) {
+                const uint8_t *src = a.packed[o.rank_of(gi, j)] + off;
+                __syncwarp();
+                for (int w = lane; w < 4 * b; w += 32) wa[w] = ld_peer4(src + 4 * w);
+                if (lane == 0) wa[4 * b] = 0u;
+                __syncwarp();
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    const float x = cw.dec(extract_code(wa, lane * 4 + h, b));
+                    if (j == 0) {
+                        s[h] = EXT ? rnd<C, A, EXT>(cw, ca, x) : x;
+                        c[h] = 0.f;
+                    } else {
+                        fold_add<C, A, EXT, KAHAN>(cw, ca, s[h], c[h], x);
+                    }
+                }
+            }
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                if (gi == 0) {
+                    S[h] = s[h];
+                    Sc[h] = 0.f;
+                } else {
+                    fold_add<C, A, EXT, KAHAN>(cw, ca, S[h], Sc[h], s[h]);
+                }
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int h = 0; h < 4; ++h) wa[lane * 4 + h] = cw.enc(S[h]);
+        __syncwarp();
+        for (int w = lane; w < 4 * b; w += 32) {
+            const uint32_t word = assemble_word(wa, w, b);
+            for (int q = 0; q < a.p; ++q) reinterpret_cast<uint32_t *>(a.packed[q] + off)[w] = word;
+        }
+    }
+    __threadfence_system();
+}
+
+// ------------------------------------------------------------------ launchers
+cudaError_t launch_peer_post_E(const PeerArgs &a, const int32_t *E_local, int n_layers, uint32_t epoch,
+                               cudaStream_t s)
+{
+    peer_post_E_kernel<<<1, 1024, 0, s>>>(a, E_local, n_layers, epoch);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_peer_collect_E(const PeerArgs &a, int32_t *E_glob, int n_layers, uint32_t epoch,
+                                  uint32_t *err_flag, cudaStream_t s)
+{
+    peer_collect_E_kernel<<<1, 1024, 0, s>>>(a, E_glob, n_layers, epoch, err_flag);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_peer_signal(const PeerArgs &a, int slot, uint32_t epoch, cudaStream_t s)
+{
+    peer_signal_kernel<<<1, 64, 0, s>>>(a, slot, epoch);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_peer_wait(const PeerArgs &a, int slot, uint32_t epoch, uint32_t *err_flag, cudaStream_t s)
+{
+    peer_wait_kernel<<<1, 32, 0, s>>>(a, slot, epoch, err_flag);
+    return cudaGetLastError();
+}
+
+template <class C, class A, bool EXT, bool KAHAN>
+static cudaError_t launch_reduce_t(const PeerArgs &a, int64_t byte_off, int64_t tile0, int64_t n_tiles, int b, C cw,
+                                   A ca, cudaStream_t s)
+{
+    const int64_t n_vec = n_tiles * b;  // a tile is 16 b bytes = b vectors
+    const int grid_direct = (int)std::min<int64_t>((n_vec + kThreads - 1) / kThreads, (int64_t)sm_count() * 8);
+    const int grid_tile =
+        (int)std::min<int64_t>((n_tiles + kThreads / 32 - 1) / (kThreads / 32), (int64_t)sm_count() * 8);
+    if constexpr (C::kB == 8 || C::kB == 16 || C::kB == 32) {
+        peer_reduce_direct_kernel<C::kB, C, A, EXT, KAHAN, kThreads><<<grid_direct, kThreads, 0, s>>>(
+            a, byte_off, tile0, n_vec, cw, ca);
+    } else if constexpr (C::kB == 0) {
+        if (b == 8)
+            peer_reduce_direct_kernel<8, C, A, EXT, KAHAN, kThreads><<<grid_direct, kThreads, 0, s>>>(a, byte_off, tile0,
+                                                                                                     n_vec, cw, ca);
+        else if (b == 16)
+            peer_reduce_direct_kernel<16, C, A, EXT, KAHAN, kThreads><<<grid_direct, kThreads, 0, s>>>(a, byte_off, tile0,
+                                                                                                      n_vec, cw, ca);
+        else if (b == 32)
+            peer_reduce_direct_kernel<32, C, A, EXT, KAHAN, kThreads><<<grid_direct, kThreads, 0, s>>>(a, byte_off, tile0,
+                                                                                                      n_vec, cw, ca);
+        else
+            peer_reduce_tile_kernel<C, A, EXT, KAHAN, kThreads><<<grid_tile, kThreads, 0, s>>>(a, byte_off, tile0,
+                                                                                              n_tiles, cw, ca);
+    } else {
+        peer_reduce_tile_kernel<C, A, EXT, KAHAN, kThreads><<<grid_tile, kThreads, 0, s>>>(a, byte_off, tile0, n_tiles,
+                                                                                          cw, ca);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_peer_reduce(const PeerArgs &a, int64_t byte_off, int64_t tile0, int64_t n_tiles, int e, int m,
+                               bool hw, int acc_e, int acc_m, bool kahan, cudaStream_t s)
+{
+    if (n_tiles <= 0) return cudaSuccess;
+    const int b = 1 + e + m;
+    const bool ext = kahan || acc_e != e || acc_m != m;
+    if (!ext)
+        return with_codec(e, m, hw, [&](auto cw) -> cudaError_t {
+            using C = decltype(cw);
+            return launch_reduce_t<C, C, false, false>(a, byte_off, tile0, n_tiles, b, cw, cw, s);
+        });
+    // accumulator variants (off the headline path): runtime wire codec (bit-identical
+    // to the specialised ones), binary32 or runtime accumulator codec
+    CRt cw;
+    cw.F = make_fmt(e, m);
+    if (acc_e == 8 && acc_m == 23) {  // binary32 accumulator: rounding is the identity
+        if (kahan) return launch_reduce_t<CRt, CF32, true, true>(a, byte_off, tile0, n_tiles, b, cw, CF32{}, s);
+        return launch_reduce_t<CRt, CF32, true, false>(a, byte_off, tile0, n_tiles, b, cw, CF32{}, s);
+    }
+    CRt ca;
+    ca.F = make_fmt(acc_e, acc_m);
+    if (kahan) return launch_reduce_t<CRt, CRt, true, true>(a, byte_off, tile0, n_tiles, b, cw, ca, s);
+    return launch_reduce_t<CRt, CRt, true, false>(a, byte_off, tile0, n_tiles, b, cw, ca, s);
+}
+
+// ------------------------------------------------------------------ Eq. (5) round-off metric
+// sum over i with h_i != 0 of |(h_i - l_i) / h_i| (binary64) and the count of such i.
+__global__ void round_off_kernel(const float *h, const float *l, int64_t n, double *sum, unsigned long long *cnt)
+{
+    double acc = 0.0;
+    unsigned long long c = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float hv = h[i];
+        if (hv != 0.f) {
+            acc += fabs(((double)hv - (double)l[i]) / (double)hv);
+            ++c;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        c += __shfl_xor_sync(0xffffffffu, c, o);
+    }
+    __shared__ double s_acc[32];
+    __shared__ unsigned long long s_c[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) {
+        s_acc[warp] = acc;
+        s_c[warp] = c;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+            acc += s_acc[w];
+            c += s_c[w];
+        }
+        atomicAdd(sum, acc);
+        atomicAdd(cnt, c);
+    }
+}
+
+cudaError_t launch_round_off(const float *h, const float *l, int64_t n, double *sum, unsigned long long *cnt,
+                             cudaStream_t s)
+{
+    if (n <= 0) return cudaSuccess;
+    const int grid = (int)std::min<int64_t>((n + 1023) / 1024, (int64_t)sm_count() * 4);
+    round_off_kernel<<<grid, 1024, 0, s>>>(h, l, n, sum, cnt);
+    return cudaGetLastError();
+}
+
+}  // namespace aps

@@ -1,0 +1,37 @@
+// aps_peer.h -- peer-memory transport (aps_peer.cu): host-side launchers and the
+// kernel argument block.  No device code.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace aps {
+
+constexpr int kMaxPeers = 64;  // ranks reachable by load/store (8 on one NVSwitch box; 64 simulated)
+
+// flag block of a rank's workspace: uint32 [kFlagWords], monotone epochs written by the peers
+constexpr int kSlotE = 0;                   // [q]: rank q posted its E vector for epoch
+constexpr int kSlotReady = kMaxPeers;       // [q]: rank q's packed codes of epoch are complete
+constexpr int kSlotDone = 2 * kMaxPeers;    // [q]: rank q stored its reduced chunk into every rank
+constexpr int kFlagWords = 3 * kMaxPeers;
+
+struct PeerArgs {
+    uint8_t *packed[kMaxPeers];   // every rank's packed buffer (own included), mapped into this process
+    uint32_t *flags[kMaxPeers];   // every rank's flag block
+    int32_t *eslots[kMaxPeers];   // every rank's E slots: int32 [2][kMaxPeers][n_layers]
+    int64_t tiles;                // T'
+    int p, rank, group_k;         // world, this rank, hierarchical group size (1 = flat ring)
+};
+
+cudaError_t launch_peer_post_E(const PeerArgs &a, const int32_t *E_local, int n_layers, uint32_t epoch,
+                               cudaStream_t s);
+cudaError_t launch_peer_collect_E(const PeerArgs &a, int32_t *E_glob, int n_layers, uint32_t epoch,
+                                  uint32_t *err_flag, cudaStream_t s);
+cudaError_t launch_peer_signal(const PeerArgs &a, int slot, uint32_t epoch, cudaStream_t s);
+cudaError_t launch_peer_wait(const PeerArgs &a, int slot, uint32_t epoch, uint32_t *err_flag, cudaStream_t s);
+// reduce n_tiles tiles of one format starting at tile0 / byte_off of the packed buffers
+cudaError_t launch_peer_reduce(const PeerArgs &a, int64_t byte_off, int64_t tile0, int64_t n_tiles, int e, int m,
+                               bool hw, int acc_e, int acc_m, bool kahan, cudaStream_t s);
+cudaError_t launch_round_off(const float *h, const float *l, int64_t n, double *sum, unsigned long long *cnt,
+                             cudaStream_t s);
+
+}  // namespace aps
