@@ -229,6 +229,8 @@ aps_status aps_set_reduction(aps_ctx *ctx, int group_k, int acc_exp_bits, int ac
  *                 allocation holding the workspace)
  *   host_offset : the workspace's byte offset in that allocation
  *   host_handles: [world_size * APS_PEER_HANDLE_BYTES], rank-major; host_offsets: [world_size]
+ * A context created with nccl_comm = NULL and world_size > 1 becomes a real
+ * rank of the peer transport here (no NCCL needed at all).
  * aps_destroy unmaps the peers (every rank must have finished its last sync). */
 #define APS_PEER_HANDLE_BYTES 64
 aps_status aps_peer_export(aps_ctx *ctx, void *host_handle, uint64_t *host_offset);

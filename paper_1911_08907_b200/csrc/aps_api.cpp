@@ -884,8 +884,7 @@ aps_status aps_peer_export(aps_ctx *c, void *host_handle, uint64_t *host_offset)
 {
     if (aps_status s = need_ws(c)) return s;
     if (!host_handle || !host_offset) return APS_ERR_ARG;
-    if (c->world < 2 || c->world > aps::kMaxPeers || c->sim)
-        return fail(c, APS_ERR_STATE, "peer transport needs 2..64 real ranks");
+    if (c->world < 2 || c->world > aps::kMaxPeers) return fail(c, APS_ERR_STATE, "peer transport needs 2..64 ranks");
     uint8_t *base = nullptr;
     APS_CUDA(c, alloc_base(c->ws, &base));
     cudaIpcMemHandle_t h;
@@ -902,8 +901,7 @@ aps_status aps_peer_import(aps_ctx *c, const void *host_handles, const uint64_t 
 {
     if (aps_status s = need_ws(c)) return s;
     if (!host_handles || !host_offsets) return APS_ERR_ARG;
-    if (c->world < 2 || c->world > aps::kMaxPeers || c->sim)
-        return fail(c, APS_ERR_STATE, "peer transport needs 2..64 real ranks");
+    if (c->world < 2 || c->world > aps::kMaxPeers) return fail(c, APS_ERR_STATE, "peer transport needs 2..64 ranks");
     if (c->peer) return fail(c, APS_ERR_STATE, "peers already imported");
     for (int q = 0; q < c->world; ++q) {
         if (q == c->rank) {
@@ -918,6 +916,7 @@ aps_status aps_peer_import(aps_ctx *c, const void *host_handles, const uint64_t 
         peer_set(c, q, static_cast<uint8_t *>(p) + host_offsets[q]);
     }
     peer_common(c);
+    c->sim = false;  // a rank created without a communicator is now a real rank of the peer transport
     return APS_OK;
 }
 

@@ -1,0 +1,85 @@
+"""The peer transport across PROCESSES: two ranks, each its own process and
+CUDA context, exchange CUDA IPC handles of their workspaces over a gloo
+group (aps_peer_export / aps_peer_import), then run aps_sync with no NCCL at
+all -- the code path a multi-GPU run takes, except that both processes share
+one B200 (kernels of two contexts time-slice, so the epoch-flag waits cross a
+context switch).  Results bit-exact against the oracle.  Needs a B200."""
+import multiprocessing as mp
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import synthetic
+
+pytestmark = pytest.mark.gpu
+
+NUMELS = synthetic.C1_NUMELS + [1000, 1, 130]
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, group_k, iters, q):
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        import torch
+        import torch.distributed as dist
+        import paper_1911_08907_b200 as aps
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        ctx = aps.ApsContext(5, 2, NUMELS, world_size=world, rank=rank)
+        ctx.connect_peers()
+        ctx.set_reduction(group_k)
+        outs = []
+        for it in range(iters):
+            grads = synthetic.make_grads(NUMELS, world, seed=synthetic.SEED + it)
+            dev = [torch.from_numpy(a).cuda() for a in grads[rank]]
+            ctx.sync(dev, average=True)
+            st = ctx.status_sync()
+            outs.append((st, ctx.scales(), ctx.packed().cpu().numpy().copy(), [t.cpu().numpy() for t in dev]))
+        dist.barrier()           # nobody unmaps a workspace a peer may still touch
+        ctx.close()
+        dist.destroy_process_group()
+        q.put((rank, outs))
+    except Exception as exc:      # pragma: no cover - reported to the parent
+        q.put((rank, repr(exc)))
+
+
+@pytest.mark.parametrize("world,group_k", [(2, 1), (4, 2)])
+def test_peer_transport_two_processes(orc, world, group_k):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    iters = 2
+    procs = [ctx.Process(target=_worker, args=(r, world, port, group_k, iters, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = {}
+    try:
+        for _ in range(world):
+            rank, res = q.get(timeout=240)
+            results[rank] = res
+    finally:
+        for p in procs:
+            p.join(timeout=30)
+            if p.is_alive():
+                p.kill()
+    for r in range(world):
+        assert not isinstance(results[r], str), results[r]
+    for it in range(iters):
+        grads = synthetic.make_grads(NUMELS, world, seed=synthetic.SEED + it)
+        ref = orc.aps_sync_ex(grads, 5, 2, average=1, group_k=group_k)
+        for r in range(world):
+            st, ft, packed, outs = results[r][it]
+            assert st == 0
+            assert np.array_equal(ft, ref.ftilde)
+            assert np.array_equal(packed, ref.reduced)
+            for a, b in zip(outs, ref.out):
+                assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
