@@ -50,6 +50,14 @@ def parse():
     ap.add_argument("--phase-steps", type=int, default=0, help="steps of the per-phase breakdown (0: max(20, K/4))")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--transport", default="auto", choices=["auto", "nccl", "peer"],
+                    help="N > 1: NCCL send/recv ring, or the peer-memory (CUDA IPC / NVLink) owner-computes "
+                         "kernel; auto = peer, falling back to the NCCL ring if the IPC mapping fails")
+    ap.add_argument("--group-k", type=int, default=1,
+                    help="hierarchical all-reduce group size (P:509-541; needs --transport peer when != 1, N)")
+    ap.add_argument("--acc", default=None, help="accumulator format e,m (CPD, P:660-678; needs --transport peer)")
+    ap.add_argument("--kahan", action="store_true", help="Kahan-compensated accumulation (needs --transport peer)")
+    ap.add_argument("--no-peer-sim", action="store_true", help="skip the simulated p = 8 peer all-reduce phase")
     return ap.parse_args()
 
 
@@ -230,16 +238,30 @@ def main():
     world, rank, local = dist_env()
     if args.gpus > 1 and world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} needs torchrun with {args.gpus} processes (WORLD_SIZE={world})")
+    # APS_BENCH_SAME_GPU=1 (plumbing check only, no valid numbers): every rank on cuda:0,
+    # a gloo group, no NCCL communicator, the peer transport across processes
+    same_gpu = os.environ.get("APS_BENCH_SAME_GPU") == "1" and world > 1
+    if same_gpu:
+        local = 0
+        args.transport = "peer"
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     comm = None
     if world > 1:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=dev)
-        uid = [aps.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        comm = aps.nccl_comm_init(uid[0], world, rank)
+        if same_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+            uid = [aps.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            comm = aps.nccl_comm_init(uid[0], world, rank)
+
+    def max_over_ranks(x: float) -> float:
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if same_gpu else dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
     e, m = map(int, args.format.split(","))
     b = 1 + e + m
@@ -255,6 +277,20 @@ def main():
     code_bytes = sum(n * (1 + f[0] + f[1]) for n, f in zip(numels, fmts)) / 8 if fmts else L * b / 8
     ctx = aps.ApsContext(e, m, numels, world_size=world, rank=rank, nccl_comm=comm, stream=stream,
                          device=dev, hw_convert=not args.no_hw, formats=fmts)
+    acc = tuple(map(int, args.acc.split(","))) if args.acc else None
+    transport = args.transport
+    if world > 1 and transport in ("auto", "peer"):
+        try:
+            ctx.connect_peers()
+            transport = "peer"
+        except Exception as exc:
+            if transport == "peer":
+                raise
+            print(f"[bench] peer transport unavailable ({exc}); using the NCCL ring", file=sys.stderr)
+            transport = "nccl"
+    args.transport = transport
+    if world > 1:
+        ctx.set_reduction(args.group_k, acc, args.kahan)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     flush_rd = torch.zeros(256 << 20, dtype=torch.uint8, device=dev)
 
@@ -301,9 +337,7 @@ def main():
     step_ms = [events[k][0].elapsed_time(events[k][1]) for k in range(K)]
     total_ms = sum(step_ms)
     if world > 1:
-        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+        total_ms = max_over_ranks(total_ms)
     ms_per_step = total_ms / K
     value = world * 4 * L / (ms_per_step * 1e-3) / 1e9
 
@@ -343,6 +377,54 @@ def main():
     torch.cuda.synchronize()
     rr_ms = rr[0].elapsed_time(rr[1]) / 50
 
+    # -------- the peer-memory all-reduce on one device: p = 8 simulated ranks of the
+    # workload (each rank's reduce reads the 8 ranks' codes of its chunk and stores the
+    # reduced chunk into all 8 buffers: 2 x packed bytes per rank, all in local HBM here)
+    peer_sim = None
+    if not args.no_peer_sim and world == 1 and not fmts:
+        P8 = 8
+        ss = torch.cuda.Stream(dev)     # graph capture needs a non-default stream
+        sim = [aps.ApsContext(e, m, numels, world_size=P8, rank=r, stream=ss, device=dev,
+                              hw_convert=not args.no_hw) for r in range(P8)]
+        aps.sim_connect(sim)
+        sgr = [[torch.from_numpy(synthetic.layer_grad(r, l, n)).to(dev) for l, n in enumerate(numels)]
+               for r in range(P8)]
+        torch.cuda.synchronize()
+        aps.sim_layer_scales(sim, sgr)
+        for r in range(P8):
+            sim[r].quantize_pack(sgr[r])
+        for _ in range(2):
+            aps.sim_allreduce(sim)
+            for r in range(P8):
+                sim[r].quantize_pack(sgr[r])
+        torch.cuda.synchronize()
+        pg = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(pg, stream=ss):
+            aps.sim_allreduce(sim)
+        pg.replay()
+        torch.cuda.synchronize()
+        pe = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        reps = 20
+        with torch.cuda.stream(ss):
+            pe[0].record(ss)
+            for _ in range(reps):
+                pg.replay()
+            pe[1].record(ss)
+        torch.cuda.synchronize()
+        ps_ms = pe[0].elapsed_time(pe[1]) / reps
+        _, pb = aps.layout(P8, e, m, numels)
+        ps_bytes = P8 * 2 * pb
+        peer_sim = {"us": round(ps_ms * 1e3, 2), "algorithmic_bytes": int(ps_bytes),
+                    "GB/s": round(ps_bytes / (ps_ms * 1e-3) / 1e9, 1),
+                    "frac": round(ps_bytes / (ps_ms * 1e-3) / 1e9 / peaks()[0], 4),
+                    "note": "aps_sim_allreduce of 8 simulated ranks through the peer transport on one "
+                            "device (CUDA-graph replay): 8 owner-computes reduce kernels (each loads the "
+                            "8 ranks' codes of its chunk, folds in ring order, stores into all 8 buffers) "
+                            "+ epoch-flag signal/wait kernels; every byte is local HBM here"}
+        for c in sim:
+            c.close()
+        del sgr
+
     # -------- roofline of the dominant kernel (algorithmic bytes / launch time)
     T, packed_bytes = aps.layout_mixed(world, numels, fmts) if fmts else aps.layout(world, e, m, numels)
     kern = {
@@ -367,6 +449,8 @@ def main():
                                      "GB/s": round(rr_bytes / (rr_ms * 1e-3) / 1e9, 1),
                                      "frac": round(rr_bytes / (rr_ms * 1e-3) / 1e9 / peak, 4),
                                      "note": "one reduce-scatter step's kernel for a p = 8 chunk (CUDA-graph replay of 50 launches)"}
+    if peer_sim:
+        phases["peer_allreduce_p8_sim"] = peer_sim
     if world == 1:
         # one fused launch per step: FindMaxExp read (4 B) + Cast read (4 B) + codes (b/8 B) + fp32 out (4 B)
         kname = ("stream_kernel<FusedP1Op>" if os.environ.get("APS_ENGINE") in ("tma", "stream")
@@ -409,9 +493,7 @@ def main():
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / E
     if world > 1:
-        t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+        e2e_ms = max_over_ranks(e2e_ms)
     e2e = {"value": round(world * 4 * L / (e2e_ms * 1e-3) / 1e9, 3), "unit": UNIT,
            "h2d_bytes_per_step": 4 * L, "d2h_bytes_per_step": 4 * L, "ms_per_step": round(e2e_ms, 4),
            "api": "aps_sync_host"}
@@ -419,6 +501,9 @@ def main():
     G = len(set(fmts)) if fmts else 1  # one quantise / unscale / fused launch per format group
     if world == 1:
         launches_per_step = G
+    elif args.transport == "peer":  # absmax, post+collect E, G quantise, 2 x (signal, wait), own-chunk runs, G unscale
+        runs = format_runs(numels, fmts or [(e, m)] * len(numels), world, (rank + 2) % world)[0]
+        launches_per_step = 1 + 2 + 2 * G + 4 + runs
     else:  # absmax + G quantise + per ring step one reduce launch per format run of the chunk + G unscale
         launches_per_step = 1 + 2 * G + sum(format_runs(numels, fmts or [(e, m)] * len(numels), world, rank))
     result = {
@@ -435,7 +520,12 @@ def main():
         "e2e": e2e, "clocks": clk.summary(),
     }
     if world > 1:
-        result["config"]["ring"] = "ncclSend/ncclRecv reduce-scatter + ncclAllGather, int32 MAX all-reduce"
+        result["config"]["ring"] = (
+            "peer memory (CUDA IPC over NVLink): owner-computes reduce + fused all-gather, E max over peer memory"
+            if args.transport == "peer" else
+            "ncclSend/ncclRecv reduce-scatter + ncclAllGather, int32 MAX all-reduce")
+        result["config"]["reduction"] = {"group_k": args.group_k, "acc": args.acc or f"{e},{m}",
+                                         "kahan": bool(args.kahan)}
     if rank == 0:
         if not args.no_cpu_baseline and world == 1:
             v, desc, t = cpu_oracle_run(numels, e, m, 1, budget_s=20.0)

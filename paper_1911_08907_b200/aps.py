@@ -299,9 +299,15 @@ class ApsContext:
         """Map every rank's workspace (CUDA IPC) and switch the all-reduce to the
         peer-memory transport.  Collective over the torch.distributed group."""
         import torch.distributed as dist
-        mine = self.peer_export()
+        try:
+            mine = self.peer_export()
+        except ApsError as exc:
+            mine = str(exc)
         allv = [None] * self.world_size
         dist.all_gather_object(allv, mine, group=group)
+        bad = [r for r, v in enumerate(allv) if not isinstance(v, tuple)]
+        if bad:  # every rank takes the same decision: nobody maps anything
+            raise ApsError(APS_ERR_STATE, f"aps_peer_export failed on ranks {bad}: {allv[bad[0]]}")
         self.peer_import([h for h, _ in allv], [o for _, o in allv])
         dist.barrier(group=group)
 

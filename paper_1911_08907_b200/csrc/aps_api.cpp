@@ -279,6 +279,10 @@ static aps_status init_common(aps_ctx **out, const int *e_arr, const int *m_arr,
     }
     const int64_t T = toff;
     c->tiles = (T + world_size - 1) / world_size * world_size;
+    if (c->tiles > INT32_MAX) {  // tile indices are 32-bit on the device
+        delete c;
+        return APS_ERR_ARG;
+    }
     const int64_t tb_last = 16 * (int64_t)(1 + c->le[n_layers - 1] + c->lm[n_layers - 1]);
     c->packed_bytes = boff + (c->tiles - T) * tb_last;  // padding tiles continue the last layer's format
     c->chunk_bytes = c->packed_bytes / world_size;     // (uniform formats)

@@ -47,22 +47,31 @@ __device__ __forceinline__ void st_release_sys(uint32_t *p, uint32_t v)
 {
     asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-// 16-byte peer load that bypasses L1 (the line may have been written by a
-// peer since this SM last saw it).
+// Peer loads: weak, L1-bypassing.  The codes were published before this kernel
+// started (the preceding wait kernel acquired every rank's ready flag at system
+// scope, and stream order carries that into this kernel); nothing else writes
+// them while this kernel runs (only the owner of a chunk reads or writes it).
 __device__ __forceinline__ uint4 ld_peer16(const void *p)
 {
     uint4 r;
-    asm volatile("ld.relaxed.sys.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+    asm volatile("ld.global.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
                  : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                 : "l"(p)
-                 : "memory");
+                 : "l"(p));
     return r;
 }
 __device__ __forceinline__ uint32_t ld_peer4(const void *p)
 {
     uint32_t r;
-    asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(r) : "l"(p) : "memory");
+    asm volatile("ld.global.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
     return r;
+}
+// end of a reduce CTA: its remote stores are made visible system-wide once
+// (bar.sync orders the CTA's stores before thread 0's fence; the signal kernel
+// that follows fences again before it raises the done flag)
+__device__ __forceinline__ void cta_fence_system()
+{
+    __syncthreads();
+    if (threadIdx.x == 0) __threadfence_system();
 }
 
 __device__ __forceinline__ int32_t ld_relaxed_i32(const int32_t *p)
@@ -89,10 +98,11 @@ __global__ void peer_post_E_kernel(PeerArgs a, const int32_t *E_local, int n_lay
         int32_t *dst = a.eslots[q] + par * (size_t)n_layers;
         for (int l = threadIdx.x; l < n_layers; l += blockDim.x) dst[l] = E_local[l];
     }
-    __threadfence_system();
-    __syncthreads();
-    if (threadIdx.x == 0)
+    __syncthreads();  // the CTA's stores precede thread 0's fence and releases (cumulativity)
+    if (threadIdx.x == 0) {
+        __threadfence_system();
         for (int q = 0; q < a.p; ++q) st_release_sys(a.flags[q] + kSlotE + a.rank, epoch);
+    }
 }
 
 // collect: wait for every rank's post, E_glob = max over the slots.
@@ -111,7 +121,8 @@ __global__ void peer_collect_E_kernel(PeerArgs a, int32_t *E_glob, int n_layers,
 // ------------------------------------------------------------------ signal / wait
 __global__ void peer_signal_kernel(PeerArgs a, int slot, uint32_t epoch)
 {
-    __threadfence_system();
+    if (threadIdx.x == 0) __threadfence_system();
+    __syncthreads();
     for (int q = threadIdx.x; q < a.p; q += blockDim.x) st_release_sys(a.flags[q] + slot + a.rank, epoch);
 }
 
@@ -128,13 +139,17 @@ struct Order {
     {
         k = a.group_k;
         G = a.p / a.group_k;
-        c1 = (int)(t / (a.tiles / k));
-        c2 = (int)(t / (a.tiles / G));
+        // T' < 2^31 tiles (aps_init); 32-bit divisions
+        c1 = (int)((uint32_t)t / (uint32_t)(a.tiles / k));
+        c2 = (int)((uint32_t)t / (uint32_t)(a.tiles / G));
     }
     __device__ __forceinline__ int rank_of(int gi, int j) const
     {
-        const int g = (c2 + 1 + gi) % G;
-        return g * k + (c1 + 1 + j) % k;
+        int g = c2 + 1 + gi;  // < 2G: one conditional subtraction is the mod
+        g = g >= G ? g - G : g;
+        int u = c1 + 1 + j;
+        u = u >= k ? u - k : u;
+        return g * k + u;
     }
 };
 
@@ -161,6 +176,89 @@ __device__ __forceinline__ void fold_add(const C &cw, const A &ca, float &s, flo
     }
 }
 
+// ------------------------------------------------------------------ fp8 fold in binary16 pairs
+// For the hardware fp8 codecs (5,2) / (4,3) with the wire-format accumulator the
+// fold runs on f16x2: dec = cvt.rn.f16x2.{e5m2,e4m3}x2 (exact: every fp8 value is a
+// binary16), add = add.rn.f16x2, re-quantise = cvt.rn.satfinite.{e5m2,e4m3}x2.f16x2.
+// Cast(fl16(a + b)) == Cast(fl32(a + b)) == the exactly rounded sum: binary16
+// carries p' = 11 >= 2p + 1 significant bits (p = 3 / 4) in every binade the
+// fp8 formats reach, including their subnormals (binary16's ulp there is 2^-24),
+// so the double rounding is innocuous (Figueroa), and APS partial sums stay
+// <= 1.5 * 2^bias < 65504 (no binary16 overflow) and below the satfinite clamp
+// (reading A12).  Exhaustively checked on the device against the oracle
+// (tests/test_gpu_peer.py::test_peer_fp8_all_code_pairs).
+template <bool E4M3>
+__device__ __forceinline__ __half2 fp8x2_to_h2(uint32_t two)
+{
+    uint32_t h2;
+    if (E4M3) asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h2) : "h"((uint16_t)two));
+    else asm("cvt.rn.f16x2.e5m2x2 %0, %1;" : "=r"(h2) : "h"((uint16_t)two));
+    return *reinterpret_cast<__half2 *>(&h2);
+}
+template <bool E4M3>
+__device__ __forceinline__ uint32_t h2_to_fp8x2(__half2 h)
+{
+    uint16_t d;
+    const uint32_t v = *reinterpret_cast<uint32_t *>(&h);
+    if (E4M3) asm("cvt.rn.satfinite.e4m3x2.f16x2 %0, %1;" : "=h"(d) : "r"(v));
+    else asm("cvt.rn.satfinite.e5m2x2.f16x2 %0, %1;" : "=h"(d) : "r"(v));
+    return d;
+}
+
+template <bool E4M3, int NT>
+__global__ void __launch_bounds__(NT) peer_reduce_fp8h_kernel(PeerArgs a, int64_t byte_off, int64_t tile0,
+                                                              int64_t n_vec)
+{
+    constexpr int kBatch = 8;
+    for (int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x; i < n_vec; i += (int64_t)gridDim.x * NT) {
+        const int64_t off = byte_off + i * 16;
+        const Order o(a, tile0 + i / 8);  // a tile is 128 bytes = 8 vectors
+        __half2 S[8], s[8];               // 16 codes as 8 pairs
+        int gi = 0, j = 0;
+        for (int idx0 = 0; idx0 < a.p; idx0 += kBatch) {
+            uint4 v[kBatch];
+            const int nb = min(kBatch, a.p - idx0);
+            {
+                int g2 = gi, j2 = j;
+#pragma unroll
+                for (int u = 0; u < kBatch; ++u) {
+                    if (u < nb) v[u] = ld_peer16(a.packed[o.rank_of(g2, j2)] + off);
+                    if (++j2 == o.k) {
+                        j2 = 0;
+                        ++g2;
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kBatch; ++u) {
+                if (u >= nb) break;
+                const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const __half2 x = fp8x2_to_h2<E4M3>((q & 1) ? (w[q >> 1] >> 16) : (w[q >> 1] & 0xffffu));
+                    s[q] = (j == 0) ? x : fp8x2_to_h2<E4M3>(h2_to_fp8x2<E4M3>(__hadd2(s[q], x)));
+                }
+                if (j == o.k - 1) {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        S[q] = (gi == 0) ? s[q] : fp8x2_to_h2<E4M3>(h2_to_fp8x2<E4M3>(__hadd2(S[q], s[q])));
+                    j = 0;
+                    ++gi;
+                } else {
+                    ++j;
+                }
+            }
+        }
+        uint4 r;
+        r.x = h2_to_fp8x2<E4M3>(S[0]) | (h2_to_fp8x2<E4M3>(S[1]) << 16);
+        r.y = h2_to_fp8x2<E4M3>(S[2]) | (h2_to_fp8x2<E4M3>(S[3]) << 16);
+        r.z = h2_to_fp8x2<E4M3>(S[4]) | (h2_to_fp8x2<E4M3>(S[5]) << 16);
+        r.w = h2_to_fp8x2<E4M3>(S[6]) | (h2_to_fp8x2<E4M3>(S[7]) << 16);
+        for (int q = 0; q < a.p; ++q) *reinterpret_cast<uint4 *>(a.packed[q] + off) = r;
+    }
+    cta_fence_system();
+}
+
 // ------------------------------------------------------------------ reduce, direct widths (b = 8, 16, 32)
 // One 16-byte vector (16 / 8 / 4 codes) per thread and iteration; all codes of
 // a vector share a tile, hence one reduction schedule.
@@ -175,44 +273,58 @@ __global__ void __launch_bounds__(NT) peer_reduce_direct_kernel(PeerArgs a, int6
     for (int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x; i < n_vec; i += (int64_t)gridDim.x * NT) {
         const int64_t off = byte_off + i * 16;
         const Order o(a, tile0 + (i * 16) / (16 * B));
-        float S[NC], Sc[NC];
-        for (int gi = 0; gi < o.G; ++gi) {
-            float s[NC], c[NC];
-            for (int j0 = 0; j0 < o.k; j0 += kBatch) {
-                uint4 v[kBatch];
-                const int nb = min(kBatch, o.k - j0);
-#pragma unroll
-                for (int u = 0; u < kBatch; ++u)
-                    if (u < nb) v[u] = ld_peer16(a.packed[o.rank_of(gi, j0 + u)] + off);
+        // the p addends in fold order (group gi = idx / k, member j = idx % k), loaded
+        // kBatch at a time so that many peer loads are in flight per thread
+        float S[NC], Sc[NC], s[NC], c[NC];
+        int gi = 0, j = 0;
+        for (int idx0 = 0; idx0 < a.p; idx0 += kBatch) {
+            uint4 v[kBatch];
+            const int nb = min(kBatch, a.p - idx0);
+            {
+                int g2 = gi, j2 = j;
 #pragma unroll
                 for (int u = 0; u < kBatch; ++u) {
-                    if (u >= nb) break;
-                    W w[G4];
-                    memcpy(w, &v[u], 16);
-#pragma unroll
-                    for (int g = 0; g < G4; ++g) {
-                        const float4 x = unpack4<B>(cw, w[g]);
-                        const float xs[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-                        for (int h = 0; h < 4; ++h) {
-                            const int n = 4 * g + h;
-                            if (j0 + u == 0) {
-                                s[n] = EXT ? rnd<C, A, EXT>(cw, ca, xs[h]) : xs[h];
-                                c[n] = 0.f;
-                            } else {
-                                fold_add<C, A, EXT, KAHAN>(cw, ca, s[n], c[n], xs[h]);
-                            }
-                        }
+                    if (u < nb) v[u] = ld_peer16(a.packed[o.rank_of(g2, j2)] + off);
+                    if (++j2 == o.k) {
+                        j2 = 0;
+                        ++g2;
                     }
                 }
             }
 #pragma unroll
-            for (int n = 0; n < NC; ++n) {
-                if (gi == 0) {
-                    S[n] = s[n];
-                    Sc[n] = 0.f;
+            for (int u = 0; u < kBatch; ++u) {
+                if (u >= nb) break;
+                W w[G4];
+                memcpy(w, &v[u], 16);
+#pragma unroll
+                for (int g = 0; g < G4; ++g) {
+                    const float4 x = unpack4<B>(cw, w[g]);
+                    const float xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {
+                        const int n = 4 * g + h;
+                        if (j == 0) {
+                            s[n] = EXT ? rnd<C, A, EXT>(cw, ca, xs[h]) : xs[h];
+                            c[n] = 0.f;
+                        } else {
+                            fold_add<C, A, EXT, KAHAN>(cw, ca, s[n], c[n], xs[h]);
+                        }
+                    }
+                }
+                if (j == o.k - 1) {  // group complete: fold its sum into the masters' sum
+#pragma unroll
+                    for (int n = 0; n < NC; ++n) {
+                        if (gi == 0) {
+                            S[n] = s[n];
+                            Sc[n] = 0.f;
+                        } else {
+                            fold_add<C, A, EXT, KAHAN>(cw, ca, S[n], Sc[n], s[n]);
+                        }
+                    }
+                    j = 0;
+                    ++gi;
                 } else {
-                    fold_add<C, A, EXT, KAHAN>(cw, ca, S[n], Sc[n], s[n]);
+                    ++j;
                 }
             }
         }
@@ -223,7 +335,7 @@ __global__ void __launch_bounds__(NT) peer_reduce_direct_kernel(PeerArgs a, int6
         memcpy(&r, w, 16);
         for (int q = 0; q < a.p; ++q) *reinterpret_cast<uint4 *>(a.packed[q] + off) = r;
     }
-    __threadfence_system();
+    cta_fence_system();
 }
 
 // ------------------------------------------------------------------ reduce, any width (per-warp tile)
@@ -277,7 +389,7 @@ __global__ void __launch_bounds__(NT) peer_reduce_tile_kernel(PeerArgs a, int64_
             for (int q = 0; q < a.p; ++q) reinterpret_cast<uint32_t *>(a.packed[q] + off)[w] = word;
         }
     }
-    __threadfence_system();
+    cta_fence_system();
 }
 
 // ------------------------------------------------------------------ launchers
@@ -312,7 +424,9 @@ static cudaError_t launch_reduce_t(const PeerArgs &a, int64_t byte_off, int64_t 
                                    A ca, cudaStream_t s)
 {
     const int64_t n_vec = n_tiles * b;  // a tile is 16 b bytes = b vectors
-    const int grid_direct = (int)std::min<int64_t>((n_vec + kThreads - 1) / kThreads, (int64_t)sm_count() * 8);
+    // one resident wave (2 CTAs of 256 threads per SM at ~96 registers): every CTA
+    // pays its closing system fence once
+    const int grid_direct = (int)std::min<int64_t>((n_vec + kThreads - 1) / kThreads, (int64_t)sm_count() * 2);
     const int grid_tile =
         (int)std::min<int64_t>((n_tiles + kThreads / 32 - 1) / (kThreads / 32), (int64_t)sm_count() * 8);
     if constexpr (C::kB == 8 || C::kB == 16 || C::kB == 32) {
@@ -344,6 +458,13 @@ cudaError_t launch_peer_reduce(const PeerArgs &a, int64_t byte_off, int64_t tile
     if (n_tiles <= 0) return cudaSuccess;
     const int b = 1 + e + m;
     const bool ext = kahan || acc_e != e || acc_m != m;
+    if (!ext && hw && ((e == 5 && m == 2) || (e == 4 && m == 3))) {
+        const int64_t n_vec = n_tiles * 8;
+        const int grid = (int)std::min<int64_t>((n_vec + kThreads - 1) / kThreads, (int64_t)sm_count() * 2);
+        if (e == 5) peer_reduce_fp8h_kernel<false, kThreads><<<grid, kThreads, 0, s>>>(a, byte_off, tile0, n_vec);
+        else peer_reduce_fp8h_kernel<true, kThreads><<<grid, kThreads, 0, s>>>(a, byte_off, tile0, n_vec);
+        return cudaGetLastError();
+    }
     if (!ext)
         return with_codec(e, m, hw, [&](auto cw) -> cudaError_t {
             using C = decltype(cw);

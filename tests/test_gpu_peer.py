@@ -194,3 +194,20 @@ def test_round_off_error_device(aps, orc):
     ref, rcnt = orc.round_off_error(h, l_)
     assert cnt == rcnt
     assert abs(err - ref) <= 1e-12 * ref
+
+
+@pytest.mark.parametrize("fmt,amax", [((5, 2), 2.0 ** 14), ((4, 3), 2.0 ** 6)], ids=["e5m2", "e4m3"])
+def test_peer_fp8_all_code_pairs(aps, orc, fmt, amax):
+    """Every pair of finite codes with |value| <= 2^(bias-1) through the binary16
+    fold of the hardware fp8 path (p = 2, f~ = 0 so the codes are the values):
+    rank 0 holds value a, rank 1 value b, for all (a, b)."""
+    e, m = fmt
+    codes = np.arange(256, dtype=np.uint32)
+    vals = orc.decode(codes, e, m)
+    vals = vals[np.isfinite(vals) & (np.abs(vals) <= amax)]
+    a = np.repeat(vals, vals.size).astype(np.float32)
+    b = np.tile(vals, vals.size).astype(np.float32)
+    grads = [[a], [b]]
+    ref = orc.aps_sync(grads, e, m, average=0)
+    assert ref.ftilde[0] == 0
+    compare(run_peer(aps, grads, e, m, True, average=0), ref)
