@@ -12,7 +12,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
-LIB = PKG / "libaps.so"
+LIB = Path(os.environ.get("APS_BUILD_OUT", PKG / "libaps.so"))  # APS_BUILD_OUT / APS_NVCC_EXTRA: A/B variants
 SOURCES = [CSRC / "aps_kernels.cu", CSRC / "aps_stream.cu", CSRC / "aps_peer.cu", CSRC / "aps_api.cpp"]
 HEADERS = [CSRC / "aps_numerics.cuh", CSRC / "aps_device.cuh", CSRC / "aps_internal.h", CSRC / "aps_peer.h",
            ROOT / "include" / "aps.h"]
@@ -34,10 +34,11 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     objdir = PKG / "build"
     objdir.mkdir(exist_ok=True)
     common = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
-              "-Xptxas", "-v" if verbose else "-O3", f"-I{ROOT / 'include'}", f"-I{inc}"]
+              "-Xptxas", "-v" if verbose else "-O3", f"-I{ROOT / 'include'}", f"-I{inc}",
+              *os.environ.get("APS_NVCC_EXTRA", "").split()]
 
     def compile_one(src: Path):
-        obj = objdir / (src.name + f".{os.getpid()}.o")
+        obj = objdir / (src.name + f".{os.getpid()}.{LIB.stem}.o")
         return obj, subprocess.run(common + ["-c", str(src), "-o", str(obj)], capture_output=True, text=True)
 
     with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:

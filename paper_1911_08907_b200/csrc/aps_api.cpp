@@ -556,6 +556,20 @@ aps_status aps_set_hw_convert(aps_ctx *c, int enable)
     return APS_OK;
 }
 
+// a1 kernel of the separate-call path: "ranges" (default: 4-item ranges with an L2
+// evict_last hint and a done counter) or "plain" (APS_ABSMAX=plain: one streaming CTA per
+// item + a finisher kernel).  Measured (profiles/r01_ab_absmax_plain_vs_ranges.txt): plain
+// 24.2 us vs 23.8 us, and without the evict_last hint the quantise pass loses its L2 hits
+// (21.1 us vs 17.1 us).
+static bool absmax_plain()
+{
+    static const bool v = [] {
+        const char *e = std::getenv("APS_ABSMAX");
+        return e && !std::strcmp(e, "plain");
+    }();
+    return v;
+}
+
 aps_status aps_layer_scales(aps_ctx *c, const float *const *grads)
 {
     if (aps_status s = need_ws(c)) return s;
@@ -568,6 +582,8 @@ aps_status aps_layer_scales(aps_ctx *c, const float *const *grads)
         APS_CUDA(c, aps::launch_stream_absmax(c->t, c->world, c->gen, tgt, c->stream));
         c->done_target = tgt;
         ++c->gen;
+    } else if (c->engine == aps_ctx::kLdg && absmax_plain()) {
+        APS_CUDA(c, aps::launch_absmax_plain(c->t, c->world, c->stream));
     } else if (c->engine == aps_ctx::kLdg) {
         const uint32_t tgt = c->done_target + (uint32_t)aps::absmax_ranges_grid(c->t.n_items);
         APS_CUDA(c, aps::launch_absmax_ranges(c->t, c->world, tgt, c->stream));

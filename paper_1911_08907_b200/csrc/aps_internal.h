@@ -68,6 +68,8 @@ cudaError_t launch_absmax_exp(const DevTables &t, int world, cudaStream_t s);
 // a1 over ranges of kAbsItemsPerCta items, one done-count per CTA (target = done counter after the call)
 int absmax_ranges_grid(int n_items);
 cudaError_t launch_absmax_ranges(const DevTables &t, int world, uint32_t target, cudaStream_t s);
+// a1 as one streaming kernel (red.max per CTA, no counters) + a one-CTA finisher
+cudaError_t launch_absmax_plain(const DevTables &t, int world, cudaStream_t s);
 cudaError_t launch_quant_pack(const DevTables &t, int e, int m, bool hw, cudaStream_t s);
 cudaError_t launch_unpack_unscale(const DevTables &t, int e, int m, bool hw, int world, int average,
                                   cudaStream_t s);

@@ -66,6 +66,50 @@ __global__ void __launch_bounds__(NT) absmax_exp_kernel(DevTables t, int N)
     }
 }
 
+// a1 as a pure streaming pass: one CTA per work item, one fire-and-forget
+// red.max per CTA into the layer's accumulator, no fence and no completion
+// counter; the kernel boundary orders the maxima before absmax_finish_kernel
+// turns them into E_l = ceil(log2(N * A_l)) and clears the accumulators.
+template <int NT>
+__global__ void __launch_bounds__(NT) absmax_plain_kernel(DevTables t)
+{
+    const Item it = t.items[blockIdx.x];
+    const float *g = t.src[it.layer] + (int64_t)it.tile_begin * kTile;
+    const float4 *g4 = reinterpret_cast<const float4 *>(g);
+    constexpr int kPer = kItemTiles * kTile / 4 / NT;
+    uint32_t mx = 0;
+    if (it.cnt == kItemTiles * kTile) {
+        float4 v[kPer];
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) v[j] = ld_stream4(g4 + threadIdx.x + j * NT);
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) mx = max(mx, absbits4(v[j]));
+    } else {
+        const int n4 = it.cnt >> 2;
+        for (int j = threadIdx.x; j < n4; j += NT) mx = max(mx, absbits4(ld_stream4(g4 + j)));
+        if ((int)threadIdx.x < (it.cnt & 3)) mx = max(mx, __float_as_uint(g[4 * n4 + threadIdx.x]) & 0x7fffffffu);
+    }
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    __shared__ uint32_t s_max[NT / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) s_max[warp] = mx;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t v = lane < NT / 32 ? s_max[lane] : 0u;
+        v = __reduce_max_sync(0xffffffffu, v);
+        if (lane == 0 && v)
+            asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(&t.amax[it.layer]), "r"(v) : "memory");
+    }
+}
+
+__global__ void absmax_finish_kernel(DevTables t, int N)
+{
+    for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < t.n_layers; l += gridDim.x * blockDim.x) {
+        t.E_local[l] = exponent_of(t.amax[l], N);
+        t.amax[l] = 0u;
+    }
+}
+
 // direct widths 8/16/32: group of 4 fp32 -> one 4-code word group
 // a1 for the separate-call path (N > 1): each CTA takes kAbsItemsPerCta
 // consecutive work items (mostly one layer), keeps a per-warp running max,
@@ -74,7 +118,10 @@ __global__ void __launch_bounds__(NT) absmax_exp_kernel(DevTables t, int N)
 // accumulators into E_l = ceil(log2(N * A_l)) and clears them.  Compared with
 // one CTA per item and a fence per CTA, the fence latency is paid 4x less
 // often and the block scheduler still balances the load.
-constexpr int kAbsItemsPerCta = 4;
+#ifndef APS_ABS_ITEMS
+#define APS_ABS_ITEMS 4
+#endif
+constexpr int kAbsItemsPerCta = APS_ABS_ITEMS;
 
 __device__ __forceinline__ float4 ld_keep4(const float4 *p, uint64_t pol)
 {
@@ -647,6 +694,14 @@ cudaError_t launch_absmax_exp(const DevTables &t, int world, cudaStream_t s)
 }
 
 int absmax_ranges_grid(int n_items) { return (n_items + kAbsItemsPerCta - 1) / kAbsItemsPerCta; }
+
+cudaError_t launch_absmax_plain(const DevTables &t, int world, cudaStream_t s)
+{
+    if (t.n_items == 0) return cudaSuccess;
+    absmax_plain_kernel<kThreads><<<t.n_items, kThreads, 0, s>>>(t);
+    absmax_finish_kernel<<<(t.n_layers + 255) / 256, 256, 0, s>>>(t, world);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_absmax_ranges(const DevTables &t, int world, uint32_t target, cudaStream_t s)
 {
