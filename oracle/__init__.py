@@ -88,6 +88,7 @@ def lib():
         L.oracle_reduce1.restype = u32
         L.oracle_round_off_error.argtypes = [vp, vp, i64, vp]
         L.oracle_round_off_error.restype = ctypes.c_double
+        L.oracle_census.argtypes = [vp, i64, i32, ci, ci, vp, vp]
         _lib = L
     return _lib
 
@@ -285,3 +286,13 @@ def round_off_error(grad_h, grad_l):
     cnt = ctypes.c_int64(0)
     err = lib().oracle_round_off_error(_ptr(h), _ptr(l_), h.size, ctypes.byref(cnt))
     return err, cnt.value
+
+
+def census(g, s: int, e: int, m: int) -> tuple[int, int]:
+    """(underflow, overflow) counts of Cast(g * 2^s) over nonzero finite g (NEXT-4)."""
+    x = np.ascontiguousarray(g, dtype=np.float32)
+    u, o = ctypes.c_int64(0), ctypes.c_int64(0)
+    rc = lib().oracle_census(_ptr(x), x.size, s, e, m, ctypes.byref(u), ctypes.byref(o))
+    if rc:
+        raise ValueError(f"oracle_census rc={rc}")
+    return u.value, o.value

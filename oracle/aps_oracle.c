@@ -669,3 +669,32 @@ double oracle_round_off_error(const float *h, const float *l, int64_t n, int64_t
     if (count_out) *count_out = cnt;
     return cnt ? sum / (double)cnt : 0.0;
 }
+
+/* ------------------------------------------------------------------ */
+/* Underflow / overflow census (section 3.1 "The   */
+/* limitation of the loss scaling algorithm" P:173-179, Fig.           */
+/* `aps_comparing` P:277-280: "scale all gradients by 2^-5 ... Although */
+/* it can avoid overflow, it will cause some small values to underflow, */
+/* which will be cast to 0"; section 3.3.2 the underflow/overflow       */
+/* trade-off).  For a tensor g and a scale exponent s (APS: f~_l; loss  */
+/* scaling: one constant for every layer; no scaling: 0), count the     */
+/* nonzero finite elements whose Cast(g * 2^s) is +-0 (underflow) and   */
+/* those whose Cast is +-Inf (overflow).                                */
+/* ------------------------------------------------------------------ */
+int oracle_census(const float *g, int64_t n, int32_t s, int e, int m, int64_t *underflow, int64_t *overflow)
+{
+    if (oracle_format_valid(e, m)) return OR_ERR_FORMAT;
+    if (n < 0 || (n > 0 && !g) || !underflow || !overflow) return OR_ERR_ARG;
+    const uint32_t mag_mask = (uint32_t)((1ull << (e + m)) - 1ull);
+    const uint32_t inf_mag = ((1u << e) - 1u) << m;
+    int64_t u = 0, o = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        if (g[i] == 0.0f || !isfinite(g[i])) continue;
+        const uint32_t c = oracle_cast1(oracle_scale(g[i], s), e, m) & mag_mask;
+        if (c == 0u) ++u;
+        else if (c == inf_mag) ++o;
+    }
+    *underflow = u;
+    *overflow = o;
+    return OR_OK;
+}

@@ -281,3 +281,46 @@ def test_round_off_error_hierarchy_beats_ring(orc):
     hier = orc.aps_sync_ex(g, 5, 2, average=1, group_k=4).out[0]
     assert orc.round_off_error(h, ring)[0] == 0.5
     assert orc.round_off_error(h, hier)[0] == 0.0
+
+
+# ---------------------------------------------------------------- underflow / overflow census (NEXT-4)
+
+def test_census_fig_aps_comparing(orc):
+    """Fig. `aps_comparing`, (5,2): a "green" layer with max 2^20 and a
+    "blue" layer whose values sit near 2^-12.  No scaling: 2^20 > 61440 overflows
+    (Inf).  Loss scaling by 2^-5 (the paper's constant): 2^20 -> 2^15 fits,
+    but 2^-12 -> 2^-17 is the tie between 0 and 2^-16 and rounds to 0 (underflow,
+    "smaller than 2^-16 ... cast to 0").  APS (N = 1): the green layer gets
+    f~ = 15 - 20 = -5, the blue one (max 2^5 -> E = 5) f~ = 10: nothing lost."""
+    green = np.array([2.0 ** 20, 1.0], np.float32)
+    blue = np.array([2.0 ** 5, 2.0 ** -12, -(2.0 ** -12)], np.float32)
+    assert orc.census(green, 0, 5, 2) == (0, 1)
+    assert orc.census(blue, 0, 5, 2) == (0, 0)          # 2^-12 is a (5,2) subnormal: kept
+    assert orc.census(green, -5, 5, 2) == (0, 0)
+    assert orc.census(blue, -5, 5, 2) == (2, 0)
+    fg = orc.scale_exp(5, orc.find_max_exp(green, 1))
+    fb = orc.scale_exp(5, orc.find_max_exp(blue, 1))
+    assert (fg, fb) == (-5, 10)
+    assert orc.census(green, fg, 5, 2) == (0, 0) and orc.census(blue, fb, 5, 2) == (0, 0)
+
+
+def test_census_thresholds(orc):
+    """Exact thresholds from O6 (A10/A11): (5,2) 2^-17 -> 0 (tie to even code 0),
+    nextafter(2^-17, inf) -> 2^-16; 61440 -> Inf (tie), 61439.99 -> 57344;
+    zeros and non-finite inputs are not counted."""
+    x = np.array([2.0 ** -17, np.nextafter(np.float32(2.0 ** -17), np.float32(1)), 61440.0, 61439.99,
+                  0.0, -0.0, np.inf, np.nan, -(2.0 ** -17), -61440.0], np.float32)
+    assert orc.census(x, 0, 5, 2) == (2, 2)
+
+
+def test_census_aps_never_overflows(orc):
+    """Eq. (1)-(4): with f~ from FindMaxExp the cast never overflows, for any N
+    (section 3.3.2: APS trades the overflow side away completely)."""
+    rng = np.random.default_rng([synthetic.SEED, 33])
+    for (e, m) in [(5, 2), (4, 3), (3, 0), (5, 10)]:
+        for N in (1, 2, 8, 256):
+            g = (rng.standard_normal(5000) * 2.0 ** rng.integers(-40, 40)).astype(np.float32)
+            f = orc.scale_exp(e, orc.find_max_exp(g, N))
+            assert orc.census(g, f, e, m)[1] == 0
+            # A * 2^f~ > 2^(bias-1) / N (maximality): log2(N) + 2 binades more and the max overflows
+            assert orc.census(g, f + 2 + int(np.log2(N)), e, m)[1] > 0
