@@ -236,6 +236,17 @@ aps_status aps_set_reduction(aps_ctx *ctx, int group_k, int acc_exp_bits, int ac
 aps_status aps_peer_export(aps_ctx *ctx, void *host_handle, uint64_t *host_offset);
 aps_status aps_peer_import(aps_ctx *ctx, const void *host_handles, const uint64_t *host_offsets);
 
+/* [sync] Underflow / overflow census (the loss-scaling
+ * comparison of section 3.1 P:173-179 and Fig. `aps_comparing` P:277-280:
+ * "it will cause some small values to underflow, which will be cast to 0").
+ * For every layer l, counts the nonzero finite elements g of grads[l] whose
+ * Cast(g * 2^s_l) (this context's format, IEEE overflow) is +-0 (underflow,
+ * host_counts[2 l]) or +-Inf (overflow, host_counts[2 l + 1]).
+ *   host_scale_exp: [n_layers] s_l -- APS: aps_get_scales' f~; constant loss
+ *   scaling: the same exponent for every layer; no scaling: 0.
+ * Needs one format for every layer. */
+aps_status aps_census(aps_ctx *ctx, const float *const *grads, const int32_t *host_scale_exp, uint64_t *host_counts);
+
 /* Eq. (5) `equation:round_off_error`, reading A25: adds
  * sum over i with h[i] != 0 of |(h[i] - l[i]) / h[i]| (binary64) to *dev_sum and
  * the number of such i to *dev_count (device scalars the caller zeroes);

@@ -29,7 +29,7 @@ EXPORTS = [
     "aps_nccl_comm_init", "aps_nccl_comm_destroy", "aps_sim_layer_scales", "aps_sim_allreduce",
     "aps_debug_cast", "aps_debug_decode", "aps_debug_ring_reduce", "aps_debug_timeline",
     "aps_init_mixed", "aps_layout_mixed", "aps_set_reduction", "aps_peer_export", "aps_peer_import",
-    "aps_sim_connect", "aps_round_off_error",
+    "aps_sim_connect", "aps_round_off_error", "aps_census",
 ]
 PEER_HANDLE_BYTES = 64
 
@@ -91,6 +91,7 @@ def load(path: Path | str | None = None):
         "aps_peer_import": ([vp, vp, vp], i32),
         "aps_sim_connect": ([vp, i32], i32),
         "aps_round_off_error": ([vp, vp, i64, vp, vp, vp], i32),
+        "aps_census": ([vp, vp, vp, vp], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -282,6 +283,17 @@ class ApsContext:
         wire = self.formats[0] if self.formats is not None else (self.exp_bits, self.man_bits)
         ae, am = acc if acc is not None else wire
         self._check(self.L.aps_set_reduction(self.h, group_k, ae, am, int(kahan)), "aps_set_reduction")
+
+    def census(self, grads, scale_exp):
+        """Underflow / overflow counts [n_layers, 2] of Cast(g * 2^s_l) (aps_census);
+        scale_exp: one exponent per layer, or one int for every layer."""
+        import numpy as np
+        if isinstance(scale_exp, int):
+            scale_exp = [scale_exp] * len(self.numels)
+        se = np.ascontiguousarray(scale_exp, dtype=np.int32)
+        out = np.zeros((len(self.numels), 2), dtype=np.uint64)
+        self._check(self.L.aps_census(self.h, self._ptrs(grads), se.ctypes.data, out.ctypes.data), "aps_census")
+        return out
 
     # -------------------------------------------------------------- peer transport
     def peer_export(self) -> tuple[bytes, int]:

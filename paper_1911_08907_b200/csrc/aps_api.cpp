@@ -97,7 +97,7 @@ struct aps_ctx {
     aps::PeerArgs pa{};
     uint32_t e_epoch = 0, r_epoch = 0;  // AllReduce(E, MAX) calls / all-reduce calls so far
     std::vector<void *> ipc_mapped;     // cudaIpcOpenMemHandle mappings (closed by aps_destroy)
-    size_t off_pflags = 0, off_eslots = 0;
+    size_t off_pflags = 0, off_eslots = 0, off_census = 0;
     std::string err;
     ~aps_ctx()
     {
@@ -367,6 +367,7 @@ static aps_status init_common(aps_ctx **out, const int *e_arr, const int *m_arr,
     // peer transport: flag block and E slots [2][world][n_layers] (world > 1 only)
     c->off_pflags = o; o = align_up(o + (world_size > 1 ? 4 * (size_t)aps::kFlagWords : 0));
     c->off_eslots = o; o = align_up(o + (world_size > 1 ? 2 * 4 * (size_t)world_size * (size_t)n_layers : 0));
+    c->off_census = o; o = align_up(o + align_up(4 * (size_t)n_layers) + 16 * (size_t)n_layers);  // exps + [2] u64 counts
     c->acc_e = c->e;
     c->acc_m = c->m;
 
@@ -937,6 +938,23 @@ aps_status aps_peer_import(aps_ctx *c, const void *host_handles, const uint64_t 
     }
     peer_common(c);
     c->sim = false;  // a rank created without a communicator is now a real rank of the peer transport
+    return APS_OK;
+}
+
+aps_status aps_census(aps_ctx *c, const float *const *grads, const int32_t *host_scale_exp, uint64_t *host_counts)
+{
+    if (aps_status s = need_ws(c)) return s;
+    if (!grads || !host_scale_exp || !host_counts) return fail(c, APS_ERR_ARG, "NULL argument");
+    if (!c->uniform) return fail(c, APS_ERR_ARG, "aps_census needs one format for every layer");
+    if (aps_status s = upload_ptrs<const float *>(c, c->src_cache, grads, c->off_src)) return s;
+    int32_t *dexp = reinterpret_cast<int32_t *>(c->ws + c->off_census);
+    unsigned long long *dcnt =
+        reinterpret_cast<unsigned long long *>(c->ws + c->off_census + align_up(4 * (size_t)c->n_layers));
+    APS_CUDA(c, cudaMemcpyAsync(dexp, host_scale_exp, 4 * (size_t)c->n_layers, cudaMemcpyHostToDevice, c->stream));
+    APS_CUDA(c, cudaMemsetAsync(dcnt, 0, 16 * (size_t)c->n_layers, c->stream));
+    APS_CUDA(c, aps::launch_census(c->t, dexp, dcnt, c->e, c->m, c->stream));
+    APS_CUDA(c, cudaMemcpyAsync(host_counts, dcnt, 16 * (size_t)c->n_layers, cudaMemcpyDeviceToHost, c->stream));
+    APS_CUDA(c, cudaStreamSynchronize(c->stream));
     return APS_OK;
 }
 

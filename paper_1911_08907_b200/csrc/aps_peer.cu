@@ -519,6 +519,42 @@ __global__ void round_off_kernel(const float *h, const float *l, int64_t n, doub
     }
 }
 
+// ------------------------------------------------------------------ underflow / overflow census
+// One CTA per work item: counts the nonzero finite elements whose Cast(g * 2^s_l)
+// (generic codec: IEEE overflow to Inf, never the saturating hardware converter)
+// is +-0 (underflow) or +-Inf (overflow); counts[2 l], counts[2 l + 1].
+template <int NT>
+__global__ void __launch_bounds__(NT) census_kernel(DevTables t, const int32_t *sexp, unsigned long long *counts,
+                                                    Fmt F)
+{
+    const Item it = t.items[blockIdx.x];
+    const float *g = t.src[it.layer] + (int64_t)it.tile_begin * kTile;
+    const Pow2 sc(sexp[it.layer]);
+    const uint32_t inf_mag = F.inf_code;
+    unsigned long long u = 0, o = 0;
+    for (int i = threadIdx.x; i < it.cnt; i += NT) {
+        const float x = g[i];
+        if (x == 0.f || !isfinite(x)) continue;
+        const uint32_t mag = encode(F, sc.apply(x)) & F.mag_mask;
+        u += (mag == 0u);
+        o += (mag == inf_mag);
+    }
+    u = __reduce_add_sync(0xffffffffu, (uint32_t)u);
+    o = __reduce_add_sync(0xffffffffu, (uint32_t)o);
+    if ((threadIdx.x & 31) == 0) {
+        if (u) atomicAdd(&counts[2 * it.layer], u);
+        if (o) atomicAdd(&counts[2 * it.layer + 1], o);
+    }
+}
+
+cudaError_t launch_census(const DevTables &t, const int32_t *sexp, unsigned long long *counts, int e, int m,
+                          cudaStream_t s)
+{
+    if (t.n_items == 0) return cudaSuccess;
+    census_kernel<kThreads><<<t.n_items, kThreads, 0, s>>>(t, sexp, counts, make_fmt(e, m));
+    return cudaGetLastError();
+}
+
 cudaError_t launch_round_off(const float *h, const float *l, int64_t n, double *sum, unsigned long long *cnt,
                              cudaStream_t s)
 {

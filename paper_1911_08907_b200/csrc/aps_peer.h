@@ -31,6 +31,9 @@ cudaError_t launch_peer_wait(const PeerArgs &a, int slot, uint32_t epoch, uint32
 // reduce n_tiles tiles of one format starting at tile0 / byte_off of the packed buffers
 cudaError_t launch_peer_reduce(const PeerArgs &a, int64_t byte_off, int64_t tile0, int64_t n_tiles, int e, int m,
                                bool hw, int acc_e, int acc_m, bool kahan, cudaStream_t s);
+struct DevTables;
+cudaError_t launch_census(const DevTables &t, const int32_t *sexp, unsigned long long *counts, int e, int m,
+                          cudaStream_t s);
 cudaError_t launch_round_off(const float *h, const float *l, int64_t n, double *sum, unsigned long long *cnt,
                              cudaStream_t s);
 
