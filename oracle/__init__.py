@@ -83,7 +83,13 @@ def lib():
         L.oracle_packed_bytes_mixed.restype = i64
         L.oracle_aps_sync_mixed.argtypes = [ctypes.c_int, vp, vp, ctypes.c_int, vp, vp, ctypes.c_int, vp, vp, vp, vp]
         ci = ctypes.c_int
-        L.oracle_aps_sync_ex.argtypes = [ci, ci, ci, ci, vp, vp, ci, ci, ci, ci, ci, vp, vp, vp, vp]
+        u64 = ctypes.c_uint64
+        L.oracle_aps_sync_ex.argtypes = [ci, ci, ci, ci, vp, vp, ci, ci, ci, ci, ci, ci, u64, vp, vp, vp, vp]
+        L.oracle_splitmix64.argtypes = [u64, u64]
+        L.oracle_splitmix64.restype = u64
+        L.oracle_cast_sr1.argtypes = [f32, ci, ci, u32]
+        L.oracle_cast_sr1.restype = u32
+        L.oracle_cast_sr.argtypes = [vp, vp, i64, ci, ci, u64, u64]
         L.oracle_reduce1.argtypes = [vp, ci, i64, i64, ci, ci, ci, ci, ci, ci]
         L.oracle_reduce1.restype = u32
         L.oracle_round_off_error.argtypes = [vp, vp, i64, vp]
@@ -249,7 +255,7 @@ def aps_sync_mixed(grads, fmts, average: int = 1, want_packed: bool = True) -> S
 
 
 def aps_sync_ex(grads, e: int, m: int, average: int = 1, group_k: int = 1, acc=None, kahan: int = 0,
-                want_packed: bool = True) -> SyncResult:
+                want_packed: bool = True, sr: int = 0, seed: int = 0) -> SyncResult:
     """APS sync with a reduction order and accumulator:
     ``group_k`` = hierarchical group size (1 or p: the flat ring, reading A23),
     ``acc`` = accumulator format (default: the wire format), ``kahan`` =
@@ -266,7 +272,8 @@ def aps_sync_ex(grads, e: int, m: int, average: int = 1, group_k: int = 1, acc=N
     reduced = np.zeros(nbytes, dtype=np.uint8)
     outs = [np.empty(int(n), dtype=np.float32) for n in numels]
     optrs = (ctypes.c_void_p * nl)(*[a.ctypes.data for a in outs])
-    rc = lib().oracle_aps_sync_ex(p, e, m, nl, _ptr(numels), gptrs, average, group_k, ae, am, kahan, _ptr(ft),
+    rc = lib().oracle_aps_sync_ex(p, e, m, nl, _ptr(numels), gptrs, average, group_k, ae, am, kahan, sr, seed,
+                                  _ptr(ft),
                                   _ptr(packed) if want_packed else None, _ptr(reduced), optrs)
     return SyncResult(rc, ft, packed, reduced, outs)
 
@@ -296,3 +303,22 @@ def census(g, s: int, e: int, m: int) -> tuple[int, int]:
     if rc:
         raise ValueError(f"oracle_census rc={rc}")
     return u.value, o.value
+
+
+def splitmix64(seed: int, ctr: int) -> int:
+    return lib().oracle_splitmix64(seed, ctr)
+
+
+def cast_sr1(x: float, e: int, m: int, r: int) -> int:
+    """Stochastic-rounding Cast of one fp32 with the 32-bit random number r (reading A26)."""
+    return lib().oracle_cast_sr1(x, e, m, r)
+
+
+def cast_sr(x, e: int, m: int, seed: int, phase: int = 0) -> np.ndarray:
+    """Stochastic-rounding Cast with r_i = SplitMix64(seed, phase << 40 | i) >> 32."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    out = np.empty(x.shape, dtype=np.uint32)
+    rc = lib().oracle_cast_sr(_ptr(x), _ptr(out), x.size, e, m, seed, phase)
+    if rc:
+        raise ValueError(f"oracle_cast_sr rc={rc}")
+    return out

@@ -517,6 +517,62 @@ int oracle_aps_sync_mixed(int p, const int *e, const int *m, int n_layers, const
 }
 
 /* ------------------------------------------------------------------ */
+/* Stochastic rounding ("some          */
+/* researchers prefer stochastic rounding ... which can get an         */
+/* unbiased estimate for high precision values").  Reading A26: x     */
+/* between its representable neighbours lo <= |x| < hi rounds to hi   */
+/* with probability (|x| - lo) / (hi - lo), decided by a 32-bit       */
+/* random number r: up iff r < (|x| - lo) / (hi - lo) * 2^32 (exact   */
+/* comparison in binary64).  r comes from the counter-based generator */
+/* SplitMix64 (Steele, Lea, Flood 2014): output = mix(seed + (ctr+1) * */
+/* 0x9E3779B97F4A7C15), r = output >> 32, keyed by ctr = phase << 40 | */
+/* i (i = the element's code index in the packed layout; phase r for  */
+/* rank r's Cast, p - 1 + a for the a-th add of the element's fold),  */
+/* so results do not depend on thread order.                          */
+/* ------------------------------------------------------------------ */
+uint64_t oracle_splitmix64(uint64_t seed, uint64_t ctr)
+{
+    uint64_t z = seed + (ctr + 1u) * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+static uint32_t sr_rand(uint64_t seed, uint64_t phase, int64_t i)
+{
+    return (uint32_t)(oracle_splitmix64(seed, (phase << 40) | (uint64_t)i) >> 32);
+}
+
+uint32_t oracle_cast_sr1(float x, int e, int m, uint32_t r)
+{
+    const int bias = oracle_bias(e);
+    const uint32_t sbit = (signbit(x) ? 1u : 0u) << (e + m);
+    const uint32_t inf_code = sbit | (((1u << e) - 1u) << m);
+    if (isnan(x) || isinf(x)) return oracle_cast1(x, e, m);
+    const double a = fabs((double)x);
+    if (a == 0.0) return sbit;
+    if (a >= ldexp(1.0, bias + 1)) return inf_code;
+    int k;
+    (void)frexp(a, &k);
+    k -= 1;
+    const int qexp = ((k > 1 - bias) ? k : (1 - bias)) - m;
+    const double quantum = ldexp(1.0, qexp);
+    const double lo = floor(a / quantum) * quantum;
+    const double hi = lo + quantum;                   /* 2^(bias+1) stands for Inf */
+    if (a == lo) return sbit | encode_magnitude(lo, e, m);
+    const double frac = (a - lo) / quantum;           /* exact: quantum is a power of two */
+    const int up = (double)r < frac * 4294967296.0;
+    return sbit | encode_magnitude(up ? hi : lo, e, m);
+}
+
+int oracle_cast_sr(const float *x, uint32_t *codes, int64_t n, int e, int m, uint64_t seed, uint64_t phase)
+{
+    if (oracle_format_valid(e, m)) return OR_ERR_FORMAT;
+    for (int64_t i = 0; i < n; ++i) codes[i] = oracle_cast_sr1(x[i], e, m, sr_rand(seed, phase, i));
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------ */
 /* Reduction order and accumulator.    */
 /*                                                                     */
 /* NEXT-3, hierarchical all-reduce: "partition the nodes   */
@@ -566,6 +622,33 @@ static float oracle_fold(const float *x, int n, int ae, int am, int kahan)
 
 /* One element's all-reduce: q[r] = rank r's wire code of the element
  * (r = 0..p-1), t = its tile, Tp = T'.  Returns the reduced wire code. */
+/* The same element's all-reduce with stochastic rounding after every add
+ * (wire-format accumulator, no compensation; reading A26): the a-th add of
+ * the fold (a = 1..p-1, in fold order across groups) draws phase p - 1 + a. */
+static uint32_t reduce1_sr(const uint32_t *q, int p, int64_t i, int64_t Tp, int group_k, int e, int m, uint64_t seed)
+{
+    const int k = group_k, G = p / group_k;
+    const int64_t t = i / OR_TILE, c1 = t / (Tp / k), c2 = t / (Tp / G);
+    int a = 0;
+    float S = 0.0f;
+    for (int gi = 0; gi < G; ++gi) {
+        const int g = (int)((c2 + 1 + gi) % G);
+        float s = oracle_decode1(q[g * k + (int)((c1 + 1) % k)], e, m);
+        for (int j = 1; j < k; ++j) {
+            const float x = oracle_decode1(q[g * k + (int)((c1 + 1 + j) % k)], e, m);
+            ++a;
+            s = oracle_decode1(oracle_cast_sr1(s + x, e, m, sr_rand(seed, (uint64_t)(p - 1 + a), i)), e, m);
+        }
+        if (gi == 0) {
+            S = s;
+        } else {
+            ++a;
+            S = oracle_decode1(oracle_cast_sr1(S + s, e, m, sr_rand(seed, (uint64_t)(p - 1 + a), i)), e, m);
+        }
+    }
+    return oracle_cast1(S, e, m); /* S is a wire value: exact */
+}
+
 uint32_t oracle_reduce1(const uint32_t *q, int p, int64_t t, int64_t Tp, int group_k, int e, int m,
                         int ae, int am, int kahan)
 {
@@ -586,12 +669,13 @@ uint32_t oracle_reduce1(const uint32_t *q, int p, int64_t t, int64_t Tp, int gro
  * compensation.  group_k = 1 (or p), (ae, am) = (e, m), kahan = 0 is
  * oracle_aps_sync. */
 int oracle_aps_sync_ex(int p, int e, int m, int n_layers, const int64_t *numels, const float *const *grads,
-                       int average, int group_k, int ae, int am, int kahan, int32_t *ftilde_out,
-                       uint8_t *packed_out, uint8_t *reduced_out, float *const *out)
+                       int average, int group_k, int ae, int am, int kahan, int sr, uint64_t seed,
+                       int32_t *ftilde_out, uint8_t *packed_out, uint8_t *reduced_out, float *const *out)
 {
     if (oracle_format_valid(e, m) || oracle_format_valid(ae, am)) return OR_ERR_FORMAT;
     if (p < 1 || p > 256 || n_layers < 1 || !numels || !grads) return OR_ERR_ARG;
     if (group_k < 1 || group_k > p || p % group_k) return OR_ERR_ARG;
+    if (sr && (kahan || ae != e || am != m)) return OR_ERR_ARG; /* A26: SR with the wire accumulator only */
     for (int l = 0; l < n_layers; ++l)
         if (numels[l] < 1) return OR_ERR_ARG;
     const int b = 1 + e + m;
@@ -619,8 +703,11 @@ int oracle_aps_sync_ex(int p, int e, int m, int n_layers, const int64_t *numels,
         int64_t off = 0;
         for (int l = 0; l < n_layers; ++l) {
             const float *g = grads[(size_t)r * n_layers + l];
-            for (int64_t i = 0; i < numels[l]; ++i)
-                q[(size_t)r * ncodes + off + i] = oracle_cast1(oracle_scale(g[i], ft[l]), e, m);
+            for (int64_t i = 0; i < numels[l]; ++i) {
+                const float y = oracle_scale(g[i], ft[l]);
+                q[(size_t)r * ncodes + off + i] =
+                    sr ? oracle_cast_sr1(y, e, m, sr_rand(seed, (uint64_t)r, off + i)) : oracle_cast1(y, e, m);
+            }
             off += OR_TILE * ((numels[l] + OR_TILE - 1) / OR_TILE);
         }
         if (packed_out) {
@@ -634,7 +721,8 @@ int oracle_aps_sync_ex(int p, int e, int m, int n_layers, const int64_t *numels,
     uint32_t col[256];
     for (int64_t i = 0; i < ncodes; ++i) {
         for (int r = 0; r < p; ++r) col[r] = q[(size_t)r * ncodes + i];
-        s[i] = oracle_reduce1(col, p, i / OR_TILE, Tp, group_k, e, m, ae, am, kahan);
+        s[i] = sr ? reduce1_sr(col, p, i, Tp, group_k, e, m, seed)
+                  : oracle_reduce1(col, p, i / OR_TILE, Tp, group_k, e, m, ae, am, kahan);
     }
     if (reduced_out) {
         memset(reduced_out, 0, (size_t)nbytes);
