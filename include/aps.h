@@ -212,6 +212,18 @@ aps_status aps_ring_step(int world_size, int rank, int step, int *send_chunk, in
  * format for every layer (aps_init).  Errors: APS_ERR_ARG, APS_ERR_FORMAT. */
 aps_status aps_set_reduction(aps_ctx *ctx, int group_k, int acc_exp_bits, int acc_man_bits, int kahan);
 
+/* Rounding mode of every Cast ("some researchers
+ * prefer stochastic rounding ... an unbiased estimate"; the paper's own runs use
+ * round-to-nearest-even, the default).  mode 0: nearest even; mode 1: stochastic
+ * (reading A26): x between its neighbours lo <= |x| < hi rounds up iff
+ * r < (|x| - lo)/(hi - lo) * 2^32, r = SplitMix64(seed, phase << 40 | i) >> 32 with i the
+ * element's code index in the packed layout and phase = the rank for the initial
+ * Cast, p - 1 + a for the a-th add of the element's fold -- reproducible and
+ * independent of thread order.  Stochastic mode needs one format, the wire-format
+ * accumulator, and (world_size > 1) the peer transport; at world_size 1 aps_sync
+ * runs the separate calls instead of the fused kernel.  Errors: APS_ERR_ARG. */
+aps_status aps_set_rounding(aps_ctx *ctx, int mode, uint64_t seed);
+
 /* ---- peer-memory transport (NVLink / NVSwitch load-store) ----------------
  * Alg. 1 line 7's all-reduce without NCCL: rank r loads the p ranks' packed
  * codes of ring chunk r straight from their workspaces (CUDA IPC mappings),
@@ -288,6 +300,10 @@ aps_status aps_debug_cast(const float *in, uint32_t *codes, int64_t n, int exp_b
                           int man_bits, int hw, void *cuda_stream);
 aps_status aps_debug_decode(const uint32_t *codes, float *out, int64_t n, int exp_bits,
                             int man_bits, int hw, void *cuda_stream);
+/* codes[i] = stochastic-rounding Cast(in[i]) with r_i = SplitMix64(seed, phase << 40 | i) >> 32
+ * (reading A26; aps_set_rounding). */
+aps_status aps_debug_cast_sr(const float *in, uint32_t *codes, int64_t n, int exp_bits, int man_bits,
+                             uint64_t seed, uint64_t phase, void *cuda_stream);
 /* [sync] Per-CTA %globaltimer stamps (start, end of abs-max pass, after the
  * grid barrier, end; 4 x uint64 per CTA, ns) of the last fused p = 1 launch
  * run with APS_FUSED_FLAGS bit 16 set (profiling aid). */

@@ -29,7 +29,7 @@ EXPORTS = [
     "aps_nccl_comm_init", "aps_nccl_comm_destroy", "aps_sim_layer_scales", "aps_sim_allreduce",
     "aps_debug_cast", "aps_debug_decode", "aps_debug_ring_reduce", "aps_debug_timeline",
     "aps_init_mixed", "aps_layout_mixed", "aps_set_reduction", "aps_peer_export", "aps_peer_import",
-    "aps_sim_connect", "aps_round_off_error", "aps_census",
+    "aps_sim_connect", "aps_round_off_error", "aps_census", "aps_set_rounding", "aps_debug_cast_sr",
 ]
 PEER_HANDLE_BYTES = 64
 
@@ -92,6 +92,8 @@ def load(path: Path | str | None = None):
         "aps_sim_connect": ([vp, i32], i32),
         "aps_round_off_error": ([vp, vp, i64, vp, vp, vp], i32),
         "aps_census": ([vp, vp, vp, vp], i32),
+        "aps_set_rounding": ([vp, i32, ctypes.c_uint64], i32),
+        "aps_debug_cast_sr": ([vp, vp, i64, i32, i32, ctypes.c_uint64, ctypes.c_uint64, vp], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -284,6 +286,10 @@ class ApsContext:
         ae, am = acc if acc is not None else wire
         self._check(self.L.aps_set_reduction(self.h, group_k, ae, am, int(kahan)), "aps_set_reduction")
 
+    def set_rounding(self, stochastic: bool = False, seed: int = 0):
+        """Nearest-even (default) or stochastic rounding of every Cast (aps_set_rounding)."""
+        self._check(self.L.aps_set_rounding(self.h, int(stochastic), seed), "aps_set_rounding")
+
     def census(self, grads, scale_exp):
         """Underflow / overflow counts [n_layers, 2] of Cast(g * 2^s_l) (aps_census);
         scale_exp: one exponent per layer, or one int for every layer."""
@@ -372,6 +378,17 @@ def debug_cast(x, exp_bits: int, man_bits: int, hw: bool = False):
                                torch.cuda.current_stream(x.device).cuda_stream)
     if st:
         raise ApsError(st, "aps_debug_cast")
+    return out
+
+
+def debug_cast_sr(x, exp_bits: int, man_bits: int, seed: int, phase: int = 0):
+    """Device stochastic-rounding cast of an fp32 CUDA tensor -> int32 codes (test only)."""
+    import torch
+    out = torch.empty(x.shape, dtype=torch.int32, device=x.device)
+    st = load().aps_debug_cast_sr(x.data_ptr(), out.data_ptr(), x.numel(), exp_bits, man_bits, seed, phase,
+                                  torch.cuda.current_stream(x.device).cuda_stream)
+    if st:
+        raise ApsError(st, "aps_debug_cast_sr")
     return out
 
 

@@ -92,6 +92,9 @@ struct aps_ctx {
     // group size (1 = flat ring), accumulator format, Kahan compensation
     int group_k = 1, acc_e = 0, acc_m = 0;
     bool kahan = false;
+    // stochastic rounding (reading A26): counter-based draws keyed by (seed, phase, element)
+    bool sr = false;
+    uint64_t sr_seed = 0;
     // peer-memory transport (aps_peer.cu): every rank's workspace mapped here
     bool peer = false;
     aps::PeerArgs pa{};
@@ -524,7 +527,8 @@ static aps_status reduce_chunk(aps_ctx *c, const aps_ctx *layout, int ch, const 
 
 static bool flat_reduction(const aps_ctx *c)
 {
-    return (c->group_k == 1 || c->group_k == c->world) && !c->kahan && c->acc_e == c->e && c->acc_m == c->m;
+    return (c->group_k == 1 || c->group_k == c->world) && !c->kahan && c->acc_e == c->e && c->acc_m == c->m &&
+           !c->sr;
 }
 
 // peer transport: announce this rank's packed codes, wait for every rank's
@@ -539,6 +543,12 @@ static aps_status peer_ready(aps_ctx *c)
 static aps_status peer_reduce_own(aps_ctx *c)
 {
     c->pa.group_k = c->group_k;
+    if (c->sr) {
+        for (const auto &sg : c->chunk_segs[c->rank])
+            APS_CUDA(c, aps::launch_peer_reduce_sr(c->pa, sg.byte_off, sg.tile0, sg.n_tiles, sg.e, sg.m, c->sr_seed,
+                                                   c->stream));
+        return APS_OK;
+    }
     for (const auto &sg : c->chunk_segs[c->rank])
         APS_CUDA(c, aps::launch_peer_reduce(c->pa, sg.byte_off, sg.tile0, sg.n_tiles, sg.e, sg.m, sg.hw,
                                             c->uniform ? c->acc_e : sg.e, c->uniform ? c->acc_m : sg.m, c->kahan,
@@ -621,6 +631,11 @@ aps_status aps_quantize_pack(aps_ctx *c, const float *const *grads)
     if (c->phase < kScales) return fail(c, APS_ERR_STATE, "aps_quantize_pack before aps_layer_scales");
     if (!grads) return fail(c, APS_ERR_ARG, "grads is NULL");
     if (aps_status s = upload_ptrs<const float *>(c, c->src_cache, grads, c->off_src)) return s;
+    if (c->sr) {  // stochastic rounding: one generic launch (uniform formats)
+        APS_CUDA(c, aps::launch_quant_pack_sr(c->t, c->e, c->m, c->sr_seed, c->rank, c->stream));
+        c->phase = kPacked;
+        return APS_OK;
+    }
     // one launch per format group (NEXT-2)
     if (aps_status s = for_groups(c, [&](const aps_ctx::Group &g, const aps::DevTables &t, cudaStream_t st, bool) {
             cudaError_t e = c->stream_engine ? aps::launch_stream_quant(t, g.e, g.m, g.hw, st) : cudaErrorNotSupported;
@@ -708,7 +723,7 @@ aps_status aps_sync_out(aps_ctx *c, const float *const *grads, float *const *out
 {
     if (aps_status s = need_ws(c)) return s;
     if (!grads || !out) return fail(c, APS_ERR_ARG, "NULL pointer array");
-    if (c->world == 1 && !c->comm && c->engine == aps_ctx::kLdg) {
+    if (c->world == 1 && !c->comm && c->engine == aps_ctx::kLdg && !c->sr) {
         // one rank: FindMaxExp -> f~ -> Cast -> pack -> Cast back -> unscale in one launch
         if (aps_status s = upload_ptrs<const float *>(c, c->src_cache, grads, c->off_src)) return s;
         if (aps_status s = upload_ptrs<float *>(c, c->dst_cache, out, c->off_dst)) return s;
@@ -775,7 +790,7 @@ aps_status aps_sync_out(aps_ctx *c, const float *const *grads, float *const *out
         c->phase = kReduced;
         return APS_OK;
     }
-    if (c->world == 1 && !c->comm && c->stream_engine && c->uniform && aps::stream_fused_supported(c->e, c->m, c->hw)) {
+    if (c->world == 1 && !c->comm && c->stream_engine && !c->sr && c->uniform && aps::stream_fused_supported(c->e, c->m, c->hw)) {
         // one rank: FindMaxExp -> f~ -> Cast -> pack -> Cast back -> unscale in one launch
         if (aps_status s = upload_ptrs<const float *>(c, c->src_cache, grads, c->off_src)) return s;
         if (aps_status s = upload_ptrs<float *>(c, c->dst_cache, out, c->off_dst)) return s;
@@ -854,12 +869,24 @@ aps_status aps_set_reduction(aps_ctx *c, int group_k, int acc_exp_bits, int acc_
     if (!format_ok(acc_exp_bits, acc_man_bits)) return fail(c, APS_ERR_FORMAT, "invalid accumulator format");
     const bool ext = kahan || acc_exp_bits != c->e || acc_man_bits != c->m;
     if (ext && !c->uniform) return fail(c, APS_ERR_ARG, "accumulator variants need one format for every layer");
+    if (ext && c->sr) return fail(c, APS_ERR_ARG, "accumulator variants are not combined with stochastic rounding");
     if (acc_exp_bits < c->e || acc_man_bits < c->m)
         return fail(c, APS_ERR_FORMAT, "the accumulator must hold every wire value (exp and man bits >= the wire's)");
     c->group_k = group_k;
     c->acc_e = acc_exp_bits;
     c->acc_m = acc_man_bits;
     c->kahan = kahan != 0;
+    return APS_OK;
+}
+
+aps_status aps_set_rounding(aps_ctx *c, int mode, uint64_t seed)
+{
+    if (!c) return APS_ERR_ARG;
+    if (mode != 0 && mode != 1) return fail(c, APS_ERR_ARG, "rounding mode must be 0 (nearest even) or 1 (stochastic)");
+    if (mode == 1 && (!c->uniform || c->kahan || c->acc_e != c->e || c->acc_m != c->m))
+        return fail(c, APS_ERR_ARG, "stochastic rounding needs one format and the wire-format accumulator");
+    c->sr = mode == 1;
+    c->sr_seed = seed;
     return APS_OK;
 }
 
@@ -1118,6 +1145,15 @@ aps_status aps_debug_decode(const uint32_t *codes, float *out, int64_t n, int e,
     if (n < 0 || (n > 0 && (!out || !codes))) return APS_ERR_ARG;
     if (hw && !aps::hw_available(e, m)) return APS_ERR_FORMAT;
     return aps::launch_debug_decode(codes, out, n, e, m, hw != 0, static_cast<cudaStream_t>(stream)) == cudaSuccess
+               ? APS_OK : APS_ERR_CUDA;
+}
+
+aps_status aps_debug_cast_sr(const float *in, uint32_t *codes, int64_t n, int e, int m, uint64_t seed, uint64_t phase,
+                             void *stream)
+{
+    if (!format_ok(e, m)) return APS_ERR_FORMAT;
+    if (n < 0 || (n > 0 && (!in || !codes))) return APS_ERR_ARG;
+    return aps::launch_debug_cast_sr(in, codes, n, e, m, seed, phase, static_cast<cudaStream_t>(stream)) == cudaSuccess
                ? APS_OK : APS_ERR_CUDA;
 }
 

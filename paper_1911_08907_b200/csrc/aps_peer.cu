@@ -392,6 +392,171 @@ __global__ void __launch_bounds__(NT) peer_reduce_tile_kernel(PeerArgs a, int64_
     cta_fence_system();
 }
 
+// ------------------------------------------------------------------ stochastic rounding (reading A26)
+// r = SplitMix64(seed, phase << 40 | i) >> 32 (the same counter-based generator the
+// oracle implements); x between its neighbours lo <= |x| < hi rounds up iff
+// r < (|x| - lo) / (hi - lo) * 2^32.  Phase: rank for the Cast of a rank's gradient,
+// p - 1 + a for the a-th add of an element's fold.
+__device__ __forceinline__ uint32_t sr_rand(uint64_t seed, uint64_t phase, int64_t i)
+{
+    uint64_t z = seed + (((phase << 40) | (uint64_t)i) + 1ull) * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return (uint32_t)((z ^ (z >> 31)) >> 32);
+}
+
+// up iff r < rem / 2^d * 2^32 (exact, any d >= 1)
+__device__ __forceinline__ uint32_t sr_up(uint32_t r, uint64_t rem, int d)
+{
+    if (rem == 0) return 0u;
+    if (d <= 32) return (uint32_t)((r >> (32 - d)) < rem);
+    if (d - 32 >= 24) return (uint32_t)(r == 0u);         // rem < 2^24 <= 2^(d-32)
+    return (uint32_t)(((uint64_t)r << (d - 32)) < rem);
+}
+
+__device__ __forceinline__ uint32_t encode_sr(const Fmt &F, float y, uint32_t r)
+{
+    const uint32_t u = __float_as_uint(y);
+    const uint32_t a = u & 0x7fffffffu;
+    const uint32_t s = (u >> 31) << (F.e + F.m);
+    if (a > 0x7f800000u) return s | F.nan_code;
+    if (a == 0u) return s;
+    if (F.m == 23) return u;                                          // (8,23): identity
+    const uint32_t inf_bits = (uint32_t)(127 + F.bias + 1) << 23;     // 2^(bias+1)
+    if (a >= inf_bits) return s | F.inf_code;
+    uint32_t mag;
+    if (a >= F.norm_min) {                                            // target normal: d = 23 - m
+        mag = (a >> F.sh) - F.rebias + sr_up(r, a & ((1u << F.sh) - 1u), (int)F.sh);
+    } else {                                                          // target subnormal
+        const uint64_t sig = (a >= 0x800000u) ? ((a & 0x7fffffu) | 0x800000u) : a;
+        const int lsb = (a >= 0x800000u) ? (int)(a >> 23) - 150 : -149;
+        const int d = (1 - F.bias - F.m) - lsb;
+        if (d <= 0) {
+            mag = (uint32_t)(sig << (-d));
+        } else {
+            const uint64_t n = d >= 64 ? 0ull : (sig >> d);
+            const uint64_t rem = d >= 64 ? sig : (sig & ((1ull << d) - 1ull));
+            mag = (uint32_t)n + sr_up(r, rem, d);
+        }
+    }
+    return s | min(mag, F.inf_code);
+}
+
+// a3+a4 with stochastic rounding, any width: per warp one tile of 128 codes
+template <int NT>
+__global__ void __launch_bounds__(NT) quant_pack_sr_kernel(DevTables t, Fmt F, uint64_t seed, int rank)
+{
+    __shared__ __align__(16) uint32_t s_codes[NT / 32][kTile + 1];
+    const Item it = t.items[blockIdx.x];
+    const LayerDev L = t.layers[it.layer];
+    const float *g = t.src[it.layer];
+    const int ft = scale_exponent(t, it.layer, F.bias, it.tile_begin == 0 && threadIdx.x == 0);
+    const Pow2 sc(ft);
+    const int b = F.b;
+    const int64_t begin = (int64_t)it.tile_begin * kTile;
+    const int64_t n = min((int64_t)it.n_tiles * kTile, L.numel - begin);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t *codes = s_codes[warp];
+    uint32_t *out = reinterpret_cast<uint32_t *>(t.packed + it.byte_pos);
+    for (int tt = warp; tt < it.n_tiles; tt += NT / 32) {
+        const int64_t e0 = (int64_t)tt * kTile + lane * 4;
+        const float4 y = sc.apply4(load_group(g + begin, e0, n));
+        const int64_t idx = (it.tile_pos + tt) * kTile + lane * 4;  // code index in the packed layout
+        const float ys[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+        for (int h = 0; h < 4; ++h) codes[lane * 4 + h] = encode_sr(F, ys[h], sr_rand(seed, (uint64_t)rank, idx + h));
+        __syncwarp();
+        uint32_t *ow = out + (int64_t)tt * (4 * b);
+        for (int w = lane; w < 4 * b; w += 32) ow[w] = assemble_word(codes, w, b);
+        __syncwarp();
+    }
+}
+
+// owner-computes reduce with a stochastic re-quantise after every add (wire accumulator)
+template <int NT>
+__global__ void __launch_bounds__(NT) peer_reduce_sr_kernel(PeerArgs a, int64_t byte_off, int64_t tile0,
+                                                            int64_t n_tiles, Fmt F, uint64_t seed)
+{
+    __shared__ __align__(16) uint32_t s_w[NT / 32][kTile + 1];
+    const int b = F.b;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t *wa = s_w[warp];
+    const int64_t warps = (int64_t)gridDim.x * (NT / 32);
+    for (int64_t tt = blockIdx.x * (int64_t)(NT / 32) + warp; tt < n_tiles; tt += warps) {
+        const int64_t off = byte_off + tt * 16 * b;
+        const int64_t t = tile0 + tt;
+        const Order o(a, t);
+        float S[4], s[4];
+        int adds = 0;
+        for (int gi = 0; gi < o.G; ++gi) {
+            for (int j = 0; j < o.k; ++j) {
+                const uint8_t *src = a.packed[o.rank_of(gi, j)] + off;
+                __syncwarp();
+                for (int w = lane; w < 4 * b; w += 32) wa[w] = ld_peer4(src + 4 * w);
+                if (lane == 0) wa[4 * b] = 0u;
+                __syncwarp();
+                if (j > 0) ++adds;
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    const float x = decode_finite(F, extract_code(wa, lane * 4 + h, b));
+                    const int64_t idx = t * kTile + lane * 4 + h;
+                    s[h] = (j == 0) ? x
+                                    : decode_finite(F, encode_sr(F, __fadd_rn(s[h], x),
+                                                                 sr_rand(seed, (uint64_t)(a.p - 1 + adds), idx)));
+                }
+            }
+            if (gi > 0) ++adds;
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                const int64_t idx = t * kTile + lane * 4 + h;
+                S[h] = (gi == 0) ? s[h]
+                                 : decode_finite(F, encode_sr(F, __fadd_rn(S[h], s[h]),
+                                                              sr_rand(seed, (uint64_t)(a.p - 1 + adds), idx)));
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int h = 0; h < 4; ++h) wa[lane * 4 + h] = encode(F, S[h]);
+        __syncwarp();
+        for (int w = lane; w < 4 * b; w += 32) {
+            const uint32_t word = assemble_word(wa, w, b);
+            for (int q = 0; q < a.p; ++q) reinterpret_cast<uint32_t *>(a.packed[q] + off)[w] = word;
+        }
+    }
+    cta_fence_system();
+}
+
+__global__ void debug_cast_sr_kernel(const float *in, uint32_t *codes, int64_t n, Fmt F, uint64_t seed, uint64_t phase)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        codes[i] = encode_sr(F, in[i], sr_rand(seed, phase, i));
+}
+
+cudaError_t launch_debug_cast_sr(const float *in, uint32_t *codes, int64_t n, int e, int m, uint64_t seed,
+                                 uint64_t phase, cudaStream_t s)
+{
+    if (n <= 0) return cudaSuccess;
+    const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 16);
+    debug_cast_sr_kernel<<<grid, 256, 0, s>>>(in, codes, n, make_fmt(e, m), seed, phase);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_quant_pack_sr(const DevTables &t, int e, int m, uint64_t seed, int rank, cudaStream_t s)
+{
+    if (t.n_items == 0) return cudaSuccess;
+    quant_pack_sr_kernel<kThreads><<<t.n_items, kThreads, 0, s>>>(t, make_fmt(e, m), seed, rank);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_peer_reduce_sr(const PeerArgs &a, int64_t byte_off, int64_t tile0, int64_t n_tiles, int e, int m,
+                                  uint64_t seed, cudaStream_t s)
+{
+    if (n_tiles <= 0) return cudaSuccess;
+    const int grid = (int)std::min<int64_t>((n_tiles + kThreads / 32 - 1) / (kThreads / 32), (int64_t)sm_count() * 8);
+    peer_reduce_sr_kernel<kThreads><<<grid, kThreads, 0, s>>>(a, byte_off, tile0, n_tiles, make_fmt(e, m), seed);
+    return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ launchers
 cudaError_t launch_peer_post_E(const PeerArgs &a, const int32_t *E_local, int n_layers, uint32_t epoch,
                                cudaStream_t s)

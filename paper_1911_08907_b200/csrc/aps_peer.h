@@ -32,6 +32,12 @@ cudaError_t launch_peer_wait(const PeerArgs &a, int slot, uint32_t epoch, uint32
 cudaError_t launch_peer_reduce(const PeerArgs &a, int64_t byte_off, int64_t tile0, int64_t n_tiles, int e, int m,
                                bool hw, int acc_e, int acc_m, bool kahan, cudaStream_t s);
 struct DevTables;
+// stochastic rounding (reading A26): quantise of rank `rank`, and the owner-computes reduce
+cudaError_t launch_debug_cast_sr(const float *in, uint32_t *codes, int64_t n, int e, int m, uint64_t seed,
+                                 uint64_t phase, cudaStream_t s);
+cudaError_t launch_quant_pack_sr(const DevTables &t, int e, int m, uint64_t seed, int rank, cudaStream_t s);
+cudaError_t launch_peer_reduce_sr(const PeerArgs &a, int64_t byte_off, int64_t tile0, int64_t n_tiles, int e, int m,
+                                  uint64_t seed, cudaStream_t s);
 cudaError_t launch_census(const DevTables &t, const int32_t *sexp, unsigned long long *counts, int e, int m,
                           cudaStream_t s);
 cudaError_t launch_round_off(const float *h, const float *l, int64_t n, double *sum, unsigned long long *cnt,
