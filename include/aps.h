@@ -212,6 +212,15 @@ aps_status aps_ring_step(int world_size, int rank, int step, int *send_chunk, in
  * format for every layer (aps_init).  Errors: APS_ERR_ARG, APS_ERR_FORMAT. */
 aps_status aps_set_reduction(aps_ctx *ctx, int group_k, int acc_exp_bits, int acc_man_bits, int kahan);
 
+/* CUDA-graph capture.  Every path takes its per-call state from device memory
+ * (peer epochs, the abs-max done counter) except the fused world_size == 1
+ * wavefront kernel, whose claim base, call index and accumulator parity are
+ * launch arguments by default (the fastest form).  enable = 1 switches it to the
+ * capture-safe form (all three derived on the device from a 64-bit claim counter;
+ * ~1 us slower per call), so a captured aps_sync replays exactly; enable = 0
+ * switches back (reads the call count the device reached).  [sync] */
+aps_status aps_set_graph_safe(aps_ctx *ctx, int enable);
+
 /* Rounding mode of every Cast ("some researchers
  * prefer stochastic rounding ... an unbiased estimate"; the paper's own runs use
  * round-to-nearest-even, the default).  mode 0: nearest even; mode 1: stochastic

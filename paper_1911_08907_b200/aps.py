@@ -30,6 +30,7 @@ EXPORTS = [
     "aps_debug_cast", "aps_debug_decode", "aps_debug_ring_reduce", "aps_debug_timeline",
     "aps_init_mixed", "aps_layout_mixed", "aps_set_reduction", "aps_peer_export", "aps_peer_import",
     "aps_sim_connect", "aps_round_off_error", "aps_census", "aps_set_rounding", "aps_debug_cast_sr",
+    "aps_set_graph_safe",
 ]
 PEER_HANDLE_BYTES = 64
 
@@ -93,11 +94,15 @@ def load(path: Path | str | None = None):
         "aps_round_off_error": ([vp, vp, i64, vp, vp, vp], i32),
         "aps_census": ([vp, vp, vp, vp], i32),
         "aps_set_rounding": ([vp, i32, ctypes.c_uint64], i32),
+        "aps_set_graph_safe": ([vp, i32], i32),
         "aps_debug_cast_sr": ([vp, vp, i64, i32, i32, ctypes.c_uint64, ctypes.c_uint64, vp], i32),
     }
     for name, (args, res) in sig.items():
-        f = getattr(L, name)
-        f.argtypes, f.restype = args, res
+        f = getattr(L, name, None)
+        if f is None and path is None and not os.environ.get("APS_LIB"):
+            raise ImportError(f"{p} lacks {name}: rebuild (__graft_entry__.build())")
+        if f is not None:  # (an APS_LIB A/B build may predate newer entry points)
+            f.argtypes, f.restype = args, res
     _lib = L
     return L
 
@@ -285,6 +290,27 @@ class ApsContext:
         wire = self.formats[0] if self.formats is not None else (self.exp_bits, self.man_bits)
         ae, am = acc if acc is not None else wire
         self._check(self.L.aps_set_reduction(self.h, group_k, ae, am, int(kahan)), "aps_set_reduction")
+
+    def capture_sync(self, grads, out=None, average: bool = True):
+        """Capture one aps_sync_out (grads -> out, default in place) into a CUDA graph
+        and return it; ``graph.replay()`` then re-runs the whole synchronisation on
+        whatever the same buffers hold.  Every kernel takes its per-call state (claim
+        bases, accumulator parity, peer epochs) from device memory, so replays are
+        exact.  The context's stream must not be the legacy default stream.  One
+        un-captured call first uploads the pointer tables."""
+        import torch
+        out = grads if out is None else out
+        self.set_graph_safe(True)
+        self.sync_out(grads, out, average)
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=self.stream):
+            self.sync_out(grads, out, average)
+        return g
+
+    def set_graph_safe(self, enable: bool = True):
+        """Capture-safe wavefront launches (aps_set_graph_safe); capture_sync sets it."""
+        self._check(self.L.aps_set_graph_safe(self.h, int(enable)), "aps_set_graph_safe")
 
     def set_rounding(self, stochastic: bool = False, seed: int = 0):
         """Nearest-even (default) or stochastic rounding of every Cast (aps_set_rounding)."""

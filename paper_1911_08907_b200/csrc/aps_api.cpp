@@ -52,7 +52,7 @@ struct aps_ctx {
         int e, m;
         bool hw;
         int item_begin, item_count, max_layer_items;
-        uint32_t wave_claim_base;  // this group's wavefront claim counter at its next launch
+        uint32_t wave_claim_base;  // this group's 32-bit wavefront claim counter at its next launch (host mode)
     };
     std::vector<Group> groups;
     struct Seg {
@@ -68,10 +68,12 @@ struct aps_ctx {
     uint8_t *ws = nullptr;
     size_t ws_bytes = 0, need = 0;
     size_t off_packed = 0, off_recv = 0, off_items = 0, off_layers = 0, off_src = 0, off_dst = 0,
-           off_amax = 0, off_count = 0, off_eloc = 0, off_eglob = 0, off_ft = 0, off_flag = 0, off_amax2 = 0, off_done = 0, off_iptr = 0, off_tl = 0, off_claim = 0, off_ldone = 0;
-    uint32_t wave_calls = 0;    // wavefront launches so far (per-layer counter targets)
+           off_amax = 0, off_count = 0, off_eloc = 0, off_eglob = 0, off_ft = 0, off_flag = 0, off_amax2 = 0, off_done = 0, off_iptr = 0, off_tl = 0, off_claim = 0, off_ldone = 0, off_claim64 = 0;
     int max_layer_items = 0;
     uint32_t claim_base = 0;   // value of the fused kernel's claim counters at the next launch
+    uint32_t wave_calls = 0;   // wavefront launches so far (host mode: per-layer counter targets)
+    bool graph_safe = false;   // wavefront kernel takes its per-call state from the device (aps_set_graph_safe)
+    std::vector<unsigned long long> claim64_init;  // host staging of the 64-bit claim counters
     bool iptr_valid = false;
     aps::DevTables t{};
     std::vector<const float *> src_cache;
@@ -98,7 +100,6 @@ struct aps_ctx {
     // peer-memory transport (aps_peer.cu): every rank's workspace mapped here
     bool peer = false;
     aps::PeerArgs pa{};
-    uint32_t e_epoch = 0, r_epoch = 0;  // AllReduce(E, MAX) calls / all-reduce calls so far
     std::vector<void *> ipc_mapped;     // cudaIpcOpenMemHandle mappings (closed by aps_destroy)
     size_t off_pflags = 0, off_eslots = 0, off_census = 0;
     std::string err;
@@ -367,6 +368,8 @@ static aps_status init_common(aps_ctx **out, const int *e_arr, const int *m_arr,
     c->off_tl = o;     o = align_up(o + sizeof(uint64_t) * aps::kTimelineSlots);
     c->off_claim = o;  o = align_up(o + 3 * sizeof(uint32_t) * c->groups.size());  // 3 per format group
     c->off_ldone = o;  o = align_up(o + 4 * (size_t)n_layers);
+    // graph-safe counters: 64-bit wavefront claim counter per format group, absmax_ranges done counter
+    c->off_claim64 = o; o = align_up(o + 8 * c->groups.size() + 4);
     // peer transport: flag block and E slots [2][world][n_layers] (world > 1 only)
     c->off_pflags = o; o = align_up(o + (world_size > 1 ? 4 * (size_t)aps::kFlagWords : 0));
     c->off_eslots = o; o = align_up(o + (world_size > 1 ? 2 * 4 * (size_t)world_size * (size_t)n_layers : 0));
@@ -446,10 +449,10 @@ aps_status aps_set_workspace(aps_ctx *c, void *dev, size_t bytes)
     t.iptr = reinterpret_cast<aps::ItemPtr *>(c->ws + c->off_iptr);
     t.timeline = reinterpret_cast<uint64_t *>(c->ws + c->off_tl);
     t.claim = reinterpret_cast<uint32_t *>(c->ws + c->off_claim);
+    t.claim64 = reinterpret_cast<unsigned long long *>(c->ws + c->off_claim64);
+    t.ranges_done = reinterpret_cast<uint32_t *>(c->ws + c->off_claim64 + 8 * c->groups.size());
     t.layer_done = reinterpret_cast<uint32_t *>(c->ws + c->off_ldone);
 
-    c->wave_calls = 0;
-    for (auto &g : c->groups) g.wave_claim_base = 0;
     if (c->groups.size() > 1 && c->side.empty()) {
         c->side.resize(c->groups.size() - 1);
         c->ev_join.resize(c->groups.size() - 1);
@@ -460,6 +463,9 @@ aps_status aps_set_workspace(aps_ctx *c, void *dev, size_t bytes)
         APS_CUDA(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     }
     c->claim_base = 0;
+    c->wave_calls = 0;
+    c->graph_safe = false;
+    for (auto &g : c->groups) g.wave_claim_base = 0;
     c->iptr_valid = false;
     c->gen = 0;
     c->done_target = 0;
@@ -480,6 +486,7 @@ static aps::DevTables group_tables(const aps_ctx *c, const aps_ctx::Group &g)
     t.iptr += g.item_begin;
     t.n_items = g.item_count;
     t.claim += 3 * (&g - c->groups.data());
+    t.claim64 += (&g - c->groups.data());
     return t;
 }
 
@@ -534,8 +541,8 @@ static bool flat_reduction(const aps_ctx *c)
 // peer transport: announce this rank's packed codes, wait for every rank's
 static aps_status peer_ready(aps_ctx *c)
 {
-    APS_CUDA(c, aps::launch_peer_signal(c->pa, aps::kSlotReady, c->r_epoch, c->stream));
-    APS_CUDA(c, aps::launch_peer_wait(c->pa, aps::kSlotReady, c->r_epoch, c->t.flag, c->stream));
+    APS_CUDA(c, aps::launch_peer_signal(c->pa, aps::kSlotReady, true, c->stream));
+    APS_CUDA(c, aps::launch_peer_wait(c->pa, aps::kSlotReady, c->t.flag, c->stream));
     return APS_OK;
 }
 
@@ -596,9 +603,7 @@ aps_status aps_layer_scales(aps_ctx *c, const float *const *grads)
     } else if (c->engine == aps_ctx::kLdg && absmax_plain()) {
         APS_CUDA(c, aps::launch_absmax_plain(c->t, c->world, c->stream));
     } else if (c->engine == aps_ctx::kLdg) {
-        const uint32_t tgt = c->done_target + (uint32_t)aps::absmax_ranges_grid(c->t.n_items);
-        APS_CUDA(c, aps::launch_absmax_ranges(c->t, c->world, tgt, c->stream));
-        c->done_target = tgt;
+        APS_CUDA(c, aps::launch_absmax_ranges(c->t, c->world, c->stream));
     } else {
         APS_CUDA(c, aps::launch_absmax_exp(c->t, c->world, c->stream));
     }
@@ -606,12 +611,11 @@ aps_status aps_layer_scales(aps_ctx *c, const float *const *grads)
         c->phase = kScales;
     } else if (c->peer) {
         // AllReduce(max_grad_exp, MAX) over peer memory: post E to every rank, collect
-        ++c->e_epoch;
-        APS_CUDA(c, aps::launch_peer_post_E(c->pa, c->t.E_local, c->n_layers, c->e_epoch, c->stream));
+        APS_CUDA(c, aps::launch_peer_post_E(c->pa, c->t.E_local, c->n_layers, c->stream));
         if (c->sim) {
             c->phase = kLocalScales;  // aps_sim_layer_scales collects after every rank posted
         } else {
-            APS_CUDA(c, aps::launch_peer_collect_E(c->pa, c->t.E_glob, c->n_layers, c->e_epoch, c->t.flag, c->stream));
+            APS_CUDA(c, aps::launch_peer_collect_E(c->pa, c->t.E_glob, c->n_layers, c->t.flag, c->stream));
             c->phase = kScales;
         }
     } else if (c->sim) {
@@ -657,11 +661,10 @@ aps_status aps_allreduce(aps_ctx *c)
     }
     if (c->sim) return fail(c, APS_ERR_STATE, "simulated rank: use aps_sim_allreduce");
     if (c->peer) {
-        ++c->r_epoch;
         if (aps_status s = peer_ready(c)) return s;
         if (aps_status s = peer_reduce_own(c)) return s;
-        APS_CUDA(c, aps::launch_peer_signal(c->pa, aps::kSlotDone, c->r_epoch, c->stream));
-        APS_CUDA(c, aps::launch_peer_wait(c->pa, aps::kSlotDone, c->r_epoch, c->t.flag, c->stream));
+        APS_CUDA(c, aps::launch_peer_signal(c->pa, aps::kSlotDone, false, c->stream));
+        APS_CUDA(c, aps::launch_peer_wait(c->pa, aps::kSlotDone, c->t.flag, c->stream));
         c->phase = kReduced;
         return APS_OK;
     }
@@ -752,9 +755,9 @@ aps_status aps_sync_out(aps_ctx *c, const float *const *grads, float *const *out
                 aps_ctx::Group &g0 = c->groups[0];  // its claim counter serves the single launch
                 const int wgrid = aps::fused_p1_wave_grid(lo.e, lo.m, lo.hw, c->t.n_items);
                 const int lag = std::min(c->t.n_items, c->max_layer_items + wgrid);
-                APS_CUDA(c, aps::launch_fused_p1_wave_hybrid32(c->t, lo.e, lo.m, lo.hw, fp32_group, average, c->gen,
-                                                               g0.wave_claim_base, c->wave_calls, lag, wgrid,
-                                                               c->stream));
+                const aps::WaveCall w{c->graph_safe, c->gen, g0.wave_claim_base, c->wave_calls};
+                APS_CUDA(c, aps::launch_fused_p1_wave_hybrid32(c->t, lo.e, lo.m, lo.hw, fp32_group, average, w, lag,
+                                                               wgrid, c->stream));
                 g0.wave_claim_base += (uint32_t)(2 * c->t.n_items + aps::kWaveOvershoot * wgrid);
                 ++c->wave_calls;
                 ++c->gen;
@@ -767,8 +770,8 @@ aps_status aps_sync_out(aps_ctx *c, const float *const *grads, float *const *out
                     aps_ctx::Group &g = const_cast<aps_ctx::Group &>(gc);
                     const int wgrid = aps::fused_p1_wave_grid(g.e, g.m, g.hw, t.n_items);
                     const int lag = std::min(t.n_items, g.max_layer_items + wgrid);
-                    cudaError_t e = aps::launch_fused_p1_wave(t, g.e, g.m, g.hw, average, c->gen, g.wave_claim_base,
-                                                              c->wave_calls, lag, wgrid, st, coop);
+                    const aps::WaveCall w{c->graph_safe, c->gen, g.wave_claim_base, c->wave_calls};
+                    cudaError_t e = aps::launch_fused_p1_wave(t, g.e, g.m, g.hw, average, w, lag, wgrid, st, coop);
                     // every position is claimed once and every CTA overshoots kWaveOvershoot times
                     if (e == cudaSuccess) g.wave_claim_base += (uint32_t)(2 * t.n_items + aps::kWaveOvershoot * wgrid);
                     return e;
@@ -879,6 +882,55 @@ aps_status aps_set_reduction(aps_ctx *c, int group_k, int acc_exp_bits, int acc_
     return APS_OK;
 }
 
+// per-call advance of group g's wavefront claim counter (as the launch in aps_sync_out)
+static unsigned long long wave_adv(const aps_ctx *c, size_t g, bool hybrid_single)
+{
+    if (hybrid_single) {
+        int lo = 0;
+        for (size_t k = 0; k < c->groups.size(); ++k)
+            if (!(c->groups[k].e == 8 && c->groups[k].m == 23)) lo = (int)k;
+        const aps_ctx::Group &L = c->groups[lo];
+        return 2ull * c->t.n_items + (unsigned long long)aps::kWaveOvershoot *
+                                         aps::fused_p1_wave_grid(L.e, L.m, L.hw, c->t.n_items);
+    }
+    const aps_ctx::Group &G = c->groups[g];
+    return 2ull * G.item_count +
+           (unsigned long long)aps::kWaveOvershoot * aps::fused_p1_wave_grid(G.e, G.m, G.hw, G.item_count);
+}
+
+aps_status aps_set_graph_safe(aps_ctx *c, int enable)
+{
+    if (aps_status s = need_ws(c)) return s;
+    const bool on = enable != 0;
+    if (on == c->graph_safe) return APS_OK;
+    // the hybrid single launch (one low format + FP32) uses group 0's counter for all items
+    bool hybrid_single = false;
+    if (c->groups.size() == 2) {
+        const char *v = std::getenv("APS_HYBRID_FUSE");
+        const bool fuse = !v || std::atoi(v) != 0;
+        for (int g = 0; g < 2; ++g)
+            if (fuse && c->groups[g].e == 8 && c->groups[g].m == 23 && c->groups[g].hw &&
+                !(c->groups[1 - g].e == 8 && c->groups[1 - g].m == 23))
+                hybrid_single = true;
+    }
+    if (on) {  // device counters := the host's call count, so both modes agree on call index and parity
+        c->claim64_init.resize(c->groups.size());
+        for (size_t g = 0; g < c->groups.size(); ++g)
+            c->claim64_init[g] = (unsigned long long)c->wave_calls * wave_adv(c, g, hybrid_single);
+        APS_CUDA(c, cudaMemcpyAsync(c->t.claim64, c->claim64_init.data(), 8 * c->groups.size(),
+                                    cudaMemcpyHostToDevice, c->stream));
+        APS_CUDA(c, cudaStreamSynchronize(c->stream));
+    } else {   // back to host mode: the call count the device reached (graph replays included)
+        unsigned long long v = 0;
+        APS_CUDA(c, cudaMemcpyAsync(&v, c->t.claim64, 8, cudaMemcpyDeviceToHost, c->stream));
+        APS_CUDA(c, cudaStreamSynchronize(c->stream));
+        c->wave_calls = (uint32_t)(v / wave_adv(c, 0, hybrid_single));
+        c->gen = c->wave_calls;
+    }
+    c->graph_safe = on;
+    return APS_OK;
+}
+
 aps_status aps_set_rounding(aps_ctx *c, int mode, uint64_t seed)
 {
     if (!c) return APS_ERR_ARG;
@@ -924,7 +976,6 @@ static void peer_common(aps_ctx *c)
     c->pa.rank = c->rank;
     c->pa.tiles = c->tiles;
     c->pa.group_k = c->group_k;
-    c->e_epoch = c->r_epoch = 0;
     c->peer = true;
 }
 
@@ -1060,7 +1111,7 @@ aps_status aps_sim_layer_scales(aps_ctx *const *ctxs, int p, const float *const 
     if (ctxs[0]->peer) {  // every rank posted its E; now every rank collects
         for (int r = 0; r < p; ++r) {
             aps_ctx *c = ctxs[r];
-            APS_CUDA(c, aps::launch_peer_collect_E(c->pa, c->t.E_glob, c->n_layers, c->e_epoch, c->t.flag, c->stream));
+            APS_CUDA(c, aps::launch_peer_collect_E(c->pa, c->t.E_glob, c->n_layers, c->t.flag, c->stream));
             c->phase = kScales;
         }
         return APS_OK;
@@ -1082,20 +1133,17 @@ aps_status aps_sim_allreduce(aps_ctx *const *ctxs, int p)
     for (int r = 0; r < p; ++r)
         if (ctxs[r]->phase != kPacked) return fail(ctxs[r], APS_ERR_STATE, "sim allreduce before quantize");
     if (ctxs[0]->peer) {  // same kernels as aps_allreduce, phase by phase over the ranks
-        for (int r = 0; r < p; ++r) {
-            ++ctxs[r]->r_epoch;
-            APS_CUDA(ctxs[r], aps::launch_peer_signal(ctxs[r]->pa, aps::kSlotReady, ctxs[r]->r_epoch, ctxs[r]->stream));
-        }
+        for (int r = 0; r < p; ++r)
+            APS_CUDA(ctxs[r], aps::launch_peer_signal(ctxs[r]->pa, aps::kSlotReady, true, ctxs[r]->stream));
         for (int r = 0; r < p; ++r) {
             aps_ctx *c = ctxs[r];
-            APS_CUDA(c, aps::launch_peer_wait(c->pa, aps::kSlotReady, c->r_epoch, c->t.flag, c->stream));
+            APS_CUDA(c, aps::launch_peer_wait(c->pa, aps::kSlotReady, c->t.flag, c->stream));
             if (aps_status s = peer_reduce_own(c)) return s;
         }
         for (int r = 0; r < p; ++r)
-            APS_CUDA(ctxs[r], aps::launch_peer_signal(ctxs[r]->pa, aps::kSlotDone, ctxs[r]->r_epoch, ctxs[r]->stream));
+            APS_CUDA(ctxs[r], aps::launch_peer_signal(ctxs[r]->pa, aps::kSlotDone, false, ctxs[r]->stream));
         for (int r = 0; r < p; ++r) {
-            APS_CUDA(ctxs[r], aps::launch_peer_wait(ctxs[r]->pa, aps::kSlotDone, ctxs[r]->r_epoch, ctxs[r]->t.flag,
-                                                    ctxs[r]->stream));
+            APS_CUDA(ctxs[r], aps::launch_peer_wait(ctxs[r]->pa, aps::kSlotDone, ctxs[r]->t.flag, ctxs[r]->stream));
             ctxs[r]->phase = kReduced;
         }
         return APS_OK;

@@ -58,6 +58,8 @@ struct DevTables {
     ItemPtr *iptr;            // [n_items] per-item addresses (fused LDG kernel)
     uint64_t *timeline;       // [kTimelineSlots] per-CTA phase stamps (flag 16)
     uint32_t *claim;          // [3] monotone work-claim counters: barrier kernel phase A, phase B; wavefront
+    unsigned long long *claim64;  // wavefront claim counter (64-bit: the call index is derived on the device)
+    uint32_t *ranges_done;    // self-resetting CTA-done counter of absmax_ranges_kernel
     uint32_t *layer_done;     // [n_layers] monotone per-layer abs-max completion counters (wavefront kernel)
     uint8_t *packed;          // packed codes
     int n_items;
@@ -67,7 +69,7 @@ struct DevTables {
 cudaError_t launch_absmax_exp(const DevTables &t, int world, cudaStream_t s);
 // a1 over ranges of kAbsItemsPerCta items, one done-count per CTA (target = done counter after the call)
 int absmax_ranges_grid(int n_items);
-cudaError_t launch_absmax_ranges(const DevTables &t, int world, uint32_t target, cudaStream_t s);
+cudaError_t launch_absmax_ranges(const DevTables &t, int world, cudaStream_t s);
 // a1 as one streaming kernel (red.max per CTA, no counters) + a one-CTA finisher
 cudaError_t launch_absmax_plain(const DevTables &t, int world, cudaStream_t s);
 cudaError_t launch_quant_pack(const DevTables &t, int e, int m, bool hw, cudaStream_t s);
@@ -118,14 +120,20 @@ int fused_p1_wave_grid(int e, int m, bool hw, int n_items);
 
 constexpr int kWaveOvershoot = 2;  // claims past the end per CTA and call (wavefront kernel claims 2 ahead)
 // claim_base advances by 2 * n_items + kWaveOvershoot * grid per call.
-cudaError_t launch_fused_p1_wave(const DevTables &t, int e, int m, bool hw, int average, uint32_t gen,
-                                 uint32_t claim_base, uint32_t call_no, int lag, int grid, cudaStream_t s,
-                                 bool cooperative = true);
+// Per-call state of a wavefront launch.  graph = false: claim base (32-bit claim
+// counter), call index and accumulator parity come from the host.  graph = true
+// (capture-safe): all three are derived on the device from the 64-bit claim counter,
+// which advances by exactly 2 * n_items + kWaveOvershoot * grid per call.
+struct WaveCall {
+    bool graph;
+    uint32_t gen, claim_base, call_no;
+};
+cudaError_t launch_fused_p1_wave(const DevTables &t, int e, int m, bool hw, int average, const WaveCall &w, int lag,
+                                 int grid, cudaStream_t s, bool cooperative = true);
 // One wavefront launch over two format groups: items whose fmt == fmt2 use the
 // binary32 codec (the hybrid FP32 classifier layer), the others (e, m, hw).
 cudaError_t launch_fused_p1_wave_hybrid32(const DevTables &t, int e, int m, bool hw, int fmt2, int average,
-                                          uint32_t gen, uint32_t claim_base, uint32_t call_no, int lag, int grid,
-                                          cudaStream_t s);
+                                          const WaveCall &w, int lag, int grid, cudaStream_t s);
 // claim_base: value of both claim counters at launch (each call advances
 // them by n_items + grid: every CTA's last claim overshoots once).
 cudaError_t launch_fused_p1_ldg(const DevTables &t, int e, int m, bool hw, int average, uint32_t gen,

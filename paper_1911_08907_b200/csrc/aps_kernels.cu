@@ -133,7 +133,7 @@ __device__ __forceinline__ float4 ld_keep4(const float4 *p, uint64_t pol)
 }
 
 template <int NT>
-__global__ void __launch_bounds__(NT, 6) absmax_ranges_kernel(DevTables t, int N, uint32_t target)
+__global__ void __launch_bounds__(NT, 6) absmax_ranges_kernel(DevTables t, int N)
 {
     __shared__ int s_last;
     const int lane = threadIdx.x & 31;
@@ -184,7 +184,11 @@ __global__ void __launch_bounds__(NT, 6) absmax_ranges_kernel(DevTables t, int N
         __threadfence();
     }
     __syncthreads();
-    if (threadIdx.x == 0) s_last = atomicAdd(t.done, 1u) == target - 1u;
+    // self-resetting done counter (graph-safe: no host-side target)
+    if (threadIdx.x == 0) {
+        s_last = atomicAdd(t.ranges_done, 1u) == gridDim.x - 1u;
+        if (s_last) *t.ranges_done = 0u;  // every CTA of this launch has counted itself
+    }
     __syncthreads();
     if (s_last) {
         __threadfence();
@@ -703,10 +707,10 @@ cudaError_t launch_absmax_plain(const DevTables &t, int world, cudaStream_t s)
     return cudaGetLastError();
 }
 
-cudaError_t launch_absmax_ranges(const DevTables &t, int world, uint32_t target, cudaStream_t s)
+cudaError_t launch_absmax_ranges(const DevTables &t, int world, cudaStream_t s)
 {
     if (t.n_items == 0) return cudaSuccess;
-    absmax_ranges_kernel<kThreads><<<absmax_ranges_grid(t.n_items), kThreads, 0, s>>>(t, world, target);
+    absmax_ranges_kernel<kThreads><<<absmax_ranges_grid(t.n_items), kThreads, 0, s>>>(t, world);
     return cudaGetLastError();
 }
 
@@ -792,11 +796,30 @@ struct CNone {
     static constexpr int kB = -1;
 };
 
-template <class C, class C2, int NT>
+// GRAPH = false: per-call state (claim base, call index, accumulator parity) comes from
+// the host as launch arguments (the fastest form).  GRAPH = true (capture-safe): the
+// call index is derived on the device from a 64-bit claim counter that advances by
+// exactly adv = 2 n + kWaveOvershoot * grid per call, so a captured CUDA graph replays
+// exactly; measured ~1 us slower per call (profiles/r01_ab_wave_graph_safe.txt).
+template <class C, class C2, bool GRAPH, int NT>
 __global__ void __launch_bounds__(NT, kWaveCtasPerSm)
-    fused_p1_wave_kernel(DevTables t, C c, C2 c2, uint32_t *amax, uint32_t *amax_next, uint32_t claim_base,
-                         uint32_t call_no, int lag, int bias, int bias2, int fmt2, int avg, int flags)
+    fused_p1_wave_kernel(DevTables t, C c, C2 c2, uint32_t *amax_h, uint32_t *amax_next_h, uint32_t claim_base,
+                         uint32_t call_no_h, unsigned long long adv, int lag, int bias, int bias2, int fmt2, int avg,
+                         int flags)
 {
+    // (graph mode keeps its call state in shared memory, not registers: the kernel sits at
+    // its 64-register budget)
+    __shared__ uint32_t s_call;
+    __shared__ unsigned long long s_base64;  // claim counter value at this call's start
+    if (GRAPH && threadIdx.x == 0) s_base64 = ~0ull;
+    auto amax_of = [&](uint32_t next) -> uint32_t * {
+        if constexpr (GRAPH) return t.amax2 + (size_t)((s_call + next) & 1u) * t.n_layers;
+        else return next ? amax_next_h : amax_h;
+    };
+    auto call_no = [&]() -> uint32_t {
+        if constexpr (GRAPH) return s_call;
+        else return call_no_h;
+    };
     constexpr bool kTwo = C2::kB > 0;  // items with fmt == fmt2 use c2 (bias2)
     __shared__ __align__(16) uint32_t s_codes[NT / 32][kTile];
     __shared__ int s_claim[3], s_ft[3], s_ok[3];  // claims run two items ahead (3 slots)
@@ -831,14 +854,25 @@ __global__ void __launch_bounds__(NT, kWaveCtasPerSm)
         return n - D + (j - (total - D));
     };
     auto ft_of = [&](const Item &it) -> int {
-        const int32_t E = exponent_of(ld_relaxed_u32(&amax[it.layer]), 1);
+        const int32_t E = exponent_of(ld_relaxed_u32(&amax_of(0)[it.layer]), 1);
         const int bs = (kTwo && it.fmt == fmt2) ? bias2 : bias;  // the layer's upper_bound_exp
         return (E == INT32_MIN || E == INT32_MAX) ? 0 : bs - E;  // f~ (Alg. 1 line 4)
     };
-    auto layer_target = [&](const Item &it) -> uint32_t { return (call_no + 1u) * (uint32_t)(8 * it.layer_items); };
+    auto layer_target = [&](const Item &it) -> uint32_t { return (call_no() + 1u) * (uint32_t)(8 * it.layer_items); };
     // thread 0: claim a position into slot sl; resolve f~ now if it is a quantise item of a complete layer
     auto claim_into = [&](int sl) {
-        const int j = (int)(atomicAdd(&t.claim[2], 1u) - claim_base);  // the wavefront's own counter
+        int j;
+        if constexpr (GRAPH) {
+            const unsigned long long raw = atomicAdd(t.claim64, 1ull);  // the wavefront's own counter
+            if (s_base64 == ~0ull) {  // first claim of this CTA: the call index (one division per CTA)
+                const unsigned long long cn = raw / adv;
+                s_base64 = cn * adv;
+                s_call = (uint32_t)cn;
+            }
+            j = (int)(raw - s_base64);
+        } else {
+            j = (int)(atomicAdd(&t.claim[2], 1u) - claim_base);
+        }
         s_claim[sl] = j;
         s_ok[sl] = 0;
         if (j < total) {
@@ -870,7 +904,8 @@ __global__ void __launch_bounds__(NT, kWaveCtasPerSm)
             uint32_t m = 0;
 #pragma unroll
             for (int w = 0; w < NT / 32; ++w) m = max(m, s_part[pp][w]);
-            asm volatile("atom.relaxed.gpu.global.max.u32 %0, [%1], %2;" : "=r"(pend_old) : "l"(&amax[l]), "r"(m) : "memory");
+            asm volatile("atom.relaxed.gpu.global.max.u32 %0, [%1], %2;"
+                         : "=r"(pend_old) : "l"(&amax_of(0)[l]), "r"(m) : "memory");
             pend_layer = l;
         }
     };
@@ -925,11 +960,11 @@ __global__ void __launch_bounds__(NT, kWaveCtasPerSm)
             }
             const int ft = s_ft[slot];
             if (it.tile_begin == 0 && threadIdx.x == 0) {  // record E, f~, flag; clear the next call's accumulator
-                const int32_t E = exponent_of(ld_relaxed_u32(&amax[it.layer]), 1);
+                const int32_t E = exponent_of(ld_relaxed_u32(&amax_of(0)[it.layer]), 1);
                 t.E_local[it.layer] = E;
                 t.ftilde[it.layer] = ft;
                 if (E == INT32_MAX) atomicOr(t.flag, 1u);
-                amax_next[it.layer] = 0u;
+                amax_of(1)[it.layer] = 0u;
             }
             const Pow2 s(ft);
             const Unscale us(ft, 1, avg);
@@ -1001,17 +1036,18 @@ __global__ void __launch_bounds__(NT, kWaveCtasPerSm)
 }
 
 template <class C, class C2>
-static cudaError_t launch_wave(const DevTables &t, C c, C2 c2, int bias, int bias2, int fmt2, int average, uint32_t gen,
-                               uint32_t claim_base, uint32_t call_no, int lag, int grid, cudaStream_t s,
-                               bool cooperative)
+static cudaError_t launch_wave(const DevTables &t, C c, C2 c2, int bias, int bias2, int fmt2, int average,
+                               const WaveCall &w, int lag, int grid, cudaStream_t s, bool cooperative)
 {
-    uint32_t *cur = t.amax2 + (size_t)(gen & 1u) * t.n_layers;
-    uint32_t *other = t.amax2 + (size_t)((gen + 1u) & 1u) * t.n_layers;
-    auto kern = fused_p1_wave_kernel<C, C2, kThreads>;
+    auto kern = w.graph ? fused_p1_wave_kernel<C, C2, true, kThreads> : fused_p1_wave_kernel<C, C2, false, kThreads>;
     int flags = kFusedDefaultFlags;
     if (const char *env = std::getenv("APS_FUSED_FLAGS")) flags = std::atoi(env);
-    void *args[] = {const_cast<DevTables *>(&t), &c, &c2, &cur, &other, &claim_base, &call_no, &lag, &bias, &bias2,
-                    &fmt2, &average, &flags};
+    unsigned long long adv = 2ull * (unsigned long long)t.n_items + (unsigned long long)kWaveOvershoot * grid;
+    uint32_t *cur = t.amax2 + (size_t)(w.gen & 1u) * t.n_layers;
+    uint32_t *other = t.amax2 + (size_t)((w.gen + 1u) & 1u) * t.n_layers;
+    uint32_t claim_base = w.claim_base, call_no = w.call_no;
+    void *args[] = {const_cast<DevTables *>(&t), &c, &c2, &cur, &other, &claim_base, &call_no, &adv, &lag, &bias,
+                    &bias2, &fmt2, &average, &flags};
     // co-residency is not needed for progress (a CTA waits only on positions claimed
     // earlier, i.e. by running CTAs); a plain launch lets a concurrent group's kernel
     // fill this one's tail
@@ -1019,23 +1055,21 @@ static cudaError_t launch_wave(const DevTables &t, C c, C2 c2, int bias, int bia
     return cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(kThreads), args, 0, s);
 }
 
-cudaError_t launch_fused_p1_wave(const DevTables &t, int e, int m, bool hw, int average, uint32_t gen,
-                                 uint32_t claim_base, uint32_t call_no, int lag, int grid, cudaStream_t s,
-                                 bool cooperative)
+cudaError_t launch_fused_p1_wave(const DevTables &t, int e, int m, bool hw, int average, const WaveCall &w, int lag,
+                                 int grid, cudaStream_t s, bool cooperative)
 {
     const int bias = (1 << (e - 1)) - 1;
     return with_codec(e, m, hw, [&](auto c) -> cudaError_t {
-        return launch_wave(t, c, CNone{}, bias, 0, -1, average, gen, claim_base, call_no, lag, grid, s, cooperative);
+        return launch_wave(t, c, CNone{}, bias, 0, -1, average, w, lag, grid, s, cooperative);
     });
 }
 
 cudaError_t launch_fused_p1_wave_hybrid32(const DevTables &t, int e, int m, bool hw, int fmt2, int average,
-                                          uint32_t gen, uint32_t claim_base, uint32_t call_no, int lag, int grid,
-                                          cudaStream_t s)
+                                          const WaveCall &w, int lag, int grid, cudaStream_t s)
 {
     const int bias = (1 << (e - 1)) - 1;
     return with_codec(e, m, hw, [&](auto c) -> cudaError_t {
-        return launch_wave(t, c, CF32{}, bias, 127, fmt2, average, gen, claim_base, call_no, lag, grid, s, true);
+        return launch_wave(t, c, CF32{}, bias, 127, fmt2, average, w, lag, grid, s, true);
     });
 }
 
@@ -1083,7 +1117,7 @@ int fused_p1_wave_grid(int e, int m, bool hw, int n_items)
     int per_sm = 0;
     with_codec(e, m, hw, [&](auto c) -> cudaError_t {
         using C = decltype(c);
-        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_p1_wave_kernel<C, CNone, kThreads>,
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_p1_wave_kernel<C, CNone, false, kThreads>,
                                                              kThreads, 0);
     });
     per_sm = std::max(1, std::min(per_sm, kWaveCtasPerSm));

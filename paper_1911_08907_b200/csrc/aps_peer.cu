@@ -90,9 +90,14 @@ __device__ void wait_all(const PeerArgs &a, int slot, uint32_t epoch, uint32_t *
 }
 
 // ------------------------------------------------------------------ AllReduce(E, MAX)
-// post: E_local -> slot [epoch & 1][rank] of every rank, then flag kSlotE.
-__global__ void peer_post_E_kernel(PeerArgs a, const int32_t *E_local, int n_layers, uint32_t epoch)
+// post: the next E epoch; E_local -> slot [epoch & 1][rank] of every rank, then flag kSlotE.
+__global__ void peer_post_E_kernel(PeerArgs a, const int32_t *E_local, int n_layers)
 {
+    __shared__ uint32_t s_epoch;
+    uint32_t *mine = a.flags[a.rank];
+    if (threadIdx.x == 0) s_epoch = mine[kMineE] + 1u;
+    __syncthreads();
+    const uint32_t epoch = s_epoch;
     const size_t par = (size_t)(epoch & 1u) * (size_t)a.p + (size_t)a.rank;
     for (int q = 0; q < a.p; ++q) {
         int32_t *dst = a.eslots[q] + par * (size_t)n_layers;
@@ -100,14 +105,16 @@ __global__ void peer_post_E_kernel(PeerArgs a, const int32_t *E_local, int n_lay
     }
     __syncthreads();  // the CTA's stores precede thread 0's fence and releases (cumulativity)
     if (threadIdx.x == 0) {
+        mine[kMineE] = epoch;
         __threadfence_system();
         for (int q = 0; q < a.p; ++q) st_release_sys(a.flags[q] + kSlotE + a.rank, epoch);
     }
 }
 
-// collect: wait for every rank's post, E_glob = max over the slots.
-__global__ void peer_collect_E_kernel(PeerArgs a, int32_t *E_glob, int n_layers, uint32_t epoch, uint32_t *err_flag)
+// collect: wait for every rank's post of this rank's current E epoch, E_glob = max over the slots.
+__global__ void peer_collect_E_kernel(PeerArgs a, int32_t *E_glob, int n_layers, uint32_t *err_flag)
 {
+    const uint32_t epoch = a.flags[a.rank][kMineE];
     if (threadIdx.x == 0) wait_all(a, kSlotE, epoch, err_flag);
     __syncthreads();
     const int32_t *base = a.eslots[a.rank] + (size_t)(epoch & 1u) * (size_t)a.p * (size_t)n_layers;
@@ -119,16 +126,23 @@ __global__ void peer_collect_E_kernel(PeerArgs a, int32_t *E_glob, int n_layers,
 }
 
 // ------------------------------------------------------------------ signal / wait
-__global__ void peer_signal_kernel(PeerArgs a, int slot, uint32_t epoch)
+__global__ void peer_signal_kernel(PeerArgs a, int slot, int next)
 {
-    if (threadIdx.x == 0) __threadfence_system();
+    __shared__ uint32_t s_epoch;
+    uint32_t *mine = a.flags[a.rank];
+    if (threadIdx.x == 0) {
+        const uint32_t e = mine[kMineR] + (next ? 1u : 0u);
+        mine[kMineR] = e;
+        s_epoch = e;
+        __threadfence_system();
+    }
     __syncthreads();
-    for (int q = threadIdx.x; q < a.p; q += blockDim.x) st_release_sys(a.flags[q] + slot + a.rank, epoch);
+    for (int q = threadIdx.x; q < a.p; q += blockDim.x) st_release_sys(a.flags[q] + slot + a.rank, s_epoch);
 }
 
-__global__ void peer_wait_kernel(PeerArgs a, int slot, uint32_t epoch, uint32_t *err_flag)
+__global__ void peer_wait_kernel(PeerArgs a, int slot, uint32_t *err_flag)
 {
-    if (threadIdx.x == 0) wait_all(a, slot, epoch, err_flag);
+    if (threadIdx.x == 0) wait_all(a, slot, a.flags[a.rank][kMineR], err_flag);
 }
 
 // ------------------------------------------------------------------ the fold
@@ -558,29 +572,28 @@ cudaError_t launch_peer_reduce_sr(const PeerArgs &a, int64_t byte_off, int64_t t
 }
 
 // ------------------------------------------------------------------ launchers
-cudaError_t launch_peer_post_E(const PeerArgs &a, const int32_t *E_local, int n_layers, uint32_t epoch,
-                               cudaStream_t s)
+cudaError_t launch_peer_post_E(const PeerArgs &a, const int32_t *E_local, int n_layers, cudaStream_t s)
 {
-    peer_post_E_kernel<<<1, 1024, 0, s>>>(a, E_local, n_layers, epoch);
+    peer_post_E_kernel<<<1, 1024, 0, s>>>(a, E_local, n_layers);
     return cudaGetLastError();
 }
 
-cudaError_t launch_peer_collect_E(const PeerArgs &a, int32_t *E_glob, int n_layers, uint32_t epoch,
-                                  uint32_t *err_flag, cudaStream_t s)
+cudaError_t launch_peer_collect_E(const PeerArgs &a, int32_t *E_glob, int n_layers, uint32_t *err_flag,
+                                  cudaStream_t s)
 {
-    peer_collect_E_kernel<<<1, 1024, 0, s>>>(a, E_glob, n_layers, epoch, err_flag);
+    peer_collect_E_kernel<<<1, 1024, 0, s>>>(a, E_glob, n_layers, err_flag);
     return cudaGetLastError();
 }
 
-cudaError_t launch_peer_signal(const PeerArgs &a, int slot, uint32_t epoch, cudaStream_t s)
+cudaError_t launch_peer_signal(const PeerArgs &a, int slot, bool next, cudaStream_t s)
 {
-    peer_signal_kernel<<<1, 64, 0, s>>>(a, slot, epoch);
+    peer_signal_kernel<<<1, 64, 0, s>>>(a, slot, next ? 1 : 0);
     return cudaGetLastError();
 }
 
-cudaError_t launch_peer_wait(const PeerArgs &a, int slot, uint32_t epoch, uint32_t *err_flag, cudaStream_t s)
+cudaError_t launch_peer_wait(const PeerArgs &a, int slot, uint32_t *err_flag, cudaStream_t s)
 {
-    peer_wait_kernel<<<1, 32, 0, s>>>(a, slot, epoch, err_flag);
+    peer_wait_kernel<<<1, 32, 0, s>>>(a, slot, err_flag);
     return cudaGetLastError();
 }
 

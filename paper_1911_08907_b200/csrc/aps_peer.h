@@ -12,7 +12,11 @@ constexpr int kMaxPeers = 64;  // ranks reachable by load/store (8 on one NVSwit
 constexpr int kSlotE = 0;                   // [q]: rank q posted its E vector for epoch
 constexpr int kSlotReady = kMaxPeers;       // [q]: rank q's packed codes of epoch are complete
 constexpr int kSlotDone = 2 * kMaxPeers;    // [q]: rank q stored its reduced chunk into every rank
-constexpr int kFlagWords = 3 * kMaxPeers;
+constexpr int kMineE = 3 * kMaxPeers;       // this rank's own E-exchange epoch (device-resident)
+constexpr int kMineR = 3 * kMaxPeers + 1;   // this rank's own all-reduce epoch (device-resident)
+constexpr int kFlagWords = 3 * kMaxPeers + 2;
+// Epochs live on the device (incremented by post_E and by the ready signal), so a
+// captured CUDA graph of a sync replays correctly.
 
 struct PeerArgs {
     uint8_t *packed[kMaxPeers];   // every rank's packed buffer (own included), mapped into this process
@@ -22,12 +26,12 @@ struct PeerArgs {
     int p, rank, group_k;         // world, this rank, hierarchical group size (1 = flat ring)
 };
 
-cudaError_t launch_peer_post_E(const PeerArgs &a, const int32_t *E_local, int n_layers, uint32_t epoch,
-                               cudaStream_t s);
-cudaError_t launch_peer_collect_E(const PeerArgs &a, int32_t *E_glob, int n_layers, uint32_t epoch,
-                                  uint32_t *err_flag, cudaStream_t s);
-cudaError_t launch_peer_signal(const PeerArgs &a, int slot, uint32_t epoch, cudaStream_t s);
-cudaError_t launch_peer_wait(const PeerArgs &a, int slot, uint32_t epoch, uint32_t *err_flag, cudaStream_t s);
+cudaError_t launch_peer_post_E(const PeerArgs &a, const int32_t *E_local, int n_layers, cudaStream_t s);
+cudaError_t launch_peer_collect_E(const PeerArgs &a, int32_t *E_glob, int n_layers, uint32_t *err_flag,
+                                  cudaStream_t s);
+// raise flag `slot` at every rank with this rank's all-reduce epoch (incremented first if `next`)
+cudaError_t launch_peer_signal(const PeerArgs &a, int slot, bool next, cudaStream_t s);
+cudaError_t launch_peer_wait(const PeerArgs &a, int slot, uint32_t *err_flag, cudaStream_t s);
 // reduce n_tiles tiles of one format starting at tile0 / byte_off of the packed buffers
 cudaError_t launch_peer_reduce(const PeerArgs &a, int64_t byte_off, int64_t tile0, int64_t n_tiles, int e, int m,
                                bool hw, int acc_e, int acc_m, bool kahan, cudaStream_t s);

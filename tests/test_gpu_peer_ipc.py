@@ -44,7 +44,24 @@ def _worker(rank, world, port, group_k, iters, q):
             ctx.sync(dev, average=True)
             st = ctx.status_sync()
             outs.append((st, ctx.scales(), ctx.packed().cpu().numpy().copy(), [t.cpu().numpy() for t in dev]))
+        # the same sync captured in a CUDA graph (device-resident epochs): replays stay exact
+        st = torch.cuda.Stream()
+        gctx = aps.ApsContext(5, 2, NUMELS, world_size=world, rank=rank, stream=st)
+        gctx.connect_peers()
+        gctx.set_reduction(group_k)
+        gdev = [torch.zeros(n, device="cuda") for n in NUMELS]
+        graph = gctx.capture_sync(gdev)
+        for it in range(iters):
+            grads = synthetic.make_grads(NUMELS, world, seed=synthetic.SEED + it)
+            for t, a in zip(gdev, grads[rank]):
+                t.copy_(torch.from_numpy(a))
+            torch.cuda.synchronize()
+            dist.barrier()
+            graph.replay()
+            torch.cuda.synchronize()
+            outs[it] = outs[it] + ([t.cpu().numpy() for t in gdev], gctx.status_sync())
         dist.barrier()           # nobody unmaps a workspace a peer may still touch
+        gctx.close()
         ctx.close()
         dist.destroy_process_group()
         q.put((rank, outs))
@@ -77,8 +94,10 @@ def test_peer_transport_two_processes(orc, world, group_k):
         grads = synthetic.make_grads(NUMELS, world, seed=synthetic.SEED + it)
         ref = orc.aps_sync_ex(grads, 5, 2, average=1, group_k=group_k)
         for r in range(world):
-            st, ft, packed, outs = results[r][it]
-            assert st == 0
+            st, ft, packed, outs, gouts, gst = results[r][it]
+            assert st == 0 and gst == 0
+            for a, b in zip(gouts, ref.out):
+                assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
             assert np.array_equal(ft, ref.ftilde)
             assert np.array_equal(packed, ref.reduced)
             for a, b in zip(outs, ref.out):
