@@ -493,27 +493,70 @@ def main():
                                 "algorithmic bytes because phase B re-reads part of the gradients from L2 "
                                 "and dirty output lines are still in L2 when the kernel ends"}
 
-    # -------- e2e through aps_sync_host (pinned host buffers, copies inside)
-    hin = [torch.from_numpy(a).pin_memory() for a in host]
-    hout = [torch.empty_like(t).pin_memory() for t in hin]
-    for _ in range(2):
-        ctx.sync_host(hin, grads, hout, average=True)
+    # -------- e2e through aps_sync_host (pinned host buffers, copies inside).  Two contexts
+    # on two streams alternate steps, so step k's device->host copy overlaps step k+1's
+    # host->device copy (PCIe is full duplex); every step still moves all of its inputs in
+    # and all of its results out inside the timed region.
+    slots = 2 if (world == 1 or args.transport == "peer") else 1
+    ectx, dgr = [ctx], [grads]
+    for _ in range(slots - 1):
+        c2 = aps.ApsContext(e, m, numels, world_size=world, rank=rank, nccl_comm=comm,
+                            stream=torch.cuda.Stream(dev), device=dev, hw_convert=not args.no_hw, formats=fmts)
+        if world > 1:
+            c2.connect_peers()
+            c2.set_reduction(args.group_k, acc, args.kahan)
+        ectx.append(c2)
+        dgr.append([torch.empty_like(g) for g in grads])
+    # flat pinned host buffers with per-layer views (every ResNet-50 / BERT layer size is a
+    # multiple of 4 elements: 16-byte aligned views), as a training loop's flat gradient
+    # buffer; aps_sync_host then moves each direction in one copy
+    offs = [0]
+    for n in numels:
+        offs.append(offs[-1] + (n + 3) // 4 * 4)
+
+    def views(flat):
+        return [flat[offs[l]:offs[l] + n] for l, n in enumerate(numels)]
+
+    hin, hout = [], []
+    for _ in range(slots):
+        fi = torch.empty(offs[-1], dtype=torch.float32).pin_memory()
+        for v, a in zip(views(fi), host):
+            v.copy_(torch.from_numpy(a))
+        hin.append(views(fi))
+        hout.append(views(torch.empty(offs[-1], dtype=torch.float32).pin_memory()))
+    for sl in range(1, slots):   # the extra contexts' device gradients: one flat buffer too
+        dgr[sl] = views(torch.empty(offs[-1], dtype=torch.float32, device=dev))
+    dgr[0] = views(torch.empty(offs[-1], dtype=torch.float32, device=dev))
+    for sl in range(slots):
+        for _ in range(2):
+            ectx[sl].sync_host(hin[sl], dgr[sl], hout[sl], average=True)
     torch.cuda.synchronize()
-    E = args.e2e_steps
+    E = max(args.e2e_steps, slots)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
     e0.record(stream)
-    for _ in range(E):
-        ctx.sync_host(hin, grads, hout, average=True)
+    for c2 in ectx[1:]:
+        c2.stream.wait_event(e0)
+    for k in range(E):
+        sl = k % slots
+        ectx[sl].sync_host(hin[sl], dgr[sl], hout[sl], average=True)
+    for c2 in ectx[1:]:
+        ev = torch.cuda.Event()
+        ev.record(c2.stream)
+        stream.wait_event(ev)
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / E
     if world > 1:
         e2e_ms = max_over_ranks(e2e_ms)
+    for c2 in ectx[1:]:
+        if world > 1:
+            dist.barrier()
+        c2.close()
     e2e = {"value": round(world * 4 * L / (e2e_ms * 1e-3) / 1e9, 3), "unit": UNIT,
            "h2d_bytes_per_step": 4 * L, "d2h_bytes_per_step": 4 * L, "ms_per_step": round(e2e_ms, 4),
-           "api": "aps_sync_host"}
+           "api": "aps_sync_host", "pipelined_contexts": slots}
 
     G = len(set(fmts)) if fmts else 1  # one quantise / unscale / fused launch per format group
     if world == 1:

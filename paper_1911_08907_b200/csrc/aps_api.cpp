@@ -74,6 +74,8 @@ struct aps_ctx {
     uint32_t wave_calls = 0;   // wavefront launches so far (host mode: per-layer counter targets)
     bool graph_safe = false;   // wavefront kernel takes its per-call state from the device (aps_set_graph_safe)
     std::vector<unsigned long long> claim64_init;  // host staging of the 64-bit claim counters
+    std::vector<const void *> host_key;            // aps_sync_host: pointer set of the cached copy runs
+    std::vector<int> h2d_runs, d2h_runs;           // end layer of each coalesced copy
     bool iptr_valid = false;
     aps::DevTables t{};
     std::vector<const float *> src_cache;
@@ -815,19 +817,74 @@ aps_status aps_sync(aps_ctx *c, float *const *grads, int average)
     return aps_sync_out(c, const_cast<const float *const *>(grads), grads, average);
 }
 
+static cudaError_t alloc_base(void *p, uint8_t **base);
+
 aps_status aps_sync_host(aps_ctx *c, const float *const *host_in, float *const *dev_grads,
                          float *const *host_out, int average)
 {
     if (aps_status s = need_ws(c)) return s;
     if (!host_in || !dev_grads || !host_out) return fail(c, APS_ERR_ARG, "NULL pointer array");
-    for (int l = 0; l < c->n_layers; ++l)
-        APS_CUDA(c, cudaMemcpyAsync(dev_grads[l], host_in[l], 4 * (size_t)c->numels[l], cudaMemcpyHostToDevice,
-                                    c->stream));
+    // one copy per run of layers that are contiguous on both sides AND inside one
+    // allocation on both sides (a flat gradient buffer with per-layer views -- DDP's
+    // buckets -- moves in one transfer each way); runs are cached per pointer set
+    std::vector<const void *> key;
+    key.reserve(3 * (size_t)c->n_layers);
+    for (int l = 0; l < c->n_layers; ++l) {
+        key.push_back(host_in[l]);
+        key.push_back(dev_grads[l]);
+        key.push_back(host_out[l]);
+    }
+    if (key != c->host_key) {
+        auto runs_of = [&](const void *const *a, const void *const *b, std::vector<int> &runs) -> aps_status {
+            runs.clear();
+            int l = 0;
+            while (l < c->n_layers) {
+                uint8_t *ba = nullptr, *bb = nullptr;  // allocation bases (unknown: never merge)
+                const bool known = alloc_base(const_cast<void *>(a[l]), &ba) == cudaSuccess &&
+                                   alloc_base(const_cast<void *>(b[l]), &bb) == cudaSuccess;
+                (void)cudaGetLastError();
+                size_t bytes = 4 * (size_t)c->numels[l];
+                int k = l + 1;
+                while (known && k < c->n_layers &&
+                       static_cast<const char *>(a[k]) == static_cast<const char *>(a[l]) + bytes &&
+                       static_cast<const char *>(b[k]) == static_cast<const char *>(b[l]) + bytes) {
+                    uint8_t *ka = nullptr, *kb = nullptr;
+                    if (alloc_base(const_cast<void *>(a[k]), &ka) != cudaSuccess || ka != ba ||
+                        alloc_base(const_cast<void *>(b[k]), &kb) != cudaSuccess || kb != bb)
+                        break;
+                    bytes += 4 * (size_t)c->numels[k];
+                    ++k;
+                }
+                runs.push_back(k);
+                l = k;
+            }
+            return APS_OK;
+        };
+        if (aps_status s = runs_of(reinterpret_cast<const void *const *>(host_in),
+                                   reinterpret_cast<const void *const *>(dev_grads), c->h2d_runs))
+            return s;
+        if (aps_status s = runs_of(reinterpret_cast<const void *const *>(dev_grads),
+                                   reinterpret_cast<const void *const *>(host_out), c->d2h_runs))
+            return s;
+        c->host_key.swap(key);
+    }
+    auto copy_runs = [&](void *const *dst, const void *const *src, const std::vector<int> &runs,
+                         cudaMemcpyKind kind) -> aps_status {
+        int l = 0;
+        for (int k : runs) {
+            size_t bytes = 0;
+            for (int q = l; q < k; ++q) bytes += 4 * (size_t)c->numels[q];
+            APS_CUDA(c, cudaMemcpyAsync(dst[l], src[l], bytes, kind, c->stream));
+            l = k;
+        }
+        return APS_OK;
+    };
+    if (aps_status s = copy_runs(reinterpret_cast<void *const *>(dev_grads),
+                                 reinterpret_cast<const void *const *>(host_in), c->h2d_runs, cudaMemcpyHostToDevice))
+        return s;
     if (aps_status s = aps_sync(c, dev_grads, average)) return s;
-    for (int l = 0; l < c->n_layers; ++l)
-        APS_CUDA(c, cudaMemcpyAsync(host_out[l], dev_grads[l], 4 * (size_t)c->numels[l], cudaMemcpyDeviceToHost,
-                                    c->stream));
-    return APS_OK;
+    return copy_runs(reinterpret_cast<void *const *>(host_out), reinterpret_cast<const void *const *>(dev_grads),
+                     c->d2h_runs, cudaMemcpyDeviceToHost);
 }
 
 aps_status aps_status_sync(aps_ctx *c)

@@ -352,3 +352,32 @@ def test_p1_fused_schedules(aps, orc, schedule, monkeypatch):
             assert ctx.status_sync() == 0
             for a, b in zip(out, ref.out):
                 assert np.array_equal(a.cpu().numpy().view(np.uint32), b.view(np.uint32)), (schedule, it)
+
+
+def test_sync_host_flat_and_separate_buffers(aps, orc):
+    """aps_sync_host coalesces copies of layers contiguous inside one allocation
+    (flat buffers with per-layer views) and never across allocations (separate
+    tensors that happen to be adjacent): both bit-exact."""
+    numels = synthetic.C1_NUMELS + [1000, 4, 16384, 1024]
+    grads = synthetic.make_grads(numels, 1)
+    ref = orc.aps_sync(grads, 5, 2, average=1)
+    offs = np.concatenate([[0], np.cumsum(numels)])
+    fi = torch.from_numpy(np.concatenate(grads[0])).pin_memory()
+    fo = torch.empty_like(fi).pin_memory()
+    fd = torch.empty(fi.numel(), device="cuda")
+    hin = [fi[offs[l]:offs[l + 1]] for l in range(len(numels))]
+    hout = [fo[offs[l]:offs[l + 1]] for l in range(len(numels))]
+    dev = [fd[offs[l]:offs[l + 1]] for l in range(len(numels))]
+    for layout in ("flat", "separate", "flat"):
+        ctx = aps.ApsContext(5, 2, numels)
+        if layout == "separate":
+            hin = [torch.from_numpy(a).pin_memory() for a in grads[0]]
+            hout = [torch.empty_like(t).pin_memory() for t in hin]
+            dev = [torch.empty(t.shape, device="cuda") for t in hin]
+        for _ in range(2):
+            for h in hout:
+                h.zero_()
+            ctx.sync_host(hin, dev, hout, average=True)
+            torch.cuda.synchronize()
+            for a, b in zip(hout, ref.out):
+                assert np.array_equal(a.numpy().view(np.uint32), b.view(np.uint32)), layout
