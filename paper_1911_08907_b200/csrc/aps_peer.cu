@@ -220,7 +220,10 @@ __device__ __forceinline__ uint32_t h2_to_fp8x2(__half2 h)
 }
 
 template <bool E4M3, int NT>
-__global__ void __launch_bounds__(NT) peer_reduce_fp8h_kernel(PeerArgs a, int64_t byte_off, int64_t tile0,
+#ifndef APS_PEER_MINB
+#define APS_PEER_MINB 3  // measured: 2 -> 19 us, 3 -> 17.2 us, 4 (64 regs, spills) -> 19.5 us (profiles/r01_ab_peer_minblocks.txt)
+#endif
+__global__ void __launch_bounds__(NT, APS_PEER_MINB) peer_reduce_fp8h_kernel(PeerArgs a, int64_t byte_off, int64_t tile0,
                                                               int64_t n_vec)
 {
     constexpr int kBatch = 8;
@@ -638,7 +641,7 @@ cudaError_t launch_peer_reduce(const PeerArgs &a, int64_t byte_off, int64_t tile
     const bool ext = kahan || acc_e != e || acc_m != m;
     if (!ext && hw && ((e == 5 && m == 2) || (e == 4 && m == 3))) {
         const int64_t n_vec = n_tiles * 8;
-        const int grid = (int)std::min<int64_t>((n_vec + kThreads - 1) / kThreads, (int64_t)sm_count() * 2);
+        const int grid = (int)std::min<int64_t>((n_vec + kThreads - 1) / kThreads, (int64_t)sm_count() * APS_PEER_MINB);
         if (e == 5) peer_reduce_fp8h_kernel<false, kThreads><<<grid, kThreads, 0, s>>>(a, byte_off, tile0, n_vec);
         else peer_reduce_fp8h_kernel<true, kThreads><<<grid, kThreads, 0, s>>>(a, byte_off, tile0, n_vec);
         return cudaGetLastError();

@@ -13,3 +13,10 @@ ncu --set full --clock-control none --import-source on -k 'regex:stream_kernel|f
 ncu -i $OUT/prof_$TAG.ncu-rep --page raw --csv > $OUT/prof_${TAG}_raw.csv 2>&1
 ncu -i $OUT/prof_$TAG.ncu-rep --page details --csv > $OUT/prof_${TAG}_details.csv 2>&1
 echo profile done
+# peer transport (simulated p = 8, ResNet-50): launch list + full capture of the reduce kernel
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/peer_launches_$TAG.csv \
+    python scripts/peer_sim.py 8 2 > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:peer_reduce -s 8 -c 1 \
+    -o $OUT/peer_$TAG -f python scripts/peer_sim.py 8 3 > $OUT/ncu_peer_$TAG.log 2>&1
+ncu -i $OUT/peer_$TAG.ncu-rep --page raw --csv > $OUT/peer_${TAG}_raw.csv 2>&1
+echo peer profile done
