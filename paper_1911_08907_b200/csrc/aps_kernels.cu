@@ -264,9 +264,30 @@ __global__ void __launch_bounds__(NT) quant_pack_tile_kernel(DevTables t, C c, i
     }
 }
 
+#ifndef APS_UNPACK_HINT
+#define APS_UNPACK_HINT 2  // measured: plain 23.5 us, evict_first 21.1 us, .cs 21.0 us (profiles/r01_ab_unpack_store_hint.txt)
+#endif
+// output store of the unpack pass: 0 plain, 1 L2 evict_first policy, 2 .cs (streaming)
+__device__ __forceinline__ void st_out4(float4 *p, float4 v, uint64_t pol)
+{
+    if constexpr (APS_UNPACK_HINT == 1) {
+        asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(v.x),
+                     "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol)
+                     : "memory");
+    } else if constexpr (APS_UNPACK_HINT == 2) {
+        asm volatile("st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+                     : "memory");
+    } else {
+        (void)pol;
+        *p = v;
+    }
+}
+
 template <int B, class C, int NT>
 __global__ void __launch_bounds__(NT) unpack_unscale_direct_kernel(DevTables t, C c, int N, int avg)
 {
+    uint64_t pol = 0;
+    if constexpr (APS_UNPACK_HINT == 1) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     const Item it = t.items[blockIdx.x];
     const LayerDev L = t.layers[it.layer];
     float *o = t.dst[it.layer];
@@ -284,7 +305,7 @@ __global__ void __launch_bounds__(NT) unpack_unscale_direct_kernel(DevTables t, 
         for (int j = 0; j < kPer; ++j) w[j] = in[threadIdx.x + j * NT];
         float4 *o4 = reinterpret_cast<float4 *>(ob);
 #pragma unroll
-        for (int j = 0; j < kPer; ++j) o4[threadIdx.x + j * NT] = us.apply4(unpack4<B>(c, w[j]));
+        for (int j = 0; j < kPer; ++j) st_out4(o4 + threadIdx.x + j * NT, us.apply4(unpack4<B>(c, w[j])), pol);
     } else {
         const int64_t ng = (n + 3) / 4;
         for (int64_t gi = threadIdx.x; gi < ng; gi += NT)
