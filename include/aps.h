@@ -240,7 +240,8 @@ aps_status aps_set_rounding(aps_ctx *ctx, int mode, uint64_t seed);
  * every rank's packed buffer (the all-gather, fused).  NVLink bytes per rank
  * equal the ring's.  The exponent MAX (Alg. 1 line 4) goes through peer
  * memory too.  Cross-rank ordering uses monotone epoch flags (system-scope
- * release/acquire); every device wait gives up after 2 s (APS_ERR_STATE from
+ * release/acquire); every cross-rank device wait gives up after
+ * APS_PEER_TIMEOUT_S seconds (environment, default 120; APS_ERR_STATE from
  * aps_status_sync).  Bit-identical to the NCCL ring for the flat order.
  * Protocol: every rank calls aps_peer_export [sync] after aps_set_workspace,
  * the host gathers the world_size (handle, offset) pairs (e.g. over

@@ -1029,6 +1029,9 @@ static void peer_set(aps_ctx *c, int q, uint8_t *ws)
 
 static void peer_common(aps_ctx *c)
 {
+    double tmo = 120.0;
+    if (const char *v = std::getenv("APS_PEER_TIMEOUT_S")) tmo = std::atof(v);
+    c->pa.timeout_ns = (uint64_t)(std::max(0.001, tmo) * 1e9);
     c->pa.p = c->world;
     c->pa.rank = c->rank;
     c->pa.tiles = c->tiles;

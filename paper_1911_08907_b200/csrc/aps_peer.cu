@@ -85,8 +85,19 @@ __device__ __forceinline__ int32_t ld_relaxed_i32(const int32_t *p)
 __device__ void wait_all(const PeerArgs &a, int slot, uint32_t epoch, uint32_t *err_flag)
 {
     const uint32_t *f = a.flags[a.rank] + slot;
-    for (int q = 0; q < a.p; ++q)
-        spin_until([&] { return (int32_t)(ld_acquire_sys(f + q) - epoch) >= 0; }, err_flag);
+    for (int q = 0; q < a.p; ++q) {
+        // a peer may lag by far more than a kernel's own bookkeeping (stragglers, a rank
+        // still starting up): this bound is the transport's, not the 2 s kernel watchdog
+        if ((int32_t)(ld_acquire_sys(f + q) - epoch) >= 0) continue;
+        const uint64_t t0 = global_ns();
+        while ((int32_t)(ld_acquire_sys(f + q) - epoch) < 0) {
+            __nanosleep(64);
+            if (global_ns() - t0 > a.timeout_ns) {
+                atomicOr(err_flag, kFlagWaitTimeout);
+                return;
+            }
+        }
+    }
 }
 
 // ------------------------------------------------------------------ AllReduce(E, MAX)

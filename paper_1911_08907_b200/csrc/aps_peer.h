@@ -19,6 +19,7 @@ constexpr int kFlagWords = 3 * kMaxPeers + 2;
 // captured CUDA graph of a sync replays correctly.
 
 struct PeerArgs {
+    uint64_t timeout_ns;          // bound of a cross-rank wait (APS_PEER_TIMEOUT_S, default 120 s)
     uint8_t *packed[kMaxPeers];   // every rank's packed buffer (own included), mapped into this process
     uint32_t *flags[kMaxPeers];   // every rank's flag block
     int32_t *eslots[kMaxPeers];   // every rank's E slots: int32 [2][kMaxPeers][n_layers]

@@ -102,3 +102,51 @@ def test_peer_transport_two_processes(orc, world, group_k):
             assert np.array_equal(packed, ref.reduced)
             for a, b in zip(outs, ref.out):
                 assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+def _straggler_worker(rank, port, q, ev):
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), APS_PEER_TIMEOUT_S="1")
+        import torch
+        import torch.distributed as dist
+        import paper_1911_08907_b200 as aps
+        dist.init_process_group("gloo", rank=rank, world_size=2)
+        torch.cuda.set_device(0)
+        ctx = aps.ApsContext(5, 2, NUMELS, world_size=2, rank=rank)
+        ctx.connect_peers()
+        res = None
+        if rank == 0:   # rank 1 never joins the sync: every wait gives up after 1 s
+            dev = [torch.from_numpy(a).cuda() for a in synthetic.make_grads(NUMELS, 2)[0]]
+            ctx.sync(dev)
+            res = ctx.status_sync()
+            ev.set()
+        else:
+            ev.wait(120)   # stay alive (its workspace stays mapped) until rank 0 is done
+        dist.barrier()
+        ctx.close()
+        dist.destroy_process_group()
+        q.put((rank, res))
+    except Exception as exc:      # pragma: no cover
+        q.put((rank, repr(exc)))
+
+
+def test_peer_wait_times_out_on_a_missing_rank():
+    """A rank that never arrives: the waiting rank's device waits are bounded
+    (APS_PEER_TIMEOUT_S) and aps_status_sync reports APS_ERR_STATE (7)."""
+    ctx = mp.get_context("spawn")
+    q, ev = ctx.Queue(), ctx.Event()
+    port = _free_port()
+    procs = [ctx.Process(target=_straggler_worker, args=(r, port, q, ev)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = {}
+    try:
+        for _ in range(2):
+            r, res = q.get(timeout=240)
+            got[r] = res
+    finally:
+        for p in procs:
+            p.join(timeout=30)
+            if p.is_alive():
+                p.kill()
+    assert got[0] == 7, got
