@@ -8,8 +8,9 @@ APS layers (Alg. 1's per-layer exponents); a parameter whose view
 does not start 16-byte aligned is merged into the preceding layer (so the
 bucket may have fewer exponents than parameters -- P:230 allows several
 consecutive layers "as a whole tensor").  The buffer is synchronised in place
-by libaps (scale, Cast, packed ring over NCCL, unscale, average) on the
-current stream and returned.
+by libaps (scale, Cast, packed ring over NCCL -- or, with
+transport="peer", the owner-computes reduce over CUDA-IPC-mapped peer memory --
+unscale, average) on the current stream and returned.
 
 Usage:
     state = ApsHookState(process_group=None, exp_bits=5, man_bits=2)
@@ -26,13 +27,17 @@ class ApsHookState:
     for its ring (created here, collectively, outside backward), and one
     ApsContext per bucket (created on the bucket's first call)."""
 
-    def __init__(self, process_group=None, exp_bits: int = 5, man_bits: int = 2, average: bool = True):
+    def __init__(self, process_group=None, exp_bits: int = 5, man_bits: int = 2, average: bool = True,
+                 transport: str = "nccl", group_k: int = 1):
+        if transport not in ("nccl", "peer"):
+            raise ValueError("transport must be 'nccl' or 'peer'")
         self.pg = process_group if process_group is not None else dist.group.WORLD
         self.exp_bits, self.man_bits, self.average = exp_bits, man_bits, average
+        self.transport, self.group_k = transport, group_k
         self.world = dist.get_world_size(self.pg)
         self.rank = dist.get_rank(self.pg)
         self.comm = None
-        if self.world > 1:
+        if self.world > 1 and transport == "nccl":
             uid = [nccl_unique_id() if self.rank == 0 else None]
             dist.broadcast_object_list(uid, src=dist.get_global_rank(self.pg, 0), group=self.pg)
             self.comm = nccl_comm_init(uid[0], self.world, self.rank)
@@ -78,6 +83,11 @@ def aps_hook(state: ApsHookState, bucket: dist.GradBucket) -> torch.futures.Futu
             entry[0].close()
         ctx = ApsContext(state.exp_bits, state.man_bits, [n for _, n in spans], world_size=state.world,
                          rank=state.rank, nccl_comm=state.comm, device=buf.device)
+        if state.world > 1 and state.transport == "peer":
+            # every rank reaches this bucket's first sync together: map the workspaces
+            ctx.connect_peers(group=state.pg)
+        if state.group_k != 1:
+            ctx.set_reduction(state.group_k)
         state.contexts[idx] = (ctx, spans)
         state.groups[idx] = groups
         state.bucket_params[idx] = list(bucket.parameters())
