@@ -561,9 +561,9 @@ def main():
     G = len(set(fmts)) if fmts else 1  # one quantise / unscale / fused launch per format group
     if world == 1:
         launches_per_step = G
-    elif args.transport == "peer":  # absmax, post+collect E, G quantise, 2 x (signal, wait), own-chunk runs, G unscale
+    elif args.transport == "peer":  # absmax, E exchange, G quantise, 2 signal+wait, own-chunk runs, G unscale
         runs = format_runs(numels, fmts or [(e, m)] * len(numels), world, (rank + 2) % world)[0]
-        launches_per_step = 1 + 2 + 2 * G + 4 + runs
+        launches_per_step = 1 + 1 + 2 * G + 2 + runs
     else:  # absmax + G quantise + per ring step one reduce launch per format run of the chunk + G unscale
         launches_per_step = 1 + 2 * G + sum(format_runs(numels, fmts or [(e, m)] * len(numels), world, rank))
     result = {

@@ -543,8 +543,7 @@ static bool flat_reduction(const aps_ctx *c)
 // peer transport: announce this rank's packed codes, wait for every rank's
 static aps_status peer_ready(aps_ctx *c)
 {
-    APS_CUDA(c, aps::launch_peer_signal(c->pa, aps::kSlotReady, true, c->stream));
-    APS_CUDA(c, aps::launch_peer_wait(c->pa, aps::kSlotReady, c->t.flag, c->stream));
+    APS_CUDA(c, aps::launch_peer_signal_wait(c->pa, aps::kSlotReady, true, c->t.flag, c->stream));
     return APS_OK;
 }
 
@@ -613,11 +612,12 @@ aps_status aps_layer_scales(aps_ctx *c, const float *const *grads)
         c->phase = kScales;
     } else if (c->peer) {
         // AllReduce(max_grad_exp, MAX) over peer memory: post E to every rank, collect
-        APS_CUDA(c, aps::launch_peer_post_E(c->pa, c->t.E_local, c->n_layers, c->stream));
         if (c->sim) {
+            APS_CUDA(c, aps::launch_peer_post_E(c->pa, c->t.E_local, c->n_layers, c->stream));
             c->phase = kLocalScales;  // aps_sim_layer_scales collects after every rank posted
         } else {
-            APS_CUDA(c, aps::launch_peer_collect_E(c->pa, c->t.E_glob, c->n_layers, c->t.flag, c->stream));
+            APS_CUDA(c, aps::launch_peer_exchange_E(c->pa, c->t.E_local, c->t.E_glob, c->n_layers, c->t.flag,
+                                                    c->stream));
             c->phase = kScales;
         }
     } else if (c->sim) {
@@ -665,8 +665,7 @@ aps_status aps_allreduce(aps_ctx *c)
     if (c->peer) {
         if (aps_status s = peer_ready(c)) return s;
         if (aps_status s = peer_reduce_own(c)) return s;
-        APS_CUDA(c, aps::launch_peer_signal(c->pa, aps::kSlotDone, false, c->stream));
-        APS_CUDA(c, aps::launch_peer_wait(c->pa, aps::kSlotDone, c->t.flag, c->stream));
+        APS_CUDA(c, aps::launch_peer_signal_wait(c->pa, aps::kSlotDone, false, c->t.flag, c->stream));
         c->phase = kReduced;
         return APS_OK;
     }

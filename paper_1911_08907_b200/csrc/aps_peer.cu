@@ -156,6 +156,49 @@ __global__ void peer_wait_kernel(PeerArgs a, int slot, uint32_t *err_flag)
     if (threadIdx.x == 0) wait_all(a, slot, a.flags[a.rank][kMineR], err_flag);
 }
 
+// signal + wait in one launch (real ranks: every rank runs it concurrently; the
+// simulated ranks of one device need the two halves as separate launches)
+__global__ void peer_signal_wait_kernel(PeerArgs a, int slot, int next, uint32_t *err_flag)
+{
+    if (threadIdx.x != 0) return;
+    uint32_t *mine = a.flags[a.rank];
+    const uint32_t e = mine[kMineR] + (next ? 1u : 0u);
+    mine[kMineR] = e;
+    __threadfence_system();
+    for (int q = 0; q < a.p; ++q) st_release_sys(a.flags[q] + slot + a.rank, e);
+    wait_all(a, slot, e, err_flag);
+}
+
+// post + collect of the E exchange in one launch (real ranks)
+__global__ void peer_exchange_E_kernel(PeerArgs a, const int32_t *E_local, int32_t *E_glob, int n_layers,
+                                       uint32_t *err_flag)
+{
+    __shared__ uint32_t s_epoch;
+    uint32_t *mine = a.flags[a.rank];
+    if (threadIdx.x == 0) s_epoch = mine[kMineE] + 1u;
+    __syncthreads();
+    const uint32_t epoch = s_epoch;
+    const size_t par = (size_t)(epoch & 1u) * (size_t)a.p + (size_t)a.rank;
+    for (int q = 0; q < a.p; ++q) {
+        int32_t *dst = a.eslots[q] + par * (size_t)n_layers;
+        for (int l = threadIdx.x; l < n_layers; l += blockDim.x) dst[l] = E_local[l];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        mine[kMineE] = epoch;
+        __threadfence_system();
+        for (int q = 0; q < a.p; ++q) st_release_sys(a.flags[q] + kSlotE + a.rank, epoch);
+        wait_all(a, kSlotE, epoch, err_flag);
+    }
+    __syncthreads();
+    const int32_t *base = a.eslots[a.rank] + (size_t)(epoch & 1u) * (size_t)a.p * (size_t)n_layers;
+    for (int l = threadIdx.x; l < n_layers; l += blockDim.x) {
+        int32_t mx = INT32_MIN;
+        for (int q = 0; q < a.p; ++q) mx = max(mx, ld_relaxed_i32(base + (size_t)q * n_layers + l));
+        E_glob[l] = mx;
+    }
+}
+
 // ------------------------------------------------------------------ the fold
 // Reduction schedule of one tile: rank of the j-th addend of group gi.
 struct Order {
@@ -602,6 +645,19 @@ cudaError_t launch_peer_collect_E(const PeerArgs &a, int32_t *E_glob, int n_laye
 cudaError_t launch_peer_signal(const PeerArgs &a, int slot, bool next, cudaStream_t s)
 {
     peer_signal_kernel<<<1, 64, 0, s>>>(a, slot, next ? 1 : 0);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_peer_signal_wait(const PeerArgs &a, int slot, bool next, uint32_t *err_flag, cudaStream_t s)
+{
+    peer_signal_wait_kernel<<<1, 32, 0, s>>>(a, slot, next ? 1 : 0, err_flag);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_peer_exchange_E(const PeerArgs &a, const int32_t *E_local, int32_t *E_glob, int n_layers,
+                                   uint32_t *err_flag, cudaStream_t s)
+{
+    peer_exchange_E_kernel<<<1, 1024, 0, s>>>(a, E_local, E_glob, n_layers, err_flag);
     return cudaGetLastError();
 }
 

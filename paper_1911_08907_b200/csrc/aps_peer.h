@@ -33,6 +33,10 @@ cudaError_t launch_peer_collect_E(const PeerArgs &a, int32_t *E_glob, int n_laye
 // raise flag `slot` at every rank with this rank's all-reduce epoch (incremented first if `next`)
 cudaError_t launch_peer_signal(const PeerArgs &a, int slot, bool next, cudaStream_t s);
 cudaError_t launch_peer_wait(const PeerArgs &a, int slot, uint32_t *err_flag, cudaStream_t s);
+// real ranks (all running concurrently): signal + wait, and post + collect, as one launch each
+cudaError_t launch_peer_signal_wait(const PeerArgs &a, int slot, bool next, uint32_t *err_flag, cudaStream_t s);
+cudaError_t launch_peer_exchange_E(const PeerArgs &a, const int32_t *E_local, int32_t *E_glob, int n_layers,
+                                   uint32_t *err_flag, cudaStream_t s);
 // reduce n_tiles tiles of one format starting at tile0 / byte_off of the packed buffers
 cudaError_t launch_peer_reduce(const PeerArgs &a, int64_t byte_off, int64_t tile0, int64_t n_tiles, int e, int m,
                                bool hw, int acc_e, int acc_m, bool kahan, cudaStream_t s);
