@@ -25,6 +25,12 @@
  *                         and all-gather of the packed codes
  *   aps_unscale        -> Cast back, unscale, average
  *   aps_sync           -> the four in order
+ * Transports for the all-reduce (N > 1): an NCCL ring (nccl_comm) or peer
+ * memory (aps_peer_export / aps_peer_import: owner-computes reduce over
+ * NVLink load/store).  Variants: per-layer formats
+ * (aps_init_mixed), reduction order and accumulator (aps_set_reduction),
+ * stochastic rounding (aps_set_rounding); analysis: aps_census,
+ * aps_round_off_error; CUDA-graph capture: aps_set_graph_safe.
  *
  * CONVENTIONS
  *  - Memory: every tensor pointer is a DEVICE pointer unless the name says
