@@ -284,6 +284,7 @@ def main():
                          device=dev, hw_convert=not args.no_hw, formats=fmts)
     acc = tuple(map(int, args.acc.split(","))) if args.acc else None
     transport = args.transport
+    os.environ.setdefault("APS_PEER_TIMEOUT_S", "20")  # a failed peer wait must not stall the bench for minutes
     if world > 1 and transport in ("auto", "peer"):
         try:
             ctx.connect_peers()
@@ -319,21 +320,39 @@ def main():
 
     # the timed step is the user's call: aps_sync_out (grads -> outs; at N = 1 one fused launch),
     # or the replay of that call captured in a CUDA graph (--graph)
-    use_graph = args.graph if args.graph is not None else int(world > 1)
+    want_graph = args.graph if args.graph is not None else int(world > 1)
     graph_note = None
-    step_fn = lambda: ctx.sync_out(grads, outs, average=True)
-    if use_graph:
-        try:
-            graph = ctx.capture_sync(grads, outs, average=True)
-            step_fn = graph.replay
-        except Exception as exc:  # capture unsupported here: time the plain calls
-            graph_note = f"capture failed ({exc}); plain calls timed"
-            use_graph = 0
-            torch.cuda.synchronize()
-    for _ in range(max(args.warmup, 3)):
-        step_fn()
-    if ctx.status_sync() != 0:
-        raise SystemExit("non-finite flag raised on synthetic data")
+
+    def prepare():
+        nonlocal graph_note
+        fn, g = (lambda: ctx.sync_out(grads, outs, average=True)), 0
+        if want_graph:
+            try:
+                graph = ctx.capture_sync(grads, outs, average=True)
+                fn, g = graph.replay, 1
+            except Exception as exc:  # capture unsupported here: time the plain calls
+                graph_note = f"capture failed ({exc}); plain calls timed"
+                torch.cuda.synchronize()
+        for _ in range(max(args.warmup, 3)):
+            fn()
+        return fn, g, ctx.status_sync()
+
+    step_fn, use_graph, st = prepare()
+    if world > 1:
+        # every rank must have synchronised cleanly; if the peer transport failed on any rank
+        # (a timed-out wait reads as APS_ERR_STATE), all ranks fall back to the NCCL ring together
+        okt = torch.tensor([1.0 if st == 0 else 0.0], dtype=torch.float64, device="cpu" if same_gpu else dev)
+        dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+        if okt.item() < 1.0 and args.transport == "peer" and comm is not None:
+            print(f"[bench] peer transport failed at warm-up (status {st}); using the NCCL ring", file=sys.stderr)
+            ctx.close()
+            ctx = aps.ApsContext(e, m, numels, world_size=world, rank=rank, nccl_comm=comm, stream=stream,
+                                 device=dev, hw_convert=not args.no_hw, formats=fmts)
+            args.transport = "nccl"
+            graph_note = (graph_note or "") + " peer transport failed at warm-up: NCCL ring timed"
+            step_fn, use_graph, st = prepare()
+    if st != 0:
+        raise SystemExit(f"sync reported status {st} on synthetic data")
     torch.cuda.synchronize()
 
     K = args.steps
