@@ -349,6 +349,7 @@ def main():
             ctx = aps.ApsContext(e, m, numels, world_size=world, rank=rank, nccl_comm=comm, stream=stream,
                                  device=dev, hw_convert=not args.no_hw, formats=fmts)
             args.transport = "nccl"
+            ctx.set_reduction(args.group_k, acc, args.kahan)  # same reduction order as requested
             graph_note = (graph_note or "") + " peer transport failed at warm-up: NCCL ring timed"
             step_fn, use_graph, st = prepare()
     if st != 0:
