@@ -122,6 +122,13 @@ __global__ void absmax_finish_kernel(DevTables t, int N)
 #define APS_ABS_ITEMS 4
 #endif
 constexpr int kAbsItemsPerCta = APS_ABS_ITEMS;
+// A/B switch: APS_ABS_STREAM loads a1's gradients with the streaming hint instead of
+// L2 evict_last (which keeps them for quant_pack's re-read)
+#ifdef APS_ABS_STREAM
+#define APS_ABS_LD(p, pol) ld_stream4(p)
+#else
+#define APS_ABS_LD(p, pol) ld_keep4(p, pol)
+#endif
 
 __device__ __forceinline__ float4 ld_keep4(const float4 *p, uint64_t pol)
 {
@@ -168,12 +175,12 @@ __global__ void __launch_bounds__(NT, 6) absmax_ranges_kernel(DevTables t, int N
         if (it.cnt == kItemTiles * kTile) {
             float4 v[kPer];
 #pragma unroll
-            for (int j = 0; j < kPer; ++j) v[j] = ld_keep4(g4 + threadIdx.x + j * NT, keep);
+            for (int j = 0; j < kPer; ++j) v[j] = APS_ABS_LD(g4 + threadIdx.x + j * NT, keep);
 #pragma unroll
             for (int j = 0; j < kPer; ++j) mx = max(mx, absbits4(v[j]));
         } else {
             const int n4 = it.cnt >> 2;
-            for (int j = threadIdx.x; j < n4; j += NT) mx = max(mx, absbits4(ld_keep4(g4 + j, keep)));
+            for (int j = threadIdx.x; j < n4; j += NT) mx = max(mx, absbits4(APS_ABS_LD(g4 + j, keep)));
             if ((int)threadIdx.x < (it.cnt & 3)) mx = max(mx, __float_as_uint(g[4 * n4 + threadIdx.x]) & 0x7fffffffu);
         }
         run = max(run, __reduce_max_sync(0xffffffffu, mx));
