@@ -36,7 +36,7 @@ def build(force: bool = False) -> Path:
         subprocess.check_call(
             ["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-fno-fast-math",
              "-ffp-contract=off", "-fexcess-precision=standard", "-Wall", "-Wextra",
-             "-o", str(tmp), str(SRC), "-lm"])
+             "-pthread", "-o", str(tmp), str(SRC), "-lm"])
         os.replace(tmp, LIB)
     return LIB
 
@@ -75,7 +75,7 @@ def lib():
         L.oracle_pack.argtypes = [vp, i64, ctypes.c_int, vp]
         L.oracle_unpack.argtypes = [vp, i64, ctypes.c_int, vp]
         L.oracle_aps_sync.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp,
-                                      vp, ctypes.c_int, vp, vp, vp, vp]
+                                      vp, ctypes.c_int, vp, vp, vp, vp, ctypes.c_int]
         L.oracle_ring_add_n.argtypes = [vp, vp, vp, i64, ctypes.c_int, ctypes.c_int]
         L.oracle_unscale_n.argtypes = [vp, vp, i64, i32, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int]
         L.oracle_scale_cast_n.argtypes = [vp, vp, i64, i32, ctypes.c_int, ctypes.c_int]
@@ -203,12 +203,13 @@ class SyncResult:
 
 
 def aps_sync(grads, e: int, m: int, average: int = 1, want_packed: bool = True,
-             want_out: bool = True) -> SyncResult:
+             want_out: bool = True, n_threads: int = 1) -> SyncResult:
     """Full APS sync (Alg. 1) over p simulated ranks.
 
     ``grads[r][l]`` is rank r's fp32 gradient of layer l (numpy).  Returns the
     scale exponents f~, each rank's packed codes, the reduced packed codes
     every rank ends with, and the unscaled/averaged fp32 outputs.
+    ``n_threads`` splits the element loops over threads (bit-identical results).
     """
     p = len(grads)
     nl = len(grads[0])
@@ -223,7 +224,7 @@ def aps_sync(grads, e: int, m: int, average: int = 1, want_packed: bool = True,
     optrs = (ctypes.c_void_p * nl)(*[a.ctypes.data for a in outs]) if want_out else None
     rc = lib().oracle_aps_sync(p, e, m, nl, _ptr(numels), gptrs, average, _ptr(ft),
                                _ptr(packed) if want_packed else None, _ptr(reduced),
-                               optrs)
+                               optrs, int(n_threads))
     return SyncResult(rc, ft, packed, reduced, outs)
 
 

@@ -30,6 +30,7 @@
  */
 #include <float.h>
 #include <math.h>
+#include <pthread.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -292,62 +293,170 @@ int oracle_unpack(const uint8_t *buf, int64_t n, int b, uint32_t *codes)
 /* rank's codes after Cast, O11); reduced_out: packed_bytes or NULL    */
 /* (the codes every rank holds after the all-reduce, O8/O9); out:      */
 /* n_layers host pointers (fp32), or NULL.                             */
+/* n_threads >= 1: the element loops of each step are split into       */
+/* contiguous ranges run by that many threads (every element's         */
+/* arithmetic is independent of the split, and a maximum is            */
+/* order-independent, so the results are bit-identical for any         */
+/* n_threads -- pinned by tests/test_oracle_aps.py).                   */
 /* Returns OR_OK, OR_ERR_ARG, OR_ERR_FORMAT or OR_ERR_NONFINITE.       */
 /* ------------------------------------------------------------------ */
+
+/* a contiguous element range [i0, i1) of layer l of rank r */
+typedef struct { int r, l; int64_t i0, i1; } or_range;
+
+typedef struct {
+    int p, e, m, n_layers, average, n_threads, tid;
+    const int64_t *numels;
+    const float *const *grads;
+    const int64_t *tile_off;   /* first tile of each layer (O7) */
+    const int32_t *ft;
+    const or_range *rng;       /* the step's ranges */
+    int64_t n_rng;
+    int32_t *rng_E;            /* step 1: FindMaxExp of each range */
+    uint32_t *q;               /* [p][ncodes] Cast codes */
+    uint32_t *s;               /* [ncodes] reduced codes */
+    int64_t ncodes, chunk_codes;
+    float *const *out;
+    int step;
+} or_job;
+
+#define OR_RANGE 262144 /* elements per range of the threaded steps */
+
+static void *or_worker(void *arg)
+{
+    const or_job *J = (const or_job *)arg;
+    if (J->step == 1) {        /* Alg. 1 line 3: FindMaxExp(g * N) of each range */
+        for (int64_t k = J->tid; k < J->n_rng; k += J->n_threads) {
+            const or_range R = J->rng[k];
+            J->rng_E[k] = oracle_find_max_exp(J->grads[(size_t)R.r * J->n_layers + R.l] + R.i0, R.i1 - R.i0, J->p);
+        }
+    } else if (J->step == 2) { /* Alg. 1 lines 5-6: Cast(g * 2^f~) into the O7 layout */
+        for (int64_t k = J->tid; k < J->n_rng; k += J->n_threads) {
+            const or_range R = J->rng[k];
+            const float *g = J->grads[(size_t)R.r * J->n_layers + R.l];
+            uint32_t *dst = J->q + (size_t)R.r * J->ncodes + J->tile_off[R.l] * OR_TILE;
+            for (int64_t i = R.i0; i < R.i1; ++i) dst[i] = oracle_cast1(oracle_scale(g[i], J->ft[R.l]), J->e, J->m);
+        }
+    } else if (J->step == 3) { /* Alg. 1 line 7: the ring sum, element by element */
+        const int64_t lo = J->ncodes * J->tid / J->n_threads, hi = J->ncodes * (J->tid + 1) / J->n_threads;
+        for (int64_t i = lo; i < hi; ++i) {
+            const int c = (int)(i / J->chunk_codes); /* the chunk (and owner) of code i */
+            uint32_t acc = J->q[(size_t)((c + 1) % J->p) * J->ncodes + i];
+            for (int j = 2; j <= J->p; ++j)
+                acc = oracle_ring_add(acc, J->q[(size_t)((c + j) % J->p) * J->ncodes + i], J->e, J->m);
+            J->s[i] = acc;
+        }
+    } else {                   /* Alg. 1 lines 8-9: Cast back, unscale, average */
+        for (int64_t k = J->tid; k < J->n_rng; k += J->n_threads) {
+            const or_range R = J->rng[k];
+            const uint32_t *src = J->s + J->tile_off[R.l] * OR_TILE;
+            for (int64_t i = R.i0; i < R.i1; ++i)
+                J->out[R.l][i] = oracle_unscale1(src[i], J->ft[R.l], J->p, J->average, J->e, J->m);
+        }
+    }
+    return NULL;
+}
+
+/* run step `step` of job J on J->n_threads threads (the calling thread is one of them) */
+static void or_run(or_job *J, int step)
+{
+    const int nt = J->n_threads;
+    or_job *jobs = (or_job *)malloc(sizeof(or_job) * (size_t)nt);
+    pthread_t *th = (pthread_t *)malloc(sizeof(pthread_t) * (size_t)nt);
+    for (int t = 0; t < nt; ++t) {
+        jobs[t] = *J;
+        jobs[t].tid = t;
+        jobs[t].step = step;
+    }
+    for (int t = 1; t < nt; ++t) pthread_create(&th[t], NULL, or_worker, &jobs[t]);
+    or_worker(&jobs[0]);
+    for (int t = 1; t < nt; ++t) pthread_join(th[t], NULL);
+    free(jobs);
+    free(th);
+}
+
+/* ranges of <= OR_RANGE elements covering every (rank < pr, layer) */
+static or_range *or_ranges(int pr, int n_layers, const int64_t *numels, int64_t *n_out)
+{
+    int64_t n = 0;
+    for (int l = 0; l < n_layers; ++l) n += (int64_t)pr * ((numels[l] + OR_RANGE - 1) / OR_RANGE);
+    or_range *R = (or_range *)malloc(sizeof(or_range) * (size_t)n);
+    int64_t k = 0;
+    for (int r = 0; r < pr; ++r)
+        for (int l = 0; l < n_layers; ++l)
+            for (int64_t i0 = 0; i0 < numels[l]; i0 += OR_RANGE) {
+                R[k].r = r;
+                R[k].l = l;
+                R[k].i0 = i0;
+                R[k].i1 = i0 + OR_RANGE < numels[l] ? i0 + OR_RANGE : numels[l];
+                ++k;
+            }
+    *n_out = n;
+    return R;
+}
+
 int oracle_aps_sync(int p, int e, int m, int n_layers, const int64_t *numels,
                     const float *const *grads, int average, int32_t *ftilde_out,
-                    uint8_t *packed_out, uint8_t *reduced_out, float *const *out)
+                    uint8_t *packed_out, uint8_t *reduced_out, float *const *out, int n_threads)
 {
     if (oracle_format_valid(e, m)) return OR_ERR_FORMAT;
-    if (p < 1 || n_layers < 1 || !numels || !grads) return OR_ERR_ARG;
+    if (p < 1 || n_layers < 1 || !numels || !grads || n_threads < 1) return OR_ERR_ARG;
     for (int l = 0; l < n_layers; ++l)
         if (numels[l] < 1) return OR_ERR_ARG;
 
     const int b = 1 + e + m;
     const int64_t Tp = oracle_total_tiles(p, n_layers, numels); /* T' */
     const int64_t ncodes = Tp * OR_TILE;
-    const int64_t chunk_codes = (Tp / p) * OR_TILE;
     const int64_t nbytes = 16 * (int64_t)b * Tp;
+    int64_t *tile_off = (int64_t *)malloc(sizeof(int64_t) * (size_t)n_layers);
+    for (int l = 0, t = 0; l < n_layers; ++l) {
+        tile_off[l] = t;
+        t += (int)((numels[l] + OR_TILE - 1) / OR_TILE);
+    }
+    or_job J;
+    memset(&J, 0, sizeof J);
+    J.p = p; J.e = e; J.m = m; J.n_layers = n_layers; J.average = average; J.n_threads = n_threads;
+    J.numels = numels; J.grads = grads; J.tile_off = tile_off;
+    J.ncodes = ncodes; J.chunk_codes = (Tp / p) * OR_TILE; J.out = out;
 
     /* Alg. 1 line 3: max_grad_exp <- FindMaxExp(g * N), on every rank;
-     * line 4: AllReduce(max_grad_exp, MAX). */
+     * line 4: AllReduce(max_grad_exp, MAX).  (The max over ranges equals
+     * FindMaxExp of the whole layer: ceil(log2(N x)) is monotone in x.) */
     int32_t *E = (int32_t *)malloc(sizeof(int32_t) * (size_t)n_layers);
     int32_t *ft = (int32_t *)malloc(sizeof(int32_t) * (size_t)n_layers);
+    int64_t n_rng;
+    or_range *rng = or_ranges(p, n_layers, numels, &n_rng);
+    int32_t *rng_E = (int32_t *)malloc(sizeof(int32_t) * (size_t)n_rng);
+    J.rng = rng; J.n_rng = n_rng; J.rng_E = rng_E;
+    or_run(&J, 1);
     int nonfinite = 0;
+    for (int l = 0; l < n_layers; ++l) E[l] = OR_EMPTY;
+    for (int64_t k = 0; k < n_rng; ++k) {
+        if (rng_E[k] == OR_NONFINITE) nonfinite = 1;
+        if (rng_E[k] > E[rng[k].l]) E[rng[k].l] = rng_E[k];
+    }
     for (int l = 0; l < n_layers; ++l) {
-        int32_t Emax = OR_EMPTY;
-        for (int r = 0; r < p; ++r) {
-            int32_t Er = oracle_find_max_exp(grads[(size_t)r * n_layers + l], numels[l], p);
-            if (Er == OR_NONFINITE) nonfinite = 1;
-            if (Er > Emax) Emax = Er;
-        }
-        E[l] = Emax;
-        ft[l] = oracle_scale_exp(e, Emax); /* f~ <- upper_bound_exp - E */
+        ft[l] = oracle_scale_exp(e, E[l]); /* f~ <- upper_bound_exp - E */
         if (ftilde_out) ftilde_out[l] = ft[l];
     }
+    free(rng_E);
     if (nonfinite) { /* A4: outputs unspecified, the error is reported */
-        free(E); free(ft);
+        free(E); free(ft); free(rng); free(tile_off);
         return OR_ERR_NONFINITE;
     }
+    J.ft = ft;
 
     /* Alg. 1 lines 5-6: g <- g * 2^f~ ; low_g <- Cast(g, exp_bit, man_bit),
      * placed in the O7 layout (padding codes are +0). */
     uint32_t *q = (uint32_t *)calloc((size_t)p * (size_t)ncodes, sizeof(uint32_t));
-    for (int r = 0; r < p; ++r) {
-        int64_t tile_off = 0;
-        for (int l = 0; l < n_layers; ++l) {
-            const float *g = grads[(size_t)r * n_layers + l];
-            uint32_t *dst = q + (size_t)r * ncodes + tile_off * OR_TILE;
-            for (int64_t i = 0; i < numels[l]; ++i)
-                dst[i] = oracle_cast1(oracle_scale(g[i], ft[l]), e, m);
-            tile_off += (numels[l] + OR_TILE - 1) / OR_TILE;
-        }
-        if (packed_out) {
+    J.q = q;
+    or_run(&J, 2);
+    if (packed_out)
+        for (int r = 0; r < p; ++r) {
             uint8_t *pk = packed_out + (size_t)r * (size_t)nbytes;
             memset(pk, 0, (size_t)nbytes);
             oracle_pack(q + (size_t)r * ncodes, ncodes, b, pk);
         }
-    }
 
     /* Alg. 1 line 7: low_g <- AllReduce(low_g, SUM), as a ring with
      * the low-precision accumulator re-quantising after each add.
@@ -356,14 +465,8 @@ int oracle_aps_sync(int p, int e, int m, int n_layers, const int64_t *numels,
      * nodes' local gradients in the last step").  O9: every rank then holds
      * the same codes. */
     uint32_t *s = (uint32_t *)calloc((size_t)ncodes, sizeof(uint32_t));
-    for (int c = 0; c < p; ++c) {
-        for (int64_t i = c * chunk_codes; i < (c + 1) * chunk_codes; ++i) {
-            uint32_t acc = q[(size_t)((c + 1) % p) * ncodes + i];
-            for (int j = 2; j <= p; ++j)
-                acc = oracle_ring_add(acc, q[(size_t)((c + j) % p) * ncodes + i], e, m);
-            s[i] = acc;
-        }
-    }
+    J.s = s;
+    or_run(&J, 3);
     if (reduced_out) {
         memset(reduced_out, 0, (size_t)nbytes);
         oracle_pack(s, ncodes, b, reduced_out);
@@ -371,15 +474,12 @@ int oracle_aps_sync(int p, int e, int m, int n_layers, const int64_t *numels,
 
     /* Alg. 1 lines 8-9: g <- Cast(low_g, 8, 23); g <- g / 2^f~; average. */
     if (out) {
-        int64_t tile_off = 0;
-        for (int l = 0; l < n_layers; ++l) {
-            const uint32_t *src = s + tile_off * OR_TILE;
-            for (int64_t i = 0; i < numels[l]; ++i)
-                out[l][i] = oracle_unscale1(src[i], ft[l], p, average, e, m);
-            tile_off += (numels[l] + OR_TILE - 1) / OR_TILE;
-        }
+        free(rng);
+        rng = or_ranges(1, n_layers, numels, &n_rng);
+        J.rng = rng; J.n_rng = n_rng;
+        or_run(&J, 4);
     }
-    free(q); free(s); free(E); free(ft);
+    free(q); free(s); free(E); free(ft); free(rng); free(tile_off);
     return OR_OK;
 }
 

@@ -205,8 +205,11 @@ class ApsContext:
             raise ApsError(st, "aps_init")
         self.h = h
         nbytes = self.L.aps_workspace_bytes(h)
-        # torch's caching allocator returns >= 512-byte aligned blocks
-        self.workspace = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.device)
+        # torch's caching allocator returns >= 512-byte aligned blocks.  Allocated on the
+        # context's stream, where every kernel that touches it runs: when the context is
+        # dropped the block is recycled only after that stream's pending work
+        with torch.cuda.stream(self.stream):
+            self.workspace = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.device)
         base = self.workspace.data_ptr()
         self._ws_ptr = (base + 255) // 256 * 256
         self._check(self.L.aps_set_workspace(h, self._ws_ptr, nbytes), "aps_set_workspace")
@@ -221,6 +224,14 @@ class ApsContext:
 
     @staticmethod
     def _ptrs(tensors):
+        if isinstance(tensors, ctypes.Array):  # already marshalled (ApsContext.ptr_array)
+            return tensors
+        return _ptr_array([t.data_ptr() for t in tensors])
+
+    @staticmethod
+    def ptr_array(tensors):
+        """Marshal a list of layer tensors once into the host pointer array the calls take
+        (pass it instead of the list to skip the per-call marshalling of many layers)."""
         return _ptr_array([t.data_ptr() for t in tensors])
 
     def close(self):

@@ -13,7 +13,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = Path(os.environ.get("APS_BUILD_OUT", PKG / "libaps.so"))  # APS_BUILD_OUT / APS_NVCC_EXTRA: A/B variants
-SOURCES = [CSRC / "aps_kernels.cu", CSRC / "aps_stream.cu", CSRC / "aps_peer.cu", CSRC / "aps_api.cpp"]
+SOURCES = [CSRC / "aps_kernels.cu", CSRC / "aps_fused.cu", CSRC / "aps_peer.cu", CSRC / "aps_api.cpp"]
 HEADERS = [CSRC / "aps_numerics.cuh", CSRC / "aps_device.cuh", CSRC / "aps_internal.h", CSRC / "aps_peer.h",
            ROOT / "include" / "aps.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

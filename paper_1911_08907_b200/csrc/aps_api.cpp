@@ -40,6 +40,8 @@ struct aps_ctx {
     std::vector<int64_t> numels;
     std::vector<aps::Item> items;
     std::vector<aps::LayerDev> layers;
+    std::vector<int64_t> voff;    // [n_layers + 1] a1's vector space (4 fp32 per vector, per layer)
+    std::vector<int32_t> cta_layer;  // a1: layer of each CTA's first vector
     int64_t tiles = 0;        // T' (padded to a multiple of world)
     int64_t packed_bytes = 0; // sum over tiles of 16 * b(tile)
     int64_t chunk_bytes = 0;  // packed_bytes / world (uniform formats)
@@ -68,9 +70,8 @@ struct aps_ctx {
     uint8_t *ws = nullptr;
     size_t ws_bytes = 0, need = 0;
     size_t off_packed = 0, off_recv = 0, off_items = 0, off_layers = 0, off_src = 0, off_dst = 0,
-           off_amax = 0, off_count = 0, off_eloc = 0, off_eglob = 0, off_ft = 0, off_flag = 0, off_amax2 = 0, off_done = 0, off_iptr = 0, off_tl = 0, off_claim = 0, off_ldone = 0, off_claim64 = 0;
+           off_amax = 0, off_eloc = 0, off_eglob = 0, off_ft = 0, off_flag = 0, off_amax2 = 0, off_iptr = 0, off_tl = 0, off_claim = 0, off_ldone = 0, off_claim64 = 0, off_voff = 0, off_ctal = 0, off_bdone = 0, off_srcall = 0;
     int max_layer_items = 0;
-    uint32_t claim_base = 0;   // value of the fused kernel's claim counters at the next launch
     uint32_t wave_calls = 0;   // wavefront launches so far (host mode: per-layer counter targets)
     bool graph_safe = false;   // wavefront kernel takes its per-call state from the device (aps_set_graph_safe)
     std::vector<unsigned long long> claim64_init;  // host staging of the 64-bit claim counters
@@ -81,12 +82,7 @@ struct aps_ctx {
     std::vector<const float *> src_cache;
     std::vector<float *> dst_cache;
     int phase = kNone;
-    // kernel engine: "ldg" (default: grid kernels + the fused p = 1 LDG kernel),
-    // "tma" (persistent TMA-bulk kernels, aps_stream.cu), "simple" (grid kernels only)
-    enum Engine { kLdg = 0, kTma = 1, kSimple = 2 } engine = kLdg;
-    bool stream_engine = false;
-    uint32_t gen = 0;           // abs-max-pass launches so far (selects the accumulator parity)
-    uint32_t done_target = 0;   // value the CTA-done counter reaches at the end of the current pass
+    uint32_t gen = 0;           // fused launches so far (selects the accumulator parity)
     // format groups after the first run on side streams, concurrently with group 0
     // (disjoint layers, packed bytes and counters): fork/join through events
     std::vector<cudaStream_t> side;
@@ -105,6 +101,7 @@ struct aps_ctx {
     std::vector<void *> ipc_mapped;     // cudaIpcOpenMemHandle mappings (closed by aps_destroy)
     size_t off_pflags = 0, off_eslots = 0, off_census = 0;
     std::string err;
+    bool stream_owned_ok() const { return ws != nullptr; }  // a workspace was attached: kernels may be queued
     ~aps_ctx()
     {
         for (void *p : ipc_mapped) cudaIpcCloseMemHandle(p);
@@ -228,14 +225,7 @@ static aps_status init_common(aps_ctx **out, const int *e_arr, const int *m_arr,
     c->comm = static_cast<ncclComm_t>(nccl_comm);
     c->sim = (world_size > 1 && !nccl_comm);
     c->stream = static_cast<cudaStream_t>(cuda_stream);
-    if (const char *env = std::getenv("APS_HW_CVT")) c->hw_enabled = std::atoi(env) != 0;
     c->hw = c->hw_enabled && aps::hw_available(c->e, c->m);
-    if (const char *env = std::getenv("APS_ENGINE")) {
-        if (!std::strcmp(env, "tma") || !std::strcmp(env, "stream")) c->engine = aps_ctx::kTma;
-        else if (!std::strcmp(env, "simple")) c->engine = aps_ctx::kSimple;
-        else c->engine = aps_ctx::kLdg;
-    }
-    c->stream_engine = c->engine == aps_ctx::kTma;
     if (c->comm) {
         int nr = 0;
         if (ncclCommCount(c->comm, &nr) != ncclSuccess || nr != world_size) {
@@ -359,17 +349,19 @@ static aps_status init_common(aps_ctx **out, const int *e_arr, const int *m_arr,
     c->off_src = o;    o = align_up(o + sizeof(void *) * (size_t)n_layers);
     c->off_dst = o;    o = align_up(o + sizeof(void *) * (size_t)n_layers);
     c->off_amax = o;   o = align_up(o + 4 * (size_t)n_layers);
-    c->off_count = o;  o = align_up(o + 4 * (size_t)n_layers);
     c->off_eloc = o;   o = align_up(o + 4 * (size_t)n_layers);
     c->off_eglob = o;  o = align_up(o + 4 * (size_t)n_layers);
     c->off_ft = o;     o = align_up(o + 4 * (size_t)n_layers);
     c->off_flag = o;   o = align_up(o + 4);
     c->off_amax2 = o;  o = align_up(o + 8 * (size_t)n_layers);
-    c->off_done = o;   o = align_up(o + 4);
     c->off_iptr = o;   o = align_up(o + sizeof(aps::ItemPtr) * c->items.size());
     c->off_tl = o;     o = align_up(o + sizeof(uint64_t) * aps::kTimelineSlots);
     c->off_claim = o;  o = align_up(o + 3 * sizeof(uint32_t) * c->groups.size());  // 3 per format group
     c->off_ldone = o;  o = align_up(o + 4 * (size_t)n_layers);
+    c->off_voff = o;   o = align_up(o + 8 * ((size_t)n_layers + 1));
+    c->off_bdone = o;  o = align_up(o + 4 * (size_t)n_layers);
+    c->off_srcall = o; o = align_up(o + 4);
+    c->off_ctal = o;   o = align_up(o + 4 * (size_t)aps::kAbsMaxCtas);
     // graph-safe counters: 64-bit wavefront claim counter per format group, absmax_ranges done counter
     c->off_claim64 = o; o = align_up(o + 8 * c->groups.size() + 4);
     // peer transport: flag block and E slots [2][world][n_layers] (world > 1 only)
@@ -380,6 +372,8 @@ static aps_status init_common(aps_ctx **out, const int *e_arr, const int *m_arr,
     c->acc_m = c->m;
 
     for (const auto &L : c->layers) c->max_layer_items = std::max(c->max_layer_items, (int)L.n_items);
+    c->voff.assign(1, 0);
+    for (int l = 0; l < n_layers; ++l) c->voff.push_back(c->voff.back() + (numels[l] + 3) / 4);
     c->need = o;
     *out = c;
     return APS_OK;
@@ -434,26 +428,43 @@ aps_status aps_set_workspace(aps_ctx *c, void *dev, size_t bytes)
                                 cudaMemcpyHostToDevice, c->stream));
     APS_CUDA(c, cudaMemcpyAsync(c->ws + c->off_layers, c->layers.data(),
                                 sizeof(aps::LayerDev) * c->layers.size(), cudaMemcpyHostToDevice, c->stream));
+    {   // a1's balanced split: CTA b streams vectors [b V / G, (b+1) V / G)
+        const int G = aps::absmax_grid();
+        const int64_t V = c->voff.back();
+        c->cta_layer.resize(G);
+        int l = 0;
+        for (int b = 0; b < G; ++b) {
+            const int64_t lo = V * b / G;
+            while (l < c->n_layers - 1 && c->voff[l + 1] <= lo) ++l;
+            c->cta_layer[b] = l;
+        }
+        APS_CUDA(c, cudaMemcpyAsync(c->ws + c->off_voff, c->voff.data(), 8 * c->voff.size(), cudaMemcpyHostToDevice,
+                                    c->stream));
+        APS_CUDA(c, cudaMemcpyAsync(c->ws + c->off_ctal, c->cta_layer.data(), 4 * (size_t)G, cudaMemcpyHostToDevice,
+                                    c->stream));
+    }
     aps::DevTables &t = c->t;
     t.items = reinterpret_cast<const aps::Item *>(c->ws + c->off_items);
     t.layers = reinterpret_cast<const aps::LayerDev *>(c->ws + c->off_layers);
     t.src = reinterpret_cast<const float *const *>(c->ws + c->off_src);
     t.dst = reinterpret_cast<float *const *>(c->ws + c->off_dst);
     t.amax = reinterpret_cast<uint32_t *>(c->ws + c->off_amax);
-    t.count = reinterpret_cast<uint32_t *>(c->ws + c->off_count);
     t.E_local = reinterpret_cast<int32_t *>(c->ws + c->off_eloc);
     // one rank: the global exponent vector IS the local one (no collective, no copy)
     t.E_glob = reinterpret_cast<int32_t *>(c->ws + (c->world == 1 ? c->off_eloc : c->off_eglob));
     t.ftilde = reinterpret_cast<int32_t *>(c->ws + c->off_ft);
     t.flag = reinterpret_cast<uint32_t *>(c->ws + c->off_flag);
     t.amax2 = reinterpret_cast<uint32_t *>(c->ws + c->off_amax2);
-    t.done = reinterpret_cast<uint32_t *>(c->ws + c->off_done);
     t.iptr = reinterpret_cast<aps::ItemPtr *>(c->ws + c->off_iptr);
     t.timeline = reinterpret_cast<uint64_t *>(c->ws + c->off_tl);
     t.claim = reinterpret_cast<uint32_t *>(c->ws + c->off_claim);
     t.claim64 = reinterpret_cast<unsigned long long *>(c->ws + c->off_claim64);
     t.ranges_done = reinterpret_cast<uint32_t *>(c->ws + c->off_claim64 + 8 * c->groups.size());
     t.layer_done = reinterpret_cast<uint32_t *>(c->ws + c->off_ldone);
+    t.voff = reinterpret_cast<const int64_t *>(c->ws + c->off_voff);
+    t.bdone = reinterpret_cast<uint32_t *>(c->ws + c->off_bdone);
+    t.sr_call = reinterpret_cast<uint32_t *>(c->ws + c->off_srcall);
+    t.cta_layer = reinterpret_cast<const int32_t *>(c->ws + c->off_ctal);
 
     if (c->groups.size() > 1 && c->side.empty()) {
         c->side.resize(c->groups.size() - 1);
@@ -464,13 +475,11 @@ aps_status aps_set_workspace(aps_ctx *c, void *dev, size_t bytes)
         }
         APS_CUDA(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     }
-    c->claim_base = 0;
     c->wave_calls = 0;
     c->graph_safe = false;
     for (auto &g : c->groups) g.wave_claim_base = 0;
     c->iptr_valid = false;
     c->gen = 0;
-    c->done_target = 0;
     t.packed = c->ws + c->off_packed;
     t.n_items = (int)c->items.size();
     t.n_layers = c->n_layers;
@@ -496,16 +505,12 @@ static aps::DevTables group_tables(const aps_ctx *c, const aps_ctx::Group &g)
 // context's stream, the others forked onto side streams and joined back (they
 // touch disjoint layers, packed bytes and claim counters), so a small group (the
 // FP32 classifier of the hybrid format) runs in the tail of the big one instead of
-// after it.  The TMA engine's kernels share the CTA-done counter: serialised.
+// after it.
 extern "C++" {
 template <class F>
 static aps_status for_groups(aps_ctx *c, F launch)
 {
-    static const bool serial_env = [] {
-        const char *v = std::getenv("APS_GROUP_STREAMS");
-        return v && std::atoi(v) == 0;
-    }();
-    const bool concurrent = c->groups.size() > 1 && !c->side.empty() && !c->stream_engine && !serial_env;
+    const bool concurrent = c->groups.size() > 1 && !c->side.empty();
     if (concurrent) {
         APS_CUDA(c, cudaEventRecord(c->ev_fork, c->stream));
         for (cudaStream_t s : c->side) APS_CUDA(c, cudaStreamWaitEvent(s, c->ev_fork, 0));
@@ -554,7 +559,7 @@ static aps_status peer_reduce_own(aps_ctx *c)
     if (c->sr) {
         for (const auto &sg : c->chunk_segs[c->rank])
             APS_CUDA(c, aps::launch_peer_reduce_sr(c->pa, sg.byte_off, sg.tile0, sg.n_tiles, sg.e, sg.m, c->sr_seed,
-                                                   c->stream));
+                                                   c->t.sr_call, c->stream));
         return APS_OK;
     }
     for (const auto &sg : c->chunk_segs[c->rank])
@@ -575,39 +580,12 @@ aps_status aps_set_hw_convert(aps_ctx *c, int enable)
     return APS_OK;
 }
 
-// a1 kernel of the separate-call path: "ranges" (default: 4-item ranges with an L2
-// evict_last hint and a done counter) or "plain" (APS_ABSMAX=plain: one streaming CTA per
-// item + a finisher kernel).  Measured (profiles/r01_ab_absmax_plain_vs_ranges.txt): plain
-// 24.2 us vs 23.8 us, and without the evict_last hint the quantise pass loses its L2 hits
-// (21.1 us vs 17.1 us).
-static bool absmax_plain()
-{
-    static const bool v = [] {
-        const char *e = std::getenv("APS_ABSMAX");
-        return e && !std::strcmp(e, "plain");
-    }();
-    return v;
-}
-
 aps_status aps_layer_scales(aps_ctx *c, const float *const *grads)
 {
     if (aps_status s = need_ws(c)) return s;
     if (!grads) return fail(c, APS_ERR_ARG, "grads is NULL");
     if (aps_status s = upload_ptrs<const float *>(c, c->src_cache, grads, c->off_src)) return s;
-    if (c->stream_engine) {
-        // commit the counter target only if the launch was accepted (a skipped
-        // increment would make a later pass wait forever)
-        const uint32_t tgt = c->done_target + (uint32_t)aps::stream_grid(c->t.n_items);
-        APS_CUDA(c, aps::launch_stream_absmax(c->t, c->world, c->gen, tgt, c->stream));
-        c->done_target = tgt;
-        ++c->gen;
-    } else if (c->engine == aps_ctx::kLdg && absmax_plain()) {
-        APS_CUDA(c, aps::launch_absmax_plain(c->t, c->world, c->stream));
-    } else if (c->engine == aps_ctx::kLdg) {
-        APS_CUDA(c, aps::launch_absmax_ranges(c->t, c->world, c->stream));
-    } else {
-        APS_CUDA(c, aps::launch_absmax_exp(c->t, c->world, c->stream));
-    }
+    APS_CUDA(c, aps::launch_absmax(c->t, c->world, c->stream));
     if (c->world == 1 && !c->comm) {
         c->phase = kScales;
     } else if (c->peer) {
@@ -644,9 +622,7 @@ aps_status aps_quantize_pack(aps_ctx *c, const float *const *grads)
     }
     // one launch per format group (NEXT-2)
     if (aps_status s = for_groups(c, [&](const aps_ctx::Group &g, const aps::DevTables &t, cudaStream_t st, bool) {
-            cudaError_t e = c->stream_engine ? aps::launch_stream_quant(t, g.e, g.m, g.hw, st) : cudaErrorNotSupported;
-            if (e == cudaErrorNotSupported) e = aps::launch_quant_pack(t, g.e, g.m, g.hw, st);
-            return e;
+            return aps::launch_quant_pack(t, g.e, g.m, g.hw, st);
         }))
         return s;
     c->phase = kPacked;
@@ -714,93 +690,87 @@ aps_status aps_unscale(aps_ctx *c, float *const *out, int average)
     if (!out) return fail(c, APS_ERR_ARG, "out is NULL");
     if (aps_status s = upload_ptrs<float *>(c, c->dst_cache, out, c->off_dst)) return s;
     if (aps_status s = for_groups(c, [&](const aps_ctx::Group &g, const aps::DevTables &t, cudaStream_t st, bool) {
-            cudaError_t e = c->stream_engine ? aps::launch_stream_unpack(t, g.e, g.m, g.hw, c->world, average, st)
-                                             : cudaErrorNotSupported;
-            if (e == cudaErrorNotSupported) e = aps::launch_unpack_unscale(t, g.e, g.m, g.hw, c->world, average, st);
-            return e;
+            return aps::launch_unpack_unscale(t, g.e, g.m, g.hw, c->world, average, st);
         }))
         return s;
+    // stochastic rounding: this sync is done, the next one draws with the next key (A27)
+    if (c->sr) APS_CUDA(c, aps::launch_sr_advance(c->t.sr_call, c->stream));
     return APS_OK;
+}
+
+// the paper's hybrid precision (one low format + the FP32 classifier layer) runs as ONE
+// wavefront launch whose binary32 items switch codec inside the kernel: the group index
+// of the FP32 layers, or -1
+static int hybrid_fp32_group(const aps_ctx *c)
+{
+    if (c->groups.size() != 2) return -1;
+    for (int g = 0; g < 2; ++g)
+        if (c->groups[g].e == 8 && c->groups[g].m == 23 && c->groups[g].hw &&
+            !(c->groups[1 - g].e == 8 && c->groups[1 - g].m == 23))
+            return g;
+    return -1;
 }
 
 aps_status aps_sync_out(aps_ctx *c, const float *const *grads, float *const *out, int average)
 {
     if (aps_status s = need_ws(c)) return s;
     if (!grads || !out) return fail(c, APS_ERR_ARG, "NULL pointer array");
-    if (c->world == 1 && !c->comm && c->engine == aps_ctx::kLdg && !c->sr) {
-        // one rank: FindMaxExp -> f~ -> Cast -> pack -> Cast back -> unscale in one launch
+    if (c->world == 1 && !c->comm && !c->sr) {
+        // one rank: FindMaxExp -> f~ -> Cast -> pack -> Cast back -> unscale in one
+        // wavefront launch per format group (quantise items trail their abs-max items by
+        // D positions; a layer's items never straddle groups)
         if (aps_status s = upload_ptrs<const float *>(c, c->src_cache, grads, c->off_src)) return s;
         if (aps_status s = upload_ptrs<float *>(c, c->dst_cache, out, c->off_dst)) return s;
         if (!c->iptr_valid) {
             APS_CUDA(c, aps::launch_build_item_ptrs(c->t, c->stream));
             c->iptr_valid = true;
         }
-        const char *sched = std::getenv("APS_FUSED_SCHEDULE");
-        if (!c->uniform || !sched || std::strcmp(sched, "barrier") != 0) {
-            // wavefront: quantise items trail their abs-max items by D positions;
-            // one launch per format group (a layer's items never straddle groups)
-            // the paper's hybrid precision (one low format + the FP32 classifier layer):
-            // ONE launch, binary32 items switch codec inside the kernel
-            static const bool hybrid_fuse = [] {
-                const char *v = std::getenv("APS_HYBRID_FUSE");
-                return !v || std::atoi(v) != 0;
-            }();
-            int fp32_group = -1;
-            if (c->groups.size() == 2 && hybrid_fuse)
-                for (int g = 0; g < 2; ++g)
-                    if (c->groups[g].e == 8 && c->groups[g].m == 23 && c->groups[g].hw &&
-                        !(c->groups[1 - g].e == 8 && c->groups[1 - g].m == 23))
-                        fp32_group = g;
-            if (fp32_group >= 0) {
-                const aps_ctx::Group &lo = c->groups[1 - fp32_group];
-                aps_ctx::Group &g0 = c->groups[0];  // its claim counter serves the single launch
-                const int wgrid = aps::fused_p1_wave_grid(lo.e, lo.m, lo.hw, c->t.n_items);
-                const int lag = std::min(c->t.n_items, c->max_layer_items + wgrid);
-                const aps::WaveCall w{c->graph_safe, c->gen, g0.wave_claim_base, c->wave_calls};
-                APS_CUDA(c, aps::launch_fused_p1_wave_hybrid32(c->t, lo.e, lo.m, lo.hw, fp32_group, average, w, lag,
-                                                               wgrid, c->stream));
-                g0.wave_claim_base += (uint32_t)(2 * c->t.n_items + aps::kWaveOvershoot * wgrid);
-                ++c->wave_calls;
-                ++c->gen;
-                c->phase = kReduced;
-                return APS_OK;
-            }
-            // one launch per format group, each with its own claim counter
-            if (aps_status s = for_groups(c, [&](const aps_ctx::Group &gc, const aps::DevTables &t, cudaStream_t st,
-                                                 bool coop) {
-                    aps_ctx::Group &g = const_cast<aps_ctx::Group &>(gc);
-                    const int wgrid = aps::fused_p1_wave_grid(g.e, g.m, g.hw, t.n_items);
-                    const int lag = std::min(t.n_items, g.max_layer_items + wgrid);
-                    const aps::WaveCall w{c->graph_safe, c->gen, g.wave_claim_base, c->wave_calls};
-                    cudaError_t e = aps::launch_fused_p1_wave(t, g.e, g.m, g.hw, average, w, lag, wgrid, st, coop);
-                    // every position is claimed once and every CTA overshoots kWaveOvershoot times
-                    if (e == cudaSuccess) g.wave_claim_base += (uint32_t)(2 * t.n_items + aps::kWaveOvershoot * wgrid);
-                    return e;
-                }))
-                return s;
+        // In graph-safe mode the kernel takes its claim base from the 64-bit device
+        // counter and never touches the 32-bit one: wave_claim_base must not advance then
+        // (aps_set_graph_safe(0) resumes host mode from it).
+        const int fp32_group = hybrid_fp32_group(c);
+#if APS_FUSED_W2
+        if (fp32_group >= 0) {
+            const aps_ctx::Group &lo = c->groups[1 - fp32_group];
+            APS_CUDA(c, aps::launch_fused_w2_hybrid32(c->t, lo.e, lo.m, lo.hw, fp32_group, average, c->max_layer_items,
+                                                      c->stream));
+        } else {
+            // one cooperative launch per format group, in order on the context's stream
+            for (const auto &g : c->groups)
+                APS_CUDA(c, aps::launch_fused_w2(group_tables(c, g), g.e, g.m, g.hw, average, g.max_layer_items,
+                                                 c->stream));
+        }
+        c->phase = kReduced;
+        return APS_OK;
+#endif
+        if (fp32_group >= 0) {
+            const aps_ctx::Group &lo = c->groups[1 - fp32_group];
+            aps_ctx::Group &g0 = c->groups[0];  // its claim counter serves the single launch
+            const int wgrid = aps::fused_p1_wave_grid(lo.e, lo.m, lo.hw, c->t.n_items);
+            const int lag = std::min(c->t.n_items, c->max_layer_items + aps::kWaveLagGrids * wgrid);
+            const aps::WaveCall w{c->graph_safe, c->gen, g0.wave_claim_base, c->wave_calls};
+            APS_CUDA(c, aps::launch_fused_p1_wave_hybrid32(c->t, lo.e, lo.m, lo.hw, fp32_group, average, w, lag,
+                                                           wgrid, c->stream));
+            if (!c->graph_safe) g0.wave_claim_base += (uint32_t)(2 * c->t.n_items + aps::kWaveOvershoot * wgrid);
             ++c->wave_calls;
             ++c->gen;
             c->phase = kReduced;
             return APS_OK;
         }
-        const int grid = aps::fused_p1_ldg_grid(c->e, c->m, c->hw, c->t.n_items);
-        const uint32_t tgt = c->done_target + (uint32_t)grid * (uint32_t)aps::kFusedWarps;
-        APS_CUDA(c, aps::launch_fused_p1_ldg(c->t, c->e, c->m, c->hw, average, c->gen, tgt, c->claim_base, grid,
-                                             c->stream));
-        c->done_target = tgt;
-        // each call claims every unit once and every CTA overshoots once
-        c->claim_base += (uint32_t)(c->t.n_items * (aps::kItemTiles / aps::kFusedUnitTiles) + grid);
-        ++c->gen;
-        c->phase = kReduced;
-        return APS_OK;
-    }
-    if (c->world == 1 && !c->comm && c->stream_engine && !c->sr && c->uniform && aps::stream_fused_supported(c->e, c->m, c->hw)) {
-        // one rank: FindMaxExp -> f~ -> Cast -> pack -> Cast back -> unscale in one launch
-        if (aps_status s = upload_ptrs<const float *>(c, c->src_cache, grads, c->off_src)) return s;
-        if (aps_status s = upload_ptrs<float *>(c, c->dst_cache, out, c->off_dst)) return s;
-        const uint32_t tgt = c->done_target + (uint32_t)aps::stream_grid(2 * c->t.n_items);
-        APS_CUDA(c, aps::launch_stream_fused_p1(c->t, c->e, c->m, c->hw, average, c->gen, tgt, c->stream));
-        c->done_target = tgt;
+        if (aps_status s = for_groups(c, [&](const aps_ctx::Group &gc, const aps::DevTables &t, cudaStream_t st,
+                                             bool coop) {
+                aps_ctx::Group &g = const_cast<aps_ctx::Group &>(gc);
+                const int wgrid = aps::fused_p1_wave_grid(g.e, g.m, g.hw, t.n_items);
+                const int lag = std::min(t.n_items, g.max_layer_items + aps::kWaveLagGrids * wgrid);
+                const aps::WaveCall w{c->graph_safe, c->gen, g.wave_claim_base, c->wave_calls};
+                cudaError_t e = aps::launch_fused_p1_wave(t, g.e, g.m, g.hw, average, w, lag, wgrid, st, coop);
+                // every position is claimed once and every CTA overshoots kWaveOvershoot times
+                if (e == cudaSuccess && !c->graph_safe)
+                    g.wave_claim_base += (uint32_t)(2 * t.n_items + aps::kWaveOvershoot * wgrid);
+                return e;
+            }))
+            return s;
+        ++c->wave_calls;
         ++c->gen;
         c->phase = kReduced;
         return APS_OK;
@@ -960,15 +930,7 @@ aps_status aps_set_graph_safe(aps_ctx *c, int enable)
     const bool on = enable != 0;
     if (on == c->graph_safe) return APS_OK;
     // the hybrid single launch (one low format + FP32) uses group 0's counter for all items
-    bool hybrid_single = false;
-    if (c->groups.size() == 2) {
-        const char *v = std::getenv("APS_HYBRID_FUSE");
-        const bool fuse = !v || std::atoi(v) != 0;
-        for (int g = 0; g < 2; ++g)
-            if (fuse && c->groups[g].e == 8 && c->groups[g].m == 23 && c->groups[g].hw &&
-                !(c->groups[1 - g].e == 8 && c->groups[1 - g].m == 23))
-                hybrid_single = true;
-    }
+    const bool hybrid_single = hybrid_fp32_group(c) >= 0;
     if (on) {  // device counters := the host's call count, so both modes agree on call index and parity
         c->claim64_init.resize(c->groups.size());
         for (size_t g = 0; g < c->groups.size(); ++g)
@@ -976,7 +938,10 @@ aps_status aps_set_graph_safe(aps_ctx *c, int enable)
         APS_CUDA(c, cudaMemcpyAsync(c->t.claim64, c->claim64_init.data(), 8 * c->groups.size(),
                                     cudaMemcpyHostToDevice, c->stream));
         APS_CUDA(c, cudaStreamSynchronize(c->stream));
-    } else {   // back to host mode: the call count the device reached (graph replays included)
+    } else {
+        // back to host mode: the call count the device reached (graph replays included).
+        // The 32-bit claim counters were not touched in graph mode, so wave_claim_base
+        // (not advanced by graph-mode calls) still equals them.
         unsigned long long v = 0;
         APS_CUDA(c, cudaMemcpyAsync(&v, c->t.claim64, 8, cudaMemcpyDeviceToHost, c->stream));
         APS_CUDA(c, cudaStreamSynchronize(c->stream));
@@ -995,6 +960,7 @@ aps_status aps_set_rounding(aps_ctx *c, int mode, uint64_t seed)
         return fail(c, APS_ERR_ARG, "stochastic rounding needs one format and the wire-format accumulator");
     c->sr = mode == 1;
     c->sr_seed = seed;
+    if (c->ws) APS_CUDA(c, cudaMemsetAsync(c->t.sr_call, 0, 4, c->stream));  // call k = 0 draws with SplitMix64(seed, 0)
     return APS_OK;
 }
 
@@ -1105,6 +1071,13 @@ aps_status aps_round_off_error(const float *h, const float *l, int64_t n, double
 
 aps_status aps_destroy(aps_ctx *c)
 {
+    // kernels still queued on the context's streams may read peer workspaces through the
+    // IPC mappings ~aps_ctx closes: drain them first
+    if (c && c->stream_owned_ok()) {
+        cudaStreamSynchronize(c->stream);
+        for (cudaStream_t s : c->side) cudaStreamSynchronize(s);
+        (void)cudaGetLastError();
+    }
     delete c;
     return APS_OK;
 }

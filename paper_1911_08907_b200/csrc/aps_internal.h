@@ -9,7 +9,6 @@ namespace aps {
 constexpr int kTile = 128;        // codes per tile (layout rule, aps.h)
 constexpr int kItemTiles = 64;    // tiles per work item (one CTA): 8192 elements
 constexpr int kThreads = 256;
-constexpr int kFusedCtasPerSm = 4;  // fused p = 1 LDG kernel: 4 x 256 threads per SM (64 regs each)
 
 // One work item = a tile-aligned slice of one layer (<= kItemTiles tiles).
 // Flat descriptor, precomputed on the host, so a kernel needs one load (no
@@ -48,30 +47,32 @@ struct DevTables {
     const float *const *src;  // [n_layers] gradient pointers
     float *const *dst;        // [n_layers] output pointers
     uint32_t *amax;           // [n_layers] running abs-max bits (self-resetting)
-    uint32_t *count;          // [n_layers] finished-CTA counters (self-resetting)
     int32_t *E_local;         // [n_layers]
     int32_t *E_glob;          // [n_layers]
     int32_t *ftilde;          // [n_layers]
     uint32_t *flag;           // non-finite flag
-    uint32_t *amax2;          // [2][n_layers] abs-max accumulators of the stream engine (call parity)
-    uint32_t *done;           // CTAs that finished the abs-max pass (monotone counter)
+    uint32_t *amax2;          // [2][n_layers] abs-max accumulators of the fused kernel (call parity)
     ItemPtr *iptr;            // [n_items] per-item addresses (fused LDG kernel)
     uint64_t *timeline;       // [kTimelineSlots] per-CTA phase stamps (flag 16)
-    uint32_t *claim;          // [3] monotone work-claim counters: barrier kernel phase A, phase B; wavefront
+    uint32_t *claim;          // [3 per format group] monotone work-claim counters (slot 2: the wavefront kernel)
     unsigned long long *claim64;  // wavefront claim counter (64-bit: the call index is derived on the device)
-    uint32_t *ranges_done;    // self-resetting CTA-done counter of absmax_ranges_kernel
-    uint32_t *layer_done;     // [n_layers] monotone per-layer abs-max completion counters (wavefront kernel)
+    uint32_t *ranges_done;    // self-resetting CTA-done counter of absmax_stream_kernel
+    const int64_t *voff;      // [n_layers + 1] first vector (4 fp32) of each layer in a1's vector space
+    const int32_t *cta_layer; // [absmax_grid()] layer holding the first vector of each a1 CTA's share
+    uint32_t *layer_done;     // [n_layers] per-layer abs-max completion counters (fused kernel)
+    uint32_t *bdone;          // [n_layers] per-layer quantise completion counters (fused kernel, self-resetting)
+    uint32_t *sr_call;        // stochastic rounding: syncs since aps_set_rounding (per-call key, reading A27)
     uint8_t *packed;          // packed codes
     int n_items;
     int n_layers;
 };
 
-cudaError_t launch_absmax_exp(const DevTables &t, int world, cudaStream_t s);
-// a1 over ranges of kAbsItemsPerCta items, one done-count per CTA (target = done counter after the call)
-int absmax_ranges_grid(int n_items);
-cudaError_t launch_absmax_ranges(const DevTables &t, int world, cudaStream_t s);
-// a1 as one streaming kernel (red.max per CTA, no counters) + a one-CTA finisher
-cudaError_t launch_absmax_plain(const DevTables &t, int world, cudaStream_t s);
+// a1: balanced abs-max stream over every layer (absmax_grid() CTAs; DevTables.voff /
+// cta_layer describe the split), self-resetting done counter
+constexpr int kAbsCtasPerSm = 4;
+constexpr int kAbsMaxCtas = 1024;  // cta_layer table size (workspace)
+int absmax_grid();
+cudaError_t launch_absmax(const DevTables &t, int world, cudaStream_t s);
 cudaError_t launch_quant_pack(const DevTables &t, int e, int m, bool hw, cudaStream_t s);
 cudaError_t launch_unpack_unscale(const DevTables &t, int e, int m, bool hw, int world, int average,
                                   cudaStream_t s);
@@ -86,29 +87,12 @@ cudaError_t launch_debug_decode(const uint32_t *codes, float *out, int64_t n, in
 
 int sm_count();
 
-// Persistent TMA-bulk streaming engine (aps_stream.cu): one CTA per SM, a
-// producer warp feeding a multi-stage shared-memory ring with
-// cp.async.bulk, eight consumer warps.
-int stream_grid(int n_work);  // CTAs a stream kernel launches for n_work items
-cudaError_t launch_stream_absmax(const DevTables &t, int world, uint32_t gen, uint32_t target, cudaStream_t s);
-cudaError_t launch_stream_quant(const DevTables &t, int e, int m, bool hw, cudaStream_t s);
-cudaError_t launch_stream_unpack(const DevTables &t, int e, int m, bool hw, int world, int average,
-                                 cudaStream_t s);
-// p = 1: FindMaxExp -> f~ -> Cast -> pack -> Cast back -> unscale in ONE
-// launch (phase A: abs-max of every work item, forward; phase B: quantise +
-// unscale, reverse order so the second read of the gradients hits L2).
-bool stream_fused_supported(int e, int m, bool hw);
-cudaError_t launch_stream_fused_p1(const DevTables &t, int e, int m, bool hw, int average, uint32_t gen,
-                                   uint32_t target, cudaStream_t s);
-
-// fused p = 1 on the LDG engine (aps_kernels.cu): cooperative grid of
-// fused_p1_ldg_grid(...) CTAs; `target` = done counter after the call.
-int fused_p1_ldg_grid(int e, int m, bool hw, int n_items);
-constexpr int kFusedWarps = kThreads / 32;  // the done counter advances by grid * kFusedWarps per call
-constexpr int kFusedDefaultFlags = 2 | 32 | 64;       // fused kernel tuning flags (aps_kernels.cu; measured in DESIGN.md)
+constexpr int kFusedWarps = kThreads / 32;
+#ifndef APS_FUSED_FLAGS
+#define APS_FUSED_FLAGS 64  // 64: code / output stores with an L2 evict_first hint; +16: per-CTA timeline stamps
+#endif
+constexpr int kFusedDefaultFlags = APS_FUSED_FLAGS;  // fused kernel flags (compile time)
 constexpr int kTimelineSlots = 4 * 2048;     // globaltimer stamps (4 per CTA) of the last fused launch
-constexpr int kFusedUnitTiles = 64;        // fused kernel claim unit (tiles): a whole item (16 KB units measured slower)
-constexpr int kFusedSmemLayers = 8192;      // f~ table in shared memory up to this many layers
 cudaError_t launch_build_item_ptrs(const DevTables &t, cudaStream_t s);
 // wavefront variant (no grid barrier): claim_base advances by 2 * n_items + grid per call;
 // call_no = wavefront calls before this one on these counters; lag = D positions.
@@ -118,6 +102,11 @@ cudaError_t launch_build_item_ptrs(const DevTables &t, cudaStream_t s);
 constexpr int kWaveCtasPerSm = APS_WAVE_CTAS_PER_SM;  // wavefront kernel occupancy (register budget)
 int fused_p1_wave_grid(int e, int m, bool hw, int n_items);
 
+#ifndef APS_WAVE_LAG_GRIDS
+#define APS_WAVE_LAG_GRIDS 2
+#endif
+// lag D of the wavefront = (items of the largest layer) + kWaveLagGrids x grid positions
+constexpr int kWaveLagGrids = APS_WAVE_LAG_GRIDS;
 constexpr int kWaveOvershoot = 2;  // claims past the end per CTA and call (wavefront kernel claims 2 ahead)
 // claim_base advances by 2 * n_items + kWaveOvershoot * grid per call.
 // Per-call state of a wavefront launch.  graph = false: claim base (32-bit claim
@@ -134,11 +123,15 @@ cudaError_t launch_fused_p1_wave(const DevTables &t, int e, int m, bool hw, int 
 // binary32 codec (the hybrid FP32 classifier layer), the others (e, m, hw).
 cudaError_t launch_fused_p1_wave_hybrid32(const DevTables &t, int e, int m, bool hw, int fmt2, int average,
                                           const WaveCall &w, int lag, int grid, cudaStream_t s);
-// claim_base: value of both claim counters at launch (each call advances
-// them by n_items + grid: every CTA's last claim overshoots once).
-cudaError_t launch_fused_p1_ldg(const DevTables &t, int e, int m, bool hw, int average, uint32_t gen,
-                                uint32_t target, uint32_t claim_base, int grid, cudaStream_t s);
-
+// fused N = 1 sync, static wavefront with per-warp work (aps_fused.cu): one cooperative
+// launch per format group (hybrid FP32 classifier: one launch), no per-call host state
+#ifndef APS_FUSED_W2
+#define APS_FUSED_W2 0
+#endif
+constexpr int kW2CtasPerSm = 4;
+cudaError_t launch_fused_w2(const DevTables &t, int e, int m, bool hw, int average, int max_layer_items, cudaStream_t s);
+cudaError_t launch_fused_w2_hybrid32(const DevTables &t, int e, int m, bool hw, int fmt2, int average,
+                                     int max_layer_items, cudaStream_t s);
 // true when (e,m) has a hardware converter that is exact on the APS path
 // formats with a hardware / exact fast codec: fp8 e5m2, e4m3 (APS regime only,
 // reading A12), binary16, bfloat16, binary32 (every non-NaN input)

@@ -20,190 +20,136 @@
 
 namespace aps {
 
-template <int NT>
-__global__ void __launch_bounds__(NT) absmax_exp_kernel(DevTables t, int N)
-{
-    const Item it = t.items[blockIdx.x];
-    const LayerDev L = t.layers[it.layer];
-    const float *g = t.src[it.layer];
-    const int64_t begin = (int64_t)it.tile_begin * kTile;
-    const int64_t n = min((int64_t)it.n_tiles * kTile, L.numel - begin);
-    const float4 *g4 = reinterpret_cast<const float4 *>(g + begin);
-    constexpr int kFull4 = kItemTiles * kTile / 4;  // float4 groups in a full item
-    constexpr int kPer = kFull4 / NT;
-    uint32_t mx = 0;
-    if (n == kItemTiles * kTile) {
-        float4 v[kPer];
-#pragma unroll
-        for (int j = 0; j < kPer; ++j) v[j] = ld_stream4(g4 + threadIdx.x + j * NT);
-#pragma unroll
-        for (int j = 0; j < kPer; ++j) mx = max(mx, absbits4(v[j]));
-    } else {
-        const int64_t n4 = n >> 2;
-        for (int64_t i = threadIdx.x; i < n4; i += NT) mx = max(mx, absbits4(ld_stream4(g4 + i)));
-        for (int64_t i = (n4 << 2) + threadIdx.x; i < n; i += NT)
-            mx = max(mx, __float_as_uint(g[begin + i]) & 0x7fffffffu);
-    }
-    mx = __reduce_max_sync(0xffffffffu, mx);
-    __shared__ uint32_t s_max[NT / 32];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (lane == 0) s_max[warp] = mx;
-    __syncthreads();
-    if (warp == 0) {
-        uint32_t v = lane < NT / 32 ? s_max[lane] : 0u;
-        v = __reduce_max_sync(0xffffffffu, v);
-        if (lane == 0) {
-            atomicMax(&t.amax[it.layer], v);
-            __threadfence();
-            const uint32_t done = atomicAdd(&t.count[it.layer], 1u);
-            if (done == (uint32_t)L.n_items - 1u) {  // last CTA of this layer
-                __threadfence();
-                const uint32_t A = atomicExch(&t.amax[it.layer], 0u);
-                t.count[it.layer] = 0u;
-                t.E_local[it.layer] = exponent_of(A, N);
-            }
-        }
-    }
-}
-
-// a1 as a pure streaming pass: one CTA per work item, one fire-and-forget
-// red.max per CTA into the layer's accumulator, no fence and no completion
-// counter; the kernel boundary orders the maxima before absmax_finish_kernel
-// turns them into E_l = ceil(log2(N * A_l)) and clears the accumulators.
-template <int NT>
-__global__ void __launch_bounds__(NT) absmax_plain_kernel(DevTables t)
-{
-    const Item it = t.items[blockIdx.x];
-    const float *g = t.src[it.layer] + (int64_t)it.tile_begin * kTile;
-    const float4 *g4 = reinterpret_cast<const float4 *>(g);
-    constexpr int kPer = kItemTiles * kTile / 4 / NT;
-    uint32_t mx = 0;
-    if (it.cnt == kItemTiles * kTile) {
-        float4 v[kPer];
-#pragma unroll
-        for (int j = 0; j < kPer; ++j) v[j] = ld_stream4(g4 + threadIdx.x + j * NT);
-#pragma unroll
-        for (int j = 0; j < kPer; ++j) mx = max(mx, absbits4(v[j]));
-    } else {
-        const int n4 = it.cnt >> 2;
-        for (int j = threadIdx.x; j < n4; j += NT) mx = max(mx, absbits4(ld_stream4(g4 + j)));
-        if ((int)threadIdx.x < (it.cnt & 3)) mx = max(mx, __float_as_uint(g[4 * n4 + threadIdx.x]) & 0x7fffffffu);
-    }
-    mx = __reduce_max_sync(0xffffffffu, mx);
-    __shared__ uint32_t s_max[NT / 32];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (lane == 0) s_max[warp] = mx;
-    __syncthreads();
-    if (warp == 0) {
-        uint32_t v = lane < NT / 32 ? s_max[lane] : 0u;
-        v = __reduce_max_sync(0xffffffffu, v);
-        if (lane == 0 && v)
-            asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(&t.amax[it.layer]), "r"(v) : "memory");
-    }
-}
-
-__global__ void absmax_finish_kernel(DevTables t, int N)
-{
-    for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < t.n_layers; l += gridDim.x * blockDim.x) {
-        t.E_local[l] = exponent_of(t.amax[l], N);
-        t.amax[l] = 0u;
-    }
-}
-
-// direct widths 8/16/32: group of 4 fp32 -> one 4-code word group
-// a1 for the separate-call path (N > 1): each CTA takes kAbsItemsPerCta
-// consecutive work items (mostly one layer), keeps a per-warp running max,
-// flushes it with a fire-and-forget red.max when the layer changes, and
-// counts itself done once (fence + atomic); the last CTA turns the
-// accumulators into E_l = ceil(log2(N * A_l)) and clears them.  Compared with
-// one CTA per item and a fence per CTA, the fence latency is paid 4x less
-// often and the block scheduler still balances the load.
-#ifndef APS_ABS_ITEMS
-#define APS_ABS_ITEMS 4
-#endif
-constexpr int kAbsItemsPerCta = APS_ABS_ITEMS;
-// A/B switch: APS_ABS_STREAM loads a1's gradients with the streaming hint instead of
-// L2 evict_last (which keeps them for quant_pack's re-read)
-#ifdef APS_ABS_STREAM
-#define APS_ABS_LD(p, pol) ld_stream4(p)
-#else
-#define APS_ABS_LD(p, pol) ld_keep4(p, pol)
-#endif
-
-__device__ __forceinline__ float4 ld_keep4(const float4 *p, uint64_t pol)
-{
-    float4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
-                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
-                 : "l"(p), "l"(pol));
-    return r;
-}
+// ------------------------------------------------------------------ a1: abs-max, balanced stream
+// FindMaxExp (Alg. 1 line 3; function P:260-271) for every layer in ONE launch of
+// exactly kAbsCtasPerSm x SMs CTAs.  The layers are laid end to end in "vector space"
+// (vector = 4 consecutive fp32 of one layer; layer l owns vectors [voff[l], voff[l+1]),
+// its last vector partial when numel % 4 != 0) and CTA b streams the equal share
+// [b V / G, (b+1) V / G): every SM moves the same number of bytes, so the launch has no
+// tail of idle SMs (the round-1 kernel, one CTA per 4 work items, left SMs idle 23 % of
+// its time: profiles/r02a_absmax_raw.csv).  A share is walked in chunks of 8 x NT
+// vectors (8 independent 128-bit loads in flight per thread):
+//   * chunk inside one layer (the common case): a running per-thread max of that layer,
+//     folded into amax[layer] (warp max, one red.max per warp) when the layer changes;
+//   * chunk crossing layer boundaries or holding a partial vector: each vector finds its
+//     layer (binary search over voff) and is folded with a shared-memory atomicMax into
+//     a per-chunk table, flushed with red.max.
+// The max of u32 abs bits is order-independent, so the result is bit-exact whatever the
+// split.  Completion: one fence by thread 0 after the CTA barrier, one count; the last
+// CTA turns the maxima into E_l = ceil(log2(N A_l)) and clears them (self-resetting:
+// capture-safe).  Gradients are loaded with an L2 evict_last hint so that quant_pack's
+// re-read (reverse order) hits L2.
+constexpr int kAbsChunk = 8 * kThreads;  // vectors per chunk (32 KB)
 
 template <int NT>
-__global__ void __launch_bounds__(NT, 6) absmax_ranges_kernel(DevTables t, int N)
+__global__ void __launch_bounds__(NT, kAbsCtasPerSm) absmax_stream_kernel(DevTables t, int N)
 {
+    constexpr int kChunk = 8 * NT;
+    __shared__ uint32_t s_tab[kChunk];  // slow path: max per layer of the chunk (index layer - l0)
     __shared__ int s_last;
     const int lane = threadIdx.x & 31;
     uint64_t keep;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
-    constexpr int kPer = kItemTiles * kTile / 4 / NT;
-    const int lo = blockIdx.x * kAbsItemsPerCta, hi = min(t.n_items, lo + kAbsItemsPerCta);
-    // all descriptors and layer pointers of the range up front (independent loads)
-    Item its[kAbsItemsPerCta];
-    const float *srcs[kAbsItemsPerCta];
-#pragma unroll
-    for (int k = 0; k < kAbsItemsPerCta; ++k)
-        if (lo + k < hi) its[k] = t.items[lo + k];
-#pragma unroll
-    for (int k = 0; k < kAbsItemsPerCta; ++k)
-        if (lo + k < hi) srcs[k] = t.src[its[k].layer] + (int64_t)its[k].tile_begin * kTile;
-    uint32_t run = 0;
-    int run_layer = -1;
-#pragma unroll
-    for (int k = 0; k < kAbsItemsPerCta; ++k) {
-        if (lo + k >= hi) break;
-        const Item it = its[k];
-        if (it.layer != run_layer) {
-            if (lane == 0 && run)
-                asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(&t.amax[run_layer]), "r"(run) : "memory");
-            run = 0;
-            run_layer = it.layer;
-        }
-        const float *g = srcs[k];
-        const float4 *g4 = reinterpret_cast<const float4 *>(g);
-        uint32_t mx = 0;
-        if (it.cnt == kItemTiles * kTile) {
-            float4 v[kPer];
-#pragma unroll
-            for (int j = 0; j < kPer; ++j) v[j] = APS_ABS_LD(g4 + threadIdx.x + j * NT, keep);
-#pragma unroll
-            for (int j = 0; j < kPer; ++j) mx = max(mx, absbits4(v[j]));
-        } else {
-            const int n4 = it.cnt >> 2;
-            for (int j = threadIdx.x; j < n4; j += NT) mx = max(mx, absbits4(APS_ABS_LD(g4 + j, keep)));
-            if ((int)threadIdx.x < (it.cnt & 3)) mx = max(mx, __float_as_uint(g[4 * n4 + threadIdx.x]) & 0x7fffffffu);
-        }
-        run = max(run, __reduce_max_sync(0xffffffffu, mx));
-    }
-    if (lane == 0) {
-        if (run && run_layer >= 0)
-            asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(&t.amax[run_layer]), "r"(run) : "memory");
-        __threadfence();
-    }
+    const int64_t V = t.voff[t.n_layers];
+    const int64_t lo = V * (int64_t)blockIdx.x / gridDim.x, hi = V * (int64_t)(blockIdx.x + 1) / gridDim.x;
+    int l = t.cta_layer[blockIdx.x];  // layer holding vector lo
+    for (int k = threadIdx.x; k < kChunk; k += NT) s_tab[k] = 0u;
     __syncthreads();
-    // self-resetting done counter (graph-safe: no host-side target)
+    uint32_t run = 0;                 // this thread's running max of layer `l` (fast path)
+    for (int64_t c0 = lo; c0 < hi; c0 += kChunk) {
+        const int64_t c1 = min(hi, c0 + kChunk);
+        while (t.voff[l + 1] <= c0) {   // advance to the layer holding c0 (flush the old one)
+            const uint32_t m = __reduce_max_sync(0xffffffffu, run);
+            if (lane == 0 && m)
+                asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(&t.amax[l]), "r"(m) : "memory");
+            run = 0;
+            ++l;
+        }
+        const int64_t base = t.voff[l];
+        const int64_t full_end = base + (t.layers[l].numel >> 2);  // first partial vector (or voff[l+1])
+        if (c1 <= full_end) {
+            // ---- fast path: the chunk lies in layer l's full vectors
+            const float4 *g4 = reinterpret_cast<const float4 *>(t.src[l]);
+            const int64_t i0 = c0 - base, i1 = c1 - base;  // vector indices within the layer
+            float4 v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int64_t i = i0 + threadIdx.x + q * NT;
+                v[q] = i < i1 ? ld_keep4(g4 + i, keep) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) run = max(run, absbits4(v[q]));
+            continue;
+        }
+        // ---- slow path: layers l .. lh meet the chunk (lh < l + kChunk)
+        {
+            const uint32_t m = __reduce_max_sync(0xffffffffu, run);
+            if (lane == 0 && m)
+                asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(&t.amax[l]), "r"(m) : "memory");
+            run = 0;
+        }
+        int lh = l;
+        {   // last layer meeting the chunk: largest layer with voff <= c1 - 1
+            int a = l, b = min(t.n_layers - 1, l + kChunk - 1);
+            while (a < b) {
+                const int mid = (a + b + 1) >> 1;
+                if (t.voff[mid] <= c1 - 1) a = mid; else b = mid - 1;
+            }
+            lh = a;
+        }
+#pragma unroll 1
+        for (int q = 0; q < 8; ++q) {
+            const int64_t i = c0 + threadIdx.x + q * NT;
+            if (i >= c1) break;
+            int a = l, b = lh;   // layer of vector i
+            while (a < b) {
+                const int mid = (a + b + 1) >> 1;
+                if (t.voff[mid] <= i) a = mid; else b = mid - 1;
+            }
+            const int64_t e0 = 4 * (i - t.voff[a]);         // first element of the vector in layer a
+            const int64_t n = t.layers[a].numel;
+            const float *g = t.src[a];
+            uint32_t mx;
+            if (e0 + 4 <= n) {
+                mx = absbits4(ld_keep4(reinterpret_cast<const float4 *>(g + e0), keep));
+            } else {
+                mx = 0;
+                for (int64_t e = e0; e < n; ++e) mx = max(mx, __float_as_uint(g[e]) & 0x7fffffffu);
+            }
+            if (mx) atomicMax(&s_tab[a - l], mx);
+        }
+        __syncthreads();
+        for (int k = threadIdx.x; k <= lh - l; k += NT) {
+            const uint32_t m = s_tab[k];
+            if (m) {
+                asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(&t.amax[l + k]), "r"(m) : "memory");
+                s_tab[k] = 0u;
+            }
+        }
+        __syncthreads();
+        l = lh;  // (the next chunk starts at or after layer lh)
+    }
+    {
+        const uint32_t m = __reduce_max_sync(0xffffffffu, run);
+        if (lane == 0 && m && l < t.n_layers)
+            asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(&t.amax[l]), "r"(m) : "memory");
+    }
+    // completion: the CTA barrier orders every warp's red.max before thread 0's fence
+    // (cumulativity), whose count the last CTA acquires
+    __syncthreads();
     if (threadIdx.x == 0) {
+        __threadfence();
         s_last = atomicAdd(t.ranges_done, 1u) == gridDim.x - 1u;
         if (s_last) *t.ranges_done = 0u;  // every CTA of this launch has counted itself
     }
     __syncthreads();
     if (s_last) {
         __threadfence();
-        for (int l = threadIdx.x; l < t.n_layers; l += NT) {
+        for (int k = threadIdx.x; k < t.n_layers; k += NT) {
             uint32_t a_;
-            asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(a_) : "l"(&t.amax[l]) : "memory");
-            t.E_local[l] = exponent_of(a_, N);
-            t.amax[l] = 0u;
+            asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(a_) : "l"(&t.amax[k]) : "memory");
+            t.E_local[k] = exponent_of(a_, N);
+            t.amax[k] = 0u;
         }
     }
 }
@@ -423,51 +369,6 @@ __global__ void __launch_bounds__(NT) ring_reduce_tile_kernel(uint8_t *own, cons
 //            pack (codes -> packed buffer), Cast back, unscale -> output.
 // Accumulators are double-buffered by call parity: buffer g&1 is used,
 // buffer (g+1)&1 is cleared by the layer's first item for the next call.
-__device__ __forceinline__ float4 ld_hint4(const float4 *p, uint64_t pol)
-{
-    float4 r;
-    asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
-                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
-                 : "l"(p), "l"(pol));
-    return r;
-}
-__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t *p)
-{
-    uint32_t v;
-    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-
-__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t *p)
-{
-    uint32_t v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-
-__device__ __forceinline__ void st_hint4(float4 *p, float4 v, uint64_t pol)
-{
-    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(v.x),
-                 "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol)
-                 : "memory");
-}
-__device__ __forceinline__ void st_hint(uint32_t *p, uint32_t v, uint64_t pol)
-{
-    asm volatile("st.global.L1::no_allocate.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
-}
-__device__ __forceinline__ void st_hint(uint2 *p, uint2 v, uint64_t pol)
-{
-    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.u32 [%0], {%1, %2}, %3;" ::"l"(p), "r"(v.x), "r"(v.y),
-                 "l"(pol)
-                 : "memory");
-}
-__device__ __forceinline__ void st_hint(uint4 *p, uint4 v, uint64_t pol)
-{
-    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(v.x),
-                 "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol)
-                 : "memory");
-}
-
 __global__ void build_item_ptrs_kernel(DevTables t)
 {
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < t.n_items; k += gridDim.x * blockDim.x) {
@@ -477,205 +378,12 @@ __global__ void build_item_ptrs_kernel(DevTables t)
     }
 }
 
-template <class C, int NT>
-__global__ void __launch_bounds__(NT, kFusedCtasPerSm)
-    fused_p1_ldg_kernel(DevTables t, C c, uint32_t *amax, uint32_t *amax_next, uint32_t target, uint32_t claim_base,
-                        int bias, int avg, int flags)
-{
-    // flags (tuning; measured in DESIGN.md "fused p = 1 kernel"):
-    //   2  f~ table in shared memory (else one abs-max load per item)
-    //   16 record %globaltimer at start / end of phase A / after the barrier / end (per CTA)
-    //   32 dynamic work claiming (atomic counters, claim prefetched one item ahead) instead of
-    //      static round-robin: the items are equal, but CTAs sharing an SM and HBM do not
-    //      progress equally (static: phase-A finish times spread 14-26 us)
-    //   64 output and code stores with an L2 evict_first hint (keep the gradients phase A left
-    //      in L2 for phase B's second read)
-    // (measured and dropped: per-warp release counting, loading the first phase-B item before the
-    //  barrier, descriptor prefetch, 16 KB claim units, L2 bulk prefetch of the next claim)
-    const bool f_table = flags & 2, f_dynamic = flags & 32, f_st_hint = flags & 64;
-    __shared__ int s_claim[2];
-    const bool f_timeline = (flags & 16) && blockIdx.x * 4 + 3 < kTimelineSlots;
-    auto stamp = [&](int k) {
-        if (f_timeline && threadIdx.x == 0) {
-            uint64_t ns;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
-            t.timeline[blockIdx.x * 4 + k] = ns;
-        }
-    };
-    stamp(0);
-    extern __shared__ int32_t s_ft[];  // f~ per layer (when n_layers <= kFusedSmemLayers)
-    __shared__ __align__(16) uint32_t s_codes[NT / 32][kTile];
-    const int G = gridDim.x;
-    const int n = t.n_items;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint64_t keep, strm;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(strm));
-    constexpr int kPer = kFusedUnitTiles * kTile / 4 / NT;  // float4 groups per thread in a full unit
-    constexpr int kSub = kItemTiles / kFusedUnitTiles;       // claim units per work item
-    const int nu = n * kSub;                                 // claim units (some empty: short items)
-    // unit u = tiles [sub * kFusedUnitTiles, ...) of item u / kSub
-    struct Unit {
-        int layer, cnt, n_tiles;
-        int64_t tile_pos, byte_pos;
-        const float *src;
-        float *dst;
-    };
-    auto unit = [&](int u) -> Unit {
-        const int k = u / kSub, sub = u - k * kSub;
-        const Item it = t.items[k];
-        const ItemPtr p = t.iptr[k];
-        Unit x;
-        const int t0 = sub * kFusedUnitTiles;
-        x.layer = it.layer;
-        x.n_tiles = min(kFusedUnitTiles, it.n_tiles - t0);
-        x.cnt = min(kFusedUnitTiles * kTile, it.cnt - t0 * kTile);
-        x.tile_pos = it.tile_pos + t0;
-        x.byte_pos = it.byte_pos + (int64_t)t0 * 16 * c.b();
-        x.src = p.src + (int64_t)t0 * kTile;
-        x.dst = p.dst + (int64_t)t0 * kTile;
-        return x;
-    };
-
-    // ---------------- phase A: abs-max
-    // next work item: static round-robin, or claimed from counter `which`
-    auto first_item = [&](int which) -> int {
-        if (!f_dynamic) return blockIdx.x;
-        if (threadIdx.x == 0) s_claim[0] = (int)(atomicAdd(&t.claim[which], 1u) - claim_base);
-        __syncthreads();
-        return s_claim[0];
-    };
-    int slot = 0;
-    auto prefetch_claim = [&](int which) {
-        if (f_dynamic && threadIdx.x == 0) {
-            const int u = (int)(atomicAdd(&t.claim[which], 1u) - claim_base);
-            s_claim[slot ^ 1] = u;
-        }
-    };
-    auto next_item = [&](int w) -> int {
-        if (!f_dynamic) return w + G;
-        __syncthreads();
-        slot ^= 1;
-        return s_claim[slot];
-    };
-    for (int w = first_item(0); w < nu; w = next_item(w)) {
-        prefetch_claim(0);
-        const Unit it = unit(w);
-        if (it.cnt <= 0) continue;  // past the end of a short item (uniform across the CTA)
-        const float *src = it.src;
-        const float4 *g4 = reinterpret_cast<const float4 *>(src);
-        uint32_t mx = 0;
-        if (it.cnt == kFusedUnitTiles * kTile) {
-            float4 v[kPer];
-#pragma unroll
-            for (int j = 0; j < kPer; ++j) v[j] = ld_hint4(g4 + threadIdx.x + j * NT, keep);
-#pragma unroll
-            for (int j = 0; j < kPer; ++j) mx = max(mx, absbits4(v[j]));
-        } else {
-            const int n4 = it.cnt >> 2;
-            for (int j = threadIdx.x; j < n4; j += NT) mx = max(mx, absbits4(ld_hint4(g4 + j, keep)));
-            if ((int)threadIdx.x < (it.cnt & 3)) mx = max(mx, __float_as_uint(src[4 * n4 + threadIdx.x]) & 0x7fffffffu);
-        }
-        mx = __reduce_max_sync(0xffffffffu, mx);
-        if (lane == 0 && mx) asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(&amax[it.layer]), "r"(mx) : "memory");
-    }
-    stamp(1);
-    constexpr int B = C::kB;
-
-    // ---------------- grid barrier: every warp's red.max ordered before its count
-    if (lane == 0) __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) atomicAdd(t.done, (uint32_t)(NT / 32));
-    if (threadIdx.x == 0)
-        spin_until([&] { return (int)(ld_acquire_u32(t.done) - target) >= 0; }, t.flag);
-    __syncthreads();
-    stamp(2);
-    const bool table = f_table && t.n_layers <= kFusedSmemLayers;
-    if (table || blockIdx.x == 0) {  // (without the table, CTA 0 still records E / f~ for every layer)
-        for (int l = threadIdx.x; l < t.n_layers; l += NT) {
-            const int32_t E = exponent_of(ld_relaxed_u32(&amax[l]), 1);
-            const int ft = (E == INT32_MIN || E == INT32_MAX) ? 0 : bias - E;  // f~ (Alg. 1 line 4)
-            if (table) s_ft[l] = ft;
-            if (blockIdx.x == 0) {  // record E, f~, the non-finite flag; clear the next call's buffer
-                t.E_local[l] = E;
-                t.ftilde[l] = ft;
-                if (E == INT32_MAX) atomicOr(t.flag, 1u);
-                amax_next[l] = 0u;
-            }
-        }
-    }
-    __syncthreads();
-
-    // ---------------- phase B: quantise + unscale, reverse order
-    slot = 0;
-    for (int wb = first_item(1); wb < nu; wb = next_item(wb)) {
-        prefetch_claim(1);
-        const Unit ib = unit(nu - 1 - wb);
-        if (ib.cnt <= 0) continue;
-        const Unit &pb = ib;
-        const int l = ib.layer;
-        int ft;
-        if (table) {
-            ft = s_ft[l];
-        } else {
-            const int32_t E = exponent_of(ld_relaxed_u32(&amax[l]), 1);
-            ft = (E == INT32_MIN || E == INT32_MAX) ? 0 : bias - E;
-        }
-        const float *g = pb.src;
-        float *o = pb.dst;
-        const float4 *g4 = reinterpret_cast<const float4 *>(g);
-        const Pow2 s(ft);
-        const Unscale us(ft, 1, avg);
-        if constexpr (B == 8 || B == 16 || B == 32) {
-            using W = typename Word4<B>::T;
-            W *out = reinterpret_cast<W *>(t.packed + ib.byte_pos);
-            if (ib.cnt == kFusedUnitTiles * kTile && !s.wide) {
-                float4 v[kPer];
-#pragma unroll
-                for (int j = 0; j < kPer; ++j) v[j] = ld_hint4(g4 + threadIdx.x + j * NT, strm);
-                float4 *o4 = reinterpret_cast<float4 *>(o);
-#pragma unroll
-                for (int j = 0; j < kPer; ++j) {
-                    const float4 y = make_float4(__fmul_rn(v[j].x, s.f), __fmul_rn(v[j].y, s.f), __fmul_rn(v[j].z, s.f),
-                                                 __fmul_rn(v[j].w, s.f));
-                    const W code = pack4<B>(c, y);
-                    const float4 r = us.apply4(unpack4<B>(c, code));
-                    if (f_st_hint) {
-                        st_hint(out + threadIdx.x + j * NT, code, strm);
-                        st_hint4(o4 + threadIdx.x + j * NT, r, strm);
-                    } else {
-                        out[threadIdx.x + j * NT] = code;
-                        o4[threadIdx.x + j * NT] = r;
-                    }
-                }
-            } else {
-                const int ng = ib.n_tiles * (kTile / 4);
-                for (int j = threadIdx.x; j < ng; j += NT) {
-                    const W code = pack4<B>(c, s.apply4(load_group(g, 4 * (int64_t)j, ib.cnt)));
-                    out[j] = code;
-                    store_group(o, 4 * (int64_t)j, ib.cnt, us.apply4(unpack4<B>(c, code)));
-                }
-            }
-        } else {
-            const int b = c.b();
-            uint32_t *codes = s_codes[warp];
-            uint32_t *outw = reinterpret_cast<uint32_t *>(t.packed + ib.byte_pos);
-            for (int tt = warp; tt < ib.n_tiles; tt += NT / 32) {
-                const int64_t e0 = (int64_t)tt * kTile + lane * 4;
-                const float4 y = s.apply4(load_group(g, e0, ib.cnt));
-                const uint4 cd = make_uint4(c.enc(y.x), c.enc(y.y), c.enc(y.z), c.enc(y.w));
-                *reinterpret_cast<uint4 *>(codes + lane * 4) = cd;
-                __syncwarp();
-                uint32_t *ow = outw + (int64_t)tt * (4 * b);
-                for (int w2 = lane; w2 < 4 * b; w2 += 32) ow[w2] = assemble_word(codes, w2, b);
-                store_group(o, e0, ib.cnt, us.apply4(make_float4(c.dec(cd.x), c.dec(cd.y), c.dec(cd.z), c.dec(cd.w))));
-                __syncwarp();
-            }
-        }
-    }
-    stamp(3);
-}
-
+#ifndef APS_DIAG_NOWAIT
+#define APS_DIAG_NOWAIT 0
+#endif
+#ifndef APS_DIAG_NOA
+#define APS_DIAG_NOA 0
+#endif
 // ------------------------------------------------------------------ sim: MAX exchange of E
 struct PtrArr {
     const int32_t *src[64];
@@ -718,27 +426,12 @@ int sm_count()
     return n;
 }
 
-cudaError_t launch_absmax_exp(const DevTables &t, int world, cudaStream_t s)
+int absmax_grid() { return std::min(kAbsMaxCtas, sm_count() * kAbsCtasPerSm); }
+
+cudaError_t launch_absmax(const DevTables &t, int world, cudaStream_t s)
 {
     if (t.n_items == 0) return cudaSuccess;
-    absmax_exp_kernel<kThreads><<<t.n_items, kThreads, 0, s>>>(t, world);
-    return cudaGetLastError();
-}
-
-int absmax_ranges_grid(int n_items) { return (n_items + kAbsItemsPerCta - 1) / kAbsItemsPerCta; }
-
-cudaError_t launch_absmax_plain(const DevTables &t, int world, cudaStream_t s)
-{
-    if (t.n_items == 0) return cudaSuccess;
-    absmax_plain_kernel<kThreads><<<t.n_items, kThreads, 0, s>>>(t);
-    absmax_finish_kernel<<<(t.n_layers + 255) / 256, 256, 0, s>>>(t, world);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_absmax_ranges(const DevTables &t, int world, cudaStream_t s)
-{
-    if (t.n_items == 0) return cudaSuccess;
-    absmax_ranges_kernel<kThreads><<<absmax_ranges_grid(t.n_items), kThreads, 0, s>>>(t, world);
+    absmax_stream_kernel<kThreads><<<absmax_grid(), kThreads, 0, s>>>(t, world);
     return cudaGetLastError();
 }
 
@@ -820,9 +513,6 @@ cudaError_t launch_ring_reduce(uint8_t *own, const uint8_t *recv, int64_t n_tile
 // positions, and each CTA holds at most its current and next claim, so the
 // earliest waiting B always completes (induction on position).
 // No second codec (uniform formats, or one launch per format group).
-struct CNone {
-    static constexpr int kB = -1;
-};
 
 // GRAPH = false: per-call state (claim base, call index, accumulator parity) comes from
 // the host as launch arguments (the fastest form).  GRAPH = true (capture-safe): the
@@ -866,6 +556,7 @@ __global__ void __launch_bounds__(NT, kWaveCtasPerSm)
         }
     };
     stamp(0);
+    uint64_t tl_wait_ns = 0, tl_waits = 0, tl_items = 0;  // timeline (flag 16): B-item waits of thread 0
     uint64_t keep, strm;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(strm));
@@ -902,7 +593,8 @@ __global__ void __launch_bounds__(NT, kWaveCtasPerSm)
             j = (int)(atomicAdd(&t.claim[2], 1u) - claim_base);
         }
         s_claim[sl] = j;
-        s_ok[sl] = 0;
+        s_ok[sl] = APS_DIAG_NOWAIT;  // (diagnostic build: never wait, results invalid)
+        if (APS_DIAG_NOWAIT) s_ft[sl] = 0;
         if (j < total) {
             bool isB;
             const int k = decode(j, isB);
@@ -958,7 +650,9 @@ __global__ void __launch_bounds__(NT, kWaveCtasPerSm)
         }
         if (threadIdx.x == 0) claim_into((slot + 2) % 3);
         if (threadIdx.x == kFlushThread) flush(par ^ 1);
-        if (!isB) {
+        if (!isB && APS_DIAG_NOA) {
+            if (threadIdx.x == 0) s_part_layer[par] = -1;  // (diagnostic build: abs-max items skipped)
+        } else if (!isB) {
             // ---------------- abs-max item
             uint32_t mx = 0;
             if (full) {
@@ -980,9 +674,14 @@ __global__ void __launch_bounds__(NT, kWaveCtasPerSm)
                 // count it first (deadlock otherwise)
                 if (threadIdx.x == kFlushThread) flush(-1);
                 if (threadIdx.x == 0) {
+                    const uint64_t w0 = f_timeline ? global_ns() : 0;
                     spin_until([&] { return (int)(ld_acquire_u32(&t.layer_done[it.layer]) - layer_target(it)) >= 0; },
                                t.flag);
                     s_ft[slot] = ft_of(it);
+                    if (f_timeline) {
+                        tl_wait_ns += global_ns() - w0;
+                        ++tl_waits;
+                    }
                 }
                 __syncthreads();
             }
@@ -1055,10 +754,15 @@ __global__ void __launch_bounds__(NT, kWaveCtasPerSm)
         slot = (slot + 1) % 3;
         par ^= 1;
         j = s_claim[slot];
+        if (f_timeline) ++tl_items;
     }
     if (threadIdx.x == kFlushThread) {  // drain: the last item's max, then its count
         flush(par ^ 1);
         flush(-1);
+    }
+    if (f_timeline && threadIdx.x == 0) {
+        t.timeline[blockIdx.x * 4 + 1] = tl_wait_ns;
+        t.timeline[blockIdx.x * 4 + 2] = (tl_waits << 32) | tl_items;
     }
     stamp(3);
 }
@@ -1068,8 +772,7 @@ static cudaError_t launch_wave(const DevTables &t, C c, C2 c2, int bias, int bia
                                const WaveCall &w, int lag, int grid, cudaStream_t s, bool cooperative)
 {
     auto kern = w.graph ? fused_p1_wave_kernel<C, C2, true, kThreads> : fused_p1_wave_kernel<C, C2, false, kThreads>;
-    int flags = kFusedDefaultFlags;
-    if (const char *env = std::getenv("APS_FUSED_FLAGS")) flags = std::atoi(env);
+    int flags = kFusedDefaultFlags;  // compile time (-DAPS_FUSED_FLAGS=...: timeline stamps, A/B builds)
     unsigned long long adv = 2ull * (unsigned long long)t.n_items + (unsigned long long)kWaveOvershoot * grid;
     uint32_t *cur = t.amax2 + (size_t)(w.gen & 1u) * t.n_layers;
     uint32_t *other = t.amax2 + (size_t)((w.gen + 1u) & 1u) * t.n_layers;
@@ -1099,45 +802,6 @@ cudaError_t launch_fused_p1_wave_hybrid32(const DevTables &t, int e, int m, bool
     return with_codec(e, m, hw, [&](auto c) -> cudaError_t {
         return launch_wave(t, c, CF32{}, bias, 127, fmt2, average, w, lag, grid, s, true);
     });
-}
-
-static size_t fused_smem(const DevTables &t)
-{
-    return t.n_layers <= kFusedSmemLayers ? sizeof(int32_t) * (size_t)t.n_layers : 0;
-}
-
-cudaError_t launch_fused_p1_ldg(const DevTables &t, int e, int m, bool hw, int average, uint32_t gen,
-                                uint32_t target, uint32_t claim_base, int grid, cudaStream_t s)
-{
-    const int bias = (1 << (e - 1)) - 1;
-    uint32_t *cur = t.amax2 + (size_t)(gen & 1u) * t.n_layers;
-    uint32_t *other = t.amax2 + (size_t)((gen + 1u) & 1u) * t.n_layers;
-    const size_t smem = fused_smem(t);
-    return with_codec(e, m, hw, [&](auto c) -> cudaError_t {
-        using C = decltype(c);
-        auto kern = fused_p1_ldg_kernel<C, kThreads>;
-        if (smem > 48 * 1024) {
-            cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (err != cudaSuccess) return err;
-        }
-        int flags = kFusedDefaultFlags;
-        if (const char *env = std::getenv("APS_FUSED_FLAGS")) flags = std::atoi(env);
-        void *args[] = {const_cast<DevTables *>(&t), &c, &cur, &other, &target, &claim_base, const_cast<int *>(&bias),
-                        &average, &flags};
-        return cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(kThreads), args, smem, s);
-    });
-}
-
-int fused_p1_ldg_grid(int e, int m, bool hw, int n_items)
-{
-    int per_sm = 0;
-    with_codec(e, m, hw, [&](auto c) -> cudaError_t {
-        using C = decltype(c);
-        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_p1_ldg_kernel<C, kThreads>, kThreads,
-                                                             sizeof(int32_t) * kFusedSmemLayers);
-    });
-    per_sm = std::max(1, std::min(per_sm, kFusedCtasPerSm));
-    return std::max(1, std::min(n_items, sm_count() * per_sm));
 }
 
 int fused_p1_wave_grid(int e, int m, bool hw, int n_items)

@@ -468,13 +468,25 @@ __global__ void __launch_bounds__(NT) peer_reduce_tile_kernel(PeerArgs a, int64_
 // oracle implements); x between its neighbours lo <= |x| < hi rounds up iff
 // r < (|x| - lo) / (hi - lo) * 2^32.  Phase: rank for the Cast of a rank's gradient,
 // p - 1 + a for the a-th add of an element's fold.
-__device__ __forceinline__ uint32_t sr_rand(uint64_t seed, uint64_t phase, int64_t i)
+__device__ __forceinline__ uint64_t splitmix64(uint64_t seed, uint64_t ctr)
 {
-    uint64_t z = seed + (((phase << 40) | (uint64_t)i) + 1ull) * 0x9E3779B97F4A7C15ull;
+    uint64_t z = seed + (ctr + 1ull) * 0x9E3779B97F4A7C15ull;
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
     z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-    return (uint32_t)((z ^ (z >> 31)) >> 32);
+    return z ^ (z >> 31);
 }
+__device__ __forceinline__ uint32_t sr_rand(uint64_t seed, uint64_t phase, int64_t i)
+{
+    return (uint32_t)(splitmix64(seed, (phase << 40) | (uint64_t)i) >> 32);
+}
+// per-call key (reading A27): the k-th sync after aps_set_rounding(seed) draws with
+// seed_k = SplitMix64(seed, k); k is the device-resident call counter (capture-safe)
+__device__ __forceinline__ uint64_t sr_call_seed(uint64_t seed, const uint32_t *call)
+{
+    return splitmix64(seed, (uint64_t)*call);
+}
+
+__global__ void sr_advance_kernel(uint32_t *call) { ++*call; }
 
 // up iff r < rem / 2^d * 2^32 (exact, any d >= 1)
 __device__ __forceinline__ uint32_t sr_up(uint32_t r, uint64_t rem, int d)
@@ -515,8 +527,9 @@ __device__ __forceinline__ uint32_t encode_sr(const Fmt &F, float y, uint32_t r)
 
 // a3+a4 with stochastic rounding, any width: per warp one tile of 128 codes
 template <int NT>
-__global__ void __launch_bounds__(NT) quant_pack_sr_kernel(DevTables t, Fmt F, uint64_t seed, int rank)
+__global__ void __launch_bounds__(NT) quant_pack_sr_kernel(DevTables t, Fmt F, uint64_t seed0, int rank)
 {
+    const uint64_t seed = sr_call_seed(seed0, t.sr_call);
     __shared__ __align__(16) uint32_t s_codes[NT / 32][kTile + 1];
     const Item it = t.items[blockIdx.x];
     const LayerDev L = t.layers[it.layer];
@@ -546,8 +559,9 @@ __global__ void __launch_bounds__(NT) quant_pack_sr_kernel(DevTables t, Fmt F, u
 // owner-computes reduce with a stochastic re-quantise after every add (wire accumulator)
 template <int NT>
 __global__ void __launch_bounds__(NT) peer_reduce_sr_kernel(PeerArgs a, int64_t byte_off, int64_t tile0,
-                                                            int64_t n_tiles, Fmt F, uint64_t seed)
+                                                            int64_t n_tiles, Fmt F, uint64_t seed0, const uint32_t *call)
 {
+    const uint64_t seed = sr_call_seed(seed0, call);
     __shared__ __align__(16) uint32_t s_w[NT / 32][kTile + 1];
     const int b = F.b;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -620,11 +634,17 @@ cudaError_t launch_quant_pack_sr(const DevTables &t, int e, int m, uint64_t seed
 }
 
 cudaError_t launch_peer_reduce_sr(const PeerArgs &a, int64_t byte_off, int64_t tile0, int64_t n_tiles, int e, int m,
-                                  uint64_t seed, cudaStream_t s)
+                                  uint64_t seed, const uint32_t *call, cudaStream_t s)
 {
     if (n_tiles <= 0) return cudaSuccess;
     const int grid = (int)std::min<int64_t>((n_tiles + kThreads / 32 - 1) / (kThreads / 32), (int64_t)sm_count() * 8);
-    peer_reduce_sr_kernel<kThreads><<<grid, kThreads, 0, s>>>(a, byte_off, tile0, n_tiles, make_fmt(e, m), seed);
+    peer_reduce_sr_kernel<kThreads><<<grid, kThreads, 0, s>>>(a, byte_off, tile0, n_tiles, make_fmt(e, m), seed, call);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sr_advance(uint32_t *call, cudaStream_t s)
+{
+    sr_advance_kernel<<<1, 1, 0, s>>>(call);
     return cudaGetLastError();
 }
 

@@ -45,8 +45,10 @@ struct DevTables;
 cudaError_t launch_debug_cast_sr(const float *in, uint32_t *codes, int64_t n, int e, int m, uint64_t seed,
                                  uint64_t phase, cudaStream_t s);
 cudaError_t launch_quant_pack_sr(const DevTables &t, int e, int m, uint64_t seed, int rank, cudaStream_t s);
+// advance the stochastic-rounding call counter (one sync done; reading A27)
+cudaError_t launch_sr_advance(uint32_t *call, cudaStream_t s);
 cudaError_t launch_peer_reduce_sr(const PeerArgs &a, int64_t byte_off, int64_t tile0, int64_t n_tiles, int e, int m,
-                                  uint64_t seed, cudaStream_t s);
+                                  uint64_t seed, const uint32_t *call, cudaStream_t s);
 cudaError_t launch_census(const DevTables &t, const int32_t *sexp, unsigned long long *counts, int e, int m,
                           cudaStream_t s);
 cudaError_t launch_round_off(const float *h, const float *l, int64_t n, double *sum, unsigned long long *cnt,

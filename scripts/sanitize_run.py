@@ -1,4 +1,4 @@
-"""Small APS syncs through every engine / path, for compute-sanitizer
+"""Small APS syncs through every path (fused, separate calls, simulated ring), for compute-sanitizer
 (memcheck, racecheck, synccheck, initcheck).  Run on the GPU box:
   compute-sanitizer --tool memcheck python scripts/sanitize_run.py"""
 import os
@@ -13,13 +13,12 @@ import paper_1911_08907_b200 as aps
 
 numels = synthetic.C1_NUMELS + [1000, 1, 130, 8195]
 grads = synthetic.make_grads(numels, 2)
-for engine in ("ldg", "simple", "tma"):
-    os.environ["APS_ENGINE"] = engine
+for engine in ("default",):
     for (e, m) in [(5, 2), (3, 0), (5, 6)]:
         g = [torch.from_numpy(a).cuda() for a in grads[0]]
         ctx = aps.ApsContext(e, m, numels)
         out = [torch.empty_like(x) for x in g]
-        ctx.sync_out(g, out)                       # fused (ldg / tma) or calls
+        ctx.sync_out(g, out)                       # fused
         ctx.layer_scales(g)
         ctx.quantize_pack(g)
         ctx.allreduce()

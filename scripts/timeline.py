@@ -1,11 +1,13 @@
-"""Per-CTA phase timeline of the fused p = 1 kernel on the bench workload
-(APS_FUSED_FLAGS bit 16).  Run on the GPU box: python scripts/timeline.py [flags]"""
+"""Per-CTA timeline of the fused N = 1 kernel on the bench workload: start / end
+stamps, quantise-item waits (count, time) and items per CTA.  Needs a build with
+-DAPS_FUSED_FLAGS=80 (flag 16 = timeline):
+  APS_BUILD_OUT=paper_1911_08907_b200/libaps_tl.so APS_NVCC_EXTRA=-DAPS_FUSED_FLAGS=80 \
+      python -m paper_1911_08907_b200.build
+  APS_LIB=paper_1911_08907_b200/libaps_tl.so python scripts/timeline.py"""
 import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-flags = int(sys.argv[1]) if len(sys.argv) > 1 else 2
-os.environ["APS_FUSED_FLAGS"] = str(flags | 16)
 import numpy as np
 import torch
 
@@ -13,25 +15,26 @@ import synthetic
 from paper_1911_08907_b200 import ApsContext
 
 numels = synthetic.RESNET50_NUMELS
-g = [torch.from_numpy(synthetic.layer_grad(0, l, n)).cuda() for l, n in enumerate(numels)]
-out = [torch.empty_like(x) for x in g]
+S = 3
+sets = []
+for s in range(S):
+    g = [torch.from_numpy(synthetic.layer_grad(0, l, n)).cuda() for l, n in enumerate(numels)]
+    sets.append((g, [torch.empty_like(x) for x in g]))
 ctx = ApsContext(5, 2, numels)
-flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-for _ in range(5):
-    ctx.sync_out(g, out)
-for rep in range(3):
-    flush.zero_()
-    torch.cuda.synchronize()
-    ctx.timeline()[:] = 0
-    ctx.sync_out(g, out)
+for k in range(6):
+    ctx.sync_out(*sets[k % S])
+torch.cuda.synchronize()
+for rep in range(4):
+    for k in range(5):               # steady state: the previous syncs' write-backs are in flight
+        ctx.sync_out(*sets[k % S])
+    ctx.sync_out(*sets[rep % S])
     torch.cuda.synchronize()
     tl = ctx.timeline().astype(np.int64)
     tl = tl[tl[:, 0] > 0]
     t0 = tl[:, 0].min()
-    rel = (tl - t0) / 1e3
+    st, en = (tl[:, 0] - t0) / 1e3, (tl[:, 3] - t0) / 1e3
+    wait_us = tl[:, 1] / 1e3
+    waits, items = tl[:, 2] >> 32, tl[:, 2] & 0xffffffff
     q = lambda a: f"min {a.min():6.2f} med {np.median(a):6.2f} max {a.max():6.2f}"
-    if (tl[:, 1] > 0).all():   # barrier schedule: 4 stamps
-        print(f"rep {rep}: CTAs {len(tl)}  start [{q(rel[:, 0])}]  endA [{q(rel[:, 1])}]  barrier-out [{q(rel[:, 2])}]  end [{q(rel[:, 3])}] us")
-        print(f"        phaseA dur [{q(rel[:, 1] - rel[:, 0])}]  wait [{q(rel[:, 2] - rel[:, 1])}]  phaseB dur [{q(rel[:, 3] - rel[:, 2])}]")
-    else:                      # wavefront schedule: start / end only
-        print(f"rep {rep}: CTAs {len(tl)}  start [{q(rel[:, 0])}]  end [{q(rel[:, 3])}] us")
+    print(f"rep {rep}: CTAs {len(tl)} start [{q(st)}] end [{q(en)}] us; thread-0 waits/CTA [{q(waits)}] "
+          f"wait us/CTA [{q(wait_us)}] sum {wait_us.sum():.0f}; items/CTA [{q(items)}]")

@@ -24,12 +24,6 @@ def aps():
     return pkg
 
 
-@pytest.fixture(params=["ldg", "tma", "simple"])
-def engine(request, monkeypatch):
-    monkeypatch.setenv("APS_ENGINE", request.param)
-    return request.param
-
-
 def _formats(n, seed):
     rng = np.random.default_rng(seed)
     return [MIXED_POOL[i] for i in rng.integers(0, len(MIXED_POOL), n)]
@@ -92,7 +86,7 @@ def check_mixed(aps, orc, grads, fmts, hw=True, average=1, fused=False, calls=1)
 @pytest.mark.parametrize("seed", [1, 2, 3])
 @pytest.mark.parametrize("hw", [True, False], ids=["hw", "sw"])
 @pytest.mark.parametrize("fused", [True, False], ids=["fused", "calls"])
-def test_p1_mixed(aps, orc, seed, hw, fused, engine):
+def test_p1_mixed(aps, orc, seed, hw, fused):
     grads = synthetic.make_grads(NUMELS, 1)
     check_mixed(aps, orc, grads, _formats(len(NUMELS), seed), hw=hw, fused=fused)
 
@@ -121,7 +115,7 @@ def test_p1_resnet50_hybrid(aps, orc, low, fused):
 
 @pytest.mark.parametrize("p", [2, 3, 4, 8])
 @pytest.mark.parametrize("seed", [1, 2])
-def test_sim_mixed(aps, orc, p, seed, engine):
+def test_sim_mixed(aps, orc, p, seed):
     grads = synthetic.make_grads(NUMELS, p)
     check_mixed(aps, orc, grads, _formats(len(NUMELS), seed + 10 * p))
 

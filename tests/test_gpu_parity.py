@@ -94,17 +94,9 @@ def check(aps, orc, grads, e, m, hw, average=1, fused=False, ref=None):
 
 # ----------------------------------------------------------------- p = 1
 
-@pytest.fixture(params=["ldg", "tma", "simple"])
-def engine(request, monkeypatch):
-    """libaps kernel engine: grid kernels + fused LDG p = 1 kernel (default),
-    persistent TMA-bulk kernels, or grid kernels only."""
-    monkeypatch.setenv("APS_ENGINE", request.param)
-    return request.param
-
-
 @pytest.mark.parametrize("fused", [True, False], ids=["fused", "calls"])
 @pytest.mark.parametrize("fmt,hw", FORMATS, ids=FMT_IDS)
-def test_p1_c1_and_edges(aps, orc, fmt, hw, fused, engine):
+def test_p1_c1_and_edges(aps, orc, fmt, hw, fused):
     e, m = fmt
     grads = synthetic.make_grads(synthetic.C1_NUMELS + [1000, 1, 9408, 130, 8195, 16387], 1)
     check(aps, orc, grads, e, m, hw, fused=fused)
@@ -168,7 +160,7 @@ def test_p1_fused_repeated_and_inplace(aps, orc):
 
 @pytest.mark.parametrize("p", [2, 3, 4, 8])
 @pytest.mark.parametrize("fmt,hw", FORMATS, ids=FMT_IDS)
-def test_sim_c1(aps, orc, fmt, hw, p, engine):
+def test_sim_c1(aps, orc, fmt, hw, p):
     """Config 1 (4K/64K/256K layers) plus ragged layers, p simulated ranks."""
     e, m = fmt
     grads = synthetic.make_grads(synthetic.C1_NUMELS + [1000, 1, 130], p)
@@ -330,12 +322,10 @@ def test_nccl_world1_path(aps, orc):
         aps.nccl_comm_destroy(comm)
 
 
-@pytest.mark.parametrize("schedule", ["wave", "barrier"])
 @pytest.mark.timeout(300)
-def test_p1_fused_schedules(aps, orc, schedule, monkeypatch):
-    """Every fused N = 1 schedule (wavefront, grid barrier) is bit-exact: edge cases and ResNet-50 at full size, in
+def test_p1_fused_repeated_formats(aps, orc):
+    """The fused N = 1 kernel is bit-exact on edge cases and ResNet-50 at full size, in
     several formats, with repeated calls on one context."""
-    monkeypatch.setenv("APS_FUSED_SCHEDULE", schedule)
     for (e, m), hw in [((5, 2), True), ((5, 2), False), ((3, 0), False), ((5, 6), False), ((5, 10), False)]:
         check(aps, orc, synthetic.edge_case_layers(1), e, m, hw, average=0, fused=True)
         grads = synthetic.make_grads(synthetic.C1_NUMELS + [1000, 1, 130, 8195, 16387], 1)

@@ -500,3 +500,25 @@ def test_mixed_hybrid_vs_torch(orc, p):
     assert np.array_equal(res.reduced, reduced)
     for a, b in zip(res.out, outs):
         assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+@pytest.mark.parametrize("p,fmt", [(1, (5, 2)), (3, (4, 3)), (4, (3, 0)), (8, (5, 6))])
+def test_oracle_threads_bit_identical(orc, p, fmt):
+    """The all-cores oracle (bench.py's cpu_baseline) splits only the element loops:
+    f~, every rank's codes, the reduced codes and the outputs are bit-identical for
+    any thread count (ranges cross layer and chunk boundaries: 600000 > OR_RANGE)."""
+    e, m = fmt
+    numels = synthetic.C1_NUMELS + [1000, 1, 9408, 130, 8195, 600000]
+    grads = synthetic.make_grads(numels, p)
+    one = orc.aps_sync(grads, e, m, n_threads=1)
+    assert one.rc == 0
+    for nt in (2, 5, 8):
+        r = orc.aps_sync(grads, e, m, n_threads=nt)
+        assert r.rc == 0
+        assert np.array_equal(r.ftilde, one.ftilde)
+        assert np.array_equal(r.packed, one.packed)
+        assert np.array_equal(r.reduced, one.reduced)
+        for a, b in zip(r.out, one.out):
+            assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    edge = synthetic.edge_case_layers(p)
+    assert np.array_equal(orc.aps_sync(edge, e, m, n_threads=4).reduced, orc.aps_sync(edge, e, m).reduced)
