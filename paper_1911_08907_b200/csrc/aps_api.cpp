@@ -729,15 +729,15 @@ aps_status aps_sync_out(aps_ctx *c, const float *const *grads, float *const *out
         // counter and never touches the 32-bit one: wave_claim_base must not advance then
         // (aps_set_graph_safe(0) resumes host mode from it).
         const int fp32_group = hybrid_fp32_group(c);
-#if APS_FUSED_W2
+#if APS_FUSED_CW
         if (fp32_group >= 0) {
             const aps_ctx::Group &lo = c->groups[1 - fp32_group];
-            APS_CUDA(c, aps::launch_fused_w2_hybrid32(c->t, lo.e, lo.m, lo.hw, fp32_group, average, c->max_layer_items,
+            APS_CUDA(c, aps::launch_fused_cw_hybrid32(c->t, lo.e, lo.m, lo.hw, fp32_group, average, c->max_layer_items,
                                                       c->stream));
         } else {
             // one cooperative launch per format group, in order on the context's stream
             for (const auto &g : c->groups)
-                APS_CUDA(c, aps::launch_fused_w2(group_tables(c, g), g.e, g.m, g.hw, average, g.max_layer_items,
+                APS_CUDA(c, aps::launch_fused_cw(group_tables(c, g), g.e, g.m, g.hw, average, g.max_layer_items,
                                                  c->stream));
         }
         c->phase = kReduced;
@@ -929,6 +929,12 @@ aps_status aps_set_graph_safe(aps_ctx *c, int enable)
     if (aps_status s = need_ws(c)) return s;
     const bool on = enable != 0;
     if (on == c->graph_safe) return APS_OK;
+#if APS_FUSED_CW
+    // the warp-specialised fused kernel keeps no per-call host state (self-resetting
+    // device counters): every launch is capture-safe, nothing to switch
+    c->graph_safe = on;
+    return APS_OK;
+#endif
     // the hybrid single launch (one low format + FP32) uses group 0's counter for all items
     const bool hybrid_single = hybrid_fp32_group(c) >= 0;
     if (on) {  // device counters := the host's call count, so both modes agree on call index and parity

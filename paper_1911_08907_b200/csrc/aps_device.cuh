@@ -181,6 +181,47 @@ __device__ __forceinline__ void st_hint(uint4 *p, uint4 v, uint64_t pol)
                  : "memory");
 }
 
+// mbarrier (shared memory) helpers: producer / consumer handoff inside a CTA
+__device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count) : "memory");
+}
+// arrive (release at CTA scope: this thread's prior shared / global writes are visible to a waiter)
+__device__ __forceinline__ void mbar_arrive(uint64_t *b)
+{
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_addr(b)) : "memory");
+}
+// non-blocking test of phase `parity` (acquire at CTA scope)
+__device__ __forceinline__ bool mbar_test(uint64_t *b, uint32_t parity)
+{
+    uint32_t ok;
+    asm volatile("{\n .reg .pred p;\n mbarrier.test_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n"
+                 " selp.u32 %0, 1, 0, p;\n}"
+                 : "=r"(ok) : "r"(smem_addr(b)), "r"(parity) : "memory");
+    return ok;
+}
+// bounded wait (2 s of %globaltimer, then flag bit 2 -> APS_ERR_STATE): a bookkeeping bug must
+// never hang the GPU
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity, uint32_t *flag)
+{
+    uint32_t ok;
+    uint64_t t0 = 0;
+    for (int it = 0;; ++it) {
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n"
+                     " selp.u32 %0, 1, 0, p;\n}"
+                     : "=r"(ok) : "r"(smem_addr(b)), "r"(parity) : "memory");
+        if (ok) return;
+        uint64_t ns;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+        if (it == 0) t0 = ns;
+        else if (ns - t0 > 2000000000ull) {
+            atomicOr(flag, 2u);
+            return;
+        }
+    }
+}
+
 // no second codec (uniform formats)
 struct CNone {
     static constexpr int kB = -1;

@@ -2,23 +2,37 @@
 // FindMaxExp (Alg. 1 line 3), f~ = upper_bound_exp - E (line 4), the scale,
 // Cast and pack (lines 5-6), Cast back, unscale and average (lines 8-9,
 // P:254-256).  With one rank no collective separates FindMaxExp from Cast, but Cast of
-// layer l still needs the abs-max of ALL of layer l.  The kernel is a wavefront over the
-// work items (32 KB of one layer each): position p of a static schedule holds the abs-max
-// of item p ("A") and the quantise of item p - D ("B"); D >= (items of the largest layer)
-// + grid, so every A item a B item needs sits in an earlier iteration of some CTA, and B
-// re-reads data read only ~D items (~28 MB) earlier -- from the 126 MB L2.
+// layer l still needs the abs-max of ALL of layer l.
 //
-// Work is per WARP (each of the 8 warps of a CTA owns a 4 KB slice of the position's
-// items): no CTA barrier, no claim counter.  Per layer, three self-resetting counters:
-//   amax[l]   u32 max of |g| bits (atom.max by each A slice)
-//   adone[l]  A slices counted (the add depends on the atom.max's returned value, so it
-//             is issued only after the max is performed at L2 -- no release fence, which
-//             would drain the lane's pending stores)
-//   bdone[l]  B slices done; the last one (8 x items of the layer) resets all three,
-// so a launch needs no call index or parity: a captured CUDA graph replays as is.
-// Progress: a B slice waits (lane 0, acquire, bounded) only on A slices at smaller
-// positions; the A part of an iteration precedes its B part, so the smallest waiting
-// position always completes (induction); the grid is co-resident (cooperative launch).
+// Schedule: a wavefront over the work items (32 KB of one layer each).  One claim
+// counter walks a merged sequence of 2n positions in which the quantise item B(i) trails
+// the abs-max item A(i) by D positions, D >= (items of the largest layer) + lag grids:
+//   A(0..D-1), then A(D) B(0) A(D+1) B(1) ..., then B(n-D..n-1)
+// so every A item a B item needs is claimed earlier, and B re-reads data read only ~D
+// items earlier -- from the 126 MB L2 (the DRAM traffic is one read, the codes and the
+// output: 8 L + L b / 8 bytes).
+//
+// Warp specialisation (the round-1 kernel did the claim, descriptor loads, readiness
+// check and abs-max fold on thread 0 between the data loads, and all 8 warps waited for
+// it at a CTA barrier every item -- measured: the B items alone ran 7 us slower than a
+// static grid-stride pass over the same bytes):
+//   * 8 DATA warps consume a ring of S slots in shared memory: wait full[s], read the
+//     slot's descriptor (addresses, count, f~), load 8 x 128-bit per lane, abs-max (A) or
+//     scale + Cast + pack + Cast back + unscale + store (B), arrive on empty[s].  No CTA
+//     barrier, no global atomics.
+//   * 1 CONTROL warp (lane 0) fills the ring: claims a position (the next claim is issued
+//     one slot early), loads the item's descriptor, for a B item waits (acquire, bounded)
+//     until every A item of its layer is folded and turns the layer's abs-max into f~,
+//     publishes the slot (arrive full[s]); when a slot comes back it folds the slot's
+//     A result into amax[layer] (returning atom.max; the count add depends on its value,
+//     so it is issued only once the max is performed at L2 -- no fence draining stores)
+//     or counts the B item done.
+// Counters are SELF-RESETTING: the last B item of a layer clears amax / adone / bdone,
+// the CTA holding the launch's final claim clears the claim counter.  A launch needs no
+// call index, parity or host-side state, so a captured CUDA graph replays as is.
+// Progress: a control warp waiting for a layer keeps folding its own finished slots; a
+// B item depends only on A items at earlier positions (claimed by running CTAs: every
+// CTA is resident, cooperative launch); every wait is bounded (2 s -> APS_ERR_STATE).
 #include <cstdint>
 #include <climits>
 #include <algorithm>
@@ -28,122 +42,236 @@
 
 namespace aps {
 
-template <class C, class C2, int NT>
-__global__ void __launch_bounds__(NT, kW2CtasPerSm)
-    fused_w2_kernel(DevTables t, C c, C2 c2, int lag, int bias, int bias2, int fmt2, int avg)
+constexpr int kCwSlots = APS_CW_SLOTS;
+constexpr int kCwDataWarps = kThreads / 32;            // 8
+constexpr int kCwThreads = kThreads + 32;               // + the control warp
+
+struct CwSlot {
+    const float *src;
+    float *dst;
+    int64_t byte_pos;
+    int cnt, n_tiles, ft, kind, fmt, layer, litems;  // kind: 0 abs-max (A), 1 quantise (B), 2 end; litems: items of the layer
+};
+
+template <class C, class C2>
+__global__ void __launch_bounds__(kCwThreads, kCwCtasPerSm)
+    fused_cw_kernel(DevTables t, C c, C2 c2, int lag, int bias, int bias2, int fmt2, int avg)
 {
-    constexpr bool kTwo = C2::kB > 0;          // items with fmt == fmt2 use c2 (bias2): hybrid FP32 layer
-    constexpr int kW = NT / 32;                // warps = slices per item
-    constexpr int kSliceEl = kItemTiles * kTile / kW;  // 1024 elements per slice
-    constexpr int kSliceTiles = kItemTiles / kW;       // 8 tiles per slice
-    constexpr int kPer = kSliceEl / 4 / 32;            // float4 per lane per slice: 8
-    __shared__ __align__(16) uint32_t s_codes[kW][kTile];  // generic widths: one tile of codes per warp
-    const int n = t.n_items, D = lag, G = gridDim.x;
+    constexpr bool kTwo = C2::kB > 0;  // items with fmt == fmt2 use c2 (bias2): the hybrid FP32 layer
+    constexpr int NT = kThreads;       // data threads
+    constexpr int kPer = kItemTiles * kTile / 4 / NT;  // float4 per data thread per item: 8
+    __shared__ CwSlot s_slot[kCwSlots];
+    __shared__ uint32_t s_part[kCwSlots][kCwDataWarps];     // per-warp abs-max of an A slot
+    __shared__ __align__(8) uint64_t s_full[kCwSlots], s_empty[kCwSlots];
+    __shared__ __align__(16) uint32_t s_codes[kCwDataWarps][kTile];  // generic widths
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int e_lo = warp * kSliceEl;          // first element of this warp's slice in an item
-    uint64_t keep, strm;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(strm));
+    const int n = t.n_items, D = lag, total = 2 * n;
     uint32_t *const amax = t.amax2, *const adone = t.layer_done, *const bdone = t.bdone;
-    // timeline (compile-time flag 16): warp 0's start / end stamps, wait time and waits per CTA
-    constexpr bool kTl = (kFusedDefaultFlags & 16) != 0;
-    uint64_t tl_t0 = 0, tl_wait = 0, tl_waits = 0, tl_items = 0;
-    if (kTl) tl_t0 = global_ns();
-    for (int p = blockIdx.x; p < n + D; p += G) {
-        // ------------------------------------------------ A: abs-max of slice `warp` of item p
-        int a_layer = -1;
-        uint32_t a_old = 0;
-        if (p < n) {
-            const Item it = t.items[p];
-            const float4 *g4 = reinterpret_cast<const float4 *>(t.iptr[p].src + e_lo);
-            uint32_t mx = 0;
-            if (e_lo + kSliceEl <= it.cnt) {
-                float4 v[kPer];
-#pragma unroll
-                for (int q = 0; q < kPer; ++q) v[q] = ld_hint4(g4 + lane + 32 * q, keep);
-#pragma unroll
-                for (int q = 0; q < kPer; ++q) mx = max(mx, absbits4(v[q]));
-            } else if (e_lo < it.cnt) {  // the layer's last, partial slice
-                const int cnt = it.cnt - e_lo, n4 = cnt >> 2;
-                for (int q = lane; q < n4; q += 32) mx = max(mx, absbits4(ld_hint4(g4 + q, keep)));
-                if (lane < (cnt & 3))
-                    mx = max(mx, __float_as_uint(t.iptr[p].src[e_lo + 4 * n4 + lane]) & 0x7fffffffu);
-            }
-            mx = __reduce_max_sync(0xffffffffu, mx);
-            if (lane == 0) {
-                asm volatile("atom.relaxed.gpu.global.max.u32 %0, [%1], %2;" : "=r"(a_old) : "l"(&amax[it.layer]), "r"(mx)
-                             : "memory");
-                a_layer = it.layer;
-            }
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kCwSlots; ++s) {
+            mbar_init(&s_full[s], 1);
+            mbar_init(&s_empty[s], kCwDataWarps);
         }
-        // ------------------------------------------------ B: quantise + unscale slice `warp` of item p - D
-        const int qi = p - D;
-        if (qi >= 0) {
-            const Item it = t.items[qi];
-            const int l = it.layer;
-            const bool two = kTwo && it.fmt == fmt2;
-            const uint32_t target = (uint32_t)(kW * it.layer_items);
-            int ft = 0;
-            if (lane == 0) {
-                if (kTl && warp == 0 && ld_acquire_u32(&adone[l]) < target) {
-                    const uint64_t w0 = global_ns();
-                    spin_until([&] { return ld_acquire_u32(&adone[l]) >= target; }, t.flag);
-                    tl_wait += global_ns() - w0;
-                    ++tl_waits;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == kCwDataWarps) {
+        // ======================================================== control warp
+        if (lane != 0) return;
+        auto decode = [&](int j, bool &isB) -> int {
+            if (j < D) { isB = false; return j; }
+            if (j < total - D) {
+                const int k = j - D;
+                isB = k & 1;
+                return isB ? (k >> 1) : D + (k >> 1);
+            }
+            isB = true;
+            return n - D + (j - (total - D));
+        };
+        // fold pipeline: the count of the A slot folded last (its add depends on the
+        // returned max) and the B item counted last (its returned count decides the reset)
+        int pa_layer = -1, pb_layer = -1;
+        uint32_t pa_old = 0, pb_old = 0, pb_target = 0;
+        auto settle = [&]() {
+            if (pa_layer >= 0) {
+                const uint32_t inc = (pa_old == 0xffffffffu) ? 0u : 1u;  // always 1: abs bits <= 0x7fffffff
+                asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(&adone[pa_layer]), "r"(inc) : "memory");
+                pa_layer = -1;
+            }
+            if (pb_layer >= 0) {
+                if (pb_old == pb_target - 1u) {  // the layer's last B item: reset its counters for the next call
+                    amax[pb_layer] = 0u;
+                    adone[pb_layer] = 0u;
+                    bdone[pb_layer] = 0u;
                 }
-                spin_until([&] { return ld_acquire_u32(&adone[l]) >= target; }, t.flag);
-                const int32_t E = exponent_of(ld_relaxed_u32(&amax[l]), 1);
-                ft = (E == INT32_MIN || E == INT32_MAX) ? 0 : (two ? bias2 : bias) - E;  // f~ (Alg. 1 line 4)
-                if (it.tile_begin == 0 && warp == 0) {  // record E, f~, the non-finite flag (A4)
-                    t.E_local[l] = E;
-                    t.ftilde[l] = ft;
+                pb_layer = -1;
+            }
+        };
+        auto fold = [&](int s) {  // slot s came back from the data warps
+            const CwSlot &sl = s_slot[s];
+            settle();
+            if (sl.kind == 0) {
+                uint32_t m = 0;
+#pragma unroll
+                for (int w = 0; w < kCwDataWarps; ++w) m = max(m, s_part[s][w]);
+                asm volatile("atom.relaxed.gpu.global.max.u32 %0, [%1], %2;" : "=r"(pa_old) : "l"(&amax[sl.layer]), "r"(m)
+                             : "memory");
+                pa_layer = sl.layer;
+            } else if (sl.kind == 1) {
+                pb_old = atomicAdd(&bdone[sl.layer], 1u);
+                pb_target = (uint32_t)sl.litems;
+                pb_layer = sl.layer;
+            }
+        };
+        int filled = 0, folded = 0;  // slots published / folded so far (slot i % S)
+        auto fold_ready = [&](bool block) {
+            while (folded < filled) {
+                const int s = folded % kCwSlots;
+                const uint32_t ph = (uint32_t)(folded / kCwSlots) & 1u;
+                if (!block && !mbar_test(&s_empty[s], ph)) break;
+                if (block) mbar_wait(&s_empty[s], ph, t.flag);
+                fold(s);
+                ++folded;
+                if (block) break;
+            }
+        };
+        int64_t raw = atomicAdd(t.claim64, 1ull);  // (the claim counter is 64-bit; reset by the last claimer)
+        for (;;) {
+            const int s = filled % kCwSlots;
+            if (filled >= kCwSlots) {  // the slot's previous item must be done: fold it
+                while (folded <= filled - kCwSlots) fold_ready(true);
+            }
+            fold_ready(false);
+            const int64_t j = raw;
+            if (j >= total) {
+                if (j == (int64_t)total + gridDim.x - 1) *t.claim64 = 0ull;  // the launch's final claim
+                s_slot[s].kind = 2;
+                mbar_arrive(&s_full[s]);
+                ++filled;
+                break;
+            }
+            raw = atomicAdd(t.claim64, 1ull);  // next claim, in flight while this slot is prepared
+            bool isB;
+            const int k = decode((int)j, isB);
+            const Item it = t.items[k];
+            const ItemPtr ip = t.iptr[k];
+            CwSlot sl;
+            sl.src = ip.src;
+            sl.dst = ip.dst;
+            sl.byte_pos = it.byte_pos;
+            sl.cnt = it.cnt;
+            sl.n_tiles = it.n_tiles;
+            sl.kind = isB ? 1 : 0;
+            sl.fmt = it.fmt;
+            sl.layer = it.layer;
+            sl.litems = it.layer_items;
+            sl.ft = 0;
+            if (isB) {
+                const uint32_t target = (uint32_t)it.layer_items;
+                if (ld_acquire_u32(&adone[it.layer]) < target) {
+                    // wait for the layer's A items; keep folding this CTA's own finished slots
+                    const uint64_t t0 = global_ns();
+                    while (ld_acquire_u32(&adone[it.layer]) < target) {
+                        fold_ready(false);
+                        settle();
+                        __nanosleep(64);
+                        if (global_ns() - t0 > 2000000000ull) {
+                            atomicOr(t.flag, kFlagWaitTimeout);
+                            break;
+                        }
+                    }
+                }
+                const int32_t E = exponent_of(ld_relaxed_u32(&amax[it.layer]), 1);
+                const int bs = (kTwo && it.fmt == fmt2) ? bias2 : bias;  // the layer's upper_bound_exp
+                sl.ft = (E == INT32_MIN || E == INT32_MAX) ? 0 : bs - E;  // f~ (Alg. 1 line 4)
+                if (it.tile_begin == 0) {  // record E, f~, the non-finite flag (A4)
+                    t.E_local[it.layer] = E;
+                    t.ftilde[it.layer] = sl.ft;
                     if (E == INT32_MAX) atomicOr(t.flag, kFlagNonfinite);
                 }
             }
-            ft = __shfl_sync(0xffffffffu, ft, 0);
-            const Pow2 s(ft);
+            s_slot[s] = sl;
+            mbar_arrive(&s_full[s]);
+            ++filled;
+        }
+        while (folded < filled - 1) fold_ready(true);  // (the end slot needs no fold)
+        settle();
+        return;
+    }
+
+    // ======================================================== data warps
+    uint64_t keep, strm;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(strm));
+    for (int i = 0;; ++i) {
+        const int s = i % kCwSlots;
+        mbar_wait(&s_full[s], (uint32_t)(i / kCwSlots) & 1u, t.flag);
+        const int kind = s_slot[s].kind;
+        if (kind == 2) break;
+        const float *src = s_slot[s].src;
+        const int cnt = s_slot[s].cnt;
+        const bool full = cnt == kItemTiles * kTile;
+        if (kind == 0) {
+            // ---------------- abs-max item
+            const float4 *g4 = reinterpret_cast<const float4 *>(src);
+            uint32_t mx = 0;
+            if (full) {
+                float4 v[kPer];
+#pragma unroll
+                for (int q = 0; q < kPer; ++q) v[q] = ld_hint4(g4 + threadIdx.x + q * NT, keep);
+#pragma unroll
+                for (int q = 0; q < kPer; ++q) mx = max(mx, absbits4(v[q]));
+            } else {
+                const int n4 = cnt >> 2;
+                for (int q = threadIdx.x; q < n4; q += NT) mx = max(mx, absbits4(ld_hint4(g4 + q, keep)));
+                if ((int)threadIdx.x < (cnt & 3)) mx = max(mx, __float_as_uint(src[4 * n4 + threadIdx.x]) & 0x7fffffffu);
+            }
+            mx = __reduce_max_sync(0xffffffffu, mx);
+            if (lane == 0) s_part[s][warp] = mx;
+        } else {
+            // ---------------- quantise + unscale item
+            float *dst = s_slot[s].dst;
+            const int ft = s_slot[s].ft;
+            const Pow2 sc(ft);
             const Unscale us(ft, 1, avg);
-            const float *src = t.iptr[qi].src + e_lo;
-            float *dst = t.iptr[qi].dst + e_lo;
-            const int cnt = it.cnt - e_lo;  // valid elements of this slice (may be <= 0)
+            uint8_t *pk = t.packed + s_slot[s].byte_pos;
+            const int n_tiles = s_slot[s].n_tiles;
             auto quantise = [&](const auto &cc) {
                 using CC = std::decay_t<decltype(cc)>;
                 constexpr int B = CC::kB;
                 if constexpr (B == 8 || B == 16 || B == 32) {
                     using W = typename Word4<B>::T;
-                    W *out = reinterpret_cast<W *>(t.packed + it.byte_pos) + e_lo / 4;
-                    if (cnt >= kSliceEl && !s.wide) {
+                    W *out = reinterpret_cast<W *>(pk);
+                    if (full && !sc.wide) {
                         const float4 *g4 = reinterpret_cast<const float4 *>(src);
                         float4 *o4 = reinterpret_cast<float4 *>(dst);
                         float4 v[kPer];
 #pragma unroll
-                        for (int q = 0; q < kPer; ++q) v[q] = ld_hint4(g4 + lane + 32 * q, strm);
+                        for (int q = 0; q < kPer; ++q) v[q] = ld_hint4(g4 + threadIdx.x + q * NT, strm);
 #pragma unroll
                         for (int q = 0; q < kPer; ++q) {
-                            const float4 y = make_float4(__fmul_rn(v[q].x, s.f), __fmul_rn(v[q].y, s.f),
-                                                         __fmul_rn(v[q].z, s.f), __fmul_rn(v[q].w, s.f));
+                            const float4 y = make_float4(__fmul_rn(v[q].x, sc.f), __fmul_rn(v[q].y, sc.f),
+                                                         __fmul_rn(v[q].z, sc.f), __fmul_rn(v[q].w, sc.f));
                             const W code = pack4<B>(cc, y);
-                            st_hint(out + lane + 32 * q, code, strm);
-                            st_hint4(o4 + lane + 32 * q, us.apply4(unpack4<B>(cc, code)), strm);
+                            st_hint(out + threadIdx.x + q * NT, code, strm);
+                            st_hint4(o4 + threadIdx.x + q * NT, us.apply4(unpack4<B>(cc, code)), strm);
                         }
-                    } else if (cnt > 0) {
-                        // the slice's tiles (codes past cnt: +0 padding of the tile)
-                        const int ng = min(kSliceTiles, it.n_tiles - warp * kSliceTiles) * (kTile / 4);
-                        for (int q = lane; q < ng; q += 32) {
-                            const W code = pack4<B>(cc, s.apply4(load_group(src, 4 * (int64_t)q, cnt)));
+                    } else {
+                        const int ng = n_tiles * (kTile / 4);
+                        for (int q = threadIdx.x; q < ng; q += NT) {
+                            const W code = pack4<B>(cc, sc.apply4(load_group(src, 4 * (int64_t)q, cnt)));
                             out[q] = code;
                             store_group(dst, 4 * (int64_t)q, cnt, us.apply4(unpack4<B>(cc, code)));
                         }
                     }
-                } else if (cnt > 0) {
-                    // any width: per-warp tiles of 128 codes through shared memory (16 b bytes each)
+                } else {
                     const int b = cc.b();
                     uint32_t *codes = s_codes[warp];
-                    uint32_t *outw = reinterpret_cast<uint32_t *>(t.packed + it.byte_pos) + warp * kSliceTiles * 4 * b;
-                    const int nt = min(kSliceTiles, it.n_tiles - warp * kSliceTiles);
-                    for (int tt = 0; tt < nt; ++tt) {
+                    uint32_t *outw = reinterpret_cast<uint32_t *>(pk);
+                    for (int tt = warp; tt < n_tiles; tt += kCwDataWarps) {
                         const int64_t e0 = (int64_t)tt * kTile + lane * 4;
-                        const float4 y = s.apply4(load_group(src, e0, cnt));
+                        const float4 y = sc.apply4(load_group(src, e0, cnt));
                         const uint4 cd = make_uint4(cc.enc(y.x), cc.enc(y.y), cc.enc(y.z), cc.enc(y.w));
                         *reinterpret_cast<uint4 *>(codes + lane * 4) = cd;
                         __syncwarp();
@@ -156,71 +284,52 @@ __global__ void __launch_bounds__(NT, kW2CtasPerSm)
                 }
             };
             if constexpr (kTwo) {
-                if (two) quantise(c2);
+                if (s_slot[s].fmt == fmt2) quantise(c2);
                 else quantise(c);
             } else {
                 quantise(c);
             }
-            if (lane == 0) {  // the last B slice of the layer resets its counters for the next call
-                const uint32_t done = atomicAdd(&bdone[l], 1u);
-                if (done == target - 1u) {
-                    amax[l] = 0u;
-                    adone[l] = 0u;
-                    bdone[l] = 0u;
-                }
-            }
         }
-        // ------------------------------------------------ count the A slice (its max is at L2 by now)
-        if (a_layer >= 0) {
-            const uint32_t inc = (a_old == 0xffffffffu) ? 0u : 1u;  // always 1: abs bits <= 0x7fffffff
-            asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(&adone[a_layer]), "r"(inc) : "memory");
-        }
-        if (kTl) ++tl_items;
-    }
-    if (kTl && threadIdx.x == 0 && blockIdx.x * 4 + 3 < kTimelineSlots) {
-        t.timeline[blockIdx.x * 4 + 0] = tl_t0;
-        t.timeline[blockIdx.x * 4 + 1] = tl_wait;
-        t.timeline[blockIdx.x * 4 + 2] = (tl_waits << 32) | tl_items;
-        t.timeline[blockIdx.x * 4 + 3] = global_ns();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_empty[s]);
     }
 }
 
 template <class C, class C2>
-static int w2_grid(int n_items)
+static int cw_grid(int n_items)
 {
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_w2_kernel<C, C2, kThreads>, kThreads, 0);
-    per_sm = std::max(1, std::min(per_sm, kW2CtasPerSm));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_cw_kernel<C, C2>, kCwThreads, 0);
+    per_sm = std::max(1, std::min(per_sm, kCwCtasPerSm));
     return std::max(1, std::min(n_items, sm_count() * per_sm));
 }
 
 template <class C, class C2>
-static cudaError_t launch_w2(const DevTables &t, C c, C2 c2, int bias, int bias2, int fmt2, int average, int max_layer_items,
-                             cudaStream_t s)
+static cudaError_t launch_cw(const DevTables &t, C c, C2 c2, int bias, int bias2, int fmt2, int average,
+                             int max_layer_items, cudaStream_t s)
 {
     if (t.n_items == 0) return cudaSuccess;
-    const int grid = w2_grid<C, C2>(t.n_items);
+    const int grid = cw_grid<C, C2>(t.n_items);
     int lag = std::min(t.n_items, max_layer_items + kWaveLagGrids * grid);
     void *args[] = {const_cast<DevTables *>(&t), &c, &c2, &lag, &bias, &bias2, &fmt2, &average};
-    // co-residency of every CTA is required (static schedule): cooperative launch
-    return cudaLaunchCooperativeKernel((const void *)fused_w2_kernel<C, C2, kThreads>, dim3(grid), dim3(kThreads), args,
-                                       0, s);
+    // every CTA resident (a control warp may wait on A items another CTA claimed)
+    return cudaLaunchCooperativeKernel((const void *)fused_cw_kernel<C, C2>, dim3(grid), dim3(kCwThreads), args, 0, s);
 }
 
-cudaError_t launch_fused_w2(const DevTables &t, int e, int m, bool hw, int average, int max_layer_items, cudaStream_t s)
+cudaError_t launch_fused_cw(const DevTables &t, int e, int m, bool hw, int average, int max_layer_items, cudaStream_t s)
 {
     const int bias = (1 << (e - 1)) - 1;
     return with_codec(e, m, hw, [&](auto c) -> cudaError_t {
-        return launch_w2(t, c, CNone{}, bias, 0, -1, average, max_layer_items, s);
+        return launch_cw(t, c, CNone{}, bias, 0, -1, average, max_layer_items, s);
     });
 }
 
-cudaError_t launch_fused_w2_hybrid32(const DevTables &t, int e, int m, bool hw, int fmt2, int average,
+cudaError_t launch_fused_cw_hybrid32(const DevTables &t, int e, int m, bool hw, int fmt2, int average,
                                      int max_layer_items, cudaStream_t s)
 {
     const int bias = (1 << (e - 1)) - 1;
     return with_codec(e, m, hw, [&](auto c) -> cudaError_t {
-        return launch_w2(t, c, CF32{}, bias, 127, fmt2, average, max_layer_items, s);
+        return launch_cw(t, c, CF32{}, bias, 127, fmt2, average, max_layer_items, s);
     });
 }
 

@@ -123,14 +123,20 @@ cudaError_t launch_fused_p1_wave(const DevTables &t, int e, int m, bool hw, int 
 // binary32 codec (the hybrid FP32 classifier layer), the others (e, m, hw).
 cudaError_t launch_fused_p1_wave_hybrid32(const DevTables &t, int e, int m, bool hw, int fmt2, int average,
                                           const WaveCall &w, int lag, int grid, cudaStream_t s);
-// fused N = 1 sync, static wavefront with per-warp work (aps_fused.cu): one cooperative
-// launch per format group (hybrid FP32 classifier: one launch), no per-call host state
-#ifndef APS_FUSED_W2
-#define APS_FUSED_W2 0
+// fused N = 1 sync, warp-specialised wavefront (aps_fused.cu): one cooperative launch per
+// format group (hybrid FP32 classifier: one launch), self-resetting counters, no per-call host state
+#ifndef APS_FUSED_CW
+#define APS_FUSED_CW 1
 #endif
-constexpr int kW2CtasPerSm = 4;
-cudaError_t launch_fused_w2(const DevTables &t, int e, int m, bool hw, int average, int max_layer_items, cudaStream_t s);
-cudaError_t launch_fused_w2_hybrid32(const DevTables &t, int e, int m, bool hw, int fmt2, int average,
+#ifndef APS_CW_SLOTS
+#define APS_CW_SLOTS 3
+#endif
+#ifndef APS_CW_CTAS_PER_SM
+#define APS_CW_CTAS_PER_SM 3
+#endif
+constexpr int kCwCtasPerSm = APS_CW_CTAS_PER_SM;
+cudaError_t launch_fused_cw(const DevTables &t, int e, int m, bool hw, int average, int max_layer_items, cudaStream_t s);
+cudaError_t launch_fused_cw_hybrid32(const DevTables &t, int e, int m, bool hw, int fmt2, int average,
                                      int max_layer_items, cudaStream_t s);
 // true when (e,m) has a hardware converter that is exact on the APS path
 // formats with a hardware / exact fast codec: fp8 e5m2, e4m3 (APS regime only,

@@ -541,6 +541,8 @@ __global__ void __launch_bounds__(NT, kWaveCtasPerSm)
     constexpr bool kTwo = C2::kB > 0;  // items with fmt == fmt2 use c2 (bias2)
     __shared__ __align__(16) uint32_t s_codes[NT / 32][kTile];
     __shared__ int s_claim[3], s_ft[3], s_ok[3];  // claims run two items ahead (3 slots)
+    __shared__ Item s_item[3];                    // ... with their descriptors and addresses, loaded by
+    __shared__ ItemPtr s_iptr[3];                 //     thread 0 at claim time (no dependent load at item start)
     __shared__ uint32_t s_part[2][NT / 32];       // per-warp maxima of the last two items
     __shared__ int s_part_layer[2];               // their layer (-1: a quantise item)
     // positions: A(0..D-1), A(D) B(0) A(D+1) B(1) ..., B(n-D..n-1)
@@ -598,8 +600,10 @@ __global__ void __launch_bounds__(NT, kWaveCtasPerSm)
         if (j < total) {
             bool isB;
             const int k = decode(j, isB);
+            const Item it = t.items[k];
+            s_item[sl] = it;
+            s_iptr[sl] = t.iptr[k];
             if (isB) {
-                const Item it = t.items[k];
                 if ((int)(ld_acquire_u32(&t.layer_done[it.layer]) - layer_target(it)) >= 0) {
                     s_ft[sl] = ft_of(it);
                     s_ok[sl] = 1;
@@ -638,9 +642,9 @@ __global__ void __launch_bounds__(NT, kWaveCtasPerSm)
     int slot = 0, par = 0;
     for (int j = s_claim[0]; j < total;) {
         bool isB;
-        const int k = decode(j, isB);
-        const Item it = t.items[k];
-        const ItemPtr p = t.iptr[k];
+        decode(j, isB);
+        const Item it = s_item[slot];
+        const ItemPtr p = s_iptr[slot];
         const float4 *g4 = reinterpret_cast<const float4 *>(p.src);
         const bool full = it.cnt == kItemTiles * kTile;
         float4 v[kPer];
