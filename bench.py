@@ -214,9 +214,11 @@ def oracle_sample(numels, p, budget_s, n_threads):
     return sample, per_elem
 
 
-def cpu_oracle_run(numels, e, m, p, budget_s=20.0):
+def cpu_oracle_run(numels, e, m, p, budget_s=20.0, min_s=10.0):
     """The CPU oracle (plain C) on all host cores, on a bounded sample of the
-    workload (a prefix of the layer list, ~budget_s of work), p simulated ranks."""
+    workload, p simulated ranks: a prefix of the layer list sized to ~budget_s of
+    work, and -- when the whole workload takes less -- whole syncs repeated until
+    at least min_s of CPU work (the 10-30 s the contract asks for)."""
     import oracle
     import synthetic
     cores, model = host_cpu()
@@ -224,13 +226,20 @@ def cpu_oracle_run(numels, e, m, p, budget_s=20.0):
     grads = synthetic.make_grads(sample, p)
     t0 = time.perf_counter()
     r = oracle.aps_sync(grads, e, m, want_packed=False, n_threads=cores)
-    t = time.perf_counter() - t0
+    t1 = time.perf_counter() - t0
     assert r.rc == 0
+    reps = 1 + max(0, int((min_s - t1) / max(t1, 1e-3)))
+    t = t1
+    if reps > 1:
+        t0 = time.perf_counter()
+        for _ in range(reps - 1):
+            oracle.aps_sync(grads, e, m, want_packed=False, n_threads=cores)
+        t += time.perf_counter() - t0
     L = sum(sample)
     desc = (f"first {len(sample)} of {len(numels)} layers ({L} of {sum(numels)} elements) x {p} simulated "
-            f"rank(s), full oracle aps_sync (FindMaxExp, MAX, cast, ring, unscale), {cores} threads")
-    return {"value": round(4 * L / t / 1e9, 6), "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc,
-            "seconds": round(t, 3), "cpu_model": model, "nproc": cores,
+            f"rank(s), full oracle aps_sync (FindMaxExp, MAX, cast, ring, unscale), {reps} sync(s), {cores} threads")
+    return {"value": round(4 * L * reps / t / 1e9, 6), "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc,
+            "seconds": round(t, 3), "syncs": reps, "cpu_model": model, "nproc": cores,
             "note": "per-rank fp32-equivalent GB/s (4 L / t, as the GPU line's per_rank)"}
 
 
@@ -705,7 +714,7 @@ class Bench:
             achieved = dbytes / (ms * 1e-3) / 1e9
             roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                     "frac": round(achieved / peak, 4), "traffic": traffic.get("fused_p1"),
-                    "kernel": "fused_p1_wave_kernel (a1 + a3 + a4 + a7, one launch)",
+                    "kernel": "fused_cw_kernel (a1 + a3 + a4 + a7, one launch)",
                     "algorithmic_bytes_per_launch": int(dbytes),
                     "algorithmic_bytes_rule": "8 L + code bytes: one fp32 read, the packed codes, one fp32 write",
                     "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",

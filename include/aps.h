@@ -219,13 +219,19 @@ aps_status aps_ring_step(int world_size, int rank, int step, int *send_chunk, in
 aps_status aps_set_reduction(aps_ctx *ctx, int group_k, int acc_exp_bits, int acc_man_bits, int kahan);
 
 /* CUDA-graph capture.  Every path takes its per-call state from device memory
- * (peer epochs, the abs-max done counter) except the fused world_size == 1
- * wavefront kernel, whose claim base, call index and accumulator parity are
- * launch arguments by default (the fastest form).  enable = 1 switches it to the
- * capture-safe form (all three derived on the device from a 64-bit claim counter;
- * ~1 us slower per call), so a captured aps_sync replays exactly; enable = 0
- * switches back (reads the call count the device reached).  [sync] */
+ * (self-resetting claim and completion counters, device-resident peer epochs and
+ * stochastic-rounding call counter), so any aps_sync / aps_sync_out can be captured
+ * and replayed as is.  Kept for source compatibility: records the flag, switches
+ * nothing.  Errors: APS_ERR_STATE (no workspace). */
 aps_status aps_set_graph_safe(aps_ctx *ctx, int enable);
+
+/* Occupancy cap of the fused one-rank launch (aps_sync / aps_sync_out at
+ * world_size 1): at most ctas_per_sm CTAs per SM (0 = as many as fit, the
+ * default).  A cap leaves registers and warps of every SM to concurrent work on
+ * other streams -- the backward kernels that the DDP hook's syncs overlap
+ * (P:637-640); the sync itself then takes longer.  Errors: APS_ERR_ARG
+ * (ctas_per_sm < 0). */
+aps_status aps_set_occupancy(aps_ctx *ctx, int ctas_per_sm);
 
 /* Rounding mode of every Cast ("some researchers
  * prefer stochastic rounding ... an unbiased estimate"; the paper's own runs use
@@ -320,10 +326,6 @@ aps_status aps_debug_decode(const uint32_t *codes, float *out, int64_t n, int ex
  * (reading A26; aps_set_rounding). */
 aps_status aps_debug_cast_sr(const float *in, uint32_t *codes, int64_t n, int exp_bits, int man_bits,
                              uint64_t seed, uint64_t phase, void *cuda_stream);
-/* [sync] Per-CTA %globaltimer stamps (start, end of abs-max pass, after the
- * grid barrier, end; 4 x uint64 per CTA, ns) of the last fused p = 1 launch
- * run with APS_FUSED_FLAGS bit 16 set (profiling aid). */
-aps_status aps_debug_timeline(aps_ctx *ctx, uint64_t *host_out, int max_slots);
 /* Reduce step on its own: own[i] <- Cast(fl32(dec(recv[i]) + dec(own[i]))),
  * over n_tiles tiles of packed codes. */
 aps_status aps_debug_ring_reduce(uint8_t *own, const uint8_t *recv, int64_t n_tiles,

@@ -27,10 +27,10 @@ EXPORTS = [
     "aps_sync_host", "aps_status_sync", "aps_get_scales", "aps_get_packed", "aps_layout",
     "aps_ring_step", "aps_last_error", "aps_destroy", "aps_version", "aps_nccl_unique_id",
     "aps_nccl_comm_init", "aps_nccl_comm_destroy", "aps_sim_layer_scales", "aps_sim_allreduce",
-    "aps_debug_cast", "aps_debug_decode", "aps_debug_ring_reduce", "aps_debug_timeline",
+    "aps_debug_cast", "aps_debug_decode", "aps_debug_ring_reduce",
     "aps_init_mixed", "aps_layout_mixed", "aps_set_reduction", "aps_peer_export", "aps_peer_import",
     "aps_sim_connect", "aps_round_off_error", "aps_census", "aps_set_rounding", "aps_debug_cast_sr",
-    "aps_set_graph_safe",
+    "aps_set_graph_safe", "aps_set_occupancy",
 ]
 PEER_HANDLE_BYTES = 64
 
@@ -84,7 +84,6 @@ def load(path: Path | str | None = None):
         "aps_debug_cast": ([vp, vp, i64, i32, i32, i32, vp], i32),
         "aps_debug_decode": ([vp, vp, i64, i32, i32, i32, vp], i32),
         "aps_debug_ring_reduce": ([vp, vp, i64, i32, i32, i32, vp], i32),
-        "aps_debug_timeline": ([vp, vp, i32], i32),
         "aps_init_mixed": ([ctypes.POINTER(vp), vp, vp, i32, i32, i32, vp, vp, vp], i32),
         "aps_layout_mixed": ([i32, i32, vp, vp, vp, ctypes.POINTER(i64), ctypes.POINTER(i64)], i32),
         "aps_set_reduction": ([vp, i32, i32, i32, i32], i32),
@@ -95,6 +94,7 @@ def load(path: Path | str | None = None):
         "aps_census": ([vp, vp, vp, vp], i32),
         "aps_set_rounding": ([vp, i32, ctypes.c_uint64], i32),
         "aps_set_graph_safe": ([vp, i32], i32),
+        "aps_set_occupancy": ([vp, i32], i32),
         "aps_debug_cast_sr": ([vp, vp, i64, i32, i32, ctypes.c_uint64, ctypes.c_uint64, vp], i32),
     }
     for name, (args, res) in sig.items():
@@ -285,13 +285,6 @@ class ApsContext:
         off = ptr.value - self.workspace.data_ptr()
         return self.workspace[off:off + nb.value]
 
-    def timeline(self):
-        """Per-CTA globaltimer stamps of the last fused launch (APS_FUSED_FLAGS & 16)."""
-        import numpy as np
-        out = np.zeros(4 * 2048, dtype=np.uint64)
-        self._check(self.L.aps_debug_timeline(self.h, out.ctypes.data, out.size), "aps_debug_timeline")
-        return out.reshape(-1, 4)
-
     def set_hw_convert(self, enable: bool):
         self._check(self.L.aps_set_hw_convert(self.h, int(enable)), "aps_set_hw_convert")
 
@@ -305,8 +298,8 @@ class ApsContext:
     def capture_sync(self, grads, out=None, average: bool = True):
         """Capture one aps_sync_out (grads -> out, default in place) into a CUDA graph
         and return it; ``graph.replay()`` then re-runs the whole synchronisation on
-        whatever the same buffers hold.  Every kernel takes its per-call state (claim
-        bases, accumulator parity, peer epochs) from device memory, so replays are
+        whatever the same buffers hold.  Every kernel takes its per-call state
+        (self-resetting counters, peer epochs) from device memory, so replays are
         exact.  The context's stream must not be the legacy default stream.  One
         un-captured call first uploads the pointer tables."""
         import torch
@@ -320,8 +313,13 @@ class ApsContext:
         return g
 
     def set_graph_safe(self, enable: bool = True):
-        """Capture-safe wavefront launches (aps_set_graph_safe); capture_sync sets it."""
+        """aps_set_graph_safe: every launch is capture-safe already (recorded only)."""
         self._check(self.L.aps_set_graph_safe(self.h, int(enable)), "aps_set_graph_safe")
+
+    def set_occupancy(self, ctas_per_sm: int = 0):
+        """Cap the fused one-rank launch at ctas_per_sm CTAs per SM (0 = as many as fit),
+        leaving SM resources to concurrent work on other streams (aps_set_occupancy)."""
+        self._check(self.L.aps_set_occupancy(self.h, int(ctas_per_sm)), "aps_set_occupancy")
 
     def set_rounding(self, stochastic: bool = False, seed: int = 0):
         """Nearest-even (default) or stochastic rounding of every Cast (aps_set_rounding)."""

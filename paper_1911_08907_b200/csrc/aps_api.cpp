@@ -41,7 +41,10 @@ struct aps_ctx {
     std::vector<aps::Item> items;
     std::vector<aps::LayerDev> layers;
     std::vector<int64_t> voff;    // [n_layers + 1] a1's vector space (4 fp32 per vector, per layer)
-    std::vector<int32_t> cta_layer;  // a1: layer of each CTA's first vector
+    std::vector<int32_t> abs_seg_off;  // a1: [G + 1] first segment of each CTA's share
+    std::vector<aps::AbsSeg> abs_segs; // a1: shares cut at layer boundaries
+    std::vector<aps::AbsSeg> abs_tails; // a1: partial last vectors
+    int ctas_per_sm = 0;                // aps_set_occupancy (0: as many as fit)
     int64_t tiles = 0;        // T' (padded to a multiple of world)
     int64_t packed_bytes = 0; // sum over tiles of 16 * b(tile)
     int64_t chunk_bytes = 0;  // packed_bytes / world (uniform formats)
@@ -54,7 +57,6 @@ struct aps_ctx {
         int e, m;
         bool hw;
         int item_begin, item_count, max_layer_items;
-        uint32_t wave_claim_base;  // this group's 32-bit wavefront claim counter at its next launch (host mode)
     };
     std::vector<Group> groups;
     struct Seg {
@@ -70,11 +72,9 @@ struct aps_ctx {
     uint8_t *ws = nullptr;
     size_t ws_bytes = 0, need = 0;
     size_t off_packed = 0, off_recv = 0, off_items = 0, off_layers = 0, off_src = 0, off_dst = 0,
-           off_amax = 0, off_eloc = 0, off_eglob = 0, off_ft = 0, off_flag = 0, off_amax2 = 0, off_iptr = 0, off_tl = 0, off_claim = 0, off_ldone = 0, off_claim64 = 0, off_voff = 0, off_ctal = 0, off_bdone = 0, off_srcall = 0;
+           off_amax = 0, off_eloc = 0, off_eglob = 0, off_ft = 0, off_flag = 0, off_amax2 = 0, off_iptr = 0, off_ldone = 0, off_claim64 = 0, off_voff = 0, off_ctal = 0, off_asegs = 0, off_atails = 0, off_bdone = 0, off_srcall = 0;
     int max_layer_items = 0;
-    uint32_t wave_calls = 0;   // wavefront launches so far (host mode: per-layer counter targets)
-    bool graph_safe = false;   // wavefront kernel takes its per-call state from the device (aps_set_graph_safe)
-    std::vector<unsigned long long> claim64_init;  // host staging of the 64-bit claim counters
+    bool graph_safe = false;   // aps_set_graph_safe (every launch is capture-safe; recorded only)
     std::vector<const void *> host_key;            // aps_sync_host: pointer set of the cached copy runs
     std::vector<int> h2d_runs, d2h_runs;           // end layer of each coalesced copy
     bool iptr_valid = false;
@@ -82,7 +82,6 @@ struct aps_ctx {
     std::vector<const float *> src_cache;
     std::vector<float *> dst_cache;
     int phase = kNone;
-    uint32_t gen = 0;           // fused launches so far (selects the accumulator parity)
     // format groups after the first run on side streams, concurrently with group 0
     // (disjoint layers, packed bytes and counters): fork/join through events
     std::vector<cudaStream_t> side;
@@ -288,7 +287,7 @@ static aps_status init_common(aps_ctx **out, const int *e_arr, const int *m_arr,
         int g = 0;
         while (g < (int)c->groups.size() && (c->groups[g].e != c->le[l] || c->groups[g].m != c->lm[l])) ++g;
         if (g == (int)c->groups.size())
-            c->groups.push_back({c->le[l], c->lm[l], c->hw_enabled && aps::hw_available(c->le[l], c->lm[l]), 0, 0, 0, 0});
+            c->groups.push_back({c->le[l], c->lm[l], c->hw_enabled && aps::hw_available(c->le[l], c->lm[l]), 0, 0, 0});
         layer_group[l] = g;
     }
     std::stable_sort(c->items.begin(), c->items.end(), [&](const aps::Item &a, const aps::Item &b) {
@@ -355,13 +354,13 @@ static aps_status init_common(aps_ctx **out, const int *e_arr, const int *m_arr,
     c->off_flag = o;   o = align_up(o + 4);
     c->off_amax2 = o;  o = align_up(o + 8 * (size_t)n_layers);
     c->off_iptr = o;   o = align_up(o + sizeof(aps::ItemPtr) * c->items.size());
-    c->off_tl = o;     o = align_up(o + sizeof(uint64_t) * aps::kTimelineSlots);
-    c->off_claim = o;  o = align_up(o + 3 * sizeof(uint32_t) * c->groups.size());  // 3 per format group
     c->off_ldone = o;  o = align_up(o + 4 * (size_t)n_layers);
     c->off_voff = o;   o = align_up(o + 8 * ((size_t)n_layers + 1));
     c->off_bdone = o;  o = align_up(o + 4 * (size_t)n_layers);
     c->off_srcall = o; o = align_up(o + 4);
-    c->off_ctal = o;   o = align_up(o + 4 * (size_t)aps::kAbsMaxCtas);
+    c->off_ctal = o;   o = align_up(o + 4 * ((size_t)aps::kAbsMaxCtas + 1));
+    c->off_asegs = o;  o = align_up(o + sizeof(aps::AbsSeg) * ((size_t)aps::kAbsMaxCtas + (size_t)n_layers));
+    c->off_atails = o; o = align_up(o + sizeof(aps::AbsSeg) * (size_t)n_layers);
     // graph-safe counters: 64-bit wavefront claim counter per format group, absmax_ranges done counter
     c->off_claim64 = o; o = align_up(o + 8 * c->groups.size() + 4);
     // peer transport: flag block and E slots [2][world][n_layers] (world > 1 only)
@@ -428,20 +427,54 @@ aps_status aps_set_workspace(aps_ctx *c, void *dev, size_t bytes)
                                 cudaMemcpyHostToDevice, c->stream));
     APS_CUDA(c, cudaMemcpyAsync(c->ws + c->off_layers, c->layers.data(),
                                 sizeof(aps::LayerDev) * c->layers.size(), cudaMemcpyHostToDevice, c->stream));
-    {   // a1's balanced split: CTA b streams vectors [b V / G, (b+1) V / G)
+    {   // a1's balanced split: CTA b streams vectors [b V / G, (b+1) V / G), cut at layer
+        // boundaries into segments (each in one layer)
+        // a1's vector space holds each layer's WHOLE vectors only; a layer's partial last
+        // vector (numel % 4 != 0) goes to the tail list (elements [e0, numel))
+        std::vector<int64_t> wvoff(1, 0);
+        c->abs_tails.clear();
+        for (int l = 0; l < c->n_layers; ++l) {
+            const int64_t n = c->layers[l].numel;
+            wvoff.push_back(wvoff.back() + n / 4);
+            if (n % 4) {
+                aps::AbsSeg tl{};
+                tl.e0 = n / 4 * 4;
+                tl.numel = n;
+                tl.layer = l;
+                c->abs_tails.push_back(tl);
+            }
+        }
         const int G = aps::absmax_grid();
-        const int64_t V = c->voff.back();
-        c->cta_layer.resize(G);
+        const int64_t V = wvoff.back();
+        c->abs_seg_off.assign(1, 0);
+        c->abs_segs.clear();
         int l = 0;
         for (int b = 0; b < G; ++b) {
-            const int64_t lo = V * b / G;
-            while (l < c->n_layers - 1 && c->voff[l + 1] <= lo) ++l;
-            c->cta_layer[b] = l;
+            const int64_t lo = V * b / G, hi = V * (b + 1) / G;
+            for (int64_t v = lo; v < hi;) {
+                while (wvoff[l + 1] <= v) ++l;
+                const int64_t v1 = std::min(hi, wvoff[l + 1]);
+                aps::AbsSeg sg{};
+                sg.v0 = v;
+                sg.v1 = v1;
+                sg.e0 = 4 * (v - wvoff[l]);
+                sg.numel = c->layers[l].numel;
+                sg.layer = l;
+                c->abs_segs.push_back(sg);
+                v = v1;
+            }
+            c->abs_seg_off.push_back((int32_t)c->abs_segs.size());
         }
+        if (!c->abs_tails.empty())
+            APS_CUDA(c, cudaMemcpyAsync(c->ws + c->off_atails, c->abs_tails.data(),
+                                        sizeof(aps::AbsSeg) * c->abs_tails.size(), cudaMemcpyHostToDevice, c->stream));
         APS_CUDA(c, cudaMemcpyAsync(c->ws + c->off_voff, c->voff.data(), 8 * c->voff.size(), cudaMemcpyHostToDevice,
                                     c->stream));
-        APS_CUDA(c, cudaMemcpyAsync(c->ws + c->off_ctal, c->cta_layer.data(), 4 * (size_t)G, cudaMemcpyHostToDevice,
-                                    c->stream));
+        APS_CUDA(c, cudaMemcpyAsync(c->ws + c->off_ctal, c->abs_seg_off.data(), 4 * c->abs_seg_off.size(),
+                                    cudaMemcpyHostToDevice, c->stream));
+        if (!c->abs_segs.empty())
+            APS_CUDA(c, cudaMemcpyAsync(c->ws + c->off_asegs, c->abs_segs.data(),
+                                        sizeof(aps::AbsSeg) * c->abs_segs.size(), cudaMemcpyHostToDevice, c->stream));
     }
     aps::DevTables &t = c->t;
     t.items = reinterpret_cast<const aps::Item *>(c->ws + c->off_items);
@@ -456,15 +489,16 @@ aps_status aps_set_workspace(aps_ctx *c, void *dev, size_t bytes)
     t.flag = reinterpret_cast<uint32_t *>(c->ws + c->off_flag);
     t.amax2 = reinterpret_cast<uint32_t *>(c->ws + c->off_amax2);
     t.iptr = reinterpret_cast<aps::ItemPtr *>(c->ws + c->off_iptr);
-    t.timeline = reinterpret_cast<uint64_t *>(c->ws + c->off_tl);
-    t.claim = reinterpret_cast<uint32_t *>(c->ws + c->off_claim);
     t.claim64 = reinterpret_cast<unsigned long long *>(c->ws + c->off_claim64);
     t.ranges_done = reinterpret_cast<uint32_t *>(c->ws + c->off_claim64 + 8 * c->groups.size());
     t.layer_done = reinterpret_cast<uint32_t *>(c->ws + c->off_ldone);
     t.voff = reinterpret_cast<const int64_t *>(c->ws + c->off_voff);
     t.bdone = reinterpret_cast<uint32_t *>(c->ws + c->off_bdone);
     t.sr_call = reinterpret_cast<uint32_t *>(c->ws + c->off_srcall);
-    t.cta_layer = reinterpret_cast<const int32_t *>(c->ws + c->off_ctal);
+    t.abs_seg_off = reinterpret_cast<const int32_t *>(c->ws + c->off_ctal);
+    t.abs_segs = reinterpret_cast<const aps::AbsSeg *>(c->ws + c->off_asegs);
+    t.abs_tails = reinterpret_cast<const aps::AbsSeg *>(c->ws + c->off_atails);
+    t.n_abs_tails = (int)c->abs_tails.size();
 
     if (c->groups.size() > 1 && c->side.empty()) {
         c->side.resize(c->groups.size() - 1);
@@ -475,11 +509,8 @@ aps_status aps_set_workspace(aps_ctx *c, void *dev, size_t bytes)
         }
         APS_CUDA(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     }
-    c->wave_calls = 0;
     c->graph_safe = false;
-    for (auto &g : c->groups) g.wave_claim_base = 0;
     c->iptr_valid = false;
-    c->gen = 0;
     t.packed = c->ws + c->off_packed;
     t.n_items = (int)c->items.size();
     t.n_layers = c->n_layers;
@@ -496,7 +527,6 @@ static aps::DevTables group_tables(const aps_ctx *c, const aps_ctx::Group &g)
     t.items += g.item_begin;
     t.iptr += g.item_begin;
     t.n_items = g.item_count;
-    t.claim += 3 * (&g - c->groups.data());
     t.claim64 += (&g - c->groups.data());
     return t;
 }
@@ -585,7 +615,15 @@ aps_status aps_layer_scales(aps_ctx *c, const float *const *grads)
     if (aps_status s = need_ws(c)) return s;
     if (!grads) return fail(c, APS_ERR_ARG, "grads is NULL");
     if (aps_status s = upload_ptrs<const float *>(c, c->src_cache, grads, c->off_src)) return s;
+#if APS_ABSMAX_CW
+    if (!c->iptr_valid) {  // per-item gradient addresses (output addresses: filled by the fused path)
+        APS_CUDA(c, aps::launch_build_item_ptrs(c->t, c->stream));
+        c->iptr_valid = true;
+    }
+    APS_CUDA(c, aps::launch_absmax_cw(c->t, c->world, c->stream));
+#else
     APS_CUDA(c, aps::launch_absmax(c->t, c->world, c->stream));
+#endif
     if (c->world == 1 && !c->comm) {
         c->phase = kScales;
     } else if (c->peer) {
@@ -717,61 +755,25 @@ aps_status aps_sync_out(aps_ctx *c, const float *const *grads, float *const *out
     if (!grads || !out) return fail(c, APS_ERR_ARG, "NULL pointer array");
     if (c->world == 1 && !c->comm && !c->sr) {
         // one rank: FindMaxExp -> f~ -> Cast -> pack -> Cast back -> unscale in one
-        // wavefront launch per format group (quantise items trail their abs-max items by
-        // D positions; a layer's items never straddle groups)
+        // launch per format group (aps_fused.cu: quantise items trail their abs-max items
+        // by D claim positions; a layer's items never straddle groups)
         if (aps_status s = upload_ptrs<const float *>(c, c->src_cache, grads, c->off_src)) return s;
         if (aps_status s = upload_ptrs<float *>(c, c->dst_cache, out, c->off_dst)) return s;
         if (!c->iptr_valid) {
             APS_CUDA(c, aps::launch_build_item_ptrs(c->t, c->stream));
             c->iptr_valid = true;
         }
-        // In graph-safe mode the kernel takes its claim base from the 64-bit device
-        // counter and never touches the 32-bit one: wave_claim_base must not advance then
-        // (aps_set_graph_safe(0) resumes host mode from it).
         const int fp32_group = hybrid_fp32_group(c);
-#if APS_FUSED_CW
         if (fp32_group >= 0) {
             const aps_ctx::Group &lo = c->groups[1 - fp32_group];
             APS_CUDA(c, aps::launch_fused_cw_hybrid32(c->t, lo.e, lo.m, lo.hw, fp32_group, average, c->max_layer_items,
-                                                      c->stream));
+                                                      c->stream, c->ctas_per_sm));
         } else {
-            // one cooperative launch per format group, in order on the context's stream
+            // one launch per format group, in order on the context's stream
             for (const auto &g : c->groups)
                 APS_CUDA(c, aps::launch_fused_cw(group_tables(c, g), g.e, g.m, g.hw, average, g.max_layer_items,
-                                                 c->stream));
+                                                 c->stream, c->ctas_per_sm));
         }
-        c->phase = kReduced;
-        return APS_OK;
-#endif
-        if (fp32_group >= 0) {
-            const aps_ctx::Group &lo = c->groups[1 - fp32_group];
-            aps_ctx::Group &g0 = c->groups[0];  // its claim counter serves the single launch
-            const int wgrid = aps::fused_p1_wave_grid(lo.e, lo.m, lo.hw, c->t.n_items);
-            const int lag = std::min(c->t.n_items, c->max_layer_items + aps::kWaveLagGrids * wgrid);
-            const aps::WaveCall w{c->graph_safe, c->gen, g0.wave_claim_base, c->wave_calls};
-            APS_CUDA(c, aps::launch_fused_p1_wave_hybrid32(c->t, lo.e, lo.m, lo.hw, fp32_group, average, w, lag,
-                                                           wgrid, c->stream));
-            if (!c->graph_safe) g0.wave_claim_base += (uint32_t)(2 * c->t.n_items + aps::kWaveOvershoot * wgrid);
-            ++c->wave_calls;
-            ++c->gen;
-            c->phase = kReduced;
-            return APS_OK;
-        }
-        if (aps_status s = for_groups(c, [&](const aps_ctx::Group &gc, const aps::DevTables &t, cudaStream_t st,
-                                             bool coop) {
-                aps_ctx::Group &g = const_cast<aps_ctx::Group &>(gc);
-                const int wgrid = aps::fused_p1_wave_grid(g.e, g.m, g.hw, t.n_items);
-                const int lag = std::min(t.n_items, g.max_layer_items + aps::kWaveLagGrids * wgrid);
-                const aps::WaveCall w{c->graph_safe, c->gen, g.wave_claim_base, c->wave_calls};
-                cudaError_t e = aps::launch_fused_p1_wave(t, g.e, g.m, g.hw, average, w, lag, wgrid, st, coop);
-                // every position is claimed once and every CTA overshoots kWaveOvershoot times
-                if (e == cudaSuccess && !c->graph_safe)
-                    g.wave_claim_base += (uint32_t)(2 * t.n_items + aps::kWaveOvershoot * wgrid);
-                return e;
-            }))
-            return s;
-        ++c->wave_calls;
-        ++c->gen;
         c->phase = kReduced;
         return APS_OK;
     }
@@ -908,53 +910,19 @@ aps_status aps_set_reduction(aps_ctx *c, int group_k, int acc_exp_bits, int acc_
     return APS_OK;
 }
 
-// per-call advance of group g's wavefront claim counter (as the launch in aps_sync_out)
-static unsigned long long wave_adv(const aps_ctx *c, size_t g, bool hybrid_single)
-{
-    if (hybrid_single) {
-        int lo = 0;
-        for (size_t k = 0; k < c->groups.size(); ++k)
-            if (!(c->groups[k].e == 8 && c->groups[k].m == 23)) lo = (int)k;
-        const aps_ctx::Group &L = c->groups[lo];
-        return 2ull * c->t.n_items + (unsigned long long)aps::kWaveOvershoot *
-                                         aps::fused_p1_wave_grid(L.e, L.m, L.hw, c->t.n_items);
-    }
-    const aps_ctx::Group &G = c->groups[g];
-    return 2ull * G.item_count +
-           (unsigned long long)aps::kWaveOvershoot * aps::fused_p1_wave_grid(G.e, G.m, G.hw, G.item_count);
-}
-
 aps_status aps_set_graph_safe(aps_ctx *c, int enable)
 {
     if (aps_status s = need_ws(c)) return s;
-    const bool on = enable != 0;
-    if (on == c->graph_safe) return APS_OK;
-#if APS_FUSED_CW
-    // the warp-specialised fused kernel keeps no per-call host state (self-resetting
-    // device counters): every launch is capture-safe, nothing to switch
-    c->graph_safe = on;
+    // every launch is capture-safe (self-resetting device counters, device-resident peer
+    // epochs): nothing to switch; the flag is recorded for aps_debug_* introspection only
+    c->graph_safe = enable != 0;
     return APS_OK;
-#endif
-    // the hybrid single launch (one low format + FP32) uses group 0's counter for all items
-    const bool hybrid_single = hybrid_fp32_group(c) >= 0;
-    if (on) {  // device counters := the host's call count, so both modes agree on call index and parity
-        c->claim64_init.resize(c->groups.size());
-        for (size_t g = 0; g < c->groups.size(); ++g)
-            c->claim64_init[g] = (unsigned long long)c->wave_calls * wave_adv(c, g, hybrid_single);
-        APS_CUDA(c, cudaMemcpyAsync(c->t.claim64, c->claim64_init.data(), 8 * c->groups.size(),
-                                    cudaMemcpyHostToDevice, c->stream));
-        APS_CUDA(c, cudaStreamSynchronize(c->stream));
-    } else {
-        // back to host mode: the call count the device reached (graph replays included).
-        // The 32-bit claim counters were not touched in graph mode, so wave_claim_base
-        // (not advanced by graph-mode calls) still equals them.
-        unsigned long long v = 0;
-        APS_CUDA(c, cudaMemcpyAsync(&v, c->t.claim64, 8, cudaMemcpyDeviceToHost, c->stream));
-        APS_CUDA(c, cudaStreamSynchronize(c->stream));
-        c->wave_calls = (uint32_t)(v / wave_adv(c, 0, hybrid_single));
-        c->gen = c->wave_calls;
-    }
-    c->graph_safe = on;
+}
+
+aps_status aps_set_occupancy(aps_ctx *c, int ctas_per_sm)
+{
+    if (!c || ctas_per_sm < 0) return c ? fail(c, APS_ERR_ARG, "ctas_per_sm < 0") : APS_ERR_ARG;
+    c->ctas_per_sm = ctas_per_sm;
     return APS_OK;
 }
 
@@ -1243,15 +1211,6 @@ aps_status aps_debug_cast_sr(const float *in, uint32_t *codes, int64_t n, int e,
                ? APS_OK : APS_ERR_CUDA;
 }
 
-aps_status aps_debug_timeline(aps_ctx *c, uint64_t *host_out, int max_slots)
-{
-    if (aps_status s = need_ws(c)) return s;
-    if (!host_out || max_slots < 0) return APS_ERR_ARG;
-    const size_t n = (size_t)std::min(max_slots, aps::kTimelineSlots);
-    APS_CUDA(c, cudaMemcpyAsync(host_out, c->t.timeline, n * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
-    APS_CUDA(c, cudaStreamSynchronize(c->stream));
-    return APS_OK;
-}
 
 aps_status aps_debug_ring_reduce(uint8_t *own, const uint8_t *recv, int64_t n_tiles, int e, int m, int hw,
                                  void *stream)

@@ -226,6 +226,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity, uint32_t
 struct CNone {
     static constexpr int kB = -1;
 };
+// marker: the control-warp kernel runs the abs-max items only (a1 alone)
+struct CAOnly {
+    static constexpr int kB = -2;
+};
 
 // 4 consecutive fp32 of a layer starting at element e0, zero-filled past n.
 __device__ __forceinline__ float4 load_group(const float *g, int64_t e0, int64_t n)
@@ -272,6 +276,13 @@ struct Pow2 {
     __device__ __forceinline__ float4 apply4(float4 v) const
     {
         return make_float4(apply(v.x), apply(v.y), apply(v.z), apply(v.w));
+    }
+    // !wide only: one FMUL per element.  Kernels branch on `wide` (uniform per layer) around
+    // whole loops -- inside a loop the compiler evaluates both sides of apply() and
+    // selects (F2F + DMUL + F2F per element)
+    __device__ __forceinline__ float4 apply4_narrow(float4 v) const
+    {
+        return make_float4(__fmul_rn(v.x, f), __fmul_rn(v.y, f), __fmul_rn(v.z, f), __fmul_rn(v.w, f));
     }
 };
 
@@ -349,6 +360,145 @@ __device__ __forceinline__ uint32_t assemble_word(const uint32_t *codes, int w, 
     return (uint32_t)acc;
 }
 
+// ------------------------------------------------------------------ generic-width tiles in registers
+// For b <= 16 (every C4 width that is not 8/16/32: 4-bit (3,0), 12-bit (5,6), runtime
+// formats) a warp packs and unpacks a whole tile in registers.  Lane l owns codes
+// 4l..4l+3 = bits [4bl, 4bl + 4b) of the tile's LSB-first stream (<= 64 bits).
+//  * unpack: each lane loads the 2-3 words its bits touch straight from memory (lanes
+//    sharing a word are served by one request) and funnel-shifts its 4 codes out;
+//  * pack: b = 4 and b = 12 pair lanes (16 + 16 bits = one word; 48 + 48 bits = three
+//    words) with ONE 32-bit shuffle; other widths assemble word w (held by lane w & 31,
+//    register w >> 5) from the lanes its bits come from with 64-bit shuffles.
+// No shared memory and no per-tile warp serialisation, so a warp keeps several tiles'
+// loads in flight.  B = the compile-time width, or 0 for the runtime b.  Every lane of
+// the warp must call the pack functions (shuffles).
+constexpr int kRegMaxB = 16;
+
+template <int B>
+__device__ __forceinline__ uint64_t lane_bits(uint4 cd, int b_)
+{
+    const int b = B ? B : b_;
+    return (uint64_t)cd.x | ((uint64_t)cd.y << b) | ((uint64_t)cd.z << (2 * b)) | ((uint64_t)cd.w << (3 * b));
+}
+
+// word w of the tile whose lanes hold `v` (lane_bits); 0 for w >= 4b
+template <int B>
+__device__ __forceinline__ uint32_t tile_word(uint64_t v, int b_, int w)
+{
+    const int b = B ? B : b_, nb = 4 * b;
+    const bool wide = nb > 32;
+    const int l0 = (32 * w) / nb;            // first lane whose bits reach word w
+    const int nl = (32 + nb - 1) / nb + 1;   // lanes one word can touch
+    uint32_t word = 0;
+#pragma unroll
+    for (int k = 0; k < nl; ++k) {
+        const int src = l0 + k;
+        uint64_t x = __shfl_sync(0xffffffffu, (uint32_t)v, src & 31);
+        if (wide) x |= (uint64_t)__shfl_sync(0xffffffffu, (uint32_t)(v >> 32), src & 31) << 32;
+        const int off = src * nb - 32 * w;   // position of lane src's bits relative to the word
+        if (src < 32 && off < 32) word |= off >= 0 ? (uint32_t)(x << off) : (uint32_t)(x >> -off);
+    }
+    return word;
+}
+
+// the (at most two) words of a tile a lane stores: word i0 = v0, word i1 = v1 (-1: none)
+struct TileSlots {
+    uint32_t v0, v1;
+    int i0, i1;
+};
+
+template <int B>
+__device__ __forceinline__ TileSlots tile_pack(uint4 cd, int b_, int lane)
+{
+    const int b = B ? B : b_;
+    const uint64_t v = lane_bits<B>(cd, b);
+    TileSlots t;
+    if constexpr (B == 4) {
+        // lanes 2i, 2i+1: 16 + 16 bits = word i (stored by the even lane)
+        const uint32_t o = __shfl_xor_sync(0xffffffffu, (uint32_t)v, 1);
+        t.v0 = (uint32_t)v | (o << 16);
+        t.i0 = (lane & 1) ? -1 : (lane >> 1);
+        t.v1 = 0u;
+        t.i1 = -1;
+    } else if constexpr (B == 12) {
+        // lanes 2i, 2i+1: 48 + 48 bits = words 3i, 3i+1, 3i+2 (even lane: 3i and 3i+1,
+        // whose high half is the odd lane's low 16 bits; odd lane: 3i+2)
+        const uint32_t o = __shfl_xor_sync(0xffffffffu, (uint32_t)v, 1);
+        const int i = 3 * (lane >> 1);
+        if (lane & 1) {
+            t.v0 = (uint32_t)(v >> 16);
+            t.i0 = i + 2;
+            t.i1 = -1;
+            t.v1 = 0u;
+        } else {
+            t.v0 = (uint32_t)v;
+            t.i0 = i;
+            t.v1 = (uint32_t)(v >> 32) | (o << 16);
+            t.i1 = i + 1;
+        }
+    } else {
+        const int nw = 4 * b;
+        t.v0 = tile_word<B>(v, b, lane);
+        t.i0 = lane < nw ? lane : -1;
+        t.v1 = (nw > 32) ? tile_word<B>(v, b, lane + 32) : 0u;
+        t.i1 = (nw > 32 && lane + 32 < nw) ? lane + 32 : -1;
+    }
+    return t;
+}
+
+// store a lane's words with st(word_index, value)
+template <class St>
+__device__ __forceinline__ void tile_store(const TileSlots &t, St st)
+{
+    if (t.i0 >= 0) st(t.i0, t.v0);
+    if (t.i1 >= 0) st(t.i1, t.v1);
+}
+
+// the words a lane's bits touch: w0 = 4bl / 32 and the next one or two
+struct TileRaw {
+    uint32_t x0, x1, x2;
+};
+
+template <int B>
+__device__ __forceinline__ constexpr bool tile_needs(int k)
+{
+    // does some lane's bit range reach word w0 + k?  (runtime widths: assume yes)
+    if (B == 0) return true;
+    for (int l = 0; l < 32; ++l)
+        if ((4 * B * l) % 32 + 4 * B > 32 * k) return true;
+    return false;
+}
+
+template <int B, class Ld>
+__device__ __forceinline__ TileRaw tile_fetch(const uint32_t *tw, int b_, int lane, Ld ld)
+{
+    const int b = B ? B : b_, nw = 4 * b;
+    const int w0 = (lane * 4 * b) >> 5;
+    TileRaw r;
+    r.x0 = ld(tw + w0);
+    r.x1 = (tile_needs<B>(1) && w0 + 1 < nw) ? ld(tw + w0 + 1) : 0u;
+    r.x2 = (tile_needs<B>(2) && nw > 32 && w0 + 2 < nw) ? ld(tw + w0 + 2) : 0u;
+    return r;
+}
+
+// the lane's 4 codes from its words
+template <int B>
+__device__ __forceinline__ uint4 tile_split(const TileRaw &r, int b_, int lane)
+{
+    const int b = B ? B : b_, nb = 4 * b;
+    const int sh = (lane * nb) & 31;
+    const uint32_t lo = __funnelshift_r(r.x0, r.x1, sh);
+    const uint32_t hi = nb > 32 ? __funnelshift_r(r.x1, r.x2, sh) : 0u;
+    const uint64_t v = lo | ((uint64_t)hi << 32);
+    const uint64_t mask = (1ull << b) - 1ull;
+    return make_uint4((uint32_t)(v & mask), (uint32_t)((v >> b) & mask), (uint32_t)((v >> (2 * b)) & mask),
+                      (uint32_t)((v >> (3 * b)) & mask));
+}
+
+struct LdPlain {
+    __device__ __forceinline__ uint32_t operator()(const uint32_t *p) const { return *p; }
+};
+
 // code k of a tile whose words are in shared memory (words[4b] is a zero pad)
 __device__ __forceinline__ uint32_t extract_code(const uint32_t *words, int k, int b)
 {
@@ -400,12 +550,27 @@ struct Unscale {
     float inv_n;    // 2^-log2(N) for power-of-two N
     float n_f;
     bool average;
+    bool fast;      // !s.wide && !div: two (or one) FMULs, see apply4_fast
+    bool scale_n;   // average by a power-of-two N > 1
     __device__ __forceinline__ Unscale(int ft, int N, int avg) : s(-ft)
     {
         average = avg != 0;
         div = (N & (N - 1)) != 0;
         n_f = (float)N;
         inv_n = div ? 1.f : __uint_as_float((uint32_t)(127 - (31 - __clz(N))) << 23);
+        fast = !s.wide && !div;
+        scale_n = average && N > 1;
+    }
+    // fl32(fl32(v 2^-f~) 2^-log2 N): x / N for a power-of-two N is the same correctly
+    // rounded result as x * 2^-log2 N (reading A16); valid when `fast`
+    __device__ __forceinline__ float apply_fast(float v) const
+    {
+        const float x = __fmul_rn(v, s.f);
+        return scale_n ? __fmul_rn(x, inv_n) : x;
+    }
+    __device__ __forceinline__ float4 apply4_fast(float4 v) const
+    {
+        return make_float4(apply_fast(v.x), apply_fast(v.y), apply_fast(v.z), apply_fast(v.w));
     }
     __device__ __forceinline__ float apply(float v) const
     {

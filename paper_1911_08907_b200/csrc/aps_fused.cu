@@ -31,8 +31,9 @@
 // the CTA holding the launch's final claim clears the claim counter.  A launch needs no
 // call index, parity or host-side state, so a captured CUDA graph replays as is.
 // Progress: a control warp waiting for a layer keeps folding its own finished slots; a
-// B item depends only on A items at earlier positions (claimed by running CTAs: every
-// CTA is resident, cooperative launch); every wait is bounded (2 s -> APS_ERR_STATE).
+// B item depends only on A items at earlier positions, each claimed by a CTA that was
+// running when it claimed it (no co-residency needed: a plain launch); every wait is
+// bounded (2 s -> APS_ERR_STATE).
 #include <cstdint>
 #include <climits>
 #include <algorithm>
@@ -53,11 +54,49 @@ struct CwSlot {
     int cnt, n_tiles, ft, kind, fmt, layer, litems;  // kind: 0 abs-max (A), 1 quantise (B), 2 end; litems: items of the layer
 };
 
+// Generic width b <= 16 (4-bit (3,0), 12-bit (5,6), runtime formats) of a quantise item:
+// each data warp owns tiles warp, warp + 8, ... of the item; all its loads are issued
+// first (8 x 128-bit per lane in flight, as the byte-code path), then every tile is
+// scaled, Cast, packed in registers (warp shuffles, aps_device.cuh) and decoded back.
+template <int B, bool FAST, class CC>
+__device__ __forceinline__ void cw_quant_reg(const CC &cc, const float *src, float *dst, uint8_t *pk, int cnt,
+                                             int n_tiles, bool full, const Pow2 &sc, const Unscale &us,
+                                             uint64_t strm, int warp, int lane)
+{
+    constexpr int kJ = kItemTiles / kCwDataWarps;
+    const int b = cc.b();
+    uint32_t *outw = reinterpret_cast<uint32_t *>(pk);
+    float4 v[kJ];
+    if (full) {  // unconditional 128-bit loads: all kJ in flight before the first use
+        const float4 *g4 = reinterpret_cast<const float4 *>(src) + lane;
+#pragma unroll
+        for (int j = 0; j < kJ; ++j) v[j] = ld_hint4(g4 + (warp + j * kCwDataWarps) * (kTile / 4), strm);
+    } else {
+#pragma unroll
+        for (int j = 0; j < kJ; ++j) v[j] = load_group(src, (int64_t)(warp + j * kCwDataWarps) * kTile + lane * 4, cnt);
+    }
+#pragma unroll
+    for (int j = 0; j < kJ; ++j) {
+        const int tt = warp + j * kCwDataWarps;
+        if (tt >= n_tiles) break;  // warp-uniform
+        const int64_t e0 = (int64_t)tt * kTile + lane * 4;
+        const float4 y = FAST ? sc.apply4_narrow(v[j]) : sc.apply4(v[j]);
+        const uint4 cd = make_uint4(cc.enc(y.x), cc.enc(y.y), cc.enc(y.z), cc.enc(y.w));
+        uint32_t *tw = outw + (int64_t)tt * (4 * b);
+        tile_store(tile_pack<B>(cd, b, lane), [&](int i, uint32_t x) { st_hint(tw + i, x, strm); });
+        const float4 d = make_float4(cc.dec(cd.x), cc.dec(cd.y), cc.dec(cd.z), cc.dec(cd.w));
+        const float4 o = FAST ? us.apply4_fast(d) : us.apply4(d);
+        if (full) st_hint4(reinterpret_cast<float4 *>(dst + e0), o, strm);
+        else store_group(dst, e0, cnt, o);
+    }
+}
+
 template <class C, class C2>
 __global__ void __launch_bounds__(kCwThreads, kCwCtasPerSm)
     fused_cw_kernel(DevTables t, C c, C2 c2, int lag, int bias, int bias2, int fmt2, int avg)
 {
     constexpr bool kTwo = C2::kB > 0;  // items with fmt == fmt2 use c2 (bias2): the hybrid FP32 layer
+    constexpr bool kAOnly = C2::kB == CAOnly::kB;  // a1 alone (aps_layer_scales): avg carries N
     constexpr int NT = kThreads;       // data threads
     constexpr int kPer = kItemTiles * kTile / 4 / NT;  // float4 per data thread per item: 8
     __shared__ CwSlot s_slot[kCwSlots];
@@ -65,7 +104,7 @@ __global__ void __launch_bounds__(kCwThreads, kCwCtasPerSm)
     __shared__ __align__(8) uint64_t s_full[kCwSlots], s_empty[kCwSlots];
     __shared__ __align__(16) uint32_t s_codes[kCwDataWarps][kTile];  // generic widths
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int n = t.n_items, D = lag, total = 2 * n;
+    const int n = t.n_items, D = lag, total = kAOnly ? n : 2 * n;
     uint32_t *const amax = t.amax2, *const adone = t.layer_done, *const bdone = t.bdone;
     if (threadIdx.x == 0) {
         for (int s = 0; s < kCwSlots; ++s) {
@@ -78,9 +117,9 @@ __global__ void __launch_bounds__(kCwThreads, kCwCtasPerSm)
 
     if (warp == kCwDataWarps) {
         // ======================================================== control warp
-        if (lane != 0) return;
+        if (lane == 0) [&]() {
         auto decode = [&](int j, bool &isB) -> int {
-            if (j < D) { isB = false; return j; }
+            if (kAOnly || j < D) { isB = false; return j; }
             if (j < total - D) {
                 const int k = j - D;
                 isB = k & 1;
@@ -115,9 +154,13 @@ __global__ void __launch_bounds__(kCwThreads, kCwCtasPerSm)
                 uint32_t m = 0;
 #pragma unroll
                 for (int w = 0; w < kCwDataWarps; ++w) m = max(m, s_part[s][w]);
-                asm volatile("atom.relaxed.gpu.global.max.u32 %0, [%1], %2;" : "=r"(pa_old) : "l"(&amax[sl.layer]), "r"(m)
-                             : "memory");
-                pa_layer = sl.layer;
+                if constexpr (kAOnly) {  // no per-layer count: the last CTA finishes (below)
+                    asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(&amax[sl.layer]), "r"(m) : "memory");
+                } else {
+                    asm volatile("atom.relaxed.gpu.global.max.u32 %0, [%1], %2;" : "=r"(pa_old) : "l"(&amax[sl.layer]), "r"(m)
+                                 : "memory");
+                    pa_layer = sl.layer;
+                }
             } else if (sl.kind == 1) {
                 pb_old = atomicAdd(&bdone[sl.layer], 1u);
                 pb_target = (uint32_t)sl.litems;
@@ -197,6 +240,26 @@ __global__ void __launch_bounds__(kCwThreads, kCwCtasPerSm)
         }
         while (folded < filled - 1) fold_ready(true);  // (the end slot needs no fold)
         settle();
+        }();
+        if constexpr (kAOnly) {
+            // a1 alone: every A item was folded with a fire-and-forget red.max; the CTA
+            // counts itself once (after a fence: cumulativity orders its red.max first),
+            // and the last CTA turns the maxima into E_l = ceil(log2(N A_l)) and clears them
+            __syncwarp();
+            uint32_t last = 0;
+            if (lane == 0) {
+                __threadfence();
+                last = atomicAdd(t.ranges_done, 1u) == gridDim.x - 1u;
+                if (last) *t.ranges_done = 0u;
+            }
+            if (__shfl_sync(0xffffffffu, last, 0)) {
+                __threadfence();
+                for (int l = lane; l < t.n_layers; l += 32) {
+                    t.E_local[l] = exponent_of(ld_relaxed_u32(&amax[l]), avg);
+                    amax[l] = 0u;
+                }
+            }
+        }
         return;
     }
 
@@ -229,7 +292,7 @@ __global__ void __launch_bounds__(kCwThreads, kCwCtasPerSm)
             }
             mx = __reduce_max_sync(0xffffffffu, mx);
             if (lane == 0) s_part[s][warp] = mx;
-        } else {
+        } else if constexpr (!kAOnly) {
             // ---------------- quantise + unscale item
             float *dst = s_slot[s].dst;
             const int ft = s_slot[s].ft;
@@ -243,7 +306,7 @@ __global__ void __launch_bounds__(kCwThreads, kCwCtasPerSm)
                 if constexpr (B == 8 || B == 16 || B == 32) {
                     using W = typename Word4<B>::T;
                     W *out = reinterpret_cast<W *>(pk);
-                    if (full && !sc.wide) {
+                    if (full && !sc.wide && us.fast) {
                         const float4 *g4 = reinterpret_cast<const float4 *>(src);
                         float4 *o4 = reinterpret_cast<float4 *>(dst);
                         float4 v[kPer];
@@ -255,7 +318,7 @@ __global__ void __launch_bounds__(kCwThreads, kCwCtasPerSm)
                                                          __fmul_rn(v[q].z, sc.f), __fmul_rn(v[q].w, sc.f));
                             const W code = pack4<B>(cc, y);
                             st_hint(out + threadIdx.x + q * NT, code, strm);
-                            st_hint4(o4 + threadIdx.x + q * NT, us.apply4(unpack4<B>(cc, code)), strm);
+                            st_hint4(o4 + threadIdx.x + q * NT, us.apply4_fast(unpack4<B>(cc, code)), strm);
                         }
                     } else {
                         const int ng = n_tiles * (kTile / 4);
@@ -265,7 +328,14 @@ __global__ void __launch_bounds__(kCwThreads, kCwCtasPerSm)
                             store_group(dst, 4 * (int64_t)q, cnt, us.apply4(unpack4<B>(cc, code)));
                         }
                     }
+                } else if constexpr (B > 0) {
+                    if (!sc.wide && us.fast) cw_quant_reg<B, true>(cc, src, dst, pk, cnt, n_tiles, full, sc, us, strm, warp, lane);
+                    else cw_quant_reg<B, false>(cc, src, dst, pk, cnt, n_tiles, full, sc, us, strm, warp, lane);
+                } else if (cc.b() <= kRegMaxB) {
+                    if (!sc.wide && us.fast) cw_quant_reg<0, true>(cc, src, dst, pk, cnt, n_tiles, full, sc, us, strm, warp, lane);
+                    else cw_quant_reg<0, false>(cc, src, dst, pk, cnt, n_tiles, full, sc, us, strm, warp, lane);
                 } else {
+                    // runtime widths 17..31: per-warp tile through shared memory
                     const int b = cc.b();
                     uint32_t *codes = s_codes[warp];
                     uint32_t *outw = reinterpret_cast<uint32_t *>(pk);
@@ -296,40 +366,58 @@ __global__ void __launch_bounds__(kCwThreads, kCwCtasPerSm)
 }
 
 template <class C, class C2>
-static int cw_grid(int n_items)
+static int cw_grid(int n_items, int cap)
 {
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_cw_kernel<C, C2>, kCwThreads, 0);
     per_sm = std::max(1, std::min(per_sm, kCwCtasPerSm));
+    if (cap > 0) per_sm = std::min(per_sm, cap);  // aps_set_occupancy
     return std::max(1, std::min(n_items, sm_count() * per_sm));
 }
 
 template <class C, class C2>
 static cudaError_t launch_cw(const DevTables &t, C c, C2 c2, int bias, int bias2, int fmt2, int average,
-                             int max_layer_items, cudaStream_t s)
+                             int max_layer_items, cudaStream_t s, int cap)
 {
     if (t.n_items == 0) return cudaSuccess;
-    const int grid = cw_grid<C, C2>(t.n_items);
+    const int grid = cw_grid<C, C2>(t.n_items, cap);
     int lag = std::min(t.n_items, max_layer_items + kWaveLagGrids * grid);
-    void *args[] = {const_cast<DevTables *>(&t), &c, &c2, &lag, &bias, &bias2, &fmt2, &average};
-    // every CTA resident (a control warp may wait on A items another CTA claimed)
-    return cudaLaunchCooperativeKernel((const void *)fused_cw_kernel<C, C2>, dim3(grid), dim3(kCwThreads), args, 0, s);
+    // A plain launch: progress needs no co-residency.  A control warp waits only for A
+    // items at earlier claim positions, and a position is claimed only by a CTA that is
+    // running and publishes it at once into its own slot ring, whose data warps never
+    // wait; a waiting control warp keeps folding its finished slots.  CTAs not yet
+    // resident hold no claims.  (A cooperative launch would also keep the kernel from
+    // sharing SMs with concurrent work -- the DDP hook's backward kernels.)
+    fused_cw_kernel<C, C2><<<grid, kCwThreads, 0, s>>>(t, c, c2, lag, bias, bias2, fmt2, average);
+    return cudaGetLastError();
 }
 
-cudaError_t launch_fused_cw(const DevTables &t, int e, int m, bool hw, int average, int max_layer_items, cudaStream_t s)
+cudaError_t launch_fused_cw(const DevTables &t, int e, int m, bool hw, int average, int max_layer_items, cudaStream_t s,
+                            int ctas_per_sm)
 {
     const int bias = (1 << (e - 1)) - 1;
     return with_codec(e, m, hw, [&](auto c) -> cudaError_t {
-        return launch_cw(t, c, CNone{}, bias, 0, -1, average, max_layer_items, s);
+        return launch_cw(t, c, CNone{}, bias, 0, -1, average, max_layer_items, s, ctas_per_sm);
     });
 }
 
+// a1 alone (aps_layer_scales, the N > 1 path): the same control-warp schedule over the
+// A items only -- dynamic claims (no tail of idle SMs), descriptor and pointer loads off
+// the data warps, 3 items per CTA in flight -- and each layer's last A item writes E_l.
+cudaError_t launch_absmax_cw(const DevTables &t, int world, cudaStream_t s)
+{
+    if (t.n_items == 0) return cudaSuccess;
+    const int grid = cw_grid<CF32, CAOnly>(t.n_items, 0);
+    fused_cw_kernel<CF32, CAOnly><<<grid, kCwThreads, 0, s>>>(t, CF32{}, CAOnly{}, 0, 0, 0, -1, world);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_fused_cw_hybrid32(const DevTables &t, int e, int m, bool hw, int fmt2, int average,
-                                     int max_layer_items, cudaStream_t s)
+                                     int max_layer_items, cudaStream_t s, int ctas_per_sm)
 {
     const int bias = (1 << (e - 1)) - 1;
     return with_codec(e, m, hw, [&](auto c) -> cudaError_t {
-        return launch_cw(t, c, CF32{}, bias, 127, fmt2, average, max_layer_items, s);
+        return launch_cw(t, c, CF32{}, bias, 127, fmt2, average, max_layer_items, s, ctas_per_sm);
     });
 }
 

@@ -41,6 +41,16 @@ struct ItemPtr {
     float *dst;
 };
 
+// a1: one CTA's share of the layers' vector space, cut at layer boundaries: vectors
+// [v0, v1) of a1's vector space, all in `layer`, starting at element e0 of it.
+struct AbsSeg {
+    int64_t v0, v1;
+    int64_t e0;       // element index (within the layer) of vector v0
+    int64_t numel;    // the layer's element count (its last vector may be partial)
+    int32_t layer;
+    int32_t pad;
+};
+
 struct DevTables {
     const Item *items;
     const LayerDev *layers;
@@ -53,26 +63,32 @@ struct DevTables {
     uint32_t *flag;           // non-finite flag
     uint32_t *amax2;          // [2][n_layers] abs-max accumulators of the fused kernel (call parity)
     ItemPtr *iptr;            // [n_items] per-item addresses (fused LDG kernel)
-    uint64_t *timeline;       // [kTimelineSlots] per-CTA phase stamps (flag 16)
-    uint32_t *claim;          // [3 per format group] monotone work-claim counters (slot 2: the wavefront kernel)
-    unsigned long long *claim64;  // wavefront claim counter (64-bit: the call index is derived on the device)
+    unsigned long long *claim64;  // claim counter of the control-warp kernel (per format group; self-resetting)
     uint32_t *ranges_done;    // self-resetting CTA-done counter of absmax_stream_kernel
     const int64_t *voff;      // [n_layers + 1] first vector (4 fp32) of each layer in a1's vector space
-    const int32_t *cta_layer; // [absmax_grid()] layer holding the first vector of each a1 CTA's share
+    const int32_t *abs_seg_off;  // [absmax_grid() + 1] a1: first segment of each CTA's share
+    const struct AbsSeg *abs_segs; // a1: the shares cut at layer boundaries (whole vectors; host-built, static)
+    const struct AbsSeg *abs_tails; // a1: each layer's partial last vector (elements [e0, numel))
     uint32_t *layer_done;     // [n_layers] per-layer abs-max completion counters (fused kernel)
     uint32_t *bdone;          // [n_layers] per-layer quantise completion counters (fused kernel, self-resetting)
     uint32_t *sr_call;        // stochastic rounding: syncs since aps_set_rounding (per-call key, reading A27)
     uint8_t *packed;          // packed codes
     int n_items;
     int n_layers;
+    int n_abs_tails;
 };
 
-// a1: balanced abs-max stream over every layer (absmax_grid() CTAs; DevTables.voff /
-// cta_layer describe the split), self-resetting done counter
+// a1: balanced abs-max stream over every layer (absmax_grid() CTAs; DevTables.abs_seg_off /
+// abs_segs describe the split), self-resetting done counter
 constexpr int kAbsCtasPerSm = 4;
-constexpr int kAbsMaxCtas = 1024;  // cta_layer table size (workspace)
+constexpr int kAbsMaxCtas = 1024;  // segment-table bound (workspace)
 int absmax_grid();
 cudaError_t launch_absmax(const DevTables &t, int world, cudaStream_t s);
+// a1 through the control-warp kernel (dynamic claims): DevTables.iptr must be current
+cudaError_t launch_absmax_cw(const DevTables &t, int world, cudaStream_t s);
+#ifndef APS_ABSMAX_CW
+#define APS_ABSMAX_CW 1  // 0: absmax_stream_kernel (static balanced shares) -- compile-time A/B
+#endif
 cudaError_t launch_quant_pack(const DevTables &t, int e, int m, bool hw, cudaStream_t s);
 cudaError_t launch_unpack_unscale(const DevTables &t, int e, int m, bool hw, int world, int average,
                                   cudaStream_t s);
@@ -87,47 +103,14 @@ cudaError_t launch_debug_decode(const uint32_t *codes, float *out, int64_t n, in
 
 int sm_count();
 
-constexpr int kFusedWarps = kThreads / 32;
-#ifndef APS_FUSED_FLAGS
-#define APS_FUSED_FLAGS 64  // 64: code / output stores with an L2 evict_first hint; +16: per-CTA timeline stamps
-#endif
-constexpr int kFusedDefaultFlags = APS_FUSED_FLAGS;  // fused kernel flags (compile time)
-constexpr int kTimelineSlots = 4 * 2048;     // globaltimer stamps (4 per CTA) of the last fused launch
 cudaError_t launch_build_item_ptrs(const DevTables &t, cudaStream_t s);
-// wavefront variant (no grid barrier): claim_base advances by 2 * n_items + grid per call;
-// call_no = wavefront calls before this one on these counters; lag = D positions.
-#ifndef APS_WAVE_CTAS_PER_SM
-#define APS_WAVE_CTAS_PER_SM 4
-#endif
-constexpr int kWaveCtasPerSm = APS_WAVE_CTAS_PER_SM;  // wavefront kernel occupancy (register budget)
-int fused_p1_wave_grid(int e, int m, bool hw, int n_items);
-
 #ifndef APS_WAVE_LAG_GRIDS
 #define APS_WAVE_LAG_GRIDS 2
 #endif
 // lag D of the wavefront = (items of the largest layer) + kWaveLagGrids x grid positions
 constexpr int kWaveLagGrids = APS_WAVE_LAG_GRIDS;
-constexpr int kWaveOvershoot = 2;  // claims past the end per CTA and call (wavefront kernel claims 2 ahead)
-// claim_base advances by 2 * n_items + kWaveOvershoot * grid per call.
-// Per-call state of a wavefront launch.  graph = false: claim base (32-bit claim
-// counter), call index and accumulator parity come from the host.  graph = true
-// (capture-safe): all three are derived on the device from the 64-bit claim counter,
-// which advances by exactly 2 * n_items + kWaveOvershoot * grid per call.
-struct WaveCall {
-    bool graph;
-    uint32_t gen, claim_base, call_no;
-};
-cudaError_t launch_fused_p1_wave(const DevTables &t, int e, int m, bool hw, int average, const WaveCall &w, int lag,
-                                 int grid, cudaStream_t s, bool cooperative = true);
-// One wavefront launch over two format groups: items whose fmt == fmt2 use the
-// binary32 codec (the hybrid FP32 classifier layer), the others (e, m, hw).
-cudaError_t launch_fused_p1_wave_hybrid32(const DevTables &t, int e, int m, bool hw, int fmt2, int average,
-                                          const WaveCall &w, int lag, int grid, cudaStream_t s);
-// fused N = 1 sync, warp-specialised wavefront (aps_fused.cu): one cooperative launch per
-// format group (hybrid FP32 classifier: one launch), self-resetting counters, no per-call host state
-#ifndef APS_FUSED_CW
-#define APS_FUSED_CW 1
-#endif
+// fused N = 1 sync, warp-specialised wavefront (aps_fused.cu): one launch per format group
+// (hybrid FP32 classifier: one launch), self-resetting counters, no per-call host state
 #ifndef APS_CW_SLOTS
 #define APS_CW_SLOTS 3
 #endif
@@ -135,9 +118,10 @@ cudaError_t launch_fused_p1_wave_hybrid32(const DevTables &t, int e, int m, bool
 #define APS_CW_CTAS_PER_SM 3
 #endif
 constexpr int kCwCtasPerSm = APS_CW_CTAS_PER_SM;
-cudaError_t launch_fused_cw(const DevTables &t, int e, int m, bool hw, int average, int max_layer_items, cudaStream_t s);
+cudaError_t launch_fused_cw(const DevTables &t, int e, int m, bool hw, int average, int max_layer_items, cudaStream_t s,
+                            int ctas_per_sm = 0);
 cudaError_t launch_fused_cw_hybrid32(const DevTables &t, int e, int m, bool hw, int fmt2, int average,
-                                     int max_layer_items, cudaStream_t s);
+                                     int max_layer_items, cudaStream_t s, int ctas_per_sm = 0);
 // true when (e,m) has a hardware converter that is exact on the APS path
 // formats with a hardware / exact fast codec: fp8 e5m2, e4m3 (APS regime only,
 // reading A12), binary16, bfloat16, binary32 (every non-NaN input)

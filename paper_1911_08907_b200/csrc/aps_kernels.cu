@@ -26,113 +26,116 @@ namespace aps {
 // (vector = 4 consecutive fp32 of one layer; layer l owns vectors [voff[l], voff[l+1]),
 // its last vector partial when numel % 4 != 0) and CTA b streams the equal share
 // [b V / G, (b+1) V / G): every SM moves the same number of bytes, so the launch has no
-// tail of idle SMs (the round-1 kernel, one CTA per 4 work items, left SMs idle 23 % of
-// its time: profiles/r02a_absmax_raw.csv).  A share is walked in chunks of 8 x NT
-// vectors (8 independent 128-bit loads in flight per thread):
-//   * chunk inside one layer (the common case): a running per-thread max of that layer,
-//     folded into amax[layer] (warp max, one red.max per warp) when the layer changes;
-//   * chunk crossing layer boundaries or holding a partial vector: each vector finds its
-//     layer (binary search over voff) and is folded with a shared-memory atomicMax into
-//     a per-chunk table, flushed with red.max.
-// The max of u32 abs bits is order-independent, so the result is bit-exact whatever the
-// split.  Completion: one fence by thread 0 after the CTA barrier, one count; the last
-// CTA turns the maxima into E_l = ceil(log2(N A_l)) and clears them (self-resetting:
-// capture-safe).  Gradients are loaded with an L2 evict_last hint so that quant_pack's
-// re-read (reverse order) hits L2.
-constexpr int kAbsChunk = 8 * kThreads;  // vectors per chunk (32 KB)
+// tail of idle SMs.  The host cuts every share at layer boundaries into segments
+// (DevTables.abs_segs, static per context), so the kernel never searches for a layer:
+// a CTA stages up to kAbsSegBatch segment descriptors (with the layer's gradient
+// pointer) in shared memory and walks their vectors in chunks of 8 x NT, each thread
+// first issuing its 8 independent 128-bit loads (its segment found by a forward scan
+// over the staged descriptors: vector indices only grow), then folding each load: a warp
+// whose 32 vectors lie in one segment reduces with a shuffle and does one shared-memory
+// atomicMax, a warp straddling a boundary folds per lane.  Each staged
+// segment's max goes to amax[layer] with one red.max.  (The previous kernel looked the
+// layer up with dependent global binary searches and loaded boundary chunks one vector at
+// a time: 43 us for ResNet-50, latency-bound.)  The max of u32 abs bits is
+// order-independent, so the result is bit-exact whatever the split.  Completion: one fence
+// by thread 0 after the CTA barrier, one count; the last CTA turns the maxima into
+// E_l = ceil(log2(N A_l)) and clears them (self-resetting: capture-safe).  Gradients are
+// loaded with an L2 evict_last hint so that quant_pack's re-read (reverse order) hits L2.
+constexpr int kAbsSegBatch = 64;
 
 template <int NT>
 __global__ void __launch_bounds__(NT, kAbsCtasPerSm) absmax_stream_kernel(DevTables t, int N)
 {
     constexpr int kChunk = 8 * NT;
-    __shared__ uint32_t s_tab[kChunk];  // slow path: max per layer of the chunk (index layer - l0)
+    __shared__ int64_t s_v1[kAbsSegBatch], s_v0[kAbsSegBatch], s_e0[kAbsSegBatch];
+    __shared__ const float *s_src[kAbsSegBatch];
+    __shared__ uint32_t s_max[kAbsSegBatch];
+    __shared__ int s_layer[kAbsSegBatch];
     __shared__ int s_last;
     const int lane = threadIdx.x & 31;
     uint64_t keep;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
-    const int64_t V = t.voff[t.n_layers];
-    const int64_t lo = V * (int64_t)blockIdx.x / gridDim.x, hi = V * (int64_t)(blockIdx.x + 1) / gridDim.x;
-    int l = t.cta_layer[blockIdx.x];  // layer holding vector lo
-    for (int k = threadIdx.x; k < kChunk; k += NT) s_tab[k] = 0u;
-    __syncthreads();
-    uint32_t run = 0;                 // this thread's running max of layer `l` (fast path)
-    for (int64_t c0 = lo; c0 < hi; c0 += kChunk) {
-        const int64_t c1 = min(hi, c0 + kChunk);
-        while (t.voff[l + 1] <= c0) {   // advance to the layer holding c0 (flush the old one)
-            const uint32_t m = __reduce_max_sync(0xffffffffu, run);
-            if (lane == 0 && m)
-                asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(&t.amax[l]), "r"(m) : "memory");
-            run = 0;
-            ++l;
+    // the layers' partial last vectors (numel % 4 != 0): one thread each, straight to amax
+    for (int k2 = blockIdx.x * NT + threadIdx.x; k2 < t.n_abs_tails; k2 += gridDim.x * NT) {
+        const AbsSeg tl = t.abs_tails[k2];
+        const float *g = t.src[tl.layer];
+        uint32_t mx = 0;
+        for (int64_t e = tl.e0; e < tl.numel; ++e) mx = max(mx, __float_as_uint(g[e]) & 0x7fffffffu);
+        if (mx) asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(&t.amax[tl.layer]), "r"(mx) : "memory");
+    }
+    const int sb = t.abs_seg_off[blockIdx.x], se = t.abs_seg_off[blockIdx.x + 1];
+    for (int b0 = sb; b0 < se; b0 += kAbsSegBatch) {
+        const int nb = min(kAbsSegBatch, se - b0);
+        if ((int)threadIdx.x < nb) {
+            const AbsSeg sg = t.abs_segs[b0 + threadIdx.x];
+            s_v0[threadIdx.x] = sg.v0;
+            s_v1[threadIdx.x] = sg.v1;
+            s_e0[threadIdx.x] = sg.e0;
+            s_layer[threadIdx.x] = sg.layer;
+            s_src[threadIdx.x] = t.src[sg.layer];
+            s_max[threadIdx.x] = 0u;
         }
-        const int64_t base = t.voff[l];
-        const int64_t full_end = base + (t.layers[l].numel >> 2);  // first partial vector (or voff[l+1])
-        if (c1 <= full_end) {
-            // ---- fast path: the chunk lies in layer l's full vectors
-            const float4 *g4 = reinterpret_cast<const float4 *>(t.src[l]);
-            const int64_t i0 = c0 - base, i1 = c1 - base;  // vector indices within the layer
+        __syncthreads();
+        const int64_t lo = s_v0[0], hi = s_v1[nb - 1];
+        int kc = 0;           // segment of the chunk's first vector (CTA-uniform)
+        int krun = 0;         // segment of this thread's running max
+        uint32_t run = 0;
+        auto flush = [&]() {  // the warp's running max -> the segment's shared-memory max
+            const uint32_t m = __reduce_max_sync(0xffffffffu, run);
+            if (lane == 0 && m) atomicMax(&s_max[krun], m);
+            run = 0;
+        };
+        for (int64_t c0 = lo; c0 < hi; c0 += kChunk) {
+            while (s_v1[kc] <= c0) ++kc;
             float4 v[8];
+            if (c0 + kChunk <= s_v1[kc]) {
+                // ---- the whole chunk lies in segment kc (CTA-uniform branch): 8
+                // unconditional 128-bit loads, a running max, no per-vector bookkeeping
+                const float4 *p = reinterpret_cast<const float4 *>(s_src[kc] + s_e0[kc]) + (c0 - s_v0[kc]) + threadIdx.x;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) v[q] = ld_keep4(p + q * NT, keep);
+                if (kc != krun) {
+                    flush();
+                    krun = kc;
+                }
+#pragma unroll
+                for (int q = 0; q < 8; ++q) run = max(run, absbits4(v[q]));
+                continue;
+            }
+            // ---- a chunk meeting a segment boundary or the batch end: per-vector segments
+            // (segments hold whole vectors only -- the layers' partial last vectors are the
+            // tail list above); all 8 loads issued before the first use
+            flush();
+            int kq[8];
+            int k = kc;
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-                const int64_t i = i0 + threadIdx.x + q * NT;
-                v[q] = i < i1 ? ld_keep4(g4 + i, keep) : make_float4(0.f, 0.f, 0.f, 0.f);
+                const int64_t i = c0 + threadIdx.x + q * NT;
+                const bool in = i < hi;
+                while (in && s_v1[k] <= i) ++k;
+                const float4 *pp = reinterpret_cast<const float4 *>(s_src[k] + s_e0[k]) + (i - s_v0[k]);
+                v[q] = in ? ld_keep4(pp, keep) : make_float4(0.f, 0.f, 0.f, 0.f);
+                kq[q] = k;
             }
 #pragma unroll
-            for (int q = 0; q < 8; ++q) run = max(run, absbits4(v[q]));
-            continue;
-        }
-        // ---- slow path: layers l .. lh meet the chunk (lh < l + kChunk)
-        {
-            const uint32_t m = __reduce_max_sync(0xffffffffu, run);
-            if (lane == 0 && m)
-                asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(&t.amax[l]), "r"(m) : "memory");
-            run = 0;
-        }
-        int lh = l;
-        {   // last layer meeting the chunk: largest layer with voff <= c1 - 1
-            int a = l, b = min(t.n_layers - 1, l + kChunk - 1);
-            while (a < b) {
-                const int mid = (a + b + 1) >> 1;
-                if (t.voff[mid] <= c1 - 1) a = mid; else b = mid - 1;
+            for (int q = 0; q < 8; ++q) {
+                uint32_t mx = absbits4(v[q]);
+                const int k0 = __shfl_sync(0xffffffffu, kq[q], 0);
+                if (__all_sync(0xffffffffu, kq[q] == k0)) {
+                    mx = __reduce_max_sync(0xffffffffu, mx);
+                    if (lane == 0 && mx) atomicMax(&s_max[k0], mx);
+                } else if (mx) {
+                    atomicMax(&s_max[kq[q]], mx);
+                }
             }
-            lh = a;
         }
-#pragma unroll 1
-        for (int q = 0; q < 8; ++q) {
-            const int64_t i = c0 + threadIdx.x + q * NT;
-            if (i >= c1) break;
-            int a = l, b = lh;   // layer of vector i
-            while (a < b) {
-                const int mid = (a + b + 1) >> 1;
-                if (t.voff[mid] <= i) a = mid; else b = mid - 1;
-            }
-            const int64_t e0 = 4 * (i - t.voff[a]);         // first element of the vector in layer a
-            const int64_t n = t.layers[a].numel;
-            const float *g = t.src[a];
-            uint32_t mx;
-            if (e0 + 4 <= n) {
-                mx = absbits4(ld_keep4(reinterpret_cast<const float4 *>(g + e0), keep));
-            } else {
-                mx = 0;
-                for (int64_t e = e0; e < n; ++e) mx = max(mx, __float_as_uint(g[e]) & 0x7fffffffu);
-            }
-            if (mx) atomicMax(&s_tab[a - l], mx);
-        }
+        flush();
         __syncthreads();
-        for (int k = threadIdx.x; k <= lh - l; k += NT) {
-            const uint32_t m = s_tab[k];
-            if (m) {
-                asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(&t.amax[l + k]), "r"(m) : "memory");
-                s_tab[k] = 0u;
-            }
-        }
+        if ((int)threadIdx.x < nb && s_max[threadIdx.x])
+            asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(&t.amax[s_layer[threadIdx.x]]),
+                         "r"(s_max[threadIdx.x])
+                         : "memory");
         __syncthreads();
-        l = lh;  // (the next chunk starts at or after layer lh)
-    }
-    {
-        const uint32_t m = __reduce_max_sync(0xffffffffu, run);
-        if (lane == 0 && m && l < t.n_layers)
-            asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(&t.amax[l]), "r"(m) : "memory");
     }
     // completion: the CTA barrier orders every warp's red.max before thread 0's fence
     // (cumulativity), whose count the last CTA acquires
@@ -203,8 +206,36 @@ __global__ void __launch_bounds__(NT) quant_pack_tile_kernel(DevTables t, C c, i
     const int64_t begin = (int64_t)it.tile_begin * kTile;
     const int64_t n = min((int64_t)it.n_tiles * kTile, L.numel - begin);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t *codes = s_codes[warp];
     uint32_t *out = reinterpret_cast<uint32_t *>(t.packed + it.byte_pos);
+    if (b <= kRegMaxB) {
+        // b <= 16: the warp's tiles (warp, warp + 8, ...) loaded first, packed in registers
+        constexpr int BB = (C::kB > 0 && C::kB <= kRegMaxB) ? C::kB : 0;
+        constexpr int kJ = kItemTiles / (NT / 32);
+        float4 v[kJ];
+        if (n == kItemTiles * kTile) {  // unconditional 128-bit loads, all in flight before the first use
+            const float4 *g4 = reinterpret_cast<const float4 *>(g + begin) + lane;
+#pragma unroll
+            for (int j = 0; j < kJ; ++j) v[j] = ld_stream4(g4 + (warp + j * (NT / 32)) * (kTile / 4));
+        } else {
+#pragma unroll
+            for (int j = 0; j < kJ; ++j) v[j] = load_group(g + begin, (int64_t)(warp + j * (NT / 32)) * kTile + lane * 4, n);
+        }
+        auto pass = [&](auto narrow) {  // (branch on s.wide around the loop: see Pow2)
+#pragma unroll
+            for (int j = 0; j < kJ; ++j) {
+                const int tt = warp + j * (NT / 32);
+                if (tt >= it.n_tiles) break;  // warp-uniform
+                const float4 y = decltype(narrow)::value ? s.apply4_narrow(v[j]) : s.apply4(v[j]);
+                const uint4 cd = make_uint4(c.enc(y.x), c.enc(y.y), c.enc(y.z), c.enc(y.w));
+                uint32_t *tw = out + (int64_t)tt * (4 * b);
+                tile_store(tile_pack<BB>(cd, b, lane), [&](int i, uint32_t x) { tw[i] = x; });
+            }
+        };
+        if (!s.wide) pass(std::true_type{});
+        else pass(std::false_type{});
+        return;
+    }
+    uint32_t *codes = s_codes[warp];
     for (int tt = warp; tt < it.n_tiles; tt += NT / 32) {
         const int64_t e0 = (int64_t)tt * kTile + lane * 4;
         const float4 y = s.apply4(load_group(g + begin, e0, n));
@@ -257,8 +288,13 @@ __global__ void __launch_bounds__(NT) unpack_unscale_direct_kernel(DevTables t, 
 #pragma unroll
         for (int j = 0; j < kPer; ++j) w[j] = in[threadIdx.x + j * NT];
         float4 *o4 = reinterpret_cast<float4 *>(ob);
+        if (us.fast) {  // (branch around the loop: see Pow2::apply4_narrow)
 #pragma unroll
-        for (int j = 0; j < kPer; ++j) st_out4(o4 + threadIdx.x + j * NT, us.apply4(unpack4<B>(c, w[j])), pol);
+            for (int j = 0; j < kPer; ++j) st_out4(o4 + threadIdx.x + j * NT, us.apply4_fast(unpack4<B>(c, w[j])), pol);
+        } else {
+#pragma unroll
+            for (int j = 0; j < kPer; ++j) st_out4(o4 + threadIdx.x + j * NT, us.apply4(unpack4<B>(c, w[j])), pol);
+        }
     } else {
         const int64_t ng = (n + 3) / 4;
         for (int64_t gi = threadIdx.x; gi < ng; gi += NT)
@@ -278,8 +314,35 @@ __global__ void __launch_bounds__(NT) unpack_unscale_tile_kernel(DevTables t, C 
     const int64_t begin = (int64_t)it.tile_begin * kTile;
     const int64_t n = min((int64_t)it.n_tiles * kTile, L.numel - begin);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t *words = s_words[warp];
     const uint32_t *in = reinterpret_cast<const uint32_t *>(t.packed + it.byte_pos);
+    if (b <= kRegMaxB) {
+        // b <= 16: the warp's tiles' words loaded first, split into codes in registers
+        constexpr int BB = (C::kB > 0 && C::kB <= kRegMaxB) ? C::kB : 0;
+        constexpr int kJ = kItemTiles / (NT / 32);
+        TileRaw wr[kJ];
+#pragma unroll
+        for (int j = 0; j < kJ; ++j) {
+            const int tt = warp + j * (NT / 32);
+            wr[j] = tt < it.n_tiles ? tile_fetch<BB>(in + (int64_t)tt * (4 * b), b, lane, LdPlain{}) : TileRaw{0u, 0u, 0u};
+        }
+        auto pass = [&](auto fast) {
+#pragma unroll
+            for (int j = 0; j < kJ; ++j) {
+                const int tt = warp + j * (NT / 32);
+                if (tt >= it.n_tiles) break;  // warp-uniform
+                const uint4 cd = tile_split<BB>(wr[j], b, lane);
+                const float4 d = make_float4(c.dec(cd.x), c.dec(cd.y), c.dec(cd.z), c.dec(cd.w));
+                const float4 v = decltype(fast)::value ? us.apply4_fast(d) : us.apply4(d);
+                const int64_t e0 = (int64_t)tt * kTile + lane * 4;
+                if (e0 + 4 <= n) st_out4(reinterpret_cast<float4 *>(o + begin + e0), v, 0);
+                else store_group(o + begin, e0, n, v);
+            }
+        };
+        if (us.fast) pass(std::true_type{});
+        else pass(std::false_type{});
+        return;
+    }
+    uint32_t *words = s_words[warp];
     for (int tt = warp; tt < it.n_tiles; tt += NT / 32) {
         const uint32_t *iw = in + (int64_t)tt * (4 * b);
         for (int w = lane; w < 4 * b; w += 32) words[w] = iw[w];
@@ -333,6 +396,18 @@ __global__ void __launch_bounds__(NT) ring_reduce_tile_kernel(uint8_t *own, cons
     uint32_t *o = reinterpret_cast<uint32_t *>(own);
     const uint32_t *r = reinterpret_cast<const uint32_t *>(recv);
     const int64_t warps = (int64_t)gridDim.x * (NT / 32);
+    if (b <= kRegMaxB) {
+        constexpr int BB = (C::kB > 0 && C::kB <= kRegMaxB) ? C::kB : 0;
+        for (int64_t tt = blockIdx.x * (int64_t)(NT / 32) + warp; tt < n_tiles; tt += warps) {
+            uint32_t *ow = o + tt * (4 * b);
+            const uint4 ca = tile_split<BB>(tile_fetch<BB>(r + tt * (4 * b), b, lane, LdPlain{}), b, lane);
+            const uint4 cb = tile_split<BB>(tile_fetch<BB>(ow, b, lane, LdPlain{}), b, lane);
+            const uint4 res = make_uint4(c.enc(__fadd_rn(c.dec(ca.x), c.dec(cb.x))), c.enc(__fadd_rn(c.dec(ca.y), c.dec(cb.y))),
+                                         c.enc(__fadd_rn(c.dec(ca.z), c.dec(cb.z))), c.enc(__fadd_rn(c.dec(ca.w), c.dec(cb.w))));
+            tile_store(tile_pack<BB>(res, b, lane), [&](int i, uint32_t x) { ow[i] = x; });
+        }
+        return;
+    }
     for (int64_t tt = blockIdx.x * (int64_t)(NT / 32) + warp; tt < n_tiles; tt += warps) {
         uint32_t *ow = o + tt * (4 * b);
         const uint32_t *rw = r + tt * (4 * b);
@@ -357,18 +432,10 @@ __global__ void __launch_bounds__(NT) ring_reduce_tile_kernel(uint8_t *own, cons
     }
 }
 
-// ------------------------------------------------------------------ fused p = 1 (LDG engine)
-// One rank: no collective separates FindMaxExp from Cast, so ONE persistent
-// cooperative launch (kFusedCtasPerSm CTAs per SM) does
-//   phase A  abs-max of every work item (forward order, L2 evict_last hint):
-//            each warp folds its max into the layer with red.max;
-//   barrier  each CTA fences once and bumps the done counter; all CTAs wait
-//            for the call's target (acquire);
-//   phase B  per item in REVERSE order (the most recently read data is still
-//            in the 126 MB L2): E_l from the accumulator, f~, scale, Cast,
-//            pack (codes -> packed buffer), Cast back, unscale -> output.
-// Accumulators are double-buffered by call parity: buffer g&1 is used,
-// buffer (g+1)&1 is cleared by the layer's first item for the next call.
+// ------------------------------------------------------------------ per-item addresses
+// The fused / A-only control warps read each item's gradient and output address from
+// one table (rebuilt when the caller's layer pointers change) instead of chaining
+// item -> layer -> pointer loads.
 __global__ void build_item_ptrs_kernel(DevTables t)
 {
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < t.n_items; k += gridDim.x * blockDim.x) {
@@ -378,12 +445,6 @@ __global__ void build_item_ptrs_kernel(DevTables t)
     }
 }
 
-#ifndef APS_DIAG_NOWAIT
-#define APS_DIAG_NOWAIT 0
-#endif
-#ifndef APS_DIAG_NOA
-#define APS_DIAG_NOA 0
-#endif
 // ------------------------------------------------------------------ sim: MAX exchange of E
 struct PtrArr {
     const int32_t *src[64];
@@ -497,327 +558,6 @@ cudaError_t launch_ring_reduce(uint8_t *own, const uint8_t *recv, int64_t n_tile
         }
         return cudaGetLastError();
     });
-}
-
-// ------------------------------------------------------------------ fused p = 1, wavefront schedule
-// No grid barrier: ONE claim counter walks a merged sequence of 2n items in
-// which quantise item B(i) trails abs-max item A(i) by `lag` positions:
-//   A(0..D-1), then A(D) B(0) A(D+1) B(1) ..., then B(n-D..n-1).
-// Every warp of an A item counts itself into the layer's completion counter
-// with a fire-and-forget red.release (after its red.max); B(i) waits
-// (acquire) until its layer's counter reaches 8 x layer_items for this call.
-// With D >= (items of the largest layer) + grid, every A item of B(i)'s layer
-// sits earlier in the sequence and is normally finished when B(i) is
-// claimed, and B(i) re-reads data read only ~D items (~D x 32 KB) ago: it is
-// still in L2.  Progress: a waiting B depends only on A items at earlier
-// positions, and each CTA holds at most its current and next claim, so the
-// earliest waiting B always completes (induction on position).
-// No second codec (uniform formats, or one launch per format group).
-
-// GRAPH = false: per-call state (claim base, call index, accumulator parity) comes from
-// the host as launch arguments (the fastest form).  GRAPH = true (capture-safe): the
-// call index is derived on the device from a 64-bit claim counter that advances by
-// exactly adv = 2 n + kWaveOvershoot * grid per call, so a captured CUDA graph replays
-// exactly; measured ~1 us slower per call (profiles/r01_ab_wave_graph_safe.txt).
-template <class C, class C2, bool GRAPH, int NT>
-__global__ void __launch_bounds__(NT, kWaveCtasPerSm)
-    fused_p1_wave_kernel(DevTables t, C c, C2 c2, uint32_t *amax_h, uint32_t *amax_next_h, uint32_t claim_base,
-                         uint32_t call_no_h, unsigned long long adv, int lag, int bias, int bias2, int fmt2, int avg,
-                         int flags)
-{
-    // (graph mode keeps its call state in shared memory, not registers: the kernel sits at
-    // its 64-register budget)
-    __shared__ uint32_t s_call;
-    __shared__ unsigned long long s_base64;  // claim counter value at this call's start
-    if (GRAPH && threadIdx.x == 0) s_base64 = ~0ull;
-    auto amax_of = [&](uint32_t next) -> uint32_t * {
-        if constexpr (GRAPH) return t.amax2 + (size_t)((s_call + next) & 1u) * t.n_layers;
-        else return next ? amax_next_h : amax_h;
-    };
-    auto call_no = [&]() -> uint32_t {
-        if constexpr (GRAPH) return s_call;
-        else return call_no_h;
-    };
-    constexpr bool kTwo = C2::kB > 0;  // items with fmt == fmt2 use c2 (bias2)
-    __shared__ __align__(16) uint32_t s_codes[NT / 32][kTile];
-    __shared__ int s_claim[3], s_ft[3], s_ok[3];  // claims run two items ahead (3 slots)
-    __shared__ Item s_item[3];                    // ... with their descriptors and addresses, loaded by
-    __shared__ ItemPtr s_iptr[3];                 //     thread 0 at claim time (no dependent load at item start)
-    __shared__ uint32_t s_part[2][NT / 32];       // per-warp maxima of the last two items
-    __shared__ int s_part_layer[2];               // their layer (-1: a quantise item)
-    // positions: A(0..D-1), A(D) B(0) A(D+1) B(1) ..., B(n-D..n-1)
-    const int n = t.n_items, D = lag, total = 2 * n;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const bool f_st_hint = flags & 64;
-    const bool f_timeline = (flags & 16) && blockIdx.x * 4 + 3 < kTimelineSlots;
-    auto stamp = [&](int k) {
-        if (f_timeline && threadIdx.x == 0) {
-            uint64_t ns;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
-            t.timeline[blockIdx.x * 4 + k] = ns;
-        }
-    };
-    stamp(0);
-    uint64_t tl_wait_ns = 0, tl_waits = 0, tl_items = 0;  // timeline (flag 16): B-item waits of thread 0
-    uint64_t keep, strm;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(strm));
-    constexpr int kPer = kItemTiles * kTile / 4 / NT;
-    constexpr int kFlushThread = 32;  // lane 0 of warp 1 folds finished abs-max items into the layer
-    auto decode = [&](int j, bool &isB) -> int {
-        if (j < D) { isB = false; return j; }
-        if (j < total - D) {
-            const int k = j - D;
-            isB = k & 1;
-            return isB ? (k >> 1) : D + (k >> 1);
-        }
-        isB = true;
-        return n - D + (j - (total - D));
-    };
-    auto ft_of = [&](const Item &it) -> int {
-        const int32_t E = exponent_of(ld_relaxed_u32(&amax_of(0)[it.layer]), 1);
-        const int bs = (kTwo && it.fmt == fmt2) ? bias2 : bias;  // the layer's upper_bound_exp
-        return (E == INT32_MIN || E == INT32_MAX) ? 0 : bs - E;  // f~ (Alg. 1 line 4)
-    };
-    auto layer_target = [&](const Item &it) -> uint32_t { return (call_no() + 1u) * (uint32_t)(8 * it.layer_items); };
-    // thread 0: claim a position into slot sl; resolve f~ now if it is a quantise item of a complete layer
-    auto claim_into = [&](int sl) {
-        int j;
-        if constexpr (GRAPH) {
-            const unsigned long long raw = atomicAdd(t.claim64, 1ull);  // the wavefront's own counter
-            if (s_base64 == ~0ull) {  // first claim of this CTA: the call index (one division per CTA)
-                const unsigned long long cn = raw / adv;
-                s_base64 = cn * adv;
-                s_call = (uint32_t)cn;
-            }
-            j = (int)(raw - s_base64);
-        } else {
-            j = (int)(atomicAdd(&t.claim[2], 1u) - claim_base);
-        }
-        s_claim[sl] = j;
-        s_ok[sl] = APS_DIAG_NOWAIT;  // (diagnostic build: never wait, results invalid)
-        if (APS_DIAG_NOWAIT) s_ft[sl] = 0;
-        if (j < total) {
-            bool isB;
-            const int k = decode(j, isB);
-            const Item it = t.items[k];
-            s_item[sl] = it;
-            s_iptr[sl] = t.iptr[k];
-            if (isB) {
-                if ((int)(ld_acquire_u32(&t.layer_done[it.layer]) - layer_target(it)) >= 0) {
-                    s_ft[sl] = ft_of(it);
-                    s_ok[sl] = 1;
-                }
-            }
-        }
-    };
-    // flush pipeline (kFlushThread): an item's max is folded in (returning atomic) one
-    // iteration after the item, and counted (add dependent on the atomic's result, so
-    // only after the max is performed at L2) one iteration after that
-    int pend_layer = -1;  // layer whose max was folded last iteration and is not yet counted
-    uint32_t pend_old = 0;
-    auto flush = [&](int pp) {
-        if (pend_layer >= 0) {
-            const uint32_t inc = (pend_old == 0xffffffffu) ? 0u : 8u;  // always 8: abs bits <= 0x7fffffff
-            asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(&t.layer_done[pend_layer]), "r"(inc)
-                         : "memory");
-            pend_layer = -1;
-        }
-        const int l = pp >= 0 ? s_part_layer[pp] : -1;
-        if (l >= 0) {
-            uint32_t m = 0;
-#pragma unroll
-            for (int w = 0; w < NT / 32; ++w) m = max(m, s_part[pp][w]);
-            asm volatile("atom.relaxed.gpu.global.max.u32 %0, [%1], %2;"
-                         : "=r"(pend_old) : "l"(&amax_of(0)[l]), "r"(m) : "memory");
-            pend_layer = l;
-        }
-    };
-    if (threadIdx.x == 0) {
-        claim_into(0);
-        claim_into(1);
-        s_part_layer[0] = s_part_layer[1] = -1;
-    }
-    __syncthreads();
-    int slot = 0, par = 0;
-    for (int j = s_claim[0]; j < total;) {
-        bool isB;
-        decode(j, isB);
-        const Item it = s_item[slot];
-        const ItemPtr p = s_iptr[slot];
-        const float4 *g4 = reinterpret_cast<const float4 *>(p.src);
-        const bool full = it.cnt == kItemTiles * kTile;
-        float4 v[kPer];
-        if (full) {
-#pragma unroll
-            for (int q = 0; q < kPer; ++q) v[q] = ld_hint4(g4 + threadIdx.x + q * NT, isB ? strm : keep);
-        }
-        if (threadIdx.x == 0) claim_into((slot + 2) % 3);
-        if (threadIdx.x == kFlushThread) flush(par ^ 1);
-        if (!isB && APS_DIAG_NOA) {
-            if (threadIdx.x == 0) s_part_layer[par] = -1;  // (diagnostic build: abs-max items skipped)
-        } else if (!isB) {
-            // ---------------- abs-max item
-            uint32_t mx = 0;
-            if (full) {
-#pragma unroll
-                for (int q = 0; q < kPer; ++q) mx = max(mx, absbits4(v[q]));
-            } else {
-                const int n4 = it.cnt >> 2;
-                for (int q = threadIdx.x; q < n4; q += NT) mx = max(mx, absbits4(ld_hint4(g4 + q, keep)));
-                if ((int)threadIdx.x < (it.cnt & 3)) mx = max(mx, __float_as_uint(p.src[4 * n4 + threadIdx.x]) & 0x7fffffffu);
-            }
-            mx = __reduce_max_sync(0xffffffffu, mx);
-            if (lane == 0) s_part[par][warp] = mx;
-            if (threadIdx.x == 0) s_part_layer[par] = it.layer;
-        } else {
-            if (threadIdx.x == 0) s_part_layer[par] = -1;
-            // ---------------- quantise + unscale item
-            if (!s_ok[slot]) {  // (uniform) layer not seen complete at claim time: wait now
-                // this CTA's own not-yet-counted abs-max item may be one the wait needs:
-                // count it first (deadlock otherwise)
-                if (threadIdx.x == kFlushThread) flush(-1);
-                if (threadIdx.x == 0) {
-                    const uint64_t w0 = f_timeline ? global_ns() : 0;
-                    spin_until([&] { return (int)(ld_acquire_u32(&t.layer_done[it.layer]) - layer_target(it)) >= 0; },
-                               t.flag);
-                    s_ft[slot] = ft_of(it);
-                    if (f_timeline) {
-                        tl_wait_ns += global_ns() - w0;
-                        ++tl_waits;
-                    }
-                }
-                __syncthreads();
-            }
-            const int ft = s_ft[slot];
-            if (it.tile_begin == 0 && threadIdx.x == 0) {  // record E, f~, flag; clear the next call's accumulator
-                const int32_t E = exponent_of(ld_relaxed_u32(&amax_of(0)[it.layer]), 1);
-                t.E_local[it.layer] = E;
-                t.ftilde[it.layer] = ft;
-                if (E == INT32_MAX) atomicOr(t.flag, 1u);
-                amax_of(1)[it.layer] = 0u;
-            }
-            const Pow2 s(ft);
-            const Unscale us(ft, 1, avg);
-            auto quantise = [&](const auto &cc) {
-                using CC = std::decay_t<decltype(cc)>;
-                constexpr int B = CC::kB;
-                if constexpr (B == 8 || B == 16 || B == 32) {
-                    using W = typename Word4<B>::T;
-                    W *out = reinterpret_cast<W *>(t.packed + it.byte_pos);
-                    if (full && !s.wide) {
-                        float4 *o4 = reinterpret_cast<float4 *>(p.dst);
-#pragma unroll
-                        for (int q = 0; q < kPer; ++q) {
-                            const float4 y = make_float4(__fmul_rn(v[q].x, s.f), __fmul_rn(v[q].y, s.f),
-                                                         __fmul_rn(v[q].z, s.f), __fmul_rn(v[q].w, s.f));
-                            const W code = pack4<B>(cc, y);
-                            const float4 r = us.apply4(unpack4<B>(cc, code));
-                            if (f_st_hint) {
-                                st_hint(out + threadIdx.x + q * NT, code, strm);
-                                st_hint4(o4 + threadIdx.x + q * NT, r, strm);
-                            } else {
-                                out[threadIdx.x + q * NT] = code;
-                                o4[threadIdx.x + q * NT] = r;
-                            }
-                        }
-                    } else {
-                        const int ng = it.n_tiles * (kTile / 4);
-                        for (int q = threadIdx.x; q < ng; q += NT) {
-                            const W code = pack4<B>(cc, s.apply4(load_group(p.src, 4 * (int64_t)q, it.cnt)));
-                            out[q] = code;
-                            store_group(p.dst, 4 * (int64_t)q, it.cnt, us.apply4(unpack4<B>(cc, code)));
-                        }
-                    }
-                } else {
-                    const int b = cc.b();
-                    uint32_t *codes = s_codes[warp];
-                    uint32_t *outw = reinterpret_cast<uint32_t *>(t.packed + it.byte_pos);
-                    for (int tt = warp; tt < it.n_tiles; tt += NT / 32) {
-                        const int64_t e0 = (int64_t)tt * kTile + lane * 4;
-                        const float4 y = s.apply4(load_group(p.src, e0, it.cnt));
-                        const uint4 cd = make_uint4(cc.enc(y.x), cc.enc(y.y), cc.enc(y.z), cc.enc(y.w));
-                        *reinterpret_cast<uint4 *>(codes + lane * 4) = cd;
-                        __syncwarp();
-                        uint32_t *ow = outw + (int64_t)tt * (4 * b);
-                        for (int w2 = lane; w2 < 4 * b; w2 += 32) ow[w2] = assemble_word(codes, w2, b);
-                        store_group(p.dst, e0, it.cnt,
-                                    us.apply4(make_float4(cc.dec(cd.x), cc.dec(cd.y), cc.dec(cd.z), cc.dec(cd.w))));
-                        __syncwarp();
-                    }
-                }
-            };
-            if constexpr (kTwo) {
-                if (it.fmt == fmt2) quantise(c2);
-                else quantise(c);
-            } else {
-                quantise(c);
-            }
-        }
-        __syncthreads();
-        slot = (slot + 1) % 3;
-        par ^= 1;
-        j = s_claim[slot];
-        if (f_timeline) ++tl_items;
-    }
-    if (threadIdx.x == kFlushThread) {  // drain: the last item's max, then its count
-        flush(par ^ 1);
-        flush(-1);
-    }
-    if (f_timeline && threadIdx.x == 0) {
-        t.timeline[blockIdx.x * 4 + 1] = tl_wait_ns;
-        t.timeline[blockIdx.x * 4 + 2] = (tl_waits << 32) | tl_items;
-    }
-    stamp(3);
-}
-
-template <class C, class C2>
-static cudaError_t launch_wave(const DevTables &t, C c, C2 c2, int bias, int bias2, int fmt2, int average,
-                               const WaveCall &w, int lag, int grid, cudaStream_t s, bool cooperative)
-{
-    auto kern = w.graph ? fused_p1_wave_kernel<C, C2, true, kThreads> : fused_p1_wave_kernel<C, C2, false, kThreads>;
-    int flags = kFusedDefaultFlags;  // compile time (-DAPS_FUSED_FLAGS=...: timeline stamps, A/B builds)
-    unsigned long long adv = 2ull * (unsigned long long)t.n_items + (unsigned long long)kWaveOvershoot * grid;
-    uint32_t *cur = t.amax2 + (size_t)(w.gen & 1u) * t.n_layers;
-    uint32_t *other = t.amax2 + (size_t)((w.gen + 1u) & 1u) * t.n_layers;
-    uint32_t claim_base = w.claim_base, call_no = w.call_no;
-    void *args[] = {const_cast<DevTables *>(&t), &c, &c2, &cur, &other, &claim_base, &call_no, &adv, &lag, &bias,
-                    &bias2, &fmt2, &average, &flags};
-    // co-residency is not needed for progress (a CTA waits only on positions claimed
-    // earlier, i.e. by running CTAs); a plain launch lets a concurrent group's kernel
-    // fill this one's tail
-    if (!cooperative) return cudaLaunchKernel((const void *)kern, dim3(grid), dim3(kThreads), args, 0, s);
-    return cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(kThreads), args, 0, s);
-}
-
-cudaError_t launch_fused_p1_wave(const DevTables &t, int e, int m, bool hw, int average, const WaveCall &w, int lag,
-                                 int grid, cudaStream_t s, bool cooperative)
-{
-    const int bias = (1 << (e - 1)) - 1;
-    return with_codec(e, m, hw, [&](auto c) -> cudaError_t {
-        return launch_wave(t, c, CNone{}, bias, 0, -1, average, w, lag, grid, s, cooperative);
-    });
-}
-
-cudaError_t launch_fused_p1_wave_hybrid32(const DevTables &t, int e, int m, bool hw, int fmt2, int average,
-                                          const WaveCall &w, int lag, int grid, cudaStream_t s)
-{
-    const int bias = (1 << (e - 1)) - 1;
-    return with_codec(e, m, hw, [&](auto c) -> cudaError_t {
-        return launch_wave(t, c, CF32{}, bias, 127, fmt2, average, w, lag, grid, s, true);
-    });
-}
-
-int fused_p1_wave_grid(int e, int m, bool hw, int n_items)
-{
-    int per_sm = 0;
-    with_codec(e, m, hw, [&](auto c) -> cudaError_t {
-        using C = decltype(c);
-        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_p1_wave_kernel<C, CNone, false, kThreads>,
-                                                             kThreads, 0);
-    });
-    per_sm = std::max(1, std::min(per_sm, kWaveCtasPerSm));
-    return std::max(1, std::min(n_items, sm_count() * per_sm));
 }
 
 cudaError_t launch_build_item_ptrs(const DevTables &t, cudaStream_t s)

@@ -273,6 +273,49 @@ __device__ __forceinline__ uint32_t h2_to_fp8x2(__half2 h)
     return d;
 }
 
+// e5m2 is binary16 with its low 8 significand bits dropped (same sign, exponent field and
+// bias; its subnormals are binary16's with the low byte zero), so on f16x2 words:
+//   decode  = move the code byte into the high byte of each half (one byte permute),
+//   Cast    = round each half to its high byte, ties to even, on the bit pattern:
+//             (u + 0x7f + lsb) & 0xff00 -- the carry runs into the exponent exactly as RNE
+//             does, and cannot cross halves (|sum| <= 1.5 * 2^15 < 0x7f80, reading A12),
+//   encode  = gather the high bytes (one byte permute),
+// all full-rate integer ops instead of the F2FP conversions (compile-time A/B switch).
+#ifndef APS_PEER_E5M2_INT
+#define APS_PEER_E5M2_INT 0  // measured: 1 (integer fold) 0.28 ms vs 0 (F2FP) 0.265 ms for the simulated p = 8 all-reduce (profiles/r02d_peer_ab.txt)
+#endif
+template <bool E4M3>
+__device__ __forceinline__ __half2 dec_pair(uint32_t w, int hi)
+{
+    if constexpr (!E4M3 && APS_PEER_E5M2_INT) {
+        const uint32_t h = __byte_perm(w, 0u, hi ? 0x3424 : 0x1404);
+        return *reinterpret_cast<const __half2 *>(&h);
+    } else {
+        return fp8x2_to_h2<E4M3>(hi ? (w >> 16) : (w & 0xffffu));
+    }
+}
+template <bool E4M3>
+__device__ __forceinline__ __half2 requant_h2(__half2 v)
+{
+    if constexpr (!E4M3 && APS_PEER_E5M2_INT) {
+        const uint32_t u = *reinterpret_cast<const uint32_t *>(&v);
+        const uint32_t r = (u + 0x007f007fu + ((u >> 8) & 0x00010001u)) & 0xff00ff00u;
+        return *reinterpret_cast<const __half2 *>(&r);
+    } else {
+        return fp8x2_to_h2<E4M3>(h2_to_fp8x2<E4M3>(v));
+    }
+}
+// two pairs already on the format's grid -> 4 codes
+template <bool E4M3>
+__device__ __forceinline__ uint32_t enc_pairs(__half2 a, __half2 b)
+{
+    if constexpr (!E4M3 && APS_PEER_E5M2_INT) {
+        return __byte_perm(*reinterpret_cast<const uint32_t *>(&a), *reinterpret_cast<const uint32_t *>(&b), 0x7531);
+    } else {
+        return h2_to_fp8x2<E4M3>(a) | (h2_to_fp8x2<E4M3>(b) << 16);
+    }
+}
+
 template <bool E4M3, int NT>
 #ifndef APS_PEER_MINB
 #define APS_PEER_MINB 3  // measured: 2 -> 19 us, 3 -> 17.2 us, 4 (64 regs, spills) -> 19.5 us (profiles/r01_ab_peer_minblocks.txt)
@@ -306,13 +349,13 @@ __global__ void __launch_bounds__(NT, APS_PEER_MINB) peer_reduce_fp8h_kernel(Pee
                 const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
-                    const __half2 x = fp8x2_to_h2<E4M3>((q & 1) ? (w[q >> 1] >> 16) : (w[q >> 1] & 0xffffu));
-                    s[q] = (j == 0) ? x : fp8x2_to_h2<E4M3>(h2_to_fp8x2<E4M3>(__hadd2(s[q], x)));
+                    const __half2 x = dec_pair<E4M3>(w[q >> 1], q & 1);
+                    s[q] = (j == 0) ? x : requant_h2<E4M3>(__hadd2(s[q], x));
                 }
                 if (j == o.k - 1) {
 #pragma unroll
                     for (int q = 0; q < 8; ++q)
-                        S[q] = (gi == 0) ? s[q] : fp8x2_to_h2<E4M3>(h2_to_fp8x2<E4M3>(__hadd2(S[q], s[q])));
+                        S[q] = (gi == 0) ? s[q] : requant_h2<E4M3>(__hadd2(S[q], s[q]));
                     j = 0;
                     ++gi;
                 } else {
@@ -321,10 +364,10 @@ __global__ void __launch_bounds__(NT, APS_PEER_MINB) peer_reduce_fp8h_kernel(Pee
             }
         }
         uint4 r;
-        r.x = h2_to_fp8x2<E4M3>(S[0]) | (h2_to_fp8x2<E4M3>(S[1]) << 16);
-        r.y = h2_to_fp8x2<E4M3>(S[2]) | (h2_to_fp8x2<E4M3>(S[3]) << 16);
-        r.z = h2_to_fp8x2<E4M3>(S[4]) | (h2_to_fp8x2<E4M3>(S[5]) << 16);
-        r.w = h2_to_fp8x2<E4M3>(S[6]) | (h2_to_fp8x2<E4M3>(S[7]) << 16);
+        r.x = enc_pairs<E4M3>(S[0], S[1]);
+        r.y = enc_pairs<E4M3>(S[2], S[3]);
+        r.z = enc_pairs<E4M3>(S[4], S[5]);
+        r.w = enc_pairs<E4M3>(S[6], S[7]);
         for (int q = 0; q < a.p; ++q) *reinterpret_cast<uint4 *>(a.packed[q] + off) = r;
     }
     cta_fence_system();
@@ -419,6 +462,52 @@ __global__ void __launch_bounds__(NT) peer_reduce_tile_kernel(PeerArgs a, int64_
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint32_t *wa = s_w[warp];
     const int64_t warps = (int64_t)gridDim.x * (NT / 32);
+    if (b <= kRegMaxB) {
+        // b <= 16: each lane loads the 2-3 words of every rank's tile its bits touch, splits
+        // its 4 codes out, folds, and the reduced tile is re-packed in registers
+        constexpr int BB = (C::kB > 0 && C::kB <= kRegMaxB) ? C::kB : 0;
+        for (int64_t tt = blockIdx.x * (int64_t)(NT / 32) + warp; tt < n_tiles; tt += warps) {
+            const int64_t off = byte_off + tt * 16 * b;
+            const Order o(a, tile0 + tt);
+            float S[4], Sc[4], s[4], c[4];
+            for (int gi = 0; gi < o.G; ++gi) {
+                for (int j = 0; j < o.k; ++j) {
+                    const uint8_t *src = a.packed[o.rank_of(gi, j)] + off;
+                    const uint4 cd = tile_split<BB>(
+                        tile_fetch<BB>(reinterpret_cast<const uint32_t *>(src), b, lane,
+                                       [](const uint32_t *q) { return ld_peer4(q); }),
+                        b, lane);
+                    const uint32_t cv[4] = {cd.x, cd.y, cd.z, cd.w};
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {
+                        const float x = cw.dec(cv[h]);
+                        if (j == 0) {
+                            s[h] = EXT ? rnd<C, A, EXT>(cw, ca, x) : x;
+                            c[h] = 0.f;
+                        } else {
+                            fold_add<C, A, EXT, KAHAN>(cw, ca, s[h], c[h], x);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    if (gi == 0) {
+                        S[h] = s[h];
+                        Sc[h] = 0.f;
+                    } else {
+                        fold_add<C, A, EXT, KAHAN>(cw, ca, S[h], Sc[h], s[h]);
+                    }
+                }
+            }
+            const TileSlots wo = tile_pack<BB>(make_uint4(cw.enc(S[0]), cw.enc(S[1]), cw.enc(S[2]), cw.enc(S[3])), b, lane);
+            for (int q = 0; q < a.p; ++q) {
+                uint32_t *tw = reinterpret_cast<uint32_t *>(a.packed[q] + off);
+                tile_store(wo, [&](int i, uint32_t x) { tw[i] = x; });
+            }
+        }
+        cta_fence_system();
+        return;
+    }
     for (int64_t tt = blockIdx.x * (int64_t)(NT / 32) + warp; tt < n_tiles; tt += warps) {
         const int64_t off = byte_off + tt * 16 * b;
         const Order o(a, tile0 + tt);

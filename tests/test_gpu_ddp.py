@@ -32,14 +32,15 @@ def pg():
     dist.destroy_process_group()
 
 
-def test_ddp_hook_matches_oracle(pg, orc):
+@pytest.mark.parametrize("overlap", [True, False], ids=["comm_stream", "same_stream"])
+def test_ddp_hook_matches_oracle(pg, orc, overlap):
     import paper_1911_08907_b200 as aps
     torch.manual_seed(1)
     model = torch.nn.Sequential(torch.nn.Linear(37, 129), torch.nn.GELU(), torch.nn.Linear(129, 515),
                                 torch.nn.GELU(), torch.nn.Linear(515, 3), torch.nn.LayerNorm(3)).cuda()
     ref = copy.deepcopy(model)
     ddp = torch.nn.parallel.DistributedDataParallel(model, device_ids=[0], bucket_cap_mb=0.1)
-    state = aps.ApsHookState(exp_bits=5, man_bits=2)
+    state = aps.ApsHookState(exp_bits=5, man_bits=2, overlap=overlap)
     ddp.register_comm_hook(state, aps.aps_hook)
     x = torch.randn(64, 37, device="cuda")
     seen_buckets = set()
@@ -69,4 +70,7 @@ def test_ddp_hook_matches_oracle(pg, orc):
                     off += n
         assert merged >= 1, "the misaligned parameter sizes should force at least one merged layer"
     assert len(seen_buckets) >= 2, "DDP's rebuilt buckets (bucket_cap_mb=0.1) should give several buckets"
+    # overlap: the APS kernels ran on the hook's own stream, not the backward stream
+    assert (state.comm_stream != torch.cuda.current_stream()) == overlap
+    assert all(ent[0].stream == state.comm_stream for ent in state.contexts.values())
     state.close()

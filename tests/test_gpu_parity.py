@@ -371,3 +371,42 @@ def test_sync_host_flat_and_separate_buffers(aps, orc):
             torch.cuda.synchronize()
             for a, b in zip(hout, ref.out):
                 assert np.array_equal(a.numpy().view(np.uint32), b.view(np.uint32)), layout
+
+
+# ----------------------------------------------------------------- every code width
+# b = 1 + e + m from 3 to 32: b <= 16 (not 8/16) packs in registers with warp shuffles
+# (runtime codec, or the compiled (3,0) / (5,6)), 17..31 through the per-warp shared-memory
+# tile; 8/16/32 the direct paths.  Each through the fused launch, the separate calls and
+# 3 simulated ranks (NCCL-ring schedule), with ragged layer tails.
+WIDTHS = [(2, 0), (2, 1), (3, 1), (3, 2), (4, 2), (4, 3), (4, 4), (5, 4), (5, 5), (4, 8), (5, 7), (6, 7),
+          (5, 9), (6, 9), (6, 10), (7, 10), (8, 10), (8, 13), (7, 17), (8, 20), (8, 22)]
+
+
+@pytest.mark.parametrize("fmt", WIDTHS, ids=lambda f: f"b{1 + f[0] + f[1]}_e{f[0]}m{f[1]}")
+def test_every_width(aps, orc, fmt):
+    e, m = fmt
+    numels = [4096, 1000, 1, 9408, 130, 8195, 65536 + 37]
+    g1 = synthetic.make_grads(numels, 1)
+    check(aps, orc, g1, e, m, False, fused=True)
+    check(aps, orc, g1, e, m, False, fused=False)
+    check(aps, orc, synthetic.make_grads(numels, 3), e, m, False)
+
+
+@pytest.mark.parametrize("cap", [1, 2])
+def test_p1_fused_occupancy_cap(aps, orc, cap):
+    """aps_set_occupancy: the fused launch with 1 or 2 CTAs per SM (the DDP hook's
+    overlap setting) gives the same bits; repeated calls keep the counters in step."""
+    numels = synthetic.RESNET50_NUMELS[:60] + [1000, 1, 8195]
+    grads = synthetic.make_grads(numels, 1)
+    ref = orc.aps_sync(grads, 5, 2, average=1)
+    g = [torch.from_numpy(a).cuda() for a in grads[0]]
+    ctx = aps.ApsContext(5, 2, numels)
+    ctx.set_occupancy(cap)
+    for _ in range(3):
+        out = [torch.empty_like(x) for x in g]
+        ctx.sync_out(g, out)
+        assert ctx.status_sync() == 0
+        assert np.array_equal(ctx.scales(), ref.ftilde)
+        assert np.array_equal(ctx.packed().cpu().numpy(), ref.packed[0])
+        for a, b in zip(out, ref.out):
+            assert np.array_equal(a.cpu().numpy().view(np.uint32), b.view(np.uint32))

@@ -211,3 +211,14 @@ def test_peer_fp8_all_code_pairs(aps, orc, fmt, amax):
     ref = orc.aps_sync(grads, e, m, average=0)
     assert ref.ftilde[0] == 0
     compare(run_peer(aps, grads, e, m, True, average=0), ref)
+
+
+@pytest.mark.parametrize("fmt", [(2, 0), (3, 2), (4, 4), (5, 6), (4, 8), (6, 9), (8, 10), (8, 20)],
+                         ids=lambda f: f"b{1 + f[0] + f[1]}")
+def test_peer_every_width(aps, orc, fmt):
+    """Register-packed (b <= 16) and shared-memory (b > 16) widths through the
+    owner-computes peer reduce, flat and hierarchical orders."""
+    e, m = fmt
+    grads = synthetic.make_grads(NUMELS + [8195], 4)
+    compare(run_peer(aps, grads, e, m, False), orc.aps_sync(grads, e, m, average=1))
+    compare(run_peer(aps, grads, e, m, False, group_k=2), orc.aps_sync_ex(grads, e, m, average=1, group_k=2))
