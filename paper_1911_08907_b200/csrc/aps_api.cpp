@@ -40,10 +40,6 @@ struct aps_ctx {
     std::vector<int64_t> numels;
     std::vector<aps::Item> items;
     std::vector<aps::LayerDev> layers;
-    std::vector<int64_t> voff;    // [n_layers + 1] a1's vector space (4 fp32 per vector, per layer)
-    std::vector<int32_t> abs_seg_off;  // a1: [G + 1] first segment of each CTA's share
-    std::vector<aps::AbsSeg> abs_segs; // a1: shares cut at layer boundaries
-    std::vector<aps::AbsSeg> abs_tails; // a1: partial last vectors
     int ctas_per_sm = 0;                // aps_set_occupancy (0: as many as fit)
     int64_t tiles = 0;        // T' (padded to a multiple of world)
     int64_t packed_bytes = 0; // sum over tiles of 16 * b(tile)
@@ -72,7 +68,7 @@ struct aps_ctx {
     uint8_t *ws = nullptr;
     size_t ws_bytes = 0, need = 0;
     size_t off_packed = 0, off_recv = 0, off_items = 0, off_layers = 0, off_src = 0, off_dst = 0,
-           off_amax = 0, off_eloc = 0, off_eglob = 0, off_ft = 0, off_flag = 0, off_amax2 = 0, off_iptr = 0, off_ldone = 0, off_claim64 = 0, off_voff = 0, off_ctal = 0, off_asegs = 0, off_atails = 0, off_bdone = 0, off_srcall = 0;
+           off_eloc = 0, off_eglob = 0, off_ft = 0, off_flag = 0, off_amax2 = 0, off_iptr = 0, off_ldone = 0, off_claim64 = 0, off_bdone = 0, off_srcall = 0;
     int max_layer_items = 0;
     bool graph_safe = false;   // aps_set_graph_safe (every launch is capture-safe; recorded only)
     std::vector<const void *> host_key;            // aps_sync_host: pointer set of the cached copy runs
@@ -347,7 +343,6 @@ static aps_status init_common(aps_ctx **out, const int *e_arr, const int *m_arr,
     c->off_layers = o; o = align_up(o + sizeof(aps::LayerDev) * c->layers.size());
     c->off_src = o;    o = align_up(o + sizeof(void *) * (size_t)n_layers);
     c->off_dst = o;    o = align_up(o + sizeof(void *) * (size_t)n_layers);
-    c->off_amax = o;   o = align_up(o + 4 * (size_t)n_layers);
     c->off_eloc = o;   o = align_up(o + 4 * (size_t)n_layers);
     c->off_eglob = o;  o = align_up(o + 4 * (size_t)n_layers);
     c->off_ft = o;     o = align_up(o + 4 * (size_t)n_layers);
@@ -355,12 +350,8 @@ static aps_status init_common(aps_ctx **out, const int *e_arr, const int *m_arr,
     c->off_amax2 = o;  o = align_up(o + 8 * (size_t)n_layers);
     c->off_iptr = o;   o = align_up(o + sizeof(aps::ItemPtr) * c->items.size());
     c->off_ldone = o;  o = align_up(o + 4 * (size_t)n_layers);
-    c->off_voff = o;   o = align_up(o + 8 * ((size_t)n_layers + 1));
     c->off_bdone = o;  o = align_up(o + 4 * (size_t)n_layers);
     c->off_srcall = o; o = align_up(o + 4);
-    c->off_ctal = o;   o = align_up(o + 4 * ((size_t)aps::kAbsMaxCtas + 1));
-    c->off_asegs = o;  o = align_up(o + sizeof(aps::AbsSeg) * ((size_t)aps::kAbsMaxCtas + (size_t)n_layers));
-    c->off_atails = o; o = align_up(o + sizeof(aps::AbsSeg) * (size_t)n_layers);
     // graph-safe counters: 64-bit wavefront claim counter per format group, absmax_ranges done counter
     c->off_claim64 = o; o = align_up(o + 8 * c->groups.size() + 4);
     // peer transport: flag block and E slots [2][world][n_layers] (world > 1 only)
@@ -371,8 +362,6 @@ static aps_status init_common(aps_ctx **out, const int *e_arr, const int *m_arr,
     c->acc_m = c->m;
 
     for (const auto &L : c->layers) c->max_layer_items = std::max(c->max_layer_items, (int)L.n_items);
-    c->voff.assign(1, 0);
-    for (int l = 0; l < n_layers; ++l) c->voff.push_back(c->voff.back() + (numels[l] + 3) / 4);
     c->need = o;
     *out = c;
     return APS_OK;
@@ -427,61 +416,11 @@ aps_status aps_set_workspace(aps_ctx *c, void *dev, size_t bytes)
                                 cudaMemcpyHostToDevice, c->stream));
     APS_CUDA(c, cudaMemcpyAsync(c->ws + c->off_layers, c->layers.data(),
                                 sizeof(aps::LayerDev) * c->layers.size(), cudaMemcpyHostToDevice, c->stream));
-    {   // a1's balanced split: CTA b streams vectors [b V / G, (b+1) V / G), cut at layer
-        // boundaries into segments (each in one layer)
-        // a1's vector space holds each layer's WHOLE vectors only; a layer's partial last
-        // vector (numel % 4 != 0) goes to the tail list (elements [e0, numel))
-        std::vector<int64_t> wvoff(1, 0);
-        c->abs_tails.clear();
-        for (int l = 0; l < c->n_layers; ++l) {
-            const int64_t n = c->layers[l].numel;
-            wvoff.push_back(wvoff.back() + n / 4);
-            if (n % 4) {
-                aps::AbsSeg tl{};
-                tl.e0 = n / 4 * 4;
-                tl.numel = n;
-                tl.layer = l;
-                c->abs_tails.push_back(tl);
-            }
-        }
-        const int G = aps::absmax_grid();
-        const int64_t V = wvoff.back();
-        c->abs_seg_off.assign(1, 0);
-        c->abs_segs.clear();
-        int l = 0;
-        for (int b = 0; b < G; ++b) {
-            const int64_t lo = V * b / G, hi = V * (b + 1) / G;
-            for (int64_t v = lo; v < hi;) {
-                while (wvoff[l + 1] <= v) ++l;
-                const int64_t v1 = std::min(hi, wvoff[l + 1]);
-                aps::AbsSeg sg{};
-                sg.v0 = v;
-                sg.v1 = v1;
-                sg.e0 = 4 * (v - wvoff[l]);
-                sg.numel = c->layers[l].numel;
-                sg.layer = l;
-                c->abs_segs.push_back(sg);
-                v = v1;
-            }
-            c->abs_seg_off.push_back((int32_t)c->abs_segs.size());
-        }
-        if (!c->abs_tails.empty())
-            APS_CUDA(c, cudaMemcpyAsync(c->ws + c->off_atails, c->abs_tails.data(),
-                                        sizeof(aps::AbsSeg) * c->abs_tails.size(), cudaMemcpyHostToDevice, c->stream));
-        APS_CUDA(c, cudaMemcpyAsync(c->ws + c->off_voff, c->voff.data(), 8 * c->voff.size(), cudaMemcpyHostToDevice,
-                                    c->stream));
-        APS_CUDA(c, cudaMemcpyAsync(c->ws + c->off_ctal, c->abs_seg_off.data(), 4 * c->abs_seg_off.size(),
-                                    cudaMemcpyHostToDevice, c->stream));
-        if (!c->abs_segs.empty())
-            APS_CUDA(c, cudaMemcpyAsync(c->ws + c->off_asegs, c->abs_segs.data(),
-                                        sizeof(aps::AbsSeg) * c->abs_segs.size(), cudaMemcpyHostToDevice, c->stream));
-    }
     aps::DevTables &t = c->t;
     t.items = reinterpret_cast<const aps::Item *>(c->ws + c->off_items);
     t.layers = reinterpret_cast<const aps::LayerDev *>(c->ws + c->off_layers);
     t.src = reinterpret_cast<const float *const *>(c->ws + c->off_src);
     t.dst = reinterpret_cast<float *const *>(c->ws + c->off_dst);
-    t.amax = reinterpret_cast<uint32_t *>(c->ws + c->off_amax);
     t.E_local = reinterpret_cast<int32_t *>(c->ws + c->off_eloc);
     // one rank: the global exponent vector IS the local one (no collective, no copy)
     t.E_glob = reinterpret_cast<int32_t *>(c->ws + (c->world == 1 ? c->off_eloc : c->off_eglob));
@@ -492,13 +431,8 @@ aps_status aps_set_workspace(aps_ctx *c, void *dev, size_t bytes)
     t.claim64 = reinterpret_cast<unsigned long long *>(c->ws + c->off_claim64);
     t.ranges_done = reinterpret_cast<uint32_t *>(c->ws + c->off_claim64 + 8 * c->groups.size());
     t.layer_done = reinterpret_cast<uint32_t *>(c->ws + c->off_ldone);
-    t.voff = reinterpret_cast<const int64_t *>(c->ws + c->off_voff);
     t.bdone = reinterpret_cast<uint32_t *>(c->ws + c->off_bdone);
     t.sr_call = reinterpret_cast<uint32_t *>(c->ws + c->off_srcall);
-    t.abs_seg_off = reinterpret_cast<const int32_t *>(c->ws + c->off_ctal);
-    t.abs_segs = reinterpret_cast<const aps::AbsSeg *>(c->ws + c->off_asegs);
-    t.abs_tails = reinterpret_cast<const aps::AbsSeg *>(c->ws + c->off_atails);
-    t.n_abs_tails = (int)c->abs_tails.size();
 
     if (c->groups.size() > 1 && c->side.empty()) {
         c->side.resize(c->groups.size() - 1);
@@ -615,15 +549,11 @@ aps_status aps_layer_scales(aps_ctx *c, const float *const *grads)
     if (aps_status s = need_ws(c)) return s;
     if (!grads) return fail(c, APS_ERR_ARG, "grads is NULL");
     if (aps_status s = upload_ptrs<const float *>(c, c->src_cache, grads, c->off_src)) return s;
-#if APS_ABSMAX_CW
     if (!c->iptr_valid) {  // per-item gradient addresses (output addresses: filled by the fused path)
         APS_CUDA(c, aps::launch_build_item_ptrs(c->t, c->stream));
         c->iptr_valid = true;
     }
     APS_CUDA(c, aps::launch_absmax_cw(c->t, c->world, c->stream));
-#else
-    APS_CUDA(c, aps::launch_absmax(c->t, c->world, c->stream));
-#endif
     if (c->world == 1 && !c->comm) {
         c->phase = kScales;
     } else if (c->peer) {

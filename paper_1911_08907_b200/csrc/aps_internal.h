@@ -41,22 +41,11 @@ struct ItemPtr {
     float *dst;
 };
 
-// a1: one CTA's share of the layers' vector space, cut at layer boundaries: vectors
-// [v0, v1) of a1's vector space, all in `layer`, starting at element e0 of it.
-struct AbsSeg {
-    int64_t v0, v1;
-    int64_t e0;       // element index (within the layer) of vector v0
-    int64_t numel;    // the layer's element count (its last vector may be partial)
-    int32_t layer;
-    int32_t pad;
-};
-
 struct DevTables {
     const Item *items;
     const LayerDev *layers;
     const float *const *src;  // [n_layers] gradient pointers
     float *const *dst;        // [n_layers] output pointers
-    uint32_t *amax;           // [n_layers] running abs-max bits (self-resetting)
     int32_t *E_local;         // [n_layers]
     int32_t *E_glob;          // [n_layers]
     int32_t *ftilde;          // [n_layers]
@@ -64,31 +53,18 @@ struct DevTables {
     uint32_t *amax2;          // [2][n_layers] abs-max accumulators of the fused kernel (call parity)
     ItemPtr *iptr;            // [n_items] per-item addresses (fused LDG kernel)
     unsigned long long *claim64;  // claim counter of the control-warp kernel (per format group; self-resetting)
-    uint32_t *ranges_done;    // self-resetting CTA-done counter of absmax_stream_kernel
-    const int64_t *voff;      // [n_layers + 1] first vector (4 fp32) of each layer in a1's vector space
-    const int32_t *abs_seg_off;  // [absmax_grid() + 1] a1: first segment of each CTA's share
-    const struct AbsSeg *abs_segs; // a1: the shares cut at layer boundaries (whole vectors; host-built, static)
-    const struct AbsSeg *abs_tails; // a1: each layer's partial last vector (elements [e0, numel))
+    uint32_t *ranges_done;    // self-resetting CTA-done counter of the a1-only launch
     uint32_t *layer_done;     // [n_layers] per-layer abs-max completion counters (fused kernel)
     uint32_t *bdone;          // [n_layers] per-layer quantise completion counters (fused kernel, self-resetting)
     uint32_t *sr_call;        // stochastic rounding: syncs since aps_set_rounding (per-call key, reading A27)
     uint8_t *packed;          // packed codes
     int n_items;
     int n_layers;
-    int n_abs_tails;
 };
 
-// a1: balanced abs-max stream over every layer (absmax_grid() CTAs; DevTables.abs_seg_off /
-// abs_segs describe the split), self-resetting done counter
-constexpr int kAbsCtasPerSm = 4;
-constexpr int kAbsMaxCtas = 1024;  // segment-table bound (workspace)
-int absmax_grid();
-cudaError_t launch_absmax(const DevTables &t, int world, cudaStream_t s);
-// a1 through the control-warp kernel (dynamic claims): DevTables.iptr must be current
+// a1 alone (aps_layer_scales): the control-warp kernel over the abs-max items
+// (aps_fused.cu); DevTables.iptr must be current
 cudaError_t launch_absmax_cw(const DevTables &t, int world, cudaStream_t s);
-#ifndef APS_ABSMAX_CW
-#define APS_ABSMAX_CW 1  // 0: absmax_stream_kernel (static balanced shares) -- compile-time A/B
-#endif
 cudaError_t launch_quant_pack(const DevTables &t, int e, int m, bool hw, cudaStream_t s);
 cudaError_t launch_unpack_unscale(const DevTables &t, int e, int m, bool hw, int world, int average,
                                   cudaStream_t s);

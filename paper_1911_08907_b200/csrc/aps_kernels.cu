@@ -1,5 +1,5 @@
-// aps_kernels.cu -- the sm_100a kernels of the APS hot path:
-//   a1  absmax_exp      FindMaxExp(g * N) for every layer, one launch      (Alg. 1)
+// aps_kernels.cu -- the separate-call sm_100a kernels of the APS hot path:
+//   (a1  absmax_exp: the control-warp kernel of aps_fused.cu over the abs-max items)
 //   a3/a4 quant_pack    f~ = upper_bound_exp - E; Cast(g * 2^f~) ; pack    (Alg. 1)
 //   a5  ring_reduce     s <- Cast(fl32(dec(recv) + dec(own)))             (Alg. 1)
 //   a7  unpack_unscale  Cast(s, 8, 23) / 2^f~ / N                         (Alg. 1)
@@ -7,8 +7,8 @@
 // not apply).  Design: one CTA per tile-aligned work item of <= 8192
 // elements of one layer (a multi-tensor launch covers every layer), 128-bit
 // coalesced loads (ld.global.nc.L1::no_allocate) and coalesced stores;
-// b = 8/16/32 pack directly from registers, other widths go through a
-// per-warp shared-memory tile.
+// b = 8/16/32 pack directly from registers, b <= 16 through register tiles
+// (aps_device.cuh), b = 17..31 through a per-warp shared-memory tile.
 #include <type_traits>
 #include <cstdint>
 #include <climits>
@@ -20,143 +20,9 @@
 
 namespace aps {
 
-// ------------------------------------------------------------------ a1: abs-max, balanced stream
-// FindMaxExp (Alg. 1 line 3; function P:260-271) for every layer in ONE launch of
-// exactly kAbsCtasPerSm x SMs CTAs.  The layers are laid end to end in "vector space"
-// (vector = 4 consecutive fp32 of one layer; layer l owns vectors [voff[l], voff[l+1]),
-// its last vector partial when numel % 4 != 0) and CTA b streams the equal share
-// [b V / G, (b+1) V / G): every SM moves the same number of bytes, so the launch has no
-// tail of idle SMs.  The host cuts every share at layer boundaries into segments
-// (DevTables.abs_segs, static per context), so the kernel never searches for a layer:
-// a CTA stages up to kAbsSegBatch segment descriptors (with the layer's gradient
-// pointer) in shared memory and walks their vectors in chunks of 8 x NT, each thread
-// first issuing its 8 independent 128-bit loads (its segment found by a forward scan
-// over the staged descriptors: vector indices only grow), then folding each load: a warp
-// whose 32 vectors lie in one segment reduces with a shuffle and does one shared-memory
-// atomicMax, a warp straddling a boundary folds per lane.  Each staged
-// segment's max goes to amax[layer] with one red.max.  (The previous kernel looked the
-// layer up with dependent global binary searches and loaded boundary chunks one vector at
-// a time: 43 us for ResNet-50, latency-bound.)  The max of u32 abs bits is
-// order-independent, so the result is bit-exact whatever the split.  Completion: one fence
-// by thread 0 after the CTA barrier, one count; the last CTA turns the maxima into
-// E_l = ceil(log2(N A_l)) and clears them (self-resetting: capture-safe).  Gradients are
-// loaded with an L2 evict_last hint so that quant_pack's re-read (reverse order) hits L2.
-constexpr int kAbsSegBatch = 64;
-
-template <int NT>
-__global__ void __launch_bounds__(NT, kAbsCtasPerSm) absmax_stream_kernel(DevTables t, int N)
-{
-    constexpr int kChunk = 8 * NT;
-    __shared__ int64_t s_v1[kAbsSegBatch], s_v0[kAbsSegBatch], s_e0[kAbsSegBatch];
-    __shared__ const float *s_src[kAbsSegBatch];
-    __shared__ uint32_t s_max[kAbsSegBatch];
-    __shared__ int s_layer[kAbsSegBatch];
-    __shared__ int s_last;
-    const int lane = threadIdx.x & 31;
-    uint64_t keep;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
-    // the layers' partial last vectors (numel % 4 != 0): one thread each, straight to amax
-    for (int k2 = blockIdx.x * NT + threadIdx.x; k2 < t.n_abs_tails; k2 += gridDim.x * NT) {
-        const AbsSeg tl = t.abs_tails[k2];
-        const float *g = t.src[tl.layer];
-        uint32_t mx = 0;
-        for (int64_t e = tl.e0; e < tl.numel; ++e) mx = max(mx, __float_as_uint(g[e]) & 0x7fffffffu);
-        if (mx) asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(&t.amax[tl.layer]), "r"(mx) : "memory");
-    }
-    const int sb = t.abs_seg_off[blockIdx.x], se = t.abs_seg_off[blockIdx.x + 1];
-    for (int b0 = sb; b0 < se; b0 += kAbsSegBatch) {
-        const int nb = min(kAbsSegBatch, se - b0);
-        if ((int)threadIdx.x < nb) {
-            const AbsSeg sg = t.abs_segs[b0 + threadIdx.x];
-            s_v0[threadIdx.x] = sg.v0;
-            s_v1[threadIdx.x] = sg.v1;
-            s_e0[threadIdx.x] = sg.e0;
-            s_layer[threadIdx.x] = sg.layer;
-            s_src[threadIdx.x] = t.src[sg.layer];
-            s_max[threadIdx.x] = 0u;
-        }
-        __syncthreads();
-        const int64_t lo = s_v0[0], hi = s_v1[nb - 1];
-        int kc = 0;           // segment of the chunk's first vector (CTA-uniform)
-        int krun = 0;         // segment of this thread's running max
-        uint32_t run = 0;
-        auto flush = [&]() {  // the warp's running max -> the segment's shared-memory max
-            const uint32_t m = __reduce_max_sync(0xffffffffu, run);
-            if (lane == 0 && m) atomicMax(&s_max[krun], m);
-            run = 0;
-        };
-        for (int64_t c0 = lo; c0 < hi; c0 += kChunk) {
-            while (s_v1[kc] <= c0) ++kc;
-            float4 v[8];
-            if (c0 + kChunk <= s_v1[kc]) {
-                // ---- the whole chunk lies in segment kc (CTA-uniform branch): 8
-                // unconditional 128-bit loads, a running max, no per-vector bookkeeping
-                const float4 *p = reinterpret_cast<const float4 *>(s_src[kc] + s_e0[kc]) + (c0 - s_v0[kc]) + threadIdx.x;
-#pragma unroll
-                for (int q = 0; q < 8; ++q) v[q] = ld_keep4(p + q * NT, keep);
-                if (kc != krun) {
-                    flush();
-                    krun = kc;
-                }
-#pragma unroll
-                for (int q = 0; q < 8; ++q) run = max(run, absbits4(v[q]));
-                continue;
-            }
-            // ---- a chunk meeting a segment boundary or the batch end: per-vector segments
-            // (segments hold whole vectors only -- the layers' partial last vectors are the
-            // tail list above); all 8 loads issued before the first use
-            flush();
-            int kq[8];
-            int k = kc;
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const int64_t i = c0 + threadIdx.x + q * NT;
-                const bool in = i < hi;
-                while (in && s_v1[k] <= i) ++k;
-                const float4 *pp = reinterpret_cast<const float4 *>(s_src[k] + s_e0[k]) + (i - s_v0[k]);
-                v[q] = in ? ld_keep4(pp, keep) : make_float4(0.f, 0.f, 0.f, 0.f);
-                kq[q] = k;
-            }
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                uint32_t mx = absbits4(v[q]);
-                const int k0 = __shfl_sync(0xffffffffu, kq[q], 0);
-                if (__all_sync(0xffffffffu, kq[q] == k0)) {
-                    mx = __reduce_max_sync(0xffffffffu, mx);
-                    if (lane == 0 && mx) atomicMax(&s_max[k0], mx);
-                } else if (mx) {
-                    atomicMax(&s_max[kq[q]], mx);
-                }
-            }
-        }
-        flush();
-        __syncthreads();
-        if ((int)threadIdx.x < nb && s_max[threadIdx.x])
-            asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(&t.amax[s_layer[threadIdx.x]]),
-                         "r"(s_max[threadIdx.x])
-                         : "memory");
-        __syncthreads();
-    }
-    // completion: the CTA barrier orders every warp's red.max before thread 0's fence
-    // (cumulativity), whose count the last CTA acquires
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        s_last = atomicAdd(t.ranges_done, 1u) == gridDim.x - 1u;
-        if (s_last) *t.ranges_done = 0u;  // every CTA of this launch has counted itself
-    }
-    __syncthreads();
-    if (s_last) {
-        __threadfence();
-        for (int k = threadIdx.x; k < t.n_layers; k += NT) {
-            uint32_t a_;
-            asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(a_) : "l"(&t.amax[k]) : "memory");
-            t.E_local[k] = exponent_of(a_, N);
-            t.amax[k] = 0u;
-        }
-    }
-}
-
+// ------------------------------------------------------------------ a3 + a4: scale, Cast, pack
+// One CTA per work item (<= 8192 elements of one layer); items in reverse order: a1
+// (forward claims, L2 evict_last loads) read these last, so they are the ones still in L2.
 template <int B, class C, int NT>
 __global__ void __launch_bounds__(NT) quant_pack_direct_kernel(DevTables t, C c, int bias)
 {
@@ -485,15 +351,6 @@ int sm_count()
         if (n <= 0) n = 148;
     }
     return n;
-}
-
-int absmax_grid() { return std::min(kAbsMaxCtas, sm_count() * kAbsCtasPerSm); }
-
-cudaError_t launch_absmax(const DevTables &t, int world, cudaStream_t s)
-{
-    if (t.n_items == 0) return cudaSuccess;
-    absmax_stream_kernel<kThreads><<<absmax_grid(), kThreads, 0, s>>>(t, world);
-    return cudaGetLastError();
 }
 
 cudaError_t launch_quant_pack(const DevTables &t, int e, int m, bool hw, cudaStream_t s)
