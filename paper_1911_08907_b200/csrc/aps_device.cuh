@@ -24,6 +24,16 @@ struct CGen {
         constexpr Fmt F = make_fmt(E, M);
         return encode(F, y);
     }
+    __device__ __forceinline__ uint32_t enc_q(float y) const  // quantise path (encode_q)
+    {
+        constexpr Fmt F = make_fmt(E, M);
+        return encode_q(F, y);
+    }
+    __device__ __forceinline__ uint32_t enc_q_dec(float y, float &d) const  // + Cast back
+    {
+        constexpr Fmt F = make_fmt(E, M);
+        return encode_q_dec(F, y, d);
+    }
     __device__ __forceinline__ float dec(uint32_t c) const
     {
         constexpr Fmt F = make_fmt(E, M);
@@ -112,6 +122,8 @@ struct CRt {
     Fmt F;
     __device__ __forceinline__ int b() const { return F.b; }
     __device__ __forceinline__ uint32_t enc(float y) const { return encode(F, y); }
+    __device__ __forceinline__ uint32_t enc_q(float y) const { return encode_q(F, y); }
+    __device__ __forceinline__ uint32_t enc_q_dec(float y, float &d) const { return encode_q_dec(F, y, d); }
     __device__ __forceinline__ float dec(uint32_t c) const { return decode_finite(F, c); }
     __device__ __forceinline__ float dec_any(uint32_t c) const { return decode(F, c); }
 };

@@ -44,6 +44,13 @@
 namespace aps {
 
 constexpr int kCwSlots = APS_CW_SLOTS;
+#ifndef APS_ABS_DEPTH
+#define APS_ABS_DEPTH 2  // measured 25.2-25.5 us vs 26.6 (3) and 26.8-27.5 (1): profiles/r02i_ab_abs.txt
+#endif
+constexpr int kAbsDepth = APS_ABS_DEPTH < kCwSlots ? APS_ABS_DEPTH : kCwSlots;
+#ifndef APS_ABS_CTAS_PER_SM
+#define APS_ABS_CTAS_PER_SM 0  // 0: as many as fit (3)
+#endif
 constexpr int kCwDataWarps = kThreads / 32;            // 8
 constexpr int kCwThreads = kThreads + 32;               // + the control warp
 
@@ -81,10 +88,11 @@ __device__ __forceinline__ void cw_quant_reg(const CC &cc, const float *src, flo
         if (tt >= n_tiles) break;  // warp-uniform
         const int64_t e0 = (int64_t)tt * kTile + lane * 4;
         const float4 y = FAST ? sc.apply4_narrow(v[j]) : sc.apply4(v[j]);
-        const uint4 cd = make_uint4(cc.enc(y.x), cc.enc(y.y), cc.enc(y.z), cc.enc(y.w));
+        float4 d;
+        const uint4 cd = make_uint4(cc.enc_q_dec(y.x, d.x), cc.enc_q_dec(y.y, d.y), cc.enc_q_dec(y.z, d.z),
+                                    cc.enc_q_dec(y.w, d.w));
         uint32_t *tw = outw + (int64_t)tt * (4 * b);
         tile_store(tile_pack<B>(cd, b, lane), [&](int i, uint32_t x) { st_hint(tw + i, x, strm); });
-        const float4 d = make_float4(cc.dec(cd.x), cc.dec(cd.y), cc.dec(cd.z), cc.dec(cd.w));
         const float4 o = FAST ? us.apply4_fast(d) : us.apply4(d);
         if (full) st_hint4(reinterpret_cast<float4 *>(dst + e0), o, strm);
         else store_group(dst, e0, cnt, o);
@@ -97,6 +105,9 @@ __global__ void __launch_bounds__(kCwThreads, kCwCtasPerSm)
 {
     constexpr bool kTwo = C2::kB > 0;  // items with fmt == fmt2 use c2 (bias2): the hybrid FP32 layer
     constexpr bool kAOnly = C2::kB == CAOnly::kB;  // a1 alone (aps_layer_scales): avg carries N
+    // items in flight per CTA: a1 alone keeps fewer (its items are short; a deep ring only
+    // lengthens the queue every CTA drains at the end of the launch)
+    constexpr int kDepth = kAOnly ? kAbsDepth : kCwSlots;
     constexpr int NT = kThreads;       // data threads
     constexpr int kPer = kItemTiles * kTile / 4 / NT;  // float4 per data thread per item: 8
     __shared__ CwSlot s_slot[kCwSlots];
@@ -179,11 +190,17 @@ __global__ void __launch_bounds__(kCwThreads, kCwCtasPerSm)
                 if (block) break;
             }
         };
-        int64_t raw = atomicAdd(t.claim64, 1ull);  // (the claim counter is 64-bit; reset by the last claimer)
+        // positions 0 .. grid-1 are claimed statically (CTA b takes b: no atomic round trip
+        // before the first load); later claims are grid + atomicAdd(claim64).  Every CTA
+        // makes exactly one claim past the end, so the launch's last claim is total + grid - 1.
+        // (Static positions are A items (D >= grid); a CTA not yet resident -- the GPU shared
+        // with other kernels -- holds one, and B items of its layer wait until it is
+        // scheduled, which happens once the other kernels' CTAs retire: the grid fits the GPU.)
+        int64_t raw = blockIdx.x;
         for (;;) {
             const int s = filled % kCwSlots;
-            if (filled >= kCwSlots) {  // the slot's previous item must be done: fold it
-                while (folded <= filled - kCwSlots) fold_ready(true);
+            if (filled >= kDepth) {  // at most kDepth items in flight: fold the oldest first
+                while (folded <= filled - kDepth) fold_ready(true);
             }
             fold_ready(false);
             const int64_t j = raw;
@@ -194,7 +211,7 @@ __global__ void __launch_bounds__(kCwThreads, kCwCtasPerSm)
                 ++filled;
                 break;
             }
-            raw = atomicAdd(t.claim64, 1ull);  // next claim, in flight while this slot is prepared
+            raw = (int64_t)gridDim.x + (int64_t)atomicAdd(t.claim64, 1ull);  // next claim, in flight while this slot is prepared
             bool isB;
             const int k = decode((int)j, isB);
             const Item it = t.items[k];
@@ -407,7 +424,7 @@ cudaError_t launch_fused_cw(const DevTables &t, int e, int m, bool hw, int avera
 cudaError_t launch_absmax_cw(const DevTables &t, int world, cudaStream_t s)
 {
     if (t.n_items == 0) return cudaSuccess;
-    const int grid = cw_grid<CF32, CAOnly>(t.n_items, 0);
+    const int grid = cw_grid<CF32, CAOnly>(t.n_items, APS_ABS_CTAS_PER_SM);
     fused_cw_kernel<CF32, CAOnly><<<grid, kCwThreads, 0, s>>>(t, CF32{}, CAOnly{}, 0, 0, 0, -1, world);
     return cudaGetLastError();
 }

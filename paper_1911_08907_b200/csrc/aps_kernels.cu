@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(NT) quant_pack_tile_kernel(DevTables t, C c, i
                 const int tt = warp + j * (NT / 32);
                 if (tt >= it.n_tiles) break;  // warp-uniform
                 const float4 y = decltype(narrow)::value ? s.apply4_narrow(v[j]) : s.apply4(v[j]);
-                const uint4 cd = make_uint4(c.enc(y.x), c.enc(y.y), c.enc(y.z), c.enc(y.w));
+                const uint4 cd = make_uint4(c.enc_q(y.x), c.enc_q(y.y), c.enc_q(y.z), c.enc_q(y.w));
                 uint32_t *tw = out + (int64_t)tt * (4 * b);
                 tile_store(tile_pack<BB>(cd, b, lane), [&](int i, uint32_t x) { tw[i] = x; });
             }

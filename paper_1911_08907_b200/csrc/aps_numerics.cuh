@@ -84,6 +84,45 @@ __device__ __forceinline__ uint32_t encode(const Fmt &f, float y)
     return s | mag;
 }
 
+// Cast on the QUANTISE path only (the scaled gradient y = g 2^f~): |y| <= 2^bias / N by
+// Eq. (1)-(4) (A2), so no result overflows, and a non-finite gradient raises the
+// deferred flag with unspecified outputs (A4) -- the NaN select and the Inf clamp of
+// `encode` are dropped (3 of ~13 integer ops: the generic-width kernels are ALU-bound).
+// Identical to `encode` for every finite |y| < 2^(emax + 1).
+__device__ __forceinline__ uint32_t encode_q(const Fmt &f, float y)
+{
+    const uint32_t u = __float_as_uint(y);
+    if (f.m == 23) return u;
+    const uint32_t a = u & 0x7fffffffu;
+    const uint32_t s = (u >> 31) << (f.e + f.m);
+    const uint32_t r = ((a + f.round_half + ((a >> f.sh) & 1u)) >> f.sh) - f.rebias;
+    const float t = __fadd_rn(__uint_as_float(a), __uint_as_float(f.magic_bits));
+    const uint32_t rs = __float_as_uint(t) - f.magic_bits;
+    return s | ((a >= f.norm_min) ? r : rs);
+}
+
+// encode_q and, from its intermediates, the decoded value (Cast back, Alg. 1 line 8):
+// target-normal R0 = (a + half + lsb) >> sh is the rounded value's fp32 bit pattern >> sh,
+// so dec = R0 << sh; target-subnormal t = |y| + M is rounded, so dec = t - M exactly.
+// Saves re-extracting the fields from the code in the fused kernel (ALU-bound widths).
+__device__ __forceinline__ uint32_t encode_q_dec(const Fmt &f, float y, float &dec)
+{
+    const uint32_t u = __float_as_uint(y);
+    if (f.m == 23) {
+        dec = y;
+        return u;
+    }
+    const uint32_t a = u & 0x7fffffffu;
+    const uint32_t sgn = u & 0x80000000u;
+    const uint32_t r0 = (a + f.round_half + ((a >> f.sh) & 1u)) >> f.sh;
+    const float t = __fadd_rn(__uint_as_float(a), __uint_as_float(f.magic_bits));
+    const bool normal = a >= f.norm_min;
+    const uint32_t mag = normal ? r0 - f.rebias : __float_as_uint(t) - f.magic_bits;
+    const uint32_t vbits = normal ? (r0 << f.sh) : __float_as_uint(__fsub_rn(t, __uint_as_float(f.magic_bits)));
+    dec = __uint_as_float(vbits | sgn);
+    return (sgn >> (31 - f.e - f.m)) | mag;
+}
+
 __device__ __forceinline__ float decode(const Fmt &f, uint32_t c)
 {
     const uint32_t s = ((c >> (f.e + f.m)) & 1u) << 31;

@@ -68,10 +68,20 @@ __device__ __forceinline__ uint32_t ld_peer4(const void *p)
 // end of a reduce CTA: its remote stores are made visible system-wide once
 // (bar.sync orders the CTA's stores before thread 0's fence; the signal kernel
 // that follows fences again before it raises the done flag)
+// APS_PEER_FENCE: 0 = fence.sc.sys (__threadfence_system), 1 = fence.acq_rel.sys (a release
+// fence is all the pattern needs: prior stores before the later flag store) -- A/B
+#ifndef APS_PEER_FENCE
+#define APS_PEER_FENCE 1
+#endif
+__device__ __forceinline__ void fence_release_sys()
+{
+    if constexpr (APS_PEER_FENCE == 1) asm volatile("fence.acq_rel.sys;" ::: "memory");
+    else __threadfence_system();
+}
 __device__ __forceinline__ void cta_fence_system()
 {
     __syncthreads();
-    if (threadIdx.x == 0) __threadfence_system();
+    if (threadIdx.x == 0) fence_release_sys();
 }
 
 __device__ __forceinline__ int32_t ld_relaxed_i32(const int32_t *p)
