@@ -125,6 +125,16 @@ def ncu_traffic():
         return {}
 
 
+def ncu_traffic_steady():
+    """DRAM bytes per fused launch in steady state (ncu application replay, caches as the
+    program leaves them): profiles/ncu_traffic_steady.json."""
+    try:
+        return int(json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic_steady.json")))
+                   ["dram_bytes_per_launch_median"])
+    except Exception:
+        return None
+
+
 def host_cpu():
     model = None
     try:
@@ -707,6 +717,8 @@ class Bench:
             phases["allreduce"]["note"] = ("busBW = 2(p-1)/p x packed bytes / t; frac of the measured 770 GB/s "
                                            "per direction (nominal 900)")
         traffic = ncu_traffic() if (args.config == "c2" and (e, m) == (5, 2) and not args.no_hw and not fmts) else {}
+        traffic_steady = (ncu_traffic_steady() if (args.config == "c2" and (e, m) == (5, 2) and not args.no_hw
+                                                   and not fmts) else None)
         if self.world == 1:
             # one fused launch per step; NECESSARY bytes: one fp32 read + codes + fp32 output (the
             # abs-max pass and the quantise pass read the same gradients; the second read is L2)
@@ -718,7 +730,10 @@ class Bench:
                     "algorithmic_bytes_per_launch": int(dbytes),
                     "algorithmic_bytes_rule": "8 L + code bytes: one fp32 read, the packed codes, one fp32 write",
                     "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
-                    "timing": "steady state (back-to-back syncs, rotating buffer sets > L2)"}
+                    "timing": "steady state (back-to-back syncs, rotating buffer sets > L2)",
+                    "traffic_note": ("traffic: one ncu --set full capture (cold caches: ~55 MB of the launch's "
+                                     "writes are still dirty in L2 at kernel end)"),
+                    "traffic_steady_state": traffic_steady}
         else:
             dom = max(kern, key=lambda k: kern[k][0])
             dms, dbytes = kern[dom]

@@ -44,10 +44,11 @@
 namespace aps {
 
 constexpr int kCwSlots = APS_CW_SLOTS;
-#ifndef APS_ABS_DEPTH
-#define APS_ABS_DEPTH 2  // measured 25.2-25.5 us vs 26.6 (3) and 26.8-27.5 (1): profiles/r02i_ab_abs.txt
-#endif
-constexpr int kAbsDepth = APS_ABS_DEPTH < kCwSlots ? APS_ABS_DEPTH : kCwSlots;
+// a1 alone: a 4-slot ring, all 4 in flight, data warps take slots two at a time (16
+// loads per lane in flight: each warp's 8 x 128-bit loads of one item left ~14 MB in
+// flight over the GPU, short of what HBM needs; one slot at a time measured 25.2 us with
+// 2 in flight, 26.6 with 3: profiles/r02i_ab_abs.txt)
+constexpr int kAbsSlots = 4;
 #ifndef APS_ABS_CTAS_PER_SM
 #define APS_ABS_CTAS_PER_SM 0  // 0: as many as fit (3)
 #endif
@@ -100,25 +101,26 @@ __device__ __forceinline__ void cw_quant_reg(const CC &cc, const float *src, flo
 }
 
 template <class C, class C2>
-__global__ void __launch_bounds__(kCwThreads, kCwCtasPerSm)
+__global__ void __launch_bounds__(kCwThreads, C2::kB == CAOnly::kB ? 2 : kCwCtasPerSm)
     fused_cw_kernel(DevTables t, C c, C2 c2, int lag, int bias, int bias2, int fmt2, int avg)
 {
     constexpr bool kTwo = C2::kB > 0;  // items with fmt == fmt2 use c2 (bias2): the hybrid FP32 layer
     constexpr bool kAOnly = C2::kB == CAOnly::kB;  // a1 alone (aps_layer_scales): avg carries N
     // items in flight per CTA: a1 alone keeps fewer (its items are short; a deep ring only
     // lengthens the queue every CTA drains at the end of the launch)
-    constexpr int kDepth = kAOnly ? kAbsDepth : kCwSlots;
+    constexpr int kSlots = kAOnly ? kAbsSlots : kCwSlots;
+    constexpr int kDepth = kSlots;
     constexpr int NT = kThreads;       // data threads
     constexpr int kPer = kItemTiles * kTile / 4 / NT;  // float4 per data thread per item: 8
-    __shared__ CwSlot s_slot[kCwSlots];
-    __shared__ uint32_t s_part[kCwSlots][kCwDataWarps];     // per-warp abs-max of an A slot
-    __shared__ __align__(8) uint64_t s_full[kCwSlots], s_empty[kCwSlots];
+    __shared__ CwSlot s_slot[kSlots];
+    __shared__ uint32_t s_part[kSlots][kCwDataWarps];     // per-warp abs-max of an A slot
+    __shared__ __align__(8) uint64_t s_full[kSlots], s_empty[kSlots];
     __shared__ __align__(16) uint32_t s_codes[kCwDataWarps][kTile];  // generic widths
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int n = t.n_items, D = lag, total = kAOnly ? n : 2 * n;
     uint32_t *const amax = t.amax2, *const adone = t.layer_done, *const bdone = t.bdone;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kCwSlots; ++s) {
+        for (int s = 0; s < kSlots; ++s) {
             mbar_init(&s_full[s], 1);
             mbar_init(&s_empty[s], kCwDataWarps);
         }
@@ -181,8 +183,8 @@ __global__ void __launch_bounds__(kCwThreads, kCwCtasPerSm)
         int filled = 0, folded = 0;  // slots published / folded so far (slot i % S)
         auto fold_ready = [&](bool block) {
             while (folded < filled) {
-                const int s = folded % kCwSlots;
-                const uint32_t ph = (uint32_t)(folded / kCwSlots) & 1u;
+                const int s = folded % kSlots;
+                const uint32_t ph = (uint32_t)(folded / kSlots) & 1u;
                 if (!block && !mbar_test(&s_empty[s], ph)) break;
                 if (block) mbar_wait(&s_empty[s], ph, t.flag);
                 fold(s);
@@ -198,7 +200,7 @@ __global__ void __launch_bounds__(kCwThreads, kCwCtasPerSm)
         // scheduled, which happens once the other kernels' CTAs retire: the grid fits the GPU.)
         int64_t raw = blockIdx.x;
         for (;;) {
-            const int s = filled % kCwSlots;
+            const int s = filled % kSlots;
             if (filled >= kDepth) {  // at most kDepth items in flight: fold the oldest first
                 while (folded <= filled - kDepth) fold_ready(true);
             }
@@ -284,6 +286,62 @@ __global__ void __launch_bounds__(kCwThreads, kCwCtasPerSm)
     uint64_t keep, strm;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(strm));
+    if constexpr (kAOnly) {
+        // a1 alone: two slots at a time (the second may be the end marker)
+        auto part_max = [&](const float *src, int cnt) {  // a partial item (a layer's last)
+            const float4 *g4 = reinterpret_cast<const float4 *>(src);
+            uint32_t mx = 0;
+            const int n4 = cnt >> 2;
+            for (int q = threadIdx.x; q < n4; q += NT) mx = max(mx, absbits4(ld_hint4(g4 + q, keep)));
+            if ((int)threadIdx.x < (cnt & 3)) mx = max(mx, __float_as_uint(src[4 * n4 + threadIdx.x]) & 0x7fffffffu);
+            return mx;
+        };
+        auto finish = [&](int s, uint32_t mx) {
+            mx = __reduce_max_sync(0xffffffffu, mx);
+            if (lane == 0) s_part[s][warp] = mx;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_empty[s]);
+        };
+        for (int i = 0;; i += 2) {
+            const int s0 = i % kSlots, s1 = (i + 1) % kSlots;
+            mbar_wait(&s_full[s0], (uint32_t)(i / kSlots) & 1u, t.flag);
+            if (s_slot[s0].kind == 2) break;
+            mbar_wait(&s_full[s1], (uint32_t)((i + 1) / kSlots) & 1u, t.flag);
+            const bool two = s_slot[s1].kind != 2;
+            const float *src0 = s_slot[s0].src, *src1 = s_slot[s1].src;
+            const int cnt0 = s_slot[s0].cnt, cnt1 = two ? s_slot[s1].cnt : 0;
+            const bool full0 = cnt0 == kItemTiles * kTile, full1 = cnt1 == kItemTiles * kTile;
+            float4 v0[kPer], v1[kPer];
+            if (full0) {
+                const float4 *g4 = reinterpret_cast<const float4 *>(src0) + threadIdx.x;
+#pragma unroll
+                for (int q = 0; q < kPer; ++q) v0[q] = ld_hint4(g4 + q * NT, keep);
+            }
+            if (full1) {
+                const float4 *g4 = reinterpret_cast<const float4 *>(src1) + threadIdx.x;
+#pragma unroll
+                for (int q = 0; q < kPer; ++q) v1[q] = ld_hint4(g4 + q * NT, keep);
+            }
+            uint32_t m0 = 0;
+            if (full0) {
+#pragma unroll
+                for (int q = 0; q < kPer; ++q) m0 = max(m0, absbits4(v0[q]));
+            } else {
+                m0 = part_max(src0, cnt0);
+            }
+            finish(s0, m0);
+            if (!two) break;
+            uint32_t m1 = 0;
+            if (full1) {
+#pragma unroll
+                for (int q = 0; q < kPer; ++q) m1 = max(m1, absbits4(v1[q]));
+            } else {
+                m1 = part_max(src1, cnt1);
+            }
+            finish(s1, m1);
+        }
+        return;
+    }
     for (int i = 0;; ++i) {
         const int s = i % kCwSlots;
         mbar_wait(&s_full[s], (uint32_t)(i / kCwSlots) & 1u, t.flag);
