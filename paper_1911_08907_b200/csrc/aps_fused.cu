@@ -48,10 +48,19 @@ constexpr int kCwSlots = APS_CW_SLOTS;
 // loads per lane in flight: each warp's 8 x 128-bit loads of one item left ~14 MB in
 // flight over the GPU, short of what HBM needs; one slot at a time measured 25.2 us with
 // 2 in flight, 26.6 with 3: profiles/r02i_ab_abs.txt)
-constexpr int kAbsSlots = 4;
-#ifndef APS_ABS_CTAS_PER_SM
-#define APS_ABS_CTAS_PER_SM 0  // 0: as many as fit (3)
+#ifndef APS_ABS_PAIR
+#define APS_ABS_PAIR 0  // 1: 25.7-26.6 us vs 23.4-23.5 (0): profiles/r02n_ab_absmax_pair.txt
 #endif
+#ifndef APS_ABS_CTAS
+#define APS_ABS_CTAS 3
+#endif
+#ifndef APS_ABS_DEPTH
+#define APS_ABS_DEPTH 2
+#endif
+constexpr int kAbsSlots = APS_ABS_PAIR ? 4 : 3;
+constexpr int kAbsDepth = APS_ABS_PAIR ? 4 : APS_ABS_DEPTH;
+constexpr int kAbsCtasPerSm = APS_ABS_PAIR ? 2 : APS_ABS_CTAS;  // (two items' loads per lane need the registers)
+
 constexpr int kCwDataWarps = kThreads / 32;            // 8
 constexpr int kCwThreads = kThreads + 32;               // + the control warp
 
@@ -101,7 +110,7 @@ __device__ __forceinline__ void cw_quant_reg(const CC &cc, const float *src, flo
 }
 
 template <class C, class C2>
-__global__ void __launch_bounds__(kCwThreads, C2::kB == CAOnly::kB ? 2 : kCwCtasPerSm)
+__global__ void __launch_bounds__(kCwThreads, C2::kB == CAOnly::kB ? kAbsCtasPerSm : kCwCtasPerSm)
     fused_cw_kernel(DevTables t, C c, C2 c2, int lag, int bias, int bias2, int fmt2, int avg)
 {
     constexpr bool kTwo = C2::kB > 0;  // items with fmt == fmt2 use c2 (bias2): the hybrid FP32 layer
@@ -109,7 +118,7 @@ __global__ void __launch_bounds__(kCwThreads, C2::kB == CAOnly::kB ? 2 : kCwCtas
     // items in flight per CTA: a1 alone keeps fewer (its items are short; a deep ring only
     // lengthens the queue every CTA drains at the end of the launch)
     constexpr int kSlots = kAOnly ? kAbsSlots : kCwSlots;
-    constexpr int kDepth = kSlots;
+    constexpr int kDepth = kAOnly ? kAbsDepth : kSlots;
     constexpr int NT = kThreads;       // data threads
     constexpr int kPer = kItemTiles * kTile / 4 / NT;  // float4 per data thread per item: 8
     __shared__ CwSlot s_slot[kSlots];
@@ -272,10 +281,25 @@ __global__ void __launch_bounds__(kCwThreads, C2::kB == CAOnly::kB ? 2 : kCwCtas
                 if (last) *t.ranges_done = 0u;
             }
             if (__shfl_sync(0xffffffffu, last, 0)) {
+                // the whole GPU waits for this: all loads of a batch in flight at once (a
+                // volatile load per layer, each behind the previous store, took ~5 us)
                 __threadfence();
-                for (int l = lane; l < t.n_layers; l += 32) {
-                    t.E_local[l] = exponent_of(ld_relaxed_u32(&amax[l]), avg);
-                    amax[l] = 0u;
+                constexpr int kB = 8;
+                for (int l0 = 0; l0 < t.n_layers; l0 += 32 * kB) {
+                    uint32_t a[kB];
+#pragma unroll
+                    for (int k = 0; k < kB; ++k) {
+                        const int l = l0 + lane + 32 * k;
+                        a[k] = l < t.n_layers ? __ldcg(amax + l) : 0u;
+                    }
+#pragma unroll
+                    for (int k = 0; k < kB; ++k) {
+                        const int l = l0 + lane + 32 * k;
+                        if (l < t.n_layers) {
+                            t.E_local[l] = exponent_of(a[k], avg);
+                            amax[l] = 0u;
+                        }
+                    }
                 }
             }
         }
@@ -286,7 +310,7 @@ __global__ void __launch_bounds__(kCwThreads, C2::kB == CAOnly::kB ? 2 : kCwCtas
     uint64_t keep, strm;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(strm));
-    if constexpr (kAOnly) {
+    if constexpr (kAOnly && APS_ABS_PAIR) {
         // a1 alone: two slots at a time (the second may be the end marker)
         auto part_max = [&](const float *src, int cnt) {  // a partial item (a layer's last)
             const float4 *g4 = reinterpret_cast<const float4 *>(src);
@@ -482,7 +506,7 @@ cudaError_t launch_fused_cw(const DevTables &t, int e, int m, bool hw, int avera
 cudaError_t launch_absmax_cw(const DevTables &t, int world, cudaStream_t s)
 {
     if (t.n_items == 0) return cudaSuccess;
-    const int grid = cw_grid<CF32, CAOnly>(t.n_items, APS_ABS_CTAS_PER_SM);
+    const int grid = cw_grid<CF32, CAOnly>(t.n_items, kAbsCtasPerSm);
     fused_cw_kernel<CF32, CAOnly><<<grid, kCwThreads, 0, s>>>(t, CF32{}, CAOnly{}, 0, 0, 0, -1, world);
     return cudaGetLastError();
 }

@@ -65,6 +65,7 @@ struct DevTables {
 // a1 alone (aps_layer_scales): the control-warp kernel over the abs-max items
 // (aps_fused.cu); DevTables.iptr must be current
 cudaError_t launch_absmax_cw(const DevTables &t, int world, cudaStream_t s);
+
 cudaError_t launch_quant_pack(const DevTables &t, int e, int m, bool hw, cudaStream_t s);
 cudaError_t launch_unpack_unscale(const DevTables &t, int e, int m, bool hw, int world, int average,
                                   cudaStream_t s);
