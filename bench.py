@@ -663,8 +663,8 @@ class Bench:
     # -------------------------------------------------------------- launches per step
     def launches(self, numels, fmts, e, m, transport):
         G = len(set(fmts)) if fmts else 1
-        if self.world == 1:
-            return G
+        if self.world == 1:   # one fused launch per format group; two formats share one launch
+            return 1 if G <= 2 else G
         if transport == "peer":   # absmax, E exchange, G quantise, ready + done flag kernels, own-chunk runs, G unscale
             runs = format_runs(numels, fmts or [(e, m)] * len(numels), self.world, (self.rank + 2) % self.world)[0]
             return 1 + 1 + 2 * G + 2 + runs

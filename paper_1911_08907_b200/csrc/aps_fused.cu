@@ -113,7 +113,7 @@ template <class C, class C2>
 __global__ void __launch_bounds__(kCwThreads, C2::kB == CAOnly::kB ? kAbsCtasPerSm : kCwCtasPerSm)
     fused_cw_kernel(DevTables t, C c, C2 c2, int lag, int bias, int bias2, int fmt2, int avg)
 {
-    constexpr bool kTwo = C2::kB > 0;  // items with fmt == fmt2 use c2 (bias2): the hybrid FP32 layer
+    constexpr bool kTwo = C2::kB >= 0;  // items with fmt == fmt2 use c2 (bias2): the hybrid layers
     constexpr bool kAOnly = C2::kB == CAOnly::kB;  // a1 alone (aps_layer_scales): avg carries N
     // items in flight per CTA: a1 alone keeps fewer (its items are short; a deep ring only
     // lengthens the queue every CTA drains at the end of the launch)
@@ -511,12 +511,16 @@ cudaError_t launch_absmax_cw(const DevTables &t, int world, cudaStream_t s)
     return cudaGetLastError();
 }
 
-cudaError_t launch_fused_cw_hybrid32(const DevTables &t, int e, int m, bool hw, int fmt2, int average,
-                                     int max_layer_items, cudaStream_t s, int ctas_per_sm)
+cudaError_t launch_fused_cw_hybrid(const DevTables &t, int e, int m, bool hw, int e2, int m2, bool hw2, int fmt2,
+                                   int average, int max_layer_items, cudaStream_t s, int ctas_per_sm)
 {
-    const int bias = (1 << (e - 1)) - 1;
+    const int bias = (1 << (e - 1)) - 1, bias2 = (1 << (e2 - 1)) - 1;
     return with_codec(e, m, hw, [&](auto c) -> cudaError_t {
-        return launch_cw(t, c, CF32{}, bias, 127, fmt2, average, max_layer_items, s, ctas_per_sm);
+        if (e2 == 8 && m2 == 23 && hw2)
+            return launch_cw(t, c, CF32{}, bias, bias2, fmt2, average, max_layer_items, s, ctas_per_sm);
+        CRt c2;
+        c2.F = make_fmt(e2, m2);
+        return launch_cw(t, c, c2, bias, bias2, fmt2, average, max_layer_items, s, ctas_per_sm);
     });
 }
 

@@ -97,8 +97,10 @@ constexpr int kWaveLagGrids = APS_WAVE_LAG_GRIDS;
 constexpr int kCwCtasPerSm = APS_CW_CTAS_PER_SM;
 cudaError_t launch_fused_cw(const DevTables &t, int e, int m, bool hw, int average, int max_layer_items, cudaStream_t s,
                             int ctas_per_sm = 0);
-cudaError_t launch_fused_cw_hybrid32(const DevTables &t, int e, int m, bool hw, int fmt2, int average,
-                                     int max_layer_items, cudaStream_t s, int ctas_per_sm = 0);
+// two format groups in one launch: items of group fmt2 use (e2, m2) (binary32 through the
+// identity codec, any other format through the runtime codec)
+cudaError_t launch_fused_cw_hybrid(const DevTables &t, int e, int m, bool hw, int e2, int m2, bool hw2, int fmt2,
+                                   int average, int max_layer_items, cudaStream_t s, int ctas_per_sm = 0);
 // true when (e,m) has a hardware converter that is exact on the APS path
 // formats with a hardware / exact fast codec: fp8 e5m2, e4m3 (APS regime only,
 // reading A12), binary16, bfloat16, binary32 (every non-NaN input)

@@ -10,8 +10,9 @@ ncu --metrics gpu__time_duration.sum --clock-control none --print-units base --c
 FULL="--set full --clock-control none --import-source on --print-units base"
 # the fused N = 1 launch (a launch of the steady-state loop), then the separate-call kernels (N > 1 path)
 ncu $FULL -k regex:fused_cw -s 10 -c 1 -o $OUT/prof_${TAG}_fused -f python bench.py $ARGS > $OUT/ncu_fused_$TAG.log 2>&1
-ncu $FULL -k regex:'absmax_stream|quant_pack|unpack_unscale' -s 6 -c 3 -o $OUT/prof_${TAG}_calls -f python bench.py $ARGS > $OUT/ncu_calls_$TAG.log 2>&1
-for r in fused calls; do
+ncu $FULL -k regex:'quant_pack|unpack_unscale' -s 6 -c 2 -o $OUT/prof_${TAG}_calls -f python bench.py $ARGS > $OUT/ncu_calls_$TAG.log 2>&1
+ncu $FULL --kernel-name-base demangled -k regex:'CAOnly' -s 2 -c 1 -o $OUT/prof_${TAG}_absmax -f python bench.py $ARGS > $OUT/ncu_absmax_$TAG.log 2>&1
+for r in fused calls absmax; do
   ncu -i $OUT/prof_${TAG}_$r.ncu-rep --print-units base --page raw --csv > $OUT/prof_${TAG}_${r}_raw.csv 2>&1
   ncu -i $OUT/prof_${TAG}_$r.ncu-rep --print-units base --page details --csv > $OUT/prof_${TAG}_${r}_details.csv 2>&1
   ncu -i $OUT/prof_${TAG}_$r.ncu-rep --page source --csv --print-units base > $OUT/prof_${TAG}_${r}_source.csv 2>&1

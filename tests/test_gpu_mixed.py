@@ -146,3 +146,22 @@ def test_mixed_uniform_matches_uniform_context(aps):
     assert torch.equal(a.packed(), b.packed())
     for x, y in zip(oa, ob):
         assert torch.equal(x.view(torch.int32), y.view(torch.int32))
+
+
+@pytest.mark.parametrize("second", [(8, 23), (5, 6), (3, 0), (4, 3), (5, 10), (6, 12), (2, 1)],
+                         ids=lambda f: f"e{f[0]}m{f[1]}")
+@pytest.mark.parametrize("hw", [True, False], ids=["hw", "gen"])
+def test_p1_two_formats_single_launch(aps, orc, second, hw):
+    """Exactly two formats: ONE fused launch whose second-format items switch codec in the
+    kernel (binary32 through the identity codec, any other through the runtime codec),
+    with the second group first, last and interleaved in layer order; repeated calls."""
+    numels = NUMELS + [65536 + 37]
+    for pattern in ("last", "first", "alternate"):
+        if pattern == "last":
+            fmts = [(5, 2)] * (len(numels) - 2) + [second] * 2
+        elif pattern == "first":
+            fmts = [second] * 2 + [(5, 2)] * (len(numels) - 2)
+        else:
+            fmts = [(5, 2) if i % 2 else second for i in range(len(numels))]
+        grads = synthetic.make_grads(numels, 1)
+        check_mixed(aps, orc, grads, fmts, hw=hw, fused=True, calls=2)
