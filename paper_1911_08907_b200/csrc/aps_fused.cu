@@ -518,6 +518,8 @@ cudaError_t launch_fused_cw_hybrid(const DevTables &t, int e, int m, bool hw, in
     return with_codec(e, m, hw, [&](auto c) -> cudaError_t {
         if (e2 == 8 && m2 == 23 && hw2)
             return launch_cw(t, c, CF32{}, bias, bias2, fmt2, average, max_layer_items, s, ctas_per_sm);
+        if (e2 == 5 && m2 == 6)  // the paper's 12-bit format: compiled (lane-pair packing), not the runtime codec
+            return launch_cw(t, c, CGen<5, 6>{}, bias, bias2, fmt2, average, max_layer_items, s, ctas_per_sm);
         CRt c2;
         c2.F = make_fmt(e2, m2);
         return launch_cw(t, c, c2, bias, bias2, fmt2, average, max_layer_items, s, ctas_per_sm);
