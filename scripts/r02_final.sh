@@ -11,4 +11,6 @@ timeout 600 python bench.py --hybrid --hybrid-last 5,6 --steps 40 --no-cpu-basel
 timeout 600 python bench.py --hybrid --steps 40 --no-cpu-baseline --no-peer-sim > $OUT/${T}_hybrid32.json 2> $OUT/${T}_hybrid32.err
 APS_BENCH_SAME_GPU=1 timeout 600 python bench.py --gpus 2 --steps 10 --warmup 3 --no-cpu-baseline > $OUT/${T}_n2_plumbing.json 2> $OUT/${T}_n2_plumbing.err
 bash scripts/profile.sh $T > $OUT/${T}_profile.log 2>&1
+
+rm -f gpurun_out/*.ncu-rep; du -sh gpurun_out
 echo done
