@@ -201,13 +201,15 @@ __global__ void __launch_bounds__(kCwThreads, C2::kB == CAOnly::kB ? kAbsCtasPer
                 if (block) break;
             }
         };
-        // positions 0 .. grid-1 are claimed statically (CTA b takes b: no atomic round trip
-        // before the first load); later claims are grid + atomicAdd(claim64).  Every CTA
-        // makes exactly one claim past the end, so the launch's last claim is total + grid - 1.
-        // (Static positions are A items (D >= grid); a CTA not yet resident -- the GPU shared
-        // with other kernels -- holds one, and B items of its layer wait until it is
-        // scheduled, which happens once the other kernels' CTAs retire: the grid fits the GPU.)
-        int64_t raw = blockIdx.x;
+        // Claims.  a1 alone: positions 0 .. grid-1 are taken statically (CTA b takes b: no
+        // atomic round trip before the first load), later ones are grid + atomicAdd; nothing
+        // waits on another CTA there.  The fused kernel claims EVERY position dynamically:
+        // a B item waits for the A items of its layer, and a position held by a CTA that is
+        // not resident (two APS launches sharing the GPU, each partly resident) could then
+        // never be processed.  Either way every CTA makes exactly one claim past the end, so
+        // the launch's last claim is total + grid - 1.
+        const int64_t claim_off = kAOnly ? (int64_t)gridDim.x : 0;
+        int64_t raw = kAOnly ? (int64_t)blockIdx.x : (int64_t)atomicAdd(t.claim64, 1ull);
         for (;;) {
             const int s = filled % kSlots;
             if (filled >= kDepth) {  // at most kDepth items in flight: fold the oldest first
@@ -222,7 +224,7 @@ __global__ void __launch_bounds__(kCwThreads, C2::kB == CAOnly::kB ? kAbsCtasPer
                 ++filled;
                 break;
             }
-            raw = (int64_t)gridDim.x + (int64_t)atomicAdd(t.claim64, 1ull);  // next claim, in flight while this slot is prepared
+            raw = claim_off + (int64_t)atomicAdd(t.claim64, 1ull);  // next claim, in flight while this slot is prepared
             bool isB;
             const int k = decode((int)j, isB);
             const Item it = t.items[k];
@@ -308,7 +310,14 @@ __global__ void __launch_bounds__(kCwThreads, C2::kB == CAOnly::kB ? kAbsCtasPer
 
     // ======================================================== data warps
     uint64_t keep, strm;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
+#ifndef APS_ABS_KEEP_FRAC
+#define APS_ABS_KEEP_FRAC 0.5  // a1 alone: fraction of its loads marked evict_last: 0.5 -> quant_pack 16.4 vs 17.2 us (1.0), a1 unchanged (profiles/r02t_ab_keep.txt)
+#endif
+    if constexpr (kAOnly) {
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, %1;" : "=l"(keep) : "f"((float)APS_ABS_KEEP_FRAC));
+    } else {
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
+    }
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(strm));
     if constexpr (kAOnly && APS_ABS_PAIR) {
         // a1 alone: two slots at a time (the second may be the end marker)

@@ -410,3 +410,29 @@ def test_p1_fused_occupancy_cap(aps, orc, cap):
         assert np.array_equal(ctx.packed().cpu().numpy(), ref.packed[0])
         for a, b in zip(out, ref.out):
             assert np.array_equal(a.cpu().numpy().view(np.uint32), b.view(np.uint32))
+
+
+@pytest.mark.timeout(300)
+def test_p1_fused_concurrent_streams(aps, orc):
+    """Two contexts' fused launches on two streams at once (a bench e2e / multi-bucket
+    pattern): neither grid is fully resident while the other runs, so no CTA may wait on
+    work held by a CTA that is not resident.  Both stay bit-exact with no wait timeout."""
+    numels = synthetic.RESNET50_NUMELS
+    grads = synthetic.make_grads(numels, 1)
+    ref = orc.aps_sync(grads, 5, 2, average=1)
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    ctxs = [aps.ApsContext(5, 2, numels, stream=s) for s in streams]
+    gs = [[torch.from_numpy(a).cuda() for a in grads[0]] for _ in range(2)]
+    outs = [[torch.empty_like(x) for x in g] for g in gs]
+    ptr_g = [aps.ApsContext.ptr_array(g) for g in gs]
+    ptr_o = [aps.ApsContext.ptr_array(o) for o in outs]
+    torch.cuda.synchronize()
+    for _ in range(20):
+        for i in range(2):
+            ctxs[i].sync_out(ptr_g[i], ptr_o[i])
+    torch.cuda.synchronize()
+    for i in range(2):
+        assert ctxs[i].status_sync() == 0
+        for a, b in zip(outs[i], ref.out):
+            assert np.array_equal(a.cpu().numpy().view(np.uint32), b.view(np.uint32))
+        ctxs[i].close()
