@@ -756,6 +756,21 @@ class Bench:
             phases["peer_allreduce_p8_sim"] = self.peer_sim(e, m, numels)
         if self.world > 1 and self.comm is not None:
             extra["references"] = self.nccl_refs(L, packed_bytes)
+            # the other transport timed too (the NCCL send/recv ring is north_star's design, the
+            # peer-memory kernel the default): sync time and the all-reduce phase's busBW of each
+            other = "nccl" if transport == "peer" else "peer"
+            tr = {transport: {"sync_us": round(ms * 1e3, 2), "allreduce_us": round(r["phase_ms"][2] * 1e3, 2),
+                              "busBW_GBps": round(2 * (self.world - 1) / self.world * packed_bytes
+                                                  / (r["phase_ms"][2] * 1e-3) / 1e9, 1)}}
+            try:
+                ro = self.measure(e, m, numels, fmts, other, want_graph, max(20, args.steps // 2), 3, args.sets)
+                tr[other] = {"sync_us": round(ro["ms"] * 1e3, 2), "allreduce_us": round(ro["phase_ms"][2] * 1e3, 2),
+                             "busBW_GBps": round(2 * (self.world - 1) / self.world * packed_bytes
+                                                 / (ro["phase_ms"][2] * 1e-3) / 1e9, 1), "ok": ro["ok"]}
+                del ro["sets"], ro["host"]
+            except (Exception, SystemExit) as exc:   # reported, never fatal (every rank raises together)
+                tr[other] = {"error": str(exc)[:200]}
+            extra["transports"] = tr
         e2e = self.e2e(e, m, numels, fmts, transport, r["host"])
         del r["sets"]
         fsweep = None
