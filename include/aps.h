@@ -151,8 +151,11 @@ aps_status aps_allreduce(aps_ctx *ctx);
 aps_status aps_unscale(aps_ctx *ctx, float *const *out, int average);
 
 /* aps_layer_scales, aps_quantize_pack, aps_allreduce, aps_unscale in order,
- * in place on grads.  With world_size == 1 the four run as ONE fused
- * persistent launch (no collective separates FindMaxExp from Cast). */
+ * in place on grads.  With world_size == 1 (no NCCL communicator, nearest-even
+ * rounding) the four run as ONE fused launch per format group -- two formats
+ * share one launch -- (no collective separates FindMaxExp from Cast): a
+ * warp-specialised wavefront over the work items that needs no co-residency
+ * and no per-call host state (capture-safe). */
 aps_status aps_sync(aps_ctx *ctx, float *const *grads, int average);
 
 /* As aps_sync, reading grads and writing the result to out (out may alias
