@@ -55,7 +55,7 @@ def _rank_main(rank, world, port, fail_rank, out):
 
 @pytest.mark.parametrize("world,fail_rank", [(2, -1), (3, -1), (2, 1), (3, 0)])
 def test_connect_peers_agreement(world, fail_rank):
-    mgr = mp.Manager()
+    mgr = mp.get_context("spawn").Manager()  # (a forked manager from a threaded process warns)
     out = mgr.dict()
     mp.spawn(_rank_main, args=(world, _free_port(), fail_rank, out), nprocs=world, join=True)
     for r in range(world):
