@@ -248,8 +248,17 @@ def cpu_oracle_run(numels, e, m, p, budget_s=20.0, min_s=10.0):
     L = sum(sample)
     desc = (f"first {len(sample)} of {len(numels)} layers ({L} of {sum(numels)} elements) x {p} simulated "
             f"rank(s), full oracle aps_sync (FindMaxExp, MAX, cast, ring, unscale), {reps} sync(s), {cores} threads")
+    # single-threaded beside it: a prefix of ~6 s of work
+    s1, _ = oracle_sample(numels, p, 6.0, 1)
+    g1 = synthetic.make_grads(s1, p)
+    t0 = time.perf_counter()
+    oracle.aps_sync(g1, e, m, want_packed=False, n_threads=1)
+    t1s = time.perf_counter() - t0
+    single = {"value": round(4 * sum(s1) / t1s / 1e9, 6), "unit": UNIT, "cores": 1, "seconds": round(t1s, 3),
+              "sample": f"first {len(s1)} layers ({sum(s1)} elements) x {p} simulated rank(s), 1 thread"}
     return {"value": round(4 * L * reps / t / 1e9, 6), "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc,
             "seconds": round(t, 3), "syncs": reps, "cpu_model": model, "nproc": cores,
+            "single_thread": single,
             "note": "per-rank fp32-equivalent GB/s (4 L / t, as the GPU line's per_rank)"}
 
 
@@ -725,7 +734,8 @@ class Bench:
             dbytes = 8 * L + code_bytes
             achieved = dbytes / (ms * 1e-3) / 1e9
             roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                    "frac": round(achieved / peak, 4), "traffic": traffic.get("fused_p1"),
+                    "frac": round(achieved / peak, 4), "frac_vs_8TBps_spec": round(achieved / 8000.0, 4),
+                    "traffic": traffic.get("fused_p1"),
                     "kernel": "fused_cw_kernel (a1 + a3 + a4 + a7, one launch)",
                     "algorithmic_bytes_per_launch": int(dbytes),
                     "algorithmic_bytes_rule": "8 L + code bytes: one fp32 read, the packed codes, one fp32 write",
