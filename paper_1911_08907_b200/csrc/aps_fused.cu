@@ -376,8 +376,8 @@ __global__ void __launch_bounds__(kCwThreads, C2::kB == CAOnly::kB ? kAbsCtasPer
         return;
     }
     for (int i = 0;; ++i) {
-        const int s = i % kCwSlots;
-        mbar_wait(&s_full[s], (uint32_t)(i / kCwSlots) & 1u, t.flag);
+        const int s = i % kSlots;
+        mbar_wait(&s_full[s], (uint32_t)(i / kSlots) & 1u, t.flag);
         const int kind = s_slot[s].kind;
         if (kind == 2) break;
         const float *src = s_slot[s].src;
