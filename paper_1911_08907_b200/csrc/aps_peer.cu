@@ -333,7 +333,10 @@ template <bool E4M3, int NT>
 __global__ void __launch_bounds__(NT, APS_PEER_MINB) peer_reduce_fp8h_kernel(PeerArgs a, int64_t byte_off, int64_t tile0,
                                                               int64_t n_vec)
 {
-    constexpr int kBatch = 8;
+#ifndef APS_PEER_BATCH
+#define APS_PEER_BATCH 8  // addends loaded per batch (registers vs loads in flight; A/B)
+#endif
+    constexpr int kBatch = APS_PEER_BATCH;
     for (int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x; i < n_vec; i += (int64_t)gridDim.x * NT) {
         const int64_t off = byte_off + i * 16;
         const Order o(a, tile0 + i / 8);  // a tile is 128 bytes = 8 vectors
