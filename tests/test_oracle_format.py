@@ -287,3 +287,39 @@ def test_scale_matches_ldexpf(orc):
     ours = np.array([orc.scale(float(a), int(k)) for a, k in zip(x[:20000], ks[:20000])], np.float32)
     r = ref[:20000]
     assert np.array_equal(ours.view(np.uint32), r.view(np.uint32))
+
+
+# SURVEY 8(c)'s constants table for the config formats, each value re-derived here from the
+# format's closed forms (O1: maxfinite = (2 - 2^-m) 2^bias, min normal 2^(1-bias), min
+# subnormal 2^(1-bias-m); the overflow threshold is the midpoint between maxfinite and
+# 2^(bias+1) and the underflow threshold half the min subnormal, each tie going to the even
+# code, A9-A11).  Values are exact in binary64 and in fp32 (all are powers of two or short
+# binary fractions within fp32's range).
+CONFIG_FORMATS = [(3, 0), (5, 2), (4, 3), (5, 6), (5, 10), (8, 7)]
+
+
+@pytest.mark.parametrize("fmt", CONFIG_FORMATS, ids=lambda f: f"e{f[0]}m{f[1]}")
+def test_survey_constants_table(orc, fmt):
+    e, m = fmt
+    cast = lambda x: int(orc.cast([x], e, m)[0])
+    bias = (1 << (e - 1)) - 1
+    maxfinite = (2.0 - 2.0 ** -m) * 2.0 ** bias
+    min_normal = 2.0 ** (1 - bias)
+    min_sub = 2.0 ** (1 - bias - m)
+    max_code = (((1 << e) - 2) << m) | ((1 << m) - 1)
+    inf_code = ((1 << e) - 1) << m
+    assert orc.bias(e) == bias
+    assert float(orc.decode([max_code], e, m)[0]) == maxfinite
+    assert float(orc.decode([1 << m], e, m)[0]) == min_normal          # first normal code
+    assert float(orc.decode([1], e, m)[0]) == min_sub                    # first subnormal code
+    assert cast(maxfinite) == max_code
+    # overflow: the midpoint between maxfinite and 2^(bias+1) is a tie; above it is Inf
+    mid = (maxfinite + 2.0 ** (bias + 1)) / 2
+    tie_to_inf = inf_code % 2 == 0 and max_code % 2 == 1
+    assert cast(mid) == (inf_code if tie_to_inf else max_code)
+    if mid < 3.4e38:
+        assert cast(float(np.nextafter(np.float32(mid), np.float32(np.inf)))) == inf_code
+    # underflow: half the min subnormal ties to the even code 0; just above rounds to code 1
+    assert cast(min_sub / 2) == 0
+    assert cast(float(np.nextafter(np.float32(min_sub / 2), np.float32(np.inf)))) == 1
+    assert cast(-min_sub / 2) == 1 << (e + m)                           # -0 code
